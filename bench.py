@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""Benchmark of the CLQA inference hot path (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] -- BetaE on the synthetic FB15k-237 shape
+(14,505 entities, 237 relations, d 400, MLP 1600x2), batch 1024, all 14 query types.
+One step = one batch of every query type through the whole path (operator chain ->
+entity scoring -> top-k 10), i.e. 14 x 1024 queries.  value = queries/s over all ranks.
+
+N > 1 (torchrun): the entity table is sharded over the ranks; queries are
+replicated; each rank returns its local top-k, an NCCL all-gather exchanges them and
+kgq_merge_topk merges -> strong scaling of the same workload.
+
+--impl reference: the float64 CPU oracle (the reference arm of this tier), on rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "queries/sec per query type (BetaE, FB15k-237 shape) at 1/2/4/8 B200; HBM GB/s"
+N_ENT, N_REL, DIM, HID, BATCH, K = 14505, 237, 400, 1600, 1024, 10
+SEED = 2503_02172 + 1
+STRUCTS = synth.STRUCTURES
+CONFIG = {
+    "workload": "BetaE FB15k-237 shape, all 14 query types (BASELINE.json configs[1])",
+    "n_entity": N_ENT, "n_relation": N_REL, "dim": DIM, "hidden": HID, "hidden_layers": 2,
+    "batch": BATCH, "k": K, "structures": list(STRUCTS), "inputs": "kgr-init (random-init), seed 2503021173",
+}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=5)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def timed_oracle_sample(n_queries, start_type=0):
+    """The float64 oracle on `n_queries` BetaE queries (types cycling) -> (seconds, queries)."""
+    import oracle
+    t = synth.make_tables("betae", N_ENT, N_REL, DIM, hidden=HID, seed=SEED)
+    m = oracle.Model("betae", t, dim=DIM)
+    t0 = time.perf_counter()
+    for i in range(n_queries):
+        s = STRUCTS[(start_type + i) % len(STRUCTS)]
+        a, r = synth.make_queries(s, 1, N_ENT, N_REL, seed=synth.query_seed(SEED, s))
+        oracle.answer(m, s, a, r, K)
+    return time.perf_counter() - t0, n_queries
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    # warmup steps, then K timed steps; each step = one oracle query (types cycling)
+    timed_oracle_sample(args.warmup, 0)
+    sec, n = timed_oracle_sample(args.steps, args.warmup)
+    v = n / sec
+    cores = blas_threads()
+    line = {"metric": METRIC, "value": v, "unit": "queries/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sec / max(1, args.steps), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": CONFIG,
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{n} BetaE queries (1 per step, types cycling), full "
+                                       f"14,505-entity literal-KL scoring + sort, float64 numpy"},
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kgq", choices=["kgq", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-queries", type=int, default=14)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2503_02172_b200 import Engine
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t = synth.make_tables("betae", N_ENT, N_REL, DIM, hidden=HID, seed=SEED)
+    eng = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K, device=local,
+                 world_size=world, rank=rank)
+    eng.load_tables(t)
+    ns = eng.shard[1] - eng.shard[0]
+    stream = torch.cuda.current_stream()
+    qs = {}
+    for s in STRUCTS:
+        a, r = synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s))
+        qs[s] = (a, r, torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda())
+    out = {s: (torch.empty((BATCH, K), device="cuda"), torch.empty((BATCH, K), dtype=torch.int32, device="cuda"))
+           for s in STRUCTS}
+    gath = (torch.empty((world, BATCH, K), device="cuda"),
+            torch.empty((world, BATCH, K), dtype=torch.int32, device="cuda"))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    launches = [0]
+
+    def one_type(s):
+        a, r, da, dr = qs[s]
+        td, ti = eng.submit(s, da, dr, K, out=out[s])
+        launches[0] += eng.last_launch_count()
+        if world > 1:
+            dist.all_gather_into_tensor(gath[0], td)
+            dist.all_gather_into_tensor(gath[1], ti)
+            eng.merge_topk(gath[0], gath[1], K)
+            launches[0] += 1
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        for s in STRUCTS:
+            one_type(s)
+    barrier()
+    eng.check_errors()
+    eng.profile(True)
+    eng.profile_read()  # reset
+    launches[0] = 0
+    per_type = {s: 0.0 for s in STRUCTS}
+    step_ms = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in STRUCTS]
+    with ClockSampler(local) as clk:
+        barrier()
+        for _ in range(args.steps):
+            flush.zero_()  # untimed L2 flush between timed steps
+            torch.cuda.synchronize()
+            for i, s in enumerate(STRUCTS):
+                ev[i][0].record(stream)
+                one_type(s)
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            tot = 0.0
+            for i, s in enumerate(STRUCTS):
+                ms = ev[i][0].elapsed_time(ev[i][1])
+                per_type[s] += ms
+                tot += ms
+            step_ms.append(tot)
+        barrier()
+    prof = eng.profile_read()
+    eng.profile(False)
+    total_ms = sum(step_ms)
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    queries = args.steps * len(STRUCTS) * BATCH
+    value = queries / (total_ms / 1e3)
+
+    # ---- end to end through the public API with host buffers (pinned) ----------------
+    pin = {s: (torch.from_numpy(qs[s][0]).pin_memory(), torch.from_numpy(qs[s][1]).pin_memory()) for s in STRUCTS}
+    hout = (torch.empty((BATCH, K)).pin_memory(), torch.empty((BATCH, K), dtype=torch.int32).pin_memory())
+    h2d = sum(BATCH * (qs[s][0].shape[1] + qs[s][1].shape[1]) * 4 for s in STRUCTS)
+    d2h = len(STRUCTS) * BATCH * K * 8
+    e2e_v = None
+    if world == 1:
+        for s in STRUCTS:
+            eng.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K, out=(hout[0].numpy(), hout[1].numpy()))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for s in STRUCTS:
+                eng.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K, out=(hout[0].numpy(), hout[1].numpy()))
+        e2e_s = time.perf_counter() - t0
+        e2e_v = queries / e2e_s
+
+    # ---- roofline of the dominant kernel (entity scorer): FP32-ALU bound ----------------
+    peaks, peak_src = load_peaks()
+    score_ms, score_n = prof["score"]
+    n_union = sum(1 for s in STRUCTS if s in ("2u", "up"))
+    ops_per_step = 4.0 * BATCH * ns * DIM * (len(STRUCTS) + n_union)   # FP32 instr (lane ops)
+    achieved = ops_per_step * args.steps / (score_ms / 1e3) / 1e12
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    peak_alu = 148 * 128 * sm_mhz * 1e6 / 1e12     # T lane-instr/s at max clock
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "score_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+    stage_share = {k: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": dict(CONFIG, l2="flushed between timed steps (256 MiB write, untimed)",
+                           parallelism=f"entity-shard x{world}" if world > 1 else "1 GPU"),
+            "per_type_qps": {s: BATCH * args.steps / (per_type[s] / 1e3) for s in STRUCTS},
+            "stage_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "stage_share": stage_share,
+            "roofline": {"kernel": "k_score<BETAE> (entity scorer)", "bound": "alu",
+                         "achieved": achieved, "peak": peak_alu, "unit": "Tinstr/s",
+                         "frac": achieved / peak_alu, "traffic": traffic,
+                         "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz ({peak_src} sm_max_mhz)",
+                         "work": "4 FP32 instr per (query, entity, dim, DNF branch)"},
+            "scorer_table_gbs": (3 * ns * DIM * 4) * score_n / (score_ms / 1e3) / 1e9,
+            "gpu_launches": launches[0],
+            "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "how": "kgq_submit_host per type from pinned host buffers, wall clock"},
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            sec, n = timed_oracle_sample(args.cpu_queries, 0)
+            line["cpu_baseline"] = {"value": n / sec, "unit": "queries/s", "cores": blas_threads(),
+                                    "kind": "oracle",
+                                    "sample": f"{n} BetaE queries (1 per type), literal-KL scoring "
+                                              f"over all 14,505 entities + full sort, float64 numpy"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,191 @@
+/*
+ * kgq.h -- C ABI of libkgq.so: batched CLQA query-embedding inference on B200 (sm_100a).
+ *
+ * The hot path this library implements is the one
+ * KGCompiler (arXiv 2503.02172) accelerates: for a batch of queries of ONE structure,
+ * run the FOL operator chain of GQE / Query2Box / BetaE (projection, intersection,
+ * negation, DNF union; Eq. 1, Eq. 2, Eq. 4,
+ * P:146-150 fusion strategies), score the query embedding against every entity of this
+ * rank's shard (the "entity similarity query") and return the k nearest.
+ *
+ * Conventions (all entry points):
+ *  - Ids are int32, everything else fp32, row-major, C order.  Entity ids are GLOBAL.
+ *  - Scores are DISTANCES (>= 0; logit = gamma - distance), returned
+ *    ascending, ties broken by ascending entity id (Q13).
+ *  - "host" pointers are ordinary CPU memory, "device" pointers are CUDA device memory on
+ *    cfg.device.  The caller owns every pointer it passes; the library copies tables into
+ *    device memory it owns and frees in kgq_destroy().
+ *  - Every call returns a kgq_status; on failure kgq_last_error() describes it.  The
+ *    library never aborts the process.  A context is not thread-safe; use one per stream.
+ *  - Asynchronous calls are stream-ordered on the cudaStream_t passed (0 = legacy default).
+ */
+#ifndef KGQ_H
+#define KGQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KGQ_ABI_VERSION 1u
+
+typedef struct kgq_ctx kgq_ctx; /* opaque */
+typedef struct CUstream_st* kgq_stream; /* == cudaStream_t */
+
+typedef enum {
+  KGQ_OK = 0,
+  KGQ_EINVAL = 1,       /* bad argument (unknown structure, k > max_k, batch > max_batch, ...) */
+  KGQ_ERANGE = 2,       /* a query id was out of range (reported by kgq_check_errors)        */
+  KGQ_EUNSUPPORTED = 3, /* e.g. negation structure on GQE / Q2B                        */
+  KGQ_ESTATE = 4,       /* missing tables, not finalized, finalized twice                     */
+  KGQ_ENOMEM = 5,       /* device allocation failed                                           */
+  KGQ_ECUDA = 6         /* CUDA runtime / launch error                                        */
+} kgq_status;
+
+typedef enum { KGQ_GQE = 0, KGQ_Q2B = 1, KGQ_BETAE = 2 } kgq_model;
+
+/* The 14 query structures of P:34 / P:421 (Fig. 1 naming).  Slot layouts
+ * (KGReasoning flattened order [ext]) with a_i = anchor slot, r_j = relation
+ * slot, P = projection, I = intersection, N = negation, U = union (DNF, Eq. 1):
+ *   1p  P(a0,r0)                         2p  P(P(a0,r0),r1)        3p  P(P(P(a0,r0),r1),r2)
+ *   2i  I(P(a0,r0),P(a1,r1))             3i  I(P(a0,r0),P(a1,r1),P(a2,r2))
+ *   pi  I(P(P(a0,r0),r1),P(a1,r2))       ip  P(I(P(a0,r0),P(a1,r1)),r2)
+ *   2u  U(P(a0,r0),P(a1,r1))             up  U(P(P(a0,r0),r2),P(P(a1,r1),r2))
+ *   2in I(P(a0,r0),N(P(a1,r1)))          3in I(P(a0,r0),P(a1,r1),N(P(a2,r2)))
+ *   inp P(I(P(a0,r0),N(P(a1,r1))),r2)    pin I(P(P(a0,r0),r1),N(P(a1,r2)))
+ *   pni I(N(P(P(a0,r0),r1)),P(a1,r2))                                                     */
+typedef enum {
+  KGQ_1P = 0, KGQ_2P, KGQ_3P, KGQ_2I, KGQ_3I, KGQ_PI, KGQ_IP, KGQ_2U, KGQ_UP,
+  KGQ_2IN, KGQ_3IN, KGQ_INP, KGQ_PIN, KGQ_PNI, KGQ_NUM_STRUCTURES
+} kgq_structure;
+
+/* BetaE projection terminal: KGReasoning regulariser clamp(y+1,0.05,1e9)
+ * (default) or the literal Eq. 4 softmax over the 2d outputs followed by max(.,1e-6). */
+typedef enum { KGQ_TERM_REGULARIZER = 0, KGQ_TERM_SOFTMAX = 1 } kgq_proj_terminal;
+
+/* Relation tables (kgq_load_relations `which`). */
+typedef enum { KGQ_REL_MAIN = 0, KGQ_REL_OFFSET = 1 /* Q2B only */ } kgq_relation_table;
+
+/* nn.Linear layers (kgq_load_linear `layer_id`); W is [out_f, in_f] row-major, b is [out_f].
+ *   BetaE projection MLP (Eq. 4; shared weights, input [alpha;beta;r], Q3/Q4):
+ *     KGQ_LAYER_PROJ_OUT      = layer0 [2d, H]
+ *     KGQ_LAYER_PROJ_HIDDEN+l = layer(l+1), l = 0..n_hidden_layers-1: layer1 [H,3d], others [H,H]
+ *   Intersection attention (all models, Q6): KGQ_LAYER_INTER_1 [e,e], KGQ_LAYER_INTER_2 [d,e]
+ *     with e = d (GQE, Q2B centre) or 2d (BetaE, input [alpha;beta]).
+ *   Q2B offset gate: KGQ_LAYER_OFFSET_1 [d,d], KGQ_LAYER_OFFSET_2 [d,d].                    */
+enum {
+  KGQ_LAYER_PROJ_OUT = 0,
+  KGQ_LAYER_PROJ_HIDDEN = 1, /* .. KGQ_LAYER_PROJ_HIDDEN + 7 */
+  KGQ_LAYER_INTER_1 = 16,
+  KGQ_LAYER_INTER_2 = 17,
+  KGQ_LAYER_OFFSET_1 = 18,
+  KGQ_LAYER_OFFSET_2 = 19
+};
+
+typedef struct {
+  uint32_t abi_version;     /* must be KGQ_ABI_VERSION */
+  int32_t model;            /* kgq_model */
+  int64_t n_entity;         /* global N */
+  int32_t n_relation;       /* R */
+  int32_t dim;              /* d (multiple of 4) */
+  int32_t hidden;           /* BetaE MLP width H (1600); ignored otherwise */
+  int32_t n_hidden_layers;  /* BetaE MLP hidden layers (2), 1..8 */
+  float cen;                /* Q2B inside-distance weight (0.02, Q10) */
+  int32_t terminal;         /* kgq_proj_terminal (BetaE) */
+  int32_t max_batch;        /* upper bound on `batch` in submit calls (scratch sizing) */
+  int32_t max_k;            /* upper bound on k, <= 256 */
+  int32_t device;           /* CUDA device ordinal */
+  int32_t world_size;       /* number of entity shards (ranks), >= 1 */
+  int32_t rank;             /* this rank's shard, 0 <= rank < world_size */
+} kgq_config;
+
+/* ---- lifetime ------------------------------------------------------------------------- */
+/* Validate cfg and create a context on cfg.device.  *out is NULL on failure. */
+kgq_status kgq_create(const kgq_config* cfg, kgq_ctx** out);
+/* Free all device memory owned by ctx.  NULL-safe.  Synchronises the device. */
+void kgq_destroy(kgq_ctx* ctx);
+/* Message describing the last failure on ctx (or of the last kgq_create when ctx is NULL).
+ * Valid until the next call on ctx. */
+const char* kgq_last_error(const kgq_ctx* ctx);
+const char* kgq_status_string(kgq_status s);
+
+/* ---- structure metadata (pure host, no GPU needed) ------------------------------------- */
+int32_t kgq_num_anchors(int32_t s);   /* -1 if s is not a kgq_structure */
+int32_t kgq_num_relations(int32_t s);
+int32_t kgq_num_branches(int32_t s);  /* DNF clauses: 2 for 2u/up, else 1 */
+int32_t kgq_uses_negation(int32_t s);
+const char* kgq_structure_name(int32_t s);       /* "1p" ... "pni", NULL if invalid */
+int32_t kgq_structure_from_name(const char* n);  /* -1 if unknown */
+/* Width of one query-embedding row: d (GQE), 2d (Q2B [centre;offset]), 2d (BetaE [alpha;beta]). */
+int32_t kgq_embedding_width(int32_t model, int32_t dim);
+/* Contiguous entity shard of `rank`: [r*ceil(N/W), min(N,(r+1)*ceil(N/W))). */
+kgq_status kgq_shard_range(int64_t n_entity, int32_t world_size, int32_t rank,
+                           int64_t* begin, int64_t* end);
+int64_t kgq_shard_begin(const kgq_ctx* ctx);
+int64_t kgq_shard_end(const kgq_ctx* ctx);
+
+/* ---- tables (host pointers, copied synchronously) --------------------------------------- */
+/* Rows [first_row, first_row+n_rows) of the GLOBAL entity table, host fp32:
+ *   GQE / Q2B: [n_rows, d];  BetaE: raw [n_rows, 2d] = [alpha_raw; beta_raw] (Eq. 3 params
+ *   before the regulariser, Q12).  May be called several times to stream a large table.
+ * Every rank keeps all rows for anchor gathers (queries are replicated, §8(e)); the scoring
+ * layout is built for this rank's shard only, at finalize. */
+kgq_status kgq_load_entities(kgq_ctx* ctx, const float* rows, int64_t first_row, int64_t n_rows);
+/* Relation table `which` (kgq_relation_table), host fp32 [n, d]; n must equal n_relation. */
+kgq_status kgq_load_relations(kgq_ctx* ctx, int32_t which, const float* rows, int32_t n);
+/* nn.Linear layer (see KGQ_LAYER_*): host W [out_f, in_f], b [out_f]; shapes are checked. */
+kgq_status kgq_load_linear(kgq_ctx* ctx, int32_t layer_id, const float* W, const float* b,
+                           int32_t out_f, int32_t in_f);
+/* Check completeness, apply the BetaE regulariser to entity rows, build this shard's scoring
+ * layout (BetaE: fp64 precompute of C, U, V per entity and dim), allocate
+ * scratch for max_batch.  Synchronous.  Required before submit. */
+kgq_status kgq_finalize(kgq_ctx* ctx);
+
+/* ---- the hot path (device pointers, asynchronous on `stream`) --------------------------- */
+/* anchors: device int32 [batch, kgq_num_anchors(s)]; rels: device int32 [batch,
+ * kgq_num_relations(s)]; k in [1, min(max_k, shard size)].
+ * Writes topk_dist fp32 [batch, k] and topk_id int32 [batch, k] (global ids, this shard's
+ * k nearest, (dist, id) ascending).  shard_dist (optional, may be NULL): fp32
+ * [batch, shard_end-shard_begin], the full distance row of every query (debug / parity).
+ * Out-of-range ids are detected on the device: that query row gets dist NaN, id -1, and
+ * kgq_check_errors() later returns KGQ_ERANGE. */
+kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                      const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
+                      float* shard_dist, kgq_stream stream);
+/* Same as kgq_submit with HOST pointers: copies anchors/rels host->device, runs the path,
+ * copies the top-k back, and synchronises `stream` before returning (end-to-end call). */
+kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                           const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
+                           kgq_stream stream);
+/* Operator chain only (parity aid): device out fp32 [batch, kgq_num_branches(s),
+ * kgq_embedding_width(model, d)]. */
+kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                               const int32_t* rels, float* out, kgq_stream stream);
+/* Cross-shard merge (§8(e), a9): device in_dist fp32 [n_parts, batch, k], in_id int32
+ * [n_parts, batch, k] (e.g. the result of an all-gather of every rank's top-k) -> device
+ * out_dist/out_id [batch, k], (dist, id) ascending.  NaN rows propagate as NaN/-1. */
+kgq_status kgq_merge_topk(kgq_ctx* ctx, int32_t n_parts, int32_t batch, int32_t k,
+                          const float* in_dist, const int32_t* in_id, float* out_dist,
+                          int32_t* out_id, kgq_stream stream);
+/* Synchronise `stream`; KGQ_ERANGE (message names query row and slot) if any submit since
+ * the last check saw an out-of-range id, KGQ_ECUDA on an asynchronous CUDA error. */
+kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream);
+
+/* ---- introspection (parity / bench) ----------------------------------------------------- */
+/* Number of this library's kernels launched by the last submit/query_embedding call. */
+int32_t kgq_last_launch_count(const kgq_ctx* ctx);
+/* BetaE only: copy this shard's precomputed entity terms to device out fp32 [3, d, n_shard]
+ * (C, U, V planes).  Parity aid for the fp64 precompute. */
+kgq_status kgq_entity_terms(kgq_ctx* ctx, float* out, kgq_stream stream);
+/* Stage timing with CUDA events recorded on the launching stream (bench roofline).  Stages:
+ * 0 operator chain, 1 scorer operand prep, 2 entity scorer, 3 top-k. */
+kgq_status kgq_profile_enable(kgq_ctx* ctx, int32_t on);
+/* Summed device milliseconds ms[4] and launch-group counts n[4] since the last read;
+ * synchronises on the recorded events, then resets. */
+kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KGQ_H */

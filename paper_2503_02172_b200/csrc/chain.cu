@@ -1,0 +1,271 @@
+// Operator-chain kernels: anchor/relation gathers, GQE/Q2B
+// translation projections, BetaE MLP input assembly, negation, attention combine.
+//
+// Layouts: split states S are [rows, w] with rows = branch * B + b; final query
+// embeddings q are [B, nb, w] fp32 (w = d GQE, 2d Q2B [centre; offset], 2d BetaE
+// [alpha; beta]).  All index reads are range-checked on the device (kgq.h: dist NaN,
+// id -1, KGQ_ERANGE), with the offending id clamped to 0 so no read is out of bounds.
+#include "common.cuh"
+#include "kgq_internal.cuh"
+
+namespace kgq {
+
+__device__ __forceinline__ int checked_id(int v, int64_t n, int32_t* err, int32_t* invalid,
+                                          int row, int slot, int kind) {
+  if (v < 0 || v >= n) {
+    if (threadIdx.x == 0) report_range(err, invalid, row, slot, kind);
+    return 0;
+  }
+  return v;
+}
+
+// ---- GQE / Q2B: q = E[a] + R[r0] + R[r1] + ...; Q2B offset o = 0 + R_o[r0] + ... --------
+// (horizontal fusion P:146: the whole projection chain of a branch in one pass; vertical
+// fusion P:148: all branches of the query in one launch, blockIdx.y = branch)
+__global__ void k_translate_chain(ChainArgs a, const float* __restrict__ ent,
+                                  const float* __restrict__ rel,
+                                  const float* __restrict__ rel_off, int B, Split out,
+                                  float* __restrict__ q) {
+  const int b = blockIdx.x;
+  const int br = blockIdx.y;
+  const BranchPlan& P = a.br[br];
+  const int d = a.d;
+  const int aid = checked_id(a.anchors[(int64_t)b * a.n_a + P.anchor], a.n_entity, a.err,
+                             a.invalid, b, P.anchor, 0);
+  int rid[kMaxOps];
+#pragma unroll
+  for (int o = 0; o < kMaxOps; ++o) {
+    rid[o] = (o < P.nops && P.ops[o] >= 0)
+                 ? checked_id(a.rels[(int64_t)b * a.n_r + P.ops[o]], a.n_relation, a.err,
+                              a.invalid, b, P.ops[o], 1)
+                 : 0;
+  }
+  const bool q2b = a.model == KGQ_Q2B;
+  const int w = q2b ? 2 * d : d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float c = ent[(int64_t)aid * d + j];
+    float off = 0.0f;
+    for (int o = 0; o < P.nops; ++o) {
+      c += rel[(int64_t)rid[o] * d + j];
+      if (q2b) off += rel_off[(int64_t)rid[o] * d + j];
+    }
+    if (out.hi) {
+      const int64_t row = (int64_t)br * B + b;
+      store_split(out.hi, out.lo, row * out.ld + j, c);
+      if (q2b) store_split(out.hi, out.lo, row * out.ld + d + j, off);
+    } else {
+      float* dst = q + ((int64_t)b * a.nb + br) * w;
+      dst[j] = c;
+      if (q2b) dst[d + j] = off;
+    }
+  }
+}
+
+int launch_translate_chain(const ChainArgs& a, const float* ent, const float* rel,
+                           const float* rel_off, int B, Split out_split, float* out_q,
+                           cudaStream_t st) {
+  dim3 grid(B, a.nb);
+  k_translate_chain<<<grid, 128, 0, st>>>(a, ent, rel, rel_off, B, out_split, out_q);
+  return 1;
+}
+
+// ---- BetaE MLP input: z = [alpha; beta; R[r]] (Eq. 4 var_S with the relation, Q3) -------
+// Group row g*B + b of Z; source = regularised anchor row or split state row.
+__global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
+                                  const float* __restrict__ rel, int B, MlpGroup g, Split src,
+                                  Split z) {
+  const int b = blockIdx.x;
+  const int gi = blockIdx.y;
+  const int d = a.d;
+  const int rslot = g.rel_slot[gi];
+  const int rid = checked_id(a.rels[(int64_t)b * a.n_r + rslot], a.n_relation, a.err,
+                             a.invalid, b, rslot, 1);
+  int aid = 0;
+  const bool from_anchor = g.anchor_slot[gi] >= 0;
+  if (from_anchor)
+    aid = checked_id(a.anchors[(int64_t)b * a.n_a + g.anchor_slot[gi]], a.n_entity, a.err,
+                     a.invalid, b, g.anchor_slot[gi], 0);
+  const int64_t zrow = ((int64_t)gi * B + b) * z.ld;
+  const int64_t srow = (g.src_row[gi] + b) * src.ld;
+  for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+    float x = from_anchor ? ent[(int64_t)aid * 2 * d + j] : load_split(src.hi, src.lo, srow + j);
+    store_split(z.hi, z.lo, zrow + j, x);
+  }
+  for (int j = threadIdx.x; j < d; j += blockDim.x)
+    store_split(z.hi, z.lo, zrow + 2 * d + j, rel[(int64_t)rid * d + j]);
+}
+
+int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
+                           const MlpGroup& g, Split src, Split z, cudaStream_t st) {
+  dim3 grid(B, g.n);
+  k_betae_mlp_input<<<grid, 128, 0, st>>>(a, ent, rel, B, g, src, z);
+  return 1;
+}
+
+// ---- BetaE Eq.-4 literal terminal: softmax over the 2d outputs, max(., 1e-6) -----------
+__global__ void k_softmax_terminal(const float* __restrict__ T, int64_t ldt, int w, Split out,
+                                   int64_t out_row0, int neg0, int neg1) {
+  const int r = blockIdx.x;
+  const float* t = T + (int64_t)r * ldt;
+  __shared__ float red[32];
+  float m = -INFINITY;
+  for (int j = threadIdx.x; j < w; j += blockDim.x) m = fmaxf(m, t[j]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  m = red[0];
+  __syncthreads();
+  float s = 0.0f;
+  for (int j = threadIdx.x; j < w; j += blockDim.x) s += expf(t[j] - m);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = 1.0f / red[0];
+  const bool neg = r >= neg0 && r < neg1;
+  for (int j = threadIdx.x; j < w; j += blockDim.x) {
+    float y = fmaxf(expf(t[j] - m) * inv, 1e-6f);
+    if (neg) y = 1.0f / y;
+    store_split(out.hi, out.lo, (out_row0 + r) * out.ld + j, y);
+  }
+}
+
+int launch_softmax_terminal(const float* T, int64_t ldt, int M, int w, Split out,
+                            int64_t out_row0, int neg0, int neg1, cudaStream_t st) {
+  k_softmax_terminal<<<M, 256, 0, st>>>(T, ldt, w, out, out_row0, neg0, neg1);
+  return 1;
+}
+
+// ---- negation (Q5): alpha -> 1/alpha, beta -> 1/beta, in place on split rows -----------
+__global__ void k_negate(Split x, int64_t r0, int64_t nrows, int w) {
+  const int64_t n = nrows * w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = r0 + i / w, j = i % w;
+    const int64_t o = r * x.ld + j;
+    store_split(x.hi, x.lo, o, 1.0f / load_split(x.hi, x.lo, o));
+  }
+}
+
+int launch_negate(Split x, int64_t r0, int64_t r1, int w, cudaStream_t st) {
+  const int64_t n = (r1 - r0) * w;
+  const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  k_negate<<<blocks, 256, 0, st>>>(x, r0, r1 - r0, w);
+  return 1;
+}
+
+// ---- Q2B offset gate input: mean over branches of ReLU(V1 o_i + c1) --------------------
+__global__ void k_branch_mean(const float* __restrict__ T, int64_t ldt, int nb, int B, int d,
+                              Split out) {
+  const int b = blockIdx.x;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float s = 0.0f;
+    for (int i = 0; i < nb; ++i) s += T[((int64_t)i * B + b) * ldt + j];
+    store_split(out.hi, out.lo, (int64_t)b * out.ld + j, s / (float)nb);
+  }
+}
+
+int launch_branch_mean(const float* T, int64_t ldt, int nb, int B, int d, Split out,
+                       cudaStream_t st) {
+  k_branch_mean<<<B, 128, 0, st>>>(T, ldt, nb, B, d, out);
+  return 1;
+}
+
+// ---- attention combine (Q6): a_i = softmax_i(logit_i) per dim; out = sum_i a_i x_i --------
+// GQE: x = state[:, :d].  BetaE: the same a_i weights alpha (cols [0,d)) and beta ([d,2d)).
+// Q2B: centre as GQE; offset o = min_i o_i * sigmoid(G) (gate logits G [B, d]).
+// Post projection (ip): + R[r] on the centre (GQE/Q2B; Q2B offset + R_o[r]).
+__global__ void k_attention_combine(CombineArgs c, Split S, const float* __restrict__ logits,
+                                    const float* __restrict__ gate, Split out,
+                                    float* __restrict__ q) {
+  const int b = blockIdx.x;
+  const int d = c.d;
+  const int B = c.B;
+  const int nb = c.nb;
+  int rid = 0;
+  if (c.post_slot >= 0)
+    rid = checked_id(c.rels[(int64_t)b * c.n_r + c.post_slot], c.n_relation, c.err, c.invalid,
+                     b, c.post_slot, 1);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float l[kMaxBranches];
+    float m = -INFINITY;
+    for (int i = 0; i < nb; ++i) {
+      l[i] = logits[((int64_t)i * B + b) * c.ldl + j];
+      m = fmaxf(m, l[i]);
+    }
+    float s = 0.0f;
+    for (int i = 0; i < nb; ++i) {
+      l[i] = expf(l[i] - m);
+      s += l[i];
+    }
+    const float inv = 1.0f / s;
+    float x0 = 0.0f, x1 = 0.0f, omin = INFINITY;
+    for (int i = 0; i < nb; ++i) {
+      const int64_t row = ((int64_t)i * B + b) * S.ld;
+      const float a = l[i] * inv;
+      x0 += a * load_split(S.hi, S.lo, row + j);
+      if (c.model == KGQ_BETAE) x1 += a * load_split(S.hi, S.lo, row + d + j);
+      if (c.model == KGQ_Q2B) omin = fminf(omin, load_split(S.hi, S.lo, row + d + j));
+    }
+    if (c.model == KGQ_Q2B) {
+      const float g = gate[(int64_t)b * c.ldg + j];
+      x1 = omin * (1.0f / (1.0f + expf(-g)));
+    }
+    if (c.post_slot >= 0) {
+      x0 += c.rel[(int64_t)rid * d + j];
+      if (c.model == KGQ_Q2B) x1 += c.rel_off[(int64_t)rid * d + j];
+    }
+    const bool two = c.model != KGQ_GQE;
+    if (out.hi) {
+      store_split(out.hi, out.lo, (int64_t)b * out.ld + j, x0);
+      if (two) store_split(out.hi, out.lo, (int64_t)b * out.ld + d + j, x1);
+    } else {
+      float* dst = q + (int64_t)b * (two ? 2 * d : d);
+      dst[j] = x0;
+      if (two) dst[d + j] = x1;
+    }
+  }
+}
+
+int launch_attention_combine(const CombineArgs& c, Split S, const float* logits,
+                             const float* gate, Split out_split, float* out_q, cudaStream_t st) {
+  k_attention_combine<<<c.B, 128, 0, st>>>(c, S, logits, gate, out_split, out_q);
+  return 1;
+}
+
+// ---- split state rows -> q[b, br, :] ---------------------------------------------------
+__global__ void k_state_to_q(Split S, int nb, int B, int w, float* __restrict__ q) {
+  const int b = blockIdx.x, br = blockIdx.y;
+  for (int j = threadIdx.x; j < w; j += blockDim.x)
+    q[((int64_t)b * nb + br) * w + j] = load_split(S.hi, S.lo, ((int64_t)br * B + b) * S.ld + j);
+}
+
+int launch_state_to_q(Split S, int nb, int B, int w, float* q, cudaStream_t st) {
+  k_state_to_q<<<dim3(B, nb), 128, 0, st>>>(S, nb, B, w, q);
+  return 1;
+}
+
+// ---- split copy (weights -> tensor-core operands) --------------------------------------
+__global__ void k_split_copy(const float* __restrict__ src, int64_t n, float* hi, float* lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    store_split(hi, lo, i, src[i]);
+}
+
+int launch_split_copy(const float* src, int64_t n, float* hi, float* lo, cudaStream_t st) {
+  k_split_copy<<<1024, 256, 0, st>>>(src, n, hi, lo);
+  return 1;
+}
+
+}  // namespace kgq

@@ -1,0 +1,726 @@
+// libkgq.so: C ABI (include/kgq.h) + host planner.
+//
+// The planner replaces the paper's Graph Capturer / Pattern Recognizer / Operator Fuser
+// (Eq. 2, Eq. 4, Alg. 1) by static per-structure plans decided
+// at compile time: for each query structure it launches a fixed chain of fused kernels
+// (horizontal fusion of projection chains, vertical fusion of branches, union fused into the
+// scorer), then the entity scorer and the top-k selection, all on the caller's stream.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kgq_internal.cuh"
+
+using namespace kgq;
+
+namespace kgq {
+
+// ---- static plans --------------------------------------------------------
+#define BR(a, n, o0, o1, o2) {a, n, {o0, o1, o2, 0}}
+static const Plan kPlans[KGQ_NUM_STRUCTURES] = {
+    /* 1p  */ {kSingle, 1, {BR(0, 1, 0, 0, 0)}, 0, {0, 0}, 1, 1, 1, false},
+    /* 2p  */ {kSingle, 1, {BR(0, 2, 0, 1, 0)}, 0, {0, 0}, 1, 2, 1, false},
+    /* 3p  */ {kSingle, 1, {BR(0, 3, 0, 1, 2)}, 0, {0, 0}, 1, 3, 1, false},
+    /* 2i  */ {kInter, 2, {BR(0, 1, 0, 0, 0), BR(1, 1, 1, 0, 0)}, 0, {0, 0}, 2, 2, 1, false},
+    /* 3i  */ {kInter, 3, {BR(0, 1, 0, 0, 0), BR(1, 1, 1, 0, 0), BR(2, 1, 2, 0, 0)}, 0, {0, 0}, 3, 3, 1, false},
+    /* pi  */ {kInter, 2, {BR(0, 2, 0, 1, 0), BR(1, 1, 2, 0, 0)}, 0, {0, 0}, 2, 3, 1, false},
+    /* ip  */ {kInter, 2, {BR(0, 1, 0, 0, 0), BR(1, 1, 1, 0, 0)}, 1, {2, 0}, 2, 3, 1, false},
+    /* 2u  */ {kUnion, 2, {BR(0, 1, 0, 0, 0), BR(1, 1, 1, 0, 0)}, 0, {0, 0}, 2, 2, 2, false},
+    /* up  */ {kUnion, 2, {BR(0, 2, 0, 2, 0), BR(1, 2, 1, 2, 0)}, 0, {0, 0}, 2, 3, 2, false},
+    /* 2in */ {kInter, 2, {BR(0, 1, 0, 0, 0), BR(1, 2, 1, kOpNeg, 0)}, 0, {0, 0}, 2, 2, 1, true},
+    /* 3in */ {kInter, 3, {BR(0, 1, 0, 0, 0), BR(1, 1, 1, 0, 0), BR(2, 2, 2, kOpNeg, 0)}, 0, {0, 0}, 3, 3, 1, true},
+    /* inp */ {kInter, 2, {BR(0, 1, 0, 0, 0), BR(1, 2, 1, kOpNeg, 0)}, 1, {2, 0}, 2, 3, 1, true},
+    /* pin */ {kInter, 2, {BR(0, 2, 0, 1, 0), BR(1, 2, 2, kOpNeg, 0)}, 0, {0, 0}, 2, 3, 1, true},
+    /* pni */ {kInter, 2, {BR(0, 3, 0, 1, kOpNeg), BR(1, 1, 2, 0, 0)}, 0, {0, 0}, 2, 3, 1, true},
+};
+#undef BR
+static const char* kNames[KGQ_NUM_STRUCTURES] = {"1p", "2p", "3p", "2i", "3i", "pi", "ip",
+                                                 "2u", "up", "2in", "3in", "inp", "pin", "pni"};
+const Plan* plan_of(int s) {
+  return (s >= 0 && s < KGQ_NUM_STRUCTURES) ? &kPlans[s] : nullptr;
+}
+
+}  // namespace kgq
+
+namespace {
+
+thread_local std::string g_create_err;
+
+kgq_status fail(kgq_ctx* c, kgq_status s, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+kgq_status fail(kgq_ctx* c, kgq_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf; else g_create_err = buf;
+  return s;
+}
+
+kgq_status cuda_fail(kgq_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, e == cudaErrorMemoryAllocation ? KGQ_ENOMEM : KGQ_ECUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+#define CK(call, what)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, what); \
+  } while (0)
+
+template <typename T>
+kgq_status dalloc(kgq_ctx* ctx, T** p, size_t n, const char* what) {
+  *p = nullptr;
+  if (n == 0) return KGQ_OK;
+  CK(cudaMalloc((void**)p, n * sizeof(T)), what);
+  return KGQ_OK;
+}
+
+kgq_status alloc_split(kgq_ctx* ctx, Split* s, int64_t rows, int64_t w, const char* what) {
+  s->ld = w;
+  kgq_status st = dalloc(ctx, &s->hi, (size_t)(rows * w), what);
+  if (st) return st;
+  return dalloc(ctx, &s->lo, (size_t)(rows * w), what);
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---- profiling (CUDA events on the launching stream) ------------------------------------
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+std::vector<ProfRec>& prof_list(kgq_ctx* ctx) {
+  static thread_local std::vector<std::pair<kgq_ctx*, std::vector<ProfRec>>> lists;
+  for (auto& l : lists)
+    if (l.first == ctx) return l.second;
+  lists.emplace_back(ctx, std::vector<ProfRec>{});
+  return lists.back().second;
+}
+struct StageTimer {
+  kgq_ctx* ctx;
+  cudaStream_t st;
+  int stage;
+  cudaEvent_t a = nullptr;
+  StageTimer(kgq_ctx* c, cudaStream_t s, int stg) : ctx(c), st(s), stage(stg) {
+    if (!ctx->profile) return;
+    cudaEventCreate(&a);
+    cudaEventRecord(a, st);
+  }
+  ~StageTimer() {
+    if (!ctx->profile) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, st);
+    prof_list(ctx).push_back({stage, a, b});
+    ctx->prof_n[stage] += 1;
+  }
+};
+
+ChainArgs chain_args(kgq_ctx* ctx, const Plan* P, int B, const int32_t* anchors,
+                     const int32_t* rels) {
+  ChainArgs a{};
+  a.model = ctx->cfg.model;
+  a.d = ctx->cfg.dim;
+  a.nb = P->nbranch;
+  for (int i = 0; i < P->nbranch; ++i) a.br[i] = P->br[i];
+  a.anchors = anchors;
+  a.n_a = P->n_anchor;
+  a.rels = rels;
+  a.n_r = P->n_rel;
+  a.n_entity = ctx->cfg.n_entity;
+  a.n_relation = ctx->cfg.n_relation;
+  a.err = ctx->d_err;
+  a.invalid = ctx->d_invalid;
+  (void)B;
+  return a;
+}
+
+Split offset_split(const Split& s, int64_t rows, int64_t cols = 0) {
+  return Split{s.hi + rows * s.ld + cols, s.lo + rows * s.ld + cols, s.ld};
+}
+
+// BetaE: one projection hop (Eq. 4 MLP) for the contiguous branch run [br0, br0+n) of rows
+// B each.  Input from anchors (hop 0) or state S; output written back into S rows; rows of
+// branches whose next op is a negation get 1/x in the same epilogue.
+int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
+              const int (*proj)[kMaxOps], const bool (*neg_after)[kMaxOps], Split src_state,
+              int64_t src_row0, cudaStream_t st) {
+  const int d = ctx->cfg.dim;
+  MlpGroup g{};
+  g.n = n;
+  for (int gi = 0; gi < n; ++gi) {
+    const int br = br0 + gi;
+    g.rel_slot[gi] = proj[br][hop];
+    g.anchor_slot[gi] = hop == 0 && src_row0 < 0 ? ca.br[br].anchor : -1;
+    g.src_row[gi] = src_row0 < 0 ? (int64_t)br * B : src_row0 + (int64_t)gi * B;
+  }
+  int L = 0;
+  L += launch_betae_mlp_input(ca, ctx->ent, ctx->rel[0], B, g, src_state, ctx->Z, st);
+  const int M = n * B;
+  Split A = ctx->Z;
+  int K = 3 * d;
+  for (int l = 0; l < ctx->cfg.n_hidden_layers; ++l) {
+    const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
+    L += launch_linear(A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
+    A = ctx->H[l & 1];
+    K = lin.out_f;
+  }
+  int neg0 = M, neg1 = M;  // rows of this group to negate (a single interval suffices for the
+  std::vector<std::pair<int, int>> extra;  // 14 plans; other patterns get extra launches)
+  for (int gi = 0; gi < n; ++gi) {
+    if (!neg_after[br0 + gi][hop]) continue;
+    const int r0 = gi * B, r1 = r0 + B;
+    if (neg0 == M) {
+      neg0 = r0;
+      neg1 = r1;
+    } else if (r0 == neg1) {
+      neg1 = r1;
+    } else {
+      extra.emplace_back(r0, r1);
+    }
+  }
+  Split out = offset_split(ctx->S, (int64_t)br0 * B);
+  const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
+  if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
+    L += launch_linear(A, M, K, lo, kEpiNone, Split{ctx->T, nullptr, 2 * d}, 0, 0, st);
+    L += launch_softmax_terminal(ctx->T, 2 * d, M, 2 * d, out, 0, neg0, neg1, st);
+  } else {
+    L += launch_linear(A, M, K, lo, kEpiBetaReg, out, neg0, neg1, st);
+  }
+  for (auto& e : extra) L += launch_negate(out, e.first, e.second, 2 * d, st);
+  return L;
+}
+
+// Operator chain for one batch: writes ctx->Q [B, n_out, qw].
+int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t* rels,
+              cudaStream_t st) {
+  const Plan* P = plan_of(s);
+  const int model = ctx->cfg.model;
+  const int d = ctx->cfg.dim;
+  ChainArgs ca = chain_args(ctx, P, B, anchors, rels);
+  int L = 0;
+  const int nb = P->nbranch;
+  const int64_t M = (int64_t)nb * B;
+
+  if (model != KGQ_BETAE) {
+    if (P->kind != kInter) {
+      return launch_translate_chain(ca, ctx->ent, ctx->rel[0], ctx->rel[1], B, Split{nullptr, nullptr, 0},
+                                    ctx->Q, st);
+    }
+    L += launch_translate_chain(ca, ctx->ent, ctx->rel[0], ctx->rel[1], B, ctx->S, nullptr, st);
+    // attention logits over centres (Q6): W2 ReLU(W1 x + b1) + b2, rows br*B + b
+    const Split centres{ctx->S.hi, ctx->S.lo, ctx->S.ld};
+    L += launch_linear(centres, (int)M, d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
+    L += launch_linear(ctx->I, (int)M, d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
+                       Split{ctx->T, nullptr, ctx->tw}, 0, 0, st);
+    const float* gate = nullptr;
+    if (model == KGQ_Q2B) {  // offset gate: sigmoid(V2 mean_i ReLU(V1 o_i + c1) + c2)
+      const Split offs{ctx->S.hi + d, ctx->S.lo + d, ctx->S.ld};
+      L += launch_linear(offs, (int)M, d, ctx->lin[KGQ_LAYER_OFFSET_1], kEpiRelu,
+                         Split{ctx->T2, nullptr, ctx->tw}, 0, 0, st);
+      L += launch_branch_mean(ctx->T2, ctx->tw, nb, B, d, ctx->M, st);
+      L += launch_linear(ctx->M, B, d, ctx->lin[KGQ_LAYER_OFFSET_2], kEpiNone,
+                         Split{ctx->T2, nullptr, ctx->tw}, 0, 0, st);
+      gate = ctx->T2;
+    }
+    CombineArgs c{};
+    c.model = model; c.nb = nb; c.B = B; c.d = d; c.ldl = ctx->tw; c.ldg = ctx->tw;
+    c.rel = ctx->rel[0]; c.rel_off = ctx->rel[1]; c.rels = rels; c.n_r = P->n_rel;
+    c.n_relation = ctx->cfg.n_relation; c.post_slot = P->npost ? P->post[0] : -1;
+    c.err = ctx->d_err; c.invalid = ctx->d_invalid;
+    L += launch_attention_combine(c, ctx->S, ctx->T, gate, Split{nullptr, nullptr, 0}, ctx->Q, st);
+    return L;
+  }
+
+  // ---- BetaE ------------------------------------------------------------------------------
+  int proj[kMaxBranches][kMaxOps];
+  bool neg_after[kMaxBranches][kMaxOps];
+  int nproj[kMaxBranches];
+  int maxh = 0;
+  for (int br = 0; br < nb; ++br) {
+    nproj[br] = 0;
+    for (int o = 0; o < P->br[br].nops; ++o) {
+      const int op = P->br[br].ops[o];
+      if (op == kOpNeg) {
+        neg_after[br][nproj[br] - 1] = true;  // plans never negate a bare anchor
+      } else {
+        proj[br][nproj[br]] = op;
+        neg_after[br][nproj[br]] = false;
+        nproj[br]++;
+      }
+    }
+    maxh = std::max(maxh, nproj[br]);
+  }
+  for (int h = 0; h < maxh; ++h) {
+    int br = 0;
+    while (br < nb) {  // contiguous runs of branches that still project at hop h
+      if (nproj[br] <= h) { ++br; continue; }
+      int e = br;
+      while (e < nb && nproj[e] > h) ++e;
+      L += betae_hop(ctx, ca, B, h, br, e - br, proj, neg_after, ctx->S, h == 0 ? -1 : (int64_t)br * B,
+                     st);
+      br = e;
+    }
+  }
+  if (P->kind != kInter) return L + launch_state_to_q(ctx->S, P->n_out, B, 2 * d, ctx->Q, st);
+  // intersection (Q6): attention over [alpha_i; beta_i] (2d -> 2d -> d), shared weights a_i
+  L += launch_linear(ctx->S, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
+  L += launch_linear(ctx->I, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
+                     Split{ctx->T, nullptr, ctx->tw}, 0, 0, st);
+  CombineArgs c{};
+  c.model = model; c.nb = nb; c.B = B; c.d = d; c.ldl = ctx->tw; c.ldg = 0;
+  c.rels = rels; c.n_r = P->n_rel; c.n_relation = ctx->cfg.n_relation; c.post_slot = -1;
+  c.err = ctx->d_err; c.invalid = ctx->d_invalid;
+  if (P->npost == 0)
+    return L + launch_attention_combine(c, ctx->S, ctx->T, nullptr, Split{nullptr, nullptr, 0}, ctx->Q, st);
+  L += launch_attention_combine(c, ctx->S, ctx->T, nullptr, ctx->M, nullptr, st);
+  // post projections (ip, inp): MLP hops on the combined state, result in S rows [0, B)
+  int pproj[kMaxBranches][kMaxOps] = {};
+  bool pneg[kMaxBranches][kMaxOps] = {};
+  Split src = ctx->M;
+  for (int p = 0; p < P->npost; ++p) {
+    pproj[0][p] = P->post[p];
+    ChainArgs cb = ca;
+    L += betae_hop(ctx, cb, B, p, 0, 1, pproj, pneg, src, 0, st);
+    src = ctx->S;
+  }
+  return L + launch_state_to_q(ctx->S, 1, B, 2 * d, ctx->Q, st);
+}
+
+kgq_status check_submit(kgq_ctx* ctx, int32_t s, int32_t batch, int32_t k, bool need_k) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (!ctx->finalized) return fail(ctx, KGQ_ESTATE, "kgq_finalize() has not been called");
+  const Plan* P = plan_of(s);
+  if (!P)
+    return fail(ctx, KGQ_EINVAL,
+                "unknown structure %d; valid: 0..13 = 1p 2p 3p 2i 3i pi ip 2u up 2in 3in inp pin pni", s);
+  if (P->negation && ctx->cfg.model != KGQ_BETAE)
+    return fail(ctx, KGQ_EUNSUPPORTED, "structure %s uses negation; GQE/Q2B do not support the n operator",
+                kNames[s]);
+  if (batch < 0 || batch > ctx->cfg.max_batch)
+    return fail(ctx, KGQ_EINVAL, "batch %d outside [0, max_batch=%d]", batch, ctx->cfg.max_batch);
+  if (need_k && (k < 1 || k > ctx->cfg.max_k || k > ctx->ns))
+    return fail(ctx, KGQ_EINVAL, "k %d outside [1, min(max_k=%d, shard size=%lld)]", k, ctx->cfg.max_k,
+                (long long)ctx->ns);
+  return KGQ_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+const char* kgq_status_string(kgq_status s) {
+  switch (s) {
+    case KGQ_OK: return "KGQ_OK";
+    case KGQ_EINVAL: return "KGQ_EINVAL";
+    case KGQ_ERANGE: return "KGQ_ERANGE";
+    case KGQ_EUNSUPPORTED: return "KGQ_EUNSUPPORTED";
+    case KGQ_ESTATE: return "KGQ_ESTATE";
+    case KGQ_ENOMEM: return "KGQ_ENOMEM";
+    case KGQ_ECUDA: return "KGQ_ECUDA";
+  }
+  return "KGQ_UNKNOWN";
+}
+
+int32_t kgq_num_anchors(int32_t s) { return plan_of(s) ? plan_of(s)->n_anchor : -1; }
+int32_t kgq_num_relations(int32_t s) { return plan_of(s) ? plan_of(s)->n_rel : -1; }
+int32_t kgq_num_branches(int32_t s) { return plan_of(s) ? plan_of(s)->n_out : -1; }
+int32_t kgq_uses_negation(int32_t s) { return plan_of(s) ? (plan_of(s)->negation ? 1 : 0) : -1; }
+const char* kgq_structure_name(int32_t s) { return plan_of(s) ? kNames[s] : nullptr; }
+int32_t kgq_structure_from_name(const char* n) {
+  if (!n) return -1;
+  for (int i = 0; i < KGQ_NUM_STRUCTURES; ++i)
+    if (strcmp(n, kNames[i]) == 0) return i;
+  return -1;
+}
+int32_t kgq_embedding_width(int32_t model, int32_t dim) {
+  if (model == KGQ_GQE) return dim;
+  if (model == KGQ_Q2B || model == KGQ_BETAE) return 2 * dim;
+  return -1;
+}
+
+kgq_status kgq_shard_range(int64_t n, int32_t w, int32_t r, int64_t* b, int64_t* e) {
+  if (n < 1 || w < 1 || r < 0 || r >= w || !b || !e) return KGQ_EINVAL;
+  const int64_t per = (n + w - 1) / w;
+  *b = std::min<int64_t>(n, (int64_t)r * per);
+  *e = std::min<int64_t>(n, (int64_t)(r + 1) * per);
+  return KGQ_OK;
+}
+int64_t kgq_shard_begin(const kgq_ctx* c) { return c ? c->e0 : -1; }
+int64_t kgq_shard_end(const kgq_ctx* c) { return c ? c->e1 : -1; }
+
+const char* kgq_last_error(const kgq_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+kgq_status kgq_create(const kgq_config* cfg, kgq_ctx** out) {
+  if (!out) return fail(nullptr, KGQ_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, KGQ_EINVAL, "cfg is NULL");
+  if (cfg->abi_version != KGQ_ABI_VERSION)
+    return fail(nullptr, KGQ_EINVAL, "abi_version %u != %u", cfg->abi_version, KGQ_ABI_VERSION);
+  if (cfg->model < KGQ_GQE || cfg->model > KGQ_BETAE) return fail(nullptr, KGQ_EINVAL, "bad model %d", cfg->model);
+  if (cfg->n_entity < 1 || cfg->n_entity > INT32_MAX) return fail(nullptr, KGQ_EINVAL, "n_entity %lld", (long long)cfg->n_entity);
+  if (cfg->n_relation < 1) return fail(nullptr, KGQ_EINVAL, "n_relation %d", cfg->n_relation);
+  if (cfg->dim < 4 || cfg->dim % 4) return fail(nullptr, KGQ_EINVAL, "dim %d must be a positive multiple of 4", cfg->dim);
+  if (cfg->model == KGQ_BETAE && (cfg->hidden < 1 || cfg->n_hidden_layers < 1 || cfg->n_hidden_layers > 8))
+    return fail(nullptr, KGQ_EINVAL, "BetaE needs hidden >= 1 and 1 <= n_hidden_layers <= 8");
+  if (cfg->terminal != KGQ_TERM_REGULARIZER && cfg->terminal != KGQ_TERM_SOFTMAX)
+    return fail(nullptr, KGQ_EINVAL, "bad terminal %d", cfg->terminal);
+  if (cfg->max_batch < 1) return fail(nullptr, KGQ_EINVAL, "max_batch %d", cfg->max_batch);
+  if (cfg->max_k < 1 || cfg->max_k > kMaxK) return fail(nullptr, KGQ_EINVAL, "max_k %d outside [1, %d]", cfg->max_k, kMaxK);
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
+    return fail(nullptr, KGQ_EINVAL, "rank %d / world_size %d", cfg->rank, cfg->world_size);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
+    return fail(nullptr, KGQ_ECUDA, "CUDA device %d not available (%d devices)", cfg->device, ndev);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, cfg->device);
+  if (prop.major != 10)
+    return fail(nullptr, KGQ_EUNSUPPORTED, "libkgq is built for sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
+  kgq_ctx* ctx = new kgq_ctx();
+  ctx->cfg = *cfg;
+  DeviceGuard g(cfg->device);
+  kgq_shard_range(cfg->n_entity, cfg->world_size, cfg->rank, &ctx->e0, &ctx->e1);
+  ctx->ns = ctx->e1 - ctx->e0;
+  ctx->np = std::max<int64_t>(kEntityPad, round_up(ctx->ns, kEntityPad));
+  ctx->ew = cfg->model == KGQ_BETAE ? 2 * cfg->dim : cfg->dim;
+  ctx->qw = kgq_embedding_width(cfg->model, cfg->dim);
+  ctx->ent_loaded.assign((size_t)cfg->n_entity, 0);
+  kgq_status st = dalloc(ctx, &ctx->ent, (size_t)(cfg->n_entity * ctx->ew), "entity table");
+  if (!st) st = dalloc(ctx, &ctx->d_err, 4, "error word");
+  if (!st) st = dalloc(ctx, &ctx->d_invalid, (size_t)cfg->max_batch, "invalid flags");
+  if (st) {
+    g_create_err = ctx->err;
+    kgq_destroy(ctx);
+    return st;
+  }
+  cudaMemset(ctx->d_err, 0, 4 * sizeof(int32_t));
+  cudaMemset(ctx->d_invalid, 0, cfg->max_batch * sizeof(int32_t));
+  *out = ctx;
+  return KGQ_OK;
+}
+
+void kgq_destroy(kgq_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard g(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  auto F = [](void* p) { if (p) cudaFree(p); };
+  F(ctx->ent); F(ctx->rel[0]); F(ctx->rel[1]); F(ctx->score_tab);
+  for (auto& l : ctx->lin) { F(l.W); F(l.W_hi); F(l.W_lo); F(l.b); }
+  for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) { F(s->hi); F(s->lo); }
+  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->d_err); F(ctx->d_invalid);
+  F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
+  for (auto& r : prof_list(ctx)) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  prof_list(ctx).clear();
+  delete ctx;
+}
+
+kgq_status kgq_load_entities(kgq_ctx* ctx, const float* rows, int64_t first, int64_t n) {
+  if (!ctx || !rows) return fail(ctx, KGQ_EINVAL, "NULL argument");
+  if (ctx->finalized) return fail(ctx, KGQ_ESTATE, "tables are frozen after kgq_finalize()");
+  if (first < 0 || n < 0 || first + n > ctx->cfg.n_entity)
+    return fail(ctx, KGQ_EINVAL, "rows [%lld, %lld) outside [0, %lld)", (long long)first,
+                (long long)(first + n), (long long)ctx->cfg.n_entity);
+  DeviceGuard g(ctx->cfg.device);
+  CK(cudaMemcpy(ctx->ent + first * ctx->ew, rows, (size_t)(n * ctx->ew) * sizeof(float),
+                cudaMemcpyHostToDevice), "entity upload");
+  for (int64_t i = first; i < first + n; ++i) {
+    if (!ctx->ent_loaded[(size_t)i]) ctx->ent_rows_loaded++;
+    ctx->ent_loaded[(size_t)i] = 1;
+  }
+  return KGQ_OK;
+}
+
+kgq_status kgq_load_relations(kgq_ctx* ctx, int32_t which, const float* rows, int32_t n) {
+  if (!ctx || !rows) return fail(ctx, KGQ_EINVAL, "NULL argument");
+  if (ctx->finalized) return fail(ctx, KGQ_ESTATE, "tables are frozen after kgq_finalize()");
+  if (which != KGQ_REL_MAIN && which != KGQ_REL_OFFSET) return fail(ctx, KGQ_EINVAL, "bad relation table %d", which);
+  if (which == KGQ_REL_OFFSET && ctx->cfg.model != KGQ_Q2B)
+    return fail(ctx, KGQ_EINVAL, "relation offsets exist only for Q2B");
+  if (n != ctx->cfg.n_relation) return fail(ctx, KGQ_EINVAL, "n %d != n_relation %d", n, ctx->cfg.n_relation);
+  DeviceGuard g(ctx->cfg.device);
+  const size_t bytes = (size_t)n * ctx->cfg.dim * sizeof(float);
+  if (!ctx->rel[which]) {
+    kgq_status st = dalloc(ctx, &ctx->rel[which], bytes / sizeof(float), "relation table");
+    if (st) return st;
+  }
+  CK(cudaMemcpy(ctx->rel[which], rows, bytes, cudaMemcpyHostToDevice), "relation upload");
+  return KGQ_OK;
+}
+
+kgq_status kgq_load_linear(kgq_ctx* ctx, int32_t id, const float* W, const float* b, int32_t out_f,
+                           int32_t in_f) {
+  if (!ctx || !W || !b) return fail(ctx, KGQ_EINVAL, "NULL argument");
+  if (ctx->finalized) return fail(ctx, KGQ_ESTATE, "tables are frozen after kgq_finalize()");
+  const int d = ctx->cfg.dim, H = ctx->cfg.hidden, m = ctx->cfg.model;
+  int eo = -1, ei = -1;
+  if (m == KGQ_BETAE && id == KGQ_LAYER_PROJ_OUT) { eo = 2 * d; ei = H; }
+  else if (m == KGQ_BETAE && id >= KGQ_LAYER_PROJ_HIDDEN && id < KGQ_LAYER_PROJ_HIDDEN + ctx->cfg.n_hidden_layers) {
+    eo = H; ei = id == KGQ_LAYER_PROJ_HIDDEN ? 3 * d : H;
+  } else if (id == KGQ_LAYER_INTER_1) { eo = ei = (m == KGQ_BETAE ? 2 * d : d); }
+  else if (id == KGQ_LAYER_INTER_2) { eo = d; ei = (m == KGQ_BETAE ? 2 * d : d); }
+  else if (m == KGQ_Q2B && (id == KGQ_LAYER_OFFSET_1 || id == KGQ_LAYER_OFFSET_2)) { eo = ei = d; }
+  if (eo < 0) return fail(ctx, KGQ_EINVAL, "layer id %d does not exist for this model", id);
+  if (out_f != eo || in_f != ei)
+    return fail(ctx, KGQ_EINVAL, "layer %d: shape [%d, %d], expected [%d, %d]", id, out_f, in_f, eo, ei);
+  DeviceGuard g(ctx->cfg.device);
+  Linear& L = ctx->lin[id];
+  const size_t n = (size_t)out_f * in_f;
+  kgq_status st = KGQ_OK;
+  if (!L.W) {
+    if (!st) st = dalloc(ctx, &L.W, n, "linear W");
+    if (!st) st = dalloc(ctx, &L.W_hi, n, "linear W_hi");
+    if (!st) st = dalloc(ctx, &L.W_lo, n, "linear W_lo");
+    if (!st) st = dalloc(ctx, &L.b, (size_t)out_f, "linear b");
+    if (st) return st;
+  }
+  L.out_f = out_f;
+  L.in_f = in_f;
+  CK(cudaMemcpy(L.W, W, n * sizeof(float), cudaMemcpyHostToDevice), "linear W upload");
+  CK(cudaMemcpy(L.b, b, (size_t)out_f * sizeof(float), cudaMemcpyHostToDevice), "linear b upload");
+  launch_split_copy(L.W, (int64_t)n, L.W_hi, L.W_lo, 0);
+  CK(cudaDeviceSynchronize(), "linear split");
+  return KGQ_OK;
+}
+
+kgq_status kgq_finalize(kgq_ctx* ctx) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (ctx->finalized) return fail(ctx, KGQ_ESTATE, "already finalized");
+  const kgq_config& c = ctx->cfg;
+  const int d = c.dim;
+  if (ctx->ent_rows_loaded != c.n_entity)
+    return fail(ctx, KGQ_ESTATE, "entity table incomplete: %lld of %lld rows loaded",
+                (long long)ctx->ent_rows_loaded, (long long)c.n_entity);
+  if (!ctx->rel[0]) return fail(ctx, KGQ_ESTATE, "relation table not loaded");
+  if (c.model == KGQ_Q2B && !ctx->rel[1]) return fail(ctx, KGQ_ESTATE, "Q2B relation offsets not loaded");
+  std::vector<int> need = {KGQ_LAYER_INTER_1, KGQ_LAYER_INTER_2};
+  if (c.model == KGQ_Q2B) { need.push_back(KGQ_LAYER_OFFSET_1); need.push_back(KGQ_LAYER_OFFSET_2); }
+  if (c.model == KGQ_BETAE) {
+    need.push_back(KGQ_LAYER_PROJ_OUT);
+    for (int l = 0; l < c.n_hidden_layers; ++l) need.push_back(KGQ_LAYER_PROJ_HIDDEN + l);
+  }
+  for (int id : need)
+    if (!ctx->lin[id].W) return fail(ctx, KGQ_ESTATE, "linear layer %d not loaded", id);
+  DeviceGuard g(c.device);
+  const int64_t Bm = c.max_batch;
+  ctx->rows_max = (int64_t)kMaxBranches * Bm;
+  ctx->tw = 2 * d;
+  ctx->rpad = round_up(2 * Bm, kRowPad);
+  const int nplanes = c.model == KGQ_GQE ? 1 : (c.model == KGQ_Q2B ? 2 : 3);
+  const int64_t budget = (int64_t)4 << 30;  // bytes for the distance scratch
+  ctx->bchunk = std::max<int64_t>(1, std::min<int64_t>(Bm, budget / (ctx->np * 4)));
+  kgq_status st = KGQ_OK;
+  const int iw = c.model == KGQ_BETAE ? 2 * d : d;
+  if (!st) st = alloc_split(ctx, &ctx->S, ctx->rows_max, ctx->qw, "state S");
+  if (!st) st = alloc_split(ctx, &ctx->I, ctx->rows_max, iw, "intersection hidden");
+  if (!st) st = alloc_split(ctx, &ctx->M, Bm, ctx->qw, "combined state");
+  if (!st && c.model == KGQ_BETAE) {
+    st = alloc_split(ctx, &ctx->Z, ctx->rows_max, 3 * d, "MLP input");
+    if (!st) st = alloc_split(ctx, &ctx->H[0], ctx->rows_max, c.hidden, "MLP hidden 0");
+    if (!st) st = alloc_split(ctx, &ctx->H[1], ctx->rows_max, c.hidden, "MLP hidden 1");
+  }
+  if (!st) st = dalloc(ctx, &ctx->T, (size_t)(ctx->rows_max * ctx->tw), "T");
+  if (!st) st = dalloc(ctx, &ctx->T2, (size_t)(ctx->rows_max * ctx->tw), "T2");
+  if (!st) st = dalloc(ctx, &ctx->Q, (size_t)(Bm * 2 * ctx->qw), "Q");
+  if (!st) st = dalloc(ctx, &ctx->Qt, (size_t)(nplanes * d * ctx->rpad), "Qt");
+  if (!st) st = dalloc(ctx, &ctx->dist, (size_t)(ctx->bchunk * ctx->np), "dist");
+  if (!st) st = dalloc(ctx, &ctx->score_tab, (size_t)((c.model == KGQ_BETAE ? 3 : 1) * d * ctx->np), "score table");
+  if (!st) st = dalloc(ctx, &ctx->d_anchor_stage, (size_t)(Bm * kMaxBranches), "staging");
+  if (!st) st = dalloc(ctx, &ctx->d_rel_stage, (size_t)(Bm * kMaxBranches), "staging");
+  if (!st) st = dalloc(ctx, &ctx->d_topd_stage, (size_t)(Bm * c.max_k), "staging");
+  if (!st) st = dalloc(ctx, &ctx->d_topi_stage, (size_t)(Bm * c.max_k), "staging");
+  if (st) return st;
+  if (c.model == KGQ_BETAE) {
+    launch_beta_regularize(ctx->ent, c.n_entity * ctx->ew, 0);
+    launch_betae_entity_terms(ctx->ent, ctx->e0, ctx->ns, d, ctx->score_tab, ctx->np, 0);
+  } else {
+    launch_transpose_shard(ctx->ent, ctx->e0, ctx->ns, d, ctx->ew, ctx->score_tab, ctx->np, 0);
+  }
+  CK(cudaGetLastError(), "finalize launch");
+  CK(cudaDeviceSynchronize(), "finalize");
+  ctx->finalized = true;
+  return KGQ_OK;
+}
+
+static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t* anchors,
+                              const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
+                              float* shard_dist, cudaStream_t st) {
+  const Plan* P = plan_of(s);
+  const kgq_config& c = ctx->cfg;
+  int L = 0;
+  CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)B * sizeof(int32_t), st), "reset flags");
+  {
+    StageTimer t(ctx, st, kStChain);
+    L += run_chain(ctx, s, B, anchors, rels, st);
+  }
+  for (int64_t b0 = 0; b0 < B; b0 += ctx->bchunk) {
+    const int nb = (int)std::min<int64_t>(ctx->bchunk, B - b0);
+    {
+      StageTimer t(ctx, st, kStPrep);
+      L += launch_score_prep(c.model, ctx->Q + b0 * P->n_out * ctx->qw, nb, P->n_out, c.dim, ctx->Qt,
+                             ctx->rpad, st);
+    }
+    {
+      StageTimer t(ctx, st, kStScore);
+      L += launch_score(c.model, P->n_out, nb, c.dim, c.cen, ctx->Qt, ctx->rpad, ctx->score_tab, ctx->np,
+                        ctx->ns, ctx->dist, ctx->np, st);
+    }
+    {
+      StageTimer t(ctx, st, kStTopk);
+      L += launch_topk(ctx->dist, ctx->np, nb, ctx->ns, k, ctx->e0, ctx->d_invalid + b0,
+                       topk_dist + b0 * k, topk_id + b0 * k, st);
+    }
+    if (shard_dist)
+      CK(cudaMemcpy2DAsync(shard_dist + b0 * ctx->ns, ctx->ns * sizeof(float), ctx->dist,
+                           ctx->np * sizeof(float), ctx->ns * sizeof(float), nb, cudaMemcpyDeviceToDevice, st),
+         "shard_dist copy");
+  }
+  ctx->launches = L;
+  CK(cudaGetLastError(), "submit launch");
+  return KGQ_OK;
+}
+
+kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors, const int32_t* rels,
+                      int32_t k, float* topk_dist, int32_t* topk_id, float* shard_dist, kgq_stream stream) {
+  kgq_status st = check_submit(ctx, s, batch, k, true);
+  if (st) return st;
+  if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
+  if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  DeviceGuard g(ctx->cfg.device);
+  return submit_impl(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, shard_dist, (cudaStream_t)stream);
+}
+
+kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                           const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
+                           kgq_stream stream) {
+  kgq_status st = check_submit(ctx, s, batch, k, true);
+  if (st) return st;
+  if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
+  if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL host pointer");
+  DeviceGuard g(ctx->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const Plan* P = plan_of(s);
+  CK(cudaMemcpyAsync(ctx->d_anchor_stage, anchors, (size_t)batch * P->n_anchor * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, cs), "anchor upload");
+  CK(cudaMemcpyAsync(ctx->d_rel_stage, rels, (size_t)batch * P->n_rel * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, cs), "relation upload");
+  st = submit_impl(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage,
+                   ctx->d_topi_stage, nullptr, cs);
+  if (st) return st;
+  CK(cudaMemcpyAsync(topk_dist, ctx->d_topd_stage, (size_t)batch * k * sizeof(float), cudaMemcpyDeviceToHost, cs),
+     "top-k download");
+  CK(cudaMemcpyAsync(topk_id, ctx->d_topi_stage, (size_t)batch * k * sizeof(int32_t), cudaMemcpyDeviceToHost, cs),
+     "top-k download");
+  CK(cudaStreamSynchronize(cs), "submit_host sync");
+  return KGQ_OK;
+}
+
+kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                               const int32_t* rels, float* out, kgq_stream stream) {
+  kgq_status st = check_submit(ctx, s, batch, 0, false);
+  if (st) return st;
+  if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
+  if (!anchors || !rels || !out) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  DeviceGuard g(ctx->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)batch * sizeof(int32_t), cs), "reset flags");
+  ctx->launches = run_chain(ctx, s, batch, anchors, rels, cs);
+  const Plan* P = plan_of(s);
+  CK(cudaMemcpyAsync(out, ctx->Q, (size_t)batch * P->n_out * ctx->qw * sizeof(float),
+                     cudaMemcpyDeviceToDevice, cs), "embedding copy");
+  CK(cudaGetLastError(), "query_embedding launch");
+  return KGQ_OK;
+}
+
+kgq_status kgq_merge_topk(kgq_ctx* ctx, int32_t parts, int32_t batch, int32_t k, const float* in_d,
+                          const int32_t* in_i, float* out_d, int32_t* out_i, kgq_stream stream) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (parts < 1 || batch < 0 || k < 1 || k > ctx->cfg.max_k || (int64_t)parts * k > 4096)
+    return fail(ctx, KGQ_EINVAL, "merge: parts %d, batch %d, k %d (need parts*k <= 4096, k <= max_k)", parts,
+                batch, k);
+  if (batch == 0) return KGQ_OK;
+  if (!in_d || !in_i || !out_d || !out_i) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  DeviceGuard g(ctx->cfg.device);
+  launch_merge(parts, batch, k, in_d, in_i, out_d, out_i, (cudaStream_t)stream);
+  ctx->launches = 1;
+  CK(cudaGetLastError(), "merge launch");
+  return KGQ_OK;
+}
+
+kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  DeviceGuard g(ctx->cfg.device);
+  CK(cudaStreamSynchronize((cudaStream_t)stream), "stream synchronize");
+  int32_t e[4];
+  CK(cudaMemcpy(e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost), "error word");
+  if (e[0]) {
+    CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
+    return fail(ctx, KGQ_ERANGE, "query row %d: %s slot %d out of range", e[1], e[3] ? "relation" : "anchor",
+                e[2]);
+  }
+  return KGQ_OK;
+}
+
+int32_t kgq_last_launch_count(const kgq_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+kgq_status kgq_entity_terms(kgq_ctx* ctx, float* out, kgq_stream stream) {
+  if (!ctx || !out) return fail(ctx, KGQ_EINVAL, "NULL argument");
+  if (!ctx->finalized) return fail(ctx, KGQ_ESTATE, "not finalized");
+  if (ctx->cfg.model != KGQ_BETAE) return fail(ctx, KGQ_EUNSUPPORTED, "entity terms exist only for BetaE");
+  DeviceGuard g(ctx->cfg.device);
+  const int d = ctx->cfg.dim;
+  // tab [d][3][np] -> out [3][d][ns]
+  for (int p = 0; p < 3; ++p)
+    CK(cudaMemcpy2DAsync(out + (int64_t)p * d * ctx->ns, ctx->ns * sizeof(float), ctx->score_tab + p * ctx->np,
+                         3 * ctx->np * sizeof(float), ctx->ns * sizeof(float), d, cudaMemcpyDeviceToDevice,
+                         (cudaStream_t)stream),
+       "entity terms copy");
+  return KGQ_OK;
+}
+
+kgq_status kgq_profile_enable(kgq_ctx* ctx, int32_t on) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  ctx->profile = on != 0;
+  return KGQ_OK;
+}
+
+kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n) {
+  if (!ctx || !ms || !n) return fail(ctx, KGQ_EINVAL, "NULL argument");
+  DeviceGuard g(ctx->cfg.device);
+  auto& lst = prof_list(ctx);
+  for (int i = 0; i < kStNum; ++i) { ms[i] = 0; n[i] = 0; }
+  for (auto& r : lst) {
+    CK(cudaEventSynchronize(r.b), "profile event");
+    float t = 0;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms[r.stage] += t;
+    n[r.stage] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  lst.clear();
+  for (int i = 0; i < kStNum; ++i) ctx->prof_n[i] = 0;
+  return KGQ_OK;
+}
+
+}  // extern "C"

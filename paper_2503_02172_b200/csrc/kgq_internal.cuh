@@ -1,0 +1,189 @@
+// Internal declarations of libkgq.so (not part of the ABI; see include/kgq.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/kgq.h"
+
+namespace kgq {
+
+constexpr int kMaxBranches = 3;   // 3i / 3in
+constexpr int kMaxOps = 4;        // ops per branch chain
+constexpr int kMaxLayers = 32;
+constexpr int kMaxK = 256;
+constexpr int kEntityPad = 128;   // scorer entity tile; shard tables are padded to it
+constexpr int kRowPad = 64;       // scorer query-row tile
+
+// ---------------------------------------------------------------------------------------
+// Static per-structure plan (SURVEY §8(b) slot table; Eq. 1 DNF; Eq. 2 mapping).
+//   A branch is an anchor slot followed by ops: >= 0 projection with that relation slot,
+//   kOpNeg = negation.  kind: single chain, intersection of branches (+ post projections),
+//   or union of branches (one query embedding per DNF clause).
+// ---------------------------------------------------------------------------------------
+constexpr int kOpNeg = -1;
+enum PlanKind { kSingle = 0, kInter = 1, kUnion = 2 };
+struct BranchPlan {
+  int anchor;
+  int nops;
+  int ops[kMaxOps];
+};
+struct Plan {
+  int kind;
+  int nbranch;
+  BranchPlan br[kMaxBranches];
+  int npost;        // projections applied after the intersection (ip, inp)
+  int post[2];
+  int n_anchor, n_rel, n_out;  // slot counts; n_out = DNF branches of the final embedding
+  bool negation;
+};
+const Plan* plan_of(int s);
+
+// fp32 tensor split into (hi = rna_tf32(x), lo = x - hi) with hi + lo == x exactly.
+// Every activation that feeds a dense layer is kept in this form (3xTF32 operands).
+struct Split {
+  float* hi;
+  float* lo;
+  int64_t ld;  // row stride in elements
+};
+
+struct Linear {
+  float* W = nullptr;     // [out, in] fp32
+  float* W_hi = nullptr;  // split copies for the tensor-core path
+  float* W_lo = nullptr;
+  float* b = nullptr;     // [out]
+  int out_f = 0, in_f = 0;
+};
+
+enum Epi { kEpiNone = 0, kEpiRelu = 1, kEpiBetaReg = 2 };
+
+// Profiling stages (kgq_profile_* in kgq_api.cu).
+enum Stage { kStChain = 0, kStPrep = 1, kStScore = 2, kStTopk = 3, kStNum = 4 };
+
+}  // namespace kgq
+
+struct kgq_ctx {
+  kgq_config cfg{};
+  std::string err;
+  int64_t e0 = 0, e1 = 0, ns = 0, np = 0;  // shard [e0, e1), size, padded size
+  int ew = 0;                              // entity / state row width (d or 2d)
+  int qw = 0;                              // query-embedding row width
+  float* ent = nullptr;                    // [N, ew] row-major (BetaE: regularised at finalize)
+  std::vector<uint8_t> ent_loaded;         // per-row loaded flags (host)
+  int64_t ent_rows_loaded = 0;
+  float* rel[2] = {nullptr, nullptr};
+  kgq::Linear lin[kgq::kMaxLayers];
+  float* score_tab = nullptr;              // GQE/Q2B: [d][np]; BetaE: [d][3][np] (C,U,V)
+  bool finalized = false;
+
+  // scratch (sized at finalize for max_batch)
+  int64_t rows_max = 0;                    // kMaxBranches * max_batch
+  kgq::Split S{}, Z{}, H[2]{}, I{}, M{};   // states, MLP input, hidden ping-pong, inter hidden, q2b mean
+  float* T = nullptr;                      // generic fp32 GEMM output [rows_max, tw]
+  int64_t tw = 0;
+  float* T2 = nullptr;
+  float* Q = nullptr;                      // final query embedding [B, 2, qw]
+  float* Qt = nullptr;                     // scorer query operand planes [nplanes][d][rpad]
+  int64_t rpad = 0;
+  float* dist = nullptr;                   // [bchunk, np]
+  int64_t bchunk = 0;
+  int32_t* d_err = nullptr;                // [4]: flag, row, slot, kind
+  int32_t* d_invalid = nullptr;            // [max_batch]
+  int32_t* d_anchor_stage = nullptr;       // kgq_submit_host staging
+  int32_t* d_rel_stage = nullptr;
+  float* d_topd_stage = nullptr;
+  int32_t* d_topi_stage = nullptr;
+
+  int launches = 0;
+  bool profile = false;
+  cudaEvent_t ev[2 * kgq::kStNum] = {};
+  double prof_ms[kgq::kStNum] = {};
+  int64_t prof_n[kgq::kStNum] = {};
+};
+
+namespace kgq {
+// ---- kernel launchers (each returns the number of kernels launched) ---------------------
+struct ChainArgs {
+  int model;          // kgq_model
+  int d;
+  int nb;             // branches in this launch
+  BranchPlan br[kMaxBranches];
+  const int32_t* anchors;
+  int n_a;
+  const int32_t* rels;
+  int n_r;
+  int64_t n_entity;
+  int n_relation;
+  int32_t* err;
+  int32_t* invalid;
+};
+// GQE/Q2B: anchor gather + translation chain for every branch (horizontal + vertical fusion).
+// Output: if out_split.hi: split state rows [br*B + b]; else fp32 q[b, br, :] (width ew).
+int launch_translate_chain(const ChainArgs& a, const float* ent, const float* rel,
+                           const float* rel_off, int B, Split out_split, float* out_q,
+                           cudaStream_t st);
+// BetaE: build MLP input rows z = [x; R[r]] for a group of branches at one hop.
+//   Group member gi -> Z rows [gi*B, gi*B+B); source = regularised anchor row (anchor_slot
+//   >= 0) or split state rows [src_row, src_row+B).
+struct MlpGroup {
+  int n;
+  int rel_slot[kMaxBranches];
+  int anchor_slot[kMaxBranches];
+  int64_t src_row[kMaxBranches];
+};
+int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
+                           const MlpGroup& g, Split src, Split z, cudaStream_t st);
+// Dense layer: out = epi(A W^T + b) for rows [0, M), A given as split (K columns).
+//   split output if out.lo != nullptr, else plain fp32 into out.hi.
+//   kEpiBetaReg: clamp(y+1, .05, 1e9), then 1/x on rows [neg0, neg1).
+int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split out,
+                  int neg0, int neg1, cudaStream_t st);
+// BetaE Eq.-4 softmax terminal over rows of T (width w) -> split state rows out_row0 + r,
+// with negation on rows r in [neg0, neg1).
+int launch_softmax_terminal(const float* T, int64_t ldt, int M, int w, Split out,
+                            int64_t out_row0, int neg0, int neg1, cudaStream_t st);
+// Negation x -> 1/x on split rows [r0, r1) (width w), in place.
+int launch_negate(Split x, int64_t r0, int64_t r1, int w, cudaStream_t st);
+// Q2B: mean over nb branches of T[br*B+b, :d] -> split [b, :d].
+int launch_branch_mean(const float* T, int64_t ldt, int nb, int B, int d, Split out,
+                       cudaStream_t st);
+// Attention combine (softmax over branches per dim, weighted sum).  Q2B also applies the
+// offset gate o = min_i o_i * sigmoid(G).  Optional post projection (GQE/Q2B only).
+// Output split state (rows b) or fp32 q[b, 0, :].
+struct CombineArgs {
+  int model, nb, B, d;
+  int64_t ldl, ldg;
+  const float* rel;
+  const float* rel_off;
+  const int32_t* rels;
+  int n_r, n_relation;
+  int post_slot;  // -1: none
+  int32_t* err;
+  int32_t* invalid;
+};
+int launch_attention_combine(const CombineArgs& c, Split S, const float* logits,
+                             const float* gate, Split out_split, float* out_q, cudaStream_t st);
+// Copy split state rows (b, branch br) to fp32 q[b, br, :].
+int launch_state_to_q(Split S, int nb, int B, int w, float* q, cudaStream_t st);
+// Scorer operands: query planes (k-major) from q[B, nbq, qw].
+int launch_score_prep(int model, const float* q, int B, int nbq, int d, float* Qt,
+                      int64_t rpad, cudaStream_t st);
+// Scorer: dist[b, e] = min over DNF branches of distance(q_b,br, entity e0+e).
+int launch_score(int model, int nbq, int B, int d, float cen, const float* Qt, int64_t rpad,
+                 const float* tab, int64_t np, int64_t ns, float* dist, int64_t ldd,
+                 cudaStream_t st);
+// Top-k per row of dist (row length n, global id = id_base + index).
+int launch_topk(const float* dist, int64_t ldd, int B, int64_t n, int k, int64_t id_base,
+                const int32_t* invalid, float* out_d, int32_t* out_i, cudaStream_t st);
+int launch_merge(int parts, int B, int k, const float* in_d, const int32_t* in_i, float* out_d,
+                 int32_t* out_i, cudaStream_t st);
+// Table preparation (finalize).
+int launch_beta_regularize(float* ent, int64_t n_elems, cudaStream_t st);
+int launch_transpose_shard(const float* ent, int64_t e0, int64_t ns, int d, int ew, float* tab,
+                           int64_t np, cudaStream_t st);
+int launch_betae_entity_terms(const float* ent, int64_t e0, int64_t ns, int d, float* tab,
+                              int64_t np, cudaStream_t st);
+int launch_split_copy(const float* src, int64_t n, float* hi, float* lo, cudaStream_t st);
+}  // namespace kgq

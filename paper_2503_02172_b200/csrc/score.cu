@@ -1,0 +1,190 @@
+// Entity scorer (SURVEY §8(a) a6 + a7): distance of every query embedding to every entity of
+// this rank's shard, min over DNF branches (union, Eq. 1), written as dist[b, e].
+//
+//   GQE   sum_d |e - q|                                   2 FP32 ops per (q, e, d)
+//   Q2B   sum_d |e-c| - (1-cen) sum_d min(|e-c|, o)         4 ops  (== sum ReLU(|e-c|-o) +
+//                                                                   cen * sum min(|e-c|, o))
+//   BetaE sum_d |L_q + C_e + a_q U_e + b_q V_e|             4 ops  (== sum_d |KL(e || q)|)
+//
+// Register-tiled SIMT "GEMM-like" kernel: the inner op is not a dot product, so tensor cores do
+// not apply.  CTA tile 64 query rows x 128 entities, 256 threads, 4x8
+// per thread; k-major operand planes staged through shared memory by cp.async, two stages.
+// Query rows are (b, branch) pairs; for 2u/up (NB = 2) a thread owns both branches of its
+// queries and takes the min in registers (a6 fused into a7).
+#include "common.cuh"
+#include "kgq_internal.cuh"
+
+namespace kgq {
+
+namespace {
+constexpr int TQ = 64, TE = 128, DK = 16;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int MODEL>
+struct Planes {
+  static constexpr int NQ = MODEL == KGQ_GQE ? 1 : (MODEL == KGQ_Q2B ? 2 : 3);
+  static constexpr int NE = MODEL == KGQ_BETAE ? 3 : 1;
+};
+
+template <int MODEL, int NB>
+__global__ void __launch_bounds__(256, 2)
+    k_score(const float* __restrict__ Qt, int64_t rpad, const float* __restrict__ tab, int64_t np,
+            int d, float cen, float* __restrict__ dist, int64_t ldd, int B) {
+  constexpr int NQ = Planes<MODEL>::NQ, NE = Planes<MODEL>::NE;
+  extern __shared__ __align__(16) float smem[];
+  float* Qs = smem;                          // [2][NQ][DK][TQ]
+  float* Es = smem + 2 * NQ * DK * TQ;       // [2][NE][DK][TE]
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int64_t e0 = (int64_t)blockIdx.x * TE;
+  const int64_t r0 = (int64_t)blockIdx.y * TQ;
+  const int64_t qplane = (int64_t)d * rpad;
+  // E tab plane p of dim j: GQE/Q2B tab + j*np; BetaE tab + (j*3+p)*np
+  auto eptr = [&](int p, int j) -> const float* {
+    return NE == 1 ? tab + (int64_t)j * np : tab + ((int64_t)j * 3 + p) * np;
+  };
+  auto load_stage = [&](int buf, int j0) {
+    // Q: NQ planes x DK x TQ floats = NQ * 256 float4, one per thread per plane
+#pragma unroll
+    for (int p = 0; p < NQ; ++p) {
+      const int k = tid >> 4, c = (tid & 15) * 4;
+      const int j = j0 + k;
+      const float* g = Qt + p * qplane + (int64_t)(j < d ? j : 0) * rpad + r0 + c;
+      cp_async16(Qs + ((buf * NQ + p) * DK + k) * TQ + c, g, j < d);
+    }
+    // E: NE planes x DK x TE floats = NE * 512 float4, two per thread per plane
+#pragma unroll
+    for (int p = 0; p < NE; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int idx = tid + h * 256;
+        const int k = idx >> 5, c = (idx & 31) * 4;
+        const int j = j0 + k;
+        const float* g = eptr(p, j < d ? j : 0) + e0 + c;
+        cp_async16(Es + ((buf * NE + p) * DK + k) * TE + c, g, j < d);
+      }
+  };
+
+  float acc[4][8], acc2[4][8];  // acc2: Q2B inside sums (dead code otherwise)
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = acc2[i][j] = 0.0f;
+
+  const int nst = (d + DK - 1) / DK;
+  load_stage(0, 0);
+  cp_async_commit();
+  for (int s = 0; s < nst; ++s) {
+    const int buf = s & 1;
+    if (s + 1 < nst) {
+      load_stage(buf ^ 1, (s + 1) * DK);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < DK; ++k) {
+      float q[NQ][4], e[NE][8];
+#pragma unroll
+      for (int p = 0; p < NQ; ++p) {
+        const float4 v = *reinterpret_cast<const float4*>(Qs + ((buf * NQ + p) * DK + k) * TQ + ty * 4);
+        q[p][0] = v.x; q[p][1] = v.y; q[p][2] = v.z; q[p][3] = v.w;
+      }
+#pragma unroll
+      for (int p = 0; p < NE; ++p) {
+        const float* row = Es + ((buf * NE + p) * DK + k) * TE;
+        const float4 v0 = *reinterpret_cast<const float4*>(row + tx * 4);
+        const float4 v1 = *reinterpret_cast<const float4*>(row + 64 + tx * 4);
+        e[p][0] = v0.x; e[p][1] = v0.y; e[p][2] = v0.z; e[p][3] = v0.w;
+        e[p][4] = v1.x; e[p][5] = v1.y; e[p][6] = v1.z; e[p][7] = v1.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (MODEL == KGQ_GQE) {
+            acc[i][j] += fabsf(e[0][j] - q[0][i]);
+          } else if (MODEL == KGQ_Q2B) {
+            const float t = fabsf(e[0][j] - q[0][i]);
+            acc[i][j] += t;
+            acc2[i][j] += fminf(t, q[1][i]);
+          } else {
+            float t = e[0][j] + q[0][i];
+            t = fmaf(q[1][i], e[1][j], t);
+            t = fmaf(q[2][i], e[2][j], t);
+            acc[i][j] += fabsf(t);
+          }
+        }
+    }
+    __syncthreads();
+  }
+
+  float res[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      res[i][j] = MODEL == KGQ_Q2B ? fmaf(-(1.0f - cen), acc2[i][j], acc[i][j]) : acc[i][j];
+
+  constexpr int QPT = 4 / NB;  // queries per thread
+#pragma unroll
+  for (int u = 0; u < QPT; ++u) {
+    const int64_t b = (r0 + ty * 4) / NB + u;
+    if (b >= B) continue;
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      o[j] = res[u * NB][j];
+      if (NB == 2) o[j] = fminf(o[j], res[u * NB + 1][j]);
+    }
+    float* drow = dist + b * ldd + e0;
+    *reinterpret_cast<float4*>(drow + tx * 4) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(drow + 64 + tx * 4) = make_float4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+template <int MODEL, int NB>
+void launch_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d, float cen,
+              float* dist, int64_t ldd, int B, cudaStream_t st) {
+  constexpr int NQ = Planes<MODEL>::NQ, NE = Planes<MODEL>::NE;
+  const size_t smem = (size_t)2 * (NQ * DK * TQ + NE * DK * TE) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_score<MODEL, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int rows = B * NB;
+  dim3 grid((unsigned)(np / TE), (unsigned)((rows + TQ - 1) / TQ));
+  k_score<MODEL, NB><<<grid, 256, smem, st>>>(Qt, rpad, tab, np, d, cen, dist, ldd, B);
+}
+}  // namespace
+
+int launch_score(int model, int nbq, int B, int d, float cen, const float* Qt, int64_t rpad,
+                 const float* tab, int64_t np, int64_t ns, float* dist, int64_t ldd,
+                 cudaStream_t st) {
+  (void)ns;
+  if (model == KGQ_GQE) {
+    if (nbq == 2) launch_t<KGQ_GQE, 2>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+    else launch_t<KGQ_GQE, 1>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+  } else if (model == KGQ_Q2B) {
+    if (nbq == 2) launch_t<KGQ_Q2B, 2>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+    else launch_t<KGQ_Q2B, 1>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+  } else {
+    if (nbq == 2) launch_t<KGQ_BETAE, 2>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+    else launch_t<KGQ_BETAE, 1>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+  }
+  return 1;
+}
+
+}  // namespace kgq

@@ -1,0 +1,283 @@
+"""Thin Python binding of libkgq.so (include/kgq.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels behind the
+C ABI.  PyTorch is used for device memory and stream handles.  There is no CPU fallback:
+if libkgq.so is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkgq.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                      " (or `make -C paper_2503_02172_b200/csrc`)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+ABI_VERSION = 1
+MODELS = {"gqe": 0, "q2b": 1, "betae": 2}
+STRUCTURES = ("1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up",
+              "2in", "3in", "inp", "pin", "pni")
+STATUS = {0: "KGQ_OK", 1: "KGQ_EINVAL", 2: "KGQ_ERANGE", 3: "KGQ_EUNSUPPORTED",
+          4: "KGQ_ESTATE", 5: "KGQ_ENOMEM", 6: "KGQ_ECUDA"}
+LAYER_PROJ_OUT, LAYER_PROJ_HIDDEN = 0, 1
+LAYER_INTER_1, LAYER_INTER_2, LAYER_OFFSET_1, LAYER_OFFSET_2 = 16, 17, 18, 19
+REL_MAIN, REL_OFFSET = 0, 1
+STAGES = ("chain", "prep", "score", "topk")
+
+# Every symbol include/kgq.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "kgq_create", "kgq_destroy", "kgq_last_error", "kgq_status_string", "kgq_num_anchors",
+    "kgq_num_relations", "kgq_num_branches", "kgq_uses_negation", "kgq_structure_name",
+    "kgq_structure_from_name", "kgq_embedding_width", "kgq_shard_range", "kgq_shard_begin",
+    "kgq_shard_end", "kgq_load_entities", "kgq_load_relations", "kgq_load_linear",
+    "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_query_embedding", "kgq_merge_topk",
+    "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
+    "kgq_profile_read",
+)
+
+
+class KgqConfig(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_uint32), ("model", ctypes.c_int32),
+                ("n_entity", ctypes.c_int64), ("n_relation", ctypes.c_int32),
+                ("dim", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("n_hidden_layers", ctypes.c_int32), ("cen", ctypes.c_float),
+                ("terminal", ctypes.c_int32), ("max_batch", ctypes.c_int32),
+                ("max_k", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+_P = ctypes.c_void_p
+_I32, _I64 = ctypes.c_int32, ctypes.c_int64
+_sig = {
+    "kgq_create": (_I32, [ctypes.POINTER(KgqConfig), ctypes.POINTER(_P)]),
+    "kgq_destroy": (None, [_P]),
+    "kgq_last_error": (ctypes.c_char_p, [_P]),
+    "kgq_status_string": (ctypes.c_char_p, [_I32]),
+    "kgq_num_anchors": (_I32, [_I32]),
+    "kgq_num_relations": (_I32, [_I32]),
+    "kgq_num_branches": (_I32, [_I32]),
+    "kgq_uses_negation": (_I32, [_I32]),
+    "kgq_structure_name": (ctypes.c_char_p, [_I32]),
+    "kgq_structure_from_name": (_I32, [ctypes.c_char_p]),
+    "kgq_embedding_width": (_I32, [_I32, _I32]),
+    "kgq_shard_range": (_I32, [_I64, _I32, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "kgq_shard_begin": (_I64, [_P]),
+    "kgq_shard_end": (_I64, [_P]),
+    "kgq_load_entities": (_I32, [_P, _P, _I64, _I64]),
+    "kgq_load_relations": (_I32, [_P, _I32, _P, _I32]),
+    "kgq_load_linear": (_I32, [_P, _I32, _P, _P, _I32, _I32]),
+    "kgq_finalize": (_I32, [_P]),
+    "kgq_submit": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P]),
+    "kgq_submit_host": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
+    "kgq_query_embedding": (_I32, [_P, _I32, _I32, _P, _P, _P, _P]),
+    "kgq_merge_topk": (_I32, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
+    "kgq_check_errors": (_I32, [_P, _P]),
+    "kgq_last_launch_count": (_I32, [_P]),
+    "kgq_entity_terms": (_I32, [_P, _P, _P]),
+    "kgq_profile_enable": (_I32, [_P, _I32]),
+    "kgq_profile_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class KgqError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = STATUS.get(status, status)
+
+
+def structure_id(s) -> int:
+    if isinstance(s, (int, np.integer)):
+        return int(s)
+    v = _lib.kgq_structure_from_name(str(s).encode())
+    if v < 0:
+        raise KgqError(1, f"unknown structure {s!r}; valid: {', '.join(STRUCTURES)}")
+    return v
+
+
+def num_anchors(s): return _lib.kgq_num_anchors(structure_id(s))
+def num_relations(s): return _lib.kgq_num_relations(structure_id(s))
+def num_branches(s): return _lib.kgq_num_branches(structure_id(s))
+def uses_negation(s): return bool(_lib.kgq_uses_negation(structure_id(s)))
+def embedding_width(model, dim): return _lib.kgq_embedding_width(MODELS[model], dim)
+
+
+def shard_range(n_entity, world_size, rank):
+    b, e = _I64(), _I64()
+    st = _lib.kgq_shard_range(n_entity, world_size, rank, ctypes.byref(b), ctypes.byref(e))
+    if st:
+        raise KgqError(st, "bad shard arguments")
+    return b.value, e.value
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def layer_id(name: str) -> int:
+    """synth / nn.Module parameter name -> KGQ_LAYER_* id."""
+    if name == "proj.layer0":
+        return LAYER_PROJ_OUT
+    if name.startswith("proj.layer"):
+        return LAYER_PROJ_HIDDEN + int(name[len("proj.layer"):]) - 1
+    return {"inter.layer1": LAYER_INTER_1, "inter.layer2": LAYER_INTER_2,
+            "offset.layer1": LAYER_OFFSET_1, "offset.layer2": LAYER_OFFSET_2}[name]
+
+
+class Engine:
+    """One libkgq context: one model, one entity shard, one device."""
+
+    def __init__(self, model, n_entity, n_relation, dim, *, hidden=1600, n_hidden_layers=2,
+                 cen=0.02, terminal="regularizer", max_batch=1024, max_k=16, device=0,
+                 world_size=1, rank=0):
+        self.model = model
+        self.dim = dim
+        cfg = KgqConfig(ABI_VERSION, MODELS[model], n_entity, n_relation, dim, hidden,
+                        n_hidden_layers, cen, 0 if terminal == "regularizer" else 1, max_batch,
+                        max_k, device, world_size, rank)
+        h = _P()
+        st = _lib.kgq_create(ctypes.byref(cfg), ctypes.byref(h))
+        if st:
+            raise KgqError(st, _lib.kgq_last_error(None).decode())
+        self._h = h
+        self.cfg = cfg
+        self.device = device
+        self.shard = (_lib.kgq_shard_begin(h), _lib.kgq_shard_end(h))
+        self.width = embedding_width(model, dim)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.kgq_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _check(self, st):
+        if st:
+            raise KgqError(st, _lib.kgq_last_error(self._h).decode())
+
+    # ---- tables ---------------------------------------------------------------------------
+    def load_entities(self, rows: np.ndarray, first_row: int = 0):
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        self._check(_lib.kgq_load_entities(self._h, rows.ctypes.data, first_row, rows.shape[0]))
+
+    def load_relations(self, rows: np.ndarray, which: int = REL_MAIN):
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        self._check(_lib.kgq_load_relations(self._h, which, rows.ctypes.data, rows.shape[0]))
+
+    def load_linear(self, name_or_id, W: np.ndarray, b: np.ndarray):
+        lid = layer_id(name_or_id) if isinstance(name_or_id, str) else int(name_or_id)
+        W = np.ascontiguousarray(W, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        self._check(_lib.kgq_load_linear(self._h, lid, W.ctypes.data, b.ctypes.data, W.shape[0],
+                                         W.shape[1]))
+
+    def load_tables(self, t: dict, finalize: bool = True):
+        """Load a synth-format table dict ('entity', 'relation', 'offset', 'W:*', 'b:*')."""
+        ent = t["entity"]
+        step = 1 << 18
+        for r0 in range(0, ent.shape[0], step):
+            self.load_entities(ent[r0:r0 + step], r0)
+        self.load_relations(t["relation"], REL_MAIN)
+        if self.model == "q2b":
+            self.load_relations(t["offset"], REL_OFFSET)
+        for k in t:
+            if k.startswith("W:"):
+                self.load_linear(k[2:], t[k], t["b:" + k[2:]])
+        if finalize:
+            self.finalize()
+
+    def finalize(self):
+        self._check(_lib.kgq_finalize(self._h))
+
+    # ---- hot path -------------------------------------------------------------------------
+    def submit(self, structure, anchors, rels, k, *, out=None, shard_dist=False, stream=None):
+        """anchors/rels: int32 CUDA tensors [B, n_a] / [B, n_r].  Returns (dist [B,k],
+        ids [B,k]) CUDA tensors (and the [B, shard] distance matrix if shard_dist)."""
+        import torch
+        s = structure_id(structure)
+        B = anchors.shape[0]
+        dev = anchors.device
+        if out is None:
+            td = torch.empty((B, k), dtype=torch.float32, device=dev)
+            ti = torch.empty((B, k), dtype=torch.int32, device=dev)
+        else:
+            td, ti = out
+        sd = (torch.empty((B, self.shard[1] - self.shard[0]), dtype=torch.float32, device=dev)
+              if shard_dist else None)
+        self._check(_lib.kgq_submit(self._h, s, B, _ptr(anchors), _ptr(rels), k, _ptr(td),
+                                    _ptr(ti), _ptr(sd), _stream(stream)))
+        return (td, ti, sd) if shard_dist else (td, ti)
+
+    def submit_host(self, structure, anchors: np.ndarray, rels: np.ndarray, k: int,
+                    out=None, stream=None):
+        """End-to-end call with host buffers (H2D + path + D2H inside the library)."""
+        s = structure_id(structure)
+        anchors = np.ascontiguousarray(anchors, dtype=np.int32)
+        rels = np.ascontiguousarray(rels, dtype=np.int32)
+        B = anchors.shape[0]
+        if out is None:
+            td = np.empty((B, k), np.float32)
+            ti = np.empty((B, k), np.int32)
+        else:
+            td, ti = out
+        self._check(_lib.kgq_submit_host(self._h, s, B, anchors.ctypes.data, rels.ctypes.data, k,
+                                         td.ctypes.data, ti.ctypes.data, _stream(stream)))
+        return td, ti
+
+    def query_embedding(self, structure, anchors, rels, stream=None):
+        import torch
+        s = structure_id(structure)
+        B = anchors.shape[0]
+        out = torch.empty((B, num_branches(s), self.width), dtype=torch.float32,
+                          device=anchors.device)
+        self._check(_lib.kgq_query_embedding(self._h, s, B, _ptr(anchors), _ptr(rels), _ptr(out),
+                                             _stream(stream)))
+        return out
+
+    def merge_topk(self, parts_dist, parts_id, k, stream=None):
+        """parts_*: CUDA tensors [W, B, k] -> (dist [B,k], ids [B,k])."""
+        import torch
+        W, B, kk = parts_dist.shape
+        od = torch.empty((B, k), dtype=torch.float32, device=parts_dist.device)
+        oi = torch.empty((B, k), dtype=torch.int32, device=parts_dist.device)
+        self._check(_lib.kgq_merge_topk(self._h, W, B, kk, _ptr(parts_dist.contiguous()),
+                                        _ptr(parts_id.contiguous()), _ptr(od), _ptr(oi),
+                                        _stream(stream)))
+        return od, oi
+
+    def check_errors(self, stream=None):
+        self._check(_lib.kgq_check_errors(self._h, _stream(stream)))
+
+    def last_launch_count(self) -> int:
+        return _lib.kgq_last_launch_count(self._h)
+
+    def entity_terms(self, stream=None):
+        import torch
+        ns = self.shard[1] - self.shard[0]
+        out = torch.empty((3, self.dim, ns), dtype=torch.float32, device=f"cuda:{self.device}")
+        self._check(_lib.kgq_entity_terms(self._h, _ptr(out), _stream(stream)))
+        return out
+
+    def profile(self, on: bool = True):
+        self._check(_lib.kgq_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self):
+        ms = (ctypes.c_double * 4)()
+        n = (_I64 * 4)()
+        self._check(_lib.kgq_profile_read(self._h, ms, n))
+        return {STAGES[i]: (ms[i], n[i]) for i in range(4)}

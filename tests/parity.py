@@ -1,0 +1,80 @@
+"""Tolerance-aware comparators for GPU-vs-oracle parity.
+
+Q14 per distance: |d_gpu - d_ref| <= rel * max(|d_ref|, s_q), s_q = 1e-3 * median_e d_ref(q)
+    (near-zero distances -- planted exact matches, KL(p||p) -- are judged against the
+    query's distance scale, because fp32 cancellation there is absolute).
+Q15 top-k: tau = oracle k-th distance, tol = rel * max(tau, s_q).  Pass iff
+    (i) every GPU id has oracle distance <= tau + tol;
+    (ii) every id with oracle distance < tau - tol is present;
+    (iii) GPU distances are non-decreasing, ids unique, each within Q14 of its oracle value;
+    (iv) among GPU entries with equal GPU distance, ids ascend (the (dist, id) order).
+"""
+import numpy as np
+
+REL = 1e-4  # BASELINE.json north_star: "within 1e-4 relative in fp32"
+
+
+def row_scale(ref):
+    return 1e-3 * np.median(ref, axis=-1, keepdims=True)
+
+
+def assert_dist_close(got, ref, rel=REL, what=""):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    assert np.all(np.isfinite(got)), f"{what}: non-finite GPU distances"
+    err = np.abs(got - ref) / np.maximum(np.abs(ref), row_scale(ref))
+    worst = np.unravel_index(np.argmax(err), err.shape)
+    assert err.max() <= rel, (f"{what}: max rel err {err.max():.3g} at {worst}: "
+                              f"gpu {got[worst]!r} ref {ref[worst]!r}")
+    return float(err.max())
+
+
+def assert_embedding_close(got, ref, rel=REL, what=""):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    floor = 1e-2 * np.max(np.abs(ref), axis=-1, keepdims=True)  # chain: see DESIGN.md tolerances
+    err = np.abs(got - ref) / np.maximum(np.abs(ref), floor)
+    assert err.max() <= rel, f"{what}: max rel err {err.max():.3g}"
+    return float(err.max())
+
+
+def assert_topk_ok(gd, gi, ref_row, k, id_base=0, rel=REL, what="", sample_ids=None):
+    """gd/gi: GPU top-k of one query; ref_row: oracle distances of this query over the ids
+    [id_base, id_base + len(ref_row)) (the full row)."""
+    gd = np.asarray(gd, np.float64)
+    gi = np.asarray(gi, np.int64)
+    loc = gi - id_base
+    assert np.all((loc >= 0) & (loc < len(ref_row))), f"{what}: ids out of range {gi}"
+    assert len(set(gi.tolist())) == k, f"{what}: duplicate ids {gi}"
+    s_q = 1e-3 * np.median(ref_row)
+    part = np.partition(ref_row, k - 1)[k - 1]
+    tau = part
+    tol = rel * max(tau, s_q)
+    assert np.all(ref_row[loc] <= tau + tol), f"{what}: id with oracle dist > tau + tol"
+    must = np.nonzero(ref_row < tau - tol)[0]
+    assert set(must.tolist()) <= set(loc.tolist()), f"{what}: missing ids {set(must.tolist()) - set(loc.tolist())}"
+    assert np.all(np.diff(gd) >= 0), f"{what}: distances not sorted"
+    err = np.abs(gd - ref_row[loc]) / np.maximum(ref_row[loc], s_q)
+    assert err.max() <= rel, f"{what}: top-k distance err {err.max():.3g}"
+    eq = np.nonzero(np.diff(gd) == 0)[0]
+    assert np.all(gi[eq] < gi[eq + 1]), f"{what}: ties not ordered by id"
+
+
+def assert_topk_ok_sampled(gd, gi, ref_of_ids, sample_ids, ref_sample, k, rel=REL, what=""):
+    """Size-independent top-k property for tables too large for a full oracle row:
+    ref_of_ids = oracle distances of the returned ids; sample_ids / ref_sample = a random
+    entity sample and its oracle distances.  Checks Q15 (iii) and that no sampled entity
+    outside the returned set beats the returned k-th oracle distance by more than tol."""
+    gd = np.asarray(gd, np.float64)
+    gi = np.asarray(gi, np.int64)
+    s_q = 1e-3 * np.median(ref_sample)
+    assert len(set(gi.tolist())) == k, f"{what}: duplicate ids"
+    assert np.all(np.diff(gd) >= 0), f"{what}: distances not sorted"
+    err = np.abs(gd - ref_of_ids) / np.maximum(ref_of_ids, s_q)
+    assert err.max() <= rel, f"{what}: top-k distance err {err.max():.3g}"
+    tau = ref_of_ids.max()
+    tol = rel * max(tau, s_q)
+    outside = ~np.isin(np.asarray(sample_ids, np.int64), gi)
+    assert np.all(ref_sample[outside] >= tau - tol), f"{what}: a sampled entity beats the k-th"

@@ -1,0 +1,73 @@
+"""CPU checks of the C ABI library: it loads, exports every symbol include/kgq.h declares,
+and its pure-host entry points (structure metadata, shard ranges, argument validation) work
+without a GPU.  No compute calls here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle as O
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+kgq = pytest.importorskip("paper_2503_02172_b200.kgq",
+                          reason="libkgq.so not built (run __graft_entry__.build())")
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "kgq.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(kgq_[a-z_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    names = header_functions()
+    assert len(names) >= 25
+    lib = ctypes.CDLL(kgq.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in kgq.h but not exported"
+    assert set(names) == set(kgq.EXPORTS)
+
+
+def test_structure_metadata_matches_oracle_plans():
+    for i, s in enumerate(O.STRUCTURES):
+        assert kgq.structure_id(s) == i
+        assert kgq.num_anchors(s) == synth.N_ANCHORS[s] == O.kgq_oracle.n_anchors(s)
+        assert kgq.num_relations(s) == synth.N_RELS[s] == O.kgq_oracle.n_relations(s)
+        assert kgq.num_branches(s) == O.kgq_oracle.n_branches(s)
+        assert kgq.uses_negation(s) == O.kgq_oracle.uses_negation(s)
+    assert kgq._lib.kgq_num_anchors(14) == -1 and kgq._lib.kgq_num_anchors(-1) == -1
+    with pytest.raises(kgq.KgqError, match="valid: 1p"):
+        kgq.structure_id("4p")
+    assert kgq.embedding_width("gqe", 400) == 400
+    assert kgq.embedding_width("q2b", 400) == 800
+    assert kgq.embedding_width("betae", 400) == 800
+
+
+@pytest.mark.parametrize("n,w", [(1, 1), (7, 3), (14505, 8), (2_000_000, 8), (30, 4)])
+def test_shard_range_matches_oracle(n, w):
+    for r in range(w):
+        assert kgq.shard_range(n, w, r) == O.shard_range(n, w, r)
+    with pytest.raises(kgq.KgqError):
+        kgq.shard_range(n, w, w)
+
+
+def test_create_rejects_bad_config_without_crashing():
+    cfg = kgq.KgqConfig(kgq.ABI_VERSION, 0, 100, 5, 30, 0, 0, 0.02, 0, 16, 10, 0, 1, 0)
+    h = ctypes.c_void_p()
+    st = kgq._lib.kgq_create(ctypes.byref(cfg), ctypes.byref(h))
+    assert st == 1 and not h.value  # dim 30 is not a multiple of 4
+    assert b"multiple of 4" in kgq._lib.kgq_last_error(None)
+    cfg.dim = 32
+    cfg.abi_version = 99
+    assert kgq._lib.kgq_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    cfg.abi_version = kgq.ABI_VERSION
+    cfg.max_k = 1000
+    assert kgq._lib.kgq_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    kgq._lib.kgq_destroy(None)  # NULL-safe
+
+
+def test_sass_is_sm100a():
+    out = os.popen(f"cuobjdump -lelf {kgq.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
