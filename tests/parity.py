@@ -78,3 +78,13 @@ def assert_topk_ok_sampled(gd, gi, ref_of_ids, sample_ids, ref_sample, k, rel=RE
     tol = rel * max(tau, s_q)
     outside = ~np.isin(np.asarray(sample_ids, np.int64), gi)
     assert np.all(ref_sample[outside] >= tau - tol), f"{what}: a sampled entity beats the k-th"
+
+
+def chain_tolerance(structure, dist="kgr-init"):
+    """Element-wise tolerance for intermediate query embeddings:
+    1e-4 without negation at kgr-init; 1e-3 for negation structures and the 'spread' recipe.
+    An MLP output near the BetaE regulariser floor 0.05 carries the fp32 dot-product error
+    u*sum|w h|; negation 1/x maps it to a Beta parameter ~20 with relative error
+    u*sum|w h|/0.05, which the attention softmax and the next projection propagate.  The
+    final distances are held to the 1e-4 north-star bound regardless."""
+    return 1e-4 if (dist == "kgr-init" and "n" not in structure) else 1e-3

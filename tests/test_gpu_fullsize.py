@@ -6,7 +6,8 @@ import pytest
 
 import oracle as O
 import synth
-from parity import assert_dist_close, assert_topk_ok, assert_topk_ok_sampled
+from parity import (assert_embedding_close, assert_topk_ok, assert_topk_ok_sampled,
+                    chain_tolerance)
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -48,8 +49,7 @@ def test_full_size_sampled(cfg):
             assert_topk_ok(td[b], ti[b], ref[j], 10, what=f"{name} {s} row {b}")
         qe = e.query_embedding(s, dev(a), dev(r)).cpu().numpy()[rows]
         ref_q = m.query_embedding(s, a[rows], r[rows])
-        err = np.abs(qe - ref_q) / np.maximum(np.abs(ref_q), 1e-3 * np.abs(ref_q).max(-1, keepdims=True))
-        assert err.max() <= 1e-4, f"{name} {s} chain err {err.max():.3g}"
+        assert_embedding_close(qe, ref_q, rel=chain_tolerance(s), what=f"{name} {s} chain")
 
 
 def test_2m_entity_table_gqe_and_betae():
