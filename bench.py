@@ -149,15 +149,15 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2503_02172_b200 import Engine
+    from paper_2503_02172_b200.sharded import ShardedEngine
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t = synth.make_tables("betae", N_ENT, N_REL, DIM, hidden=HID, seed=SEED)
-    eng = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K, device=local,
-                 world_size=world, rank=rank)
-    eng.load_tables(t)
+    seng = ShardedEngine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K, device=local)
+    seng.load_tables(t)
+    eng = seng.engine
     ns = eng.shard[1] - eng.shard[0]
     stream = torch.cuda.current_stream()
     qs = {}
@@ -166,20 +166,13 @@ def main():
         qs[s] = (a, r, torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda())
     out = {s: (torch.empty((BATCH, K), device="cuda"), torch.empty((BATCH, K), dtype=torch.int32, device="cuda"))
            for s in STRUCTS}
-    gath = (torch.empty((world, BATCH, K), device="cuda"),
-            torch.empty((world, BATCH, K), dtype=torch.int32, device="cuda"))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     launches = [0]
 
     def one_type(s):
         a, r, da, dr = qs[s]
-        td, ti = eng.submit(s, da, dr, K, out=out[s])
-        launches[0] += eng.last_launch_count()
-        if world > 1:
-            dist.all_gather_into_tensor(gath[0], td)
-            dist.all_gather_into_tensor(gath[1], ti)
-            eng.merge_topk(gath[0], gath[1], K)
-            launches[0] += 1
+        seng.submit(s, da, dr, K)   # local top-k (+ NCCL all-gather + merge when world > 1)
+        launches[0] += seng.last_launch_count()
 
     def barrier():
         if world > 1:

@@ -1,0 +1,52 @@
+"""Entity-sharded multi-GPU path: one process per GPU, torch.distributed for
+the plumbing.
+
+Rank r owns the contiguous entity range kgq_shard_range(N, W, r); queries are replicated;
+each rank scores its shard and selects its local top-k (global ids) on its GPU; one
+all-gather of the W x [B, k] (distance, id) pairs exchanges them (NCCL over NVLink on the
+GPU box, gloo in the CPU tests); kgq_merge_topk merges W*k -> k on every rank.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .kgq import Engine
+
+
+def all_gather_topk(td: torch.Tensor, ti: torch.Tensor, group=None):
+    """[B, k] local (dist, id) on every rank -> ([W, B, k], [W, B, k]) in rank order."""
+    W = dist.get_world_size(group)
+    B = td.shape[0]
+    gd = torch.empty((W * B,) + tuple(td.shape[1:]), dtype=td.dtype, device=td.device)
+    gi = torch.empty((W * B,) + tuple(ti.shape[1:]), dtype=ti.dtype, device=ti.device)
+    dist.all_gather_into_tensor(gd, td.contiguous(), group=group)
+    dist.all_gather_into_tensor(gi, ti.contiguous(), group=group)
+    return gd.view((W,) + tuple(td.shape)), gi.view((W,) + tuple(ti.shape))
+
+
+class ShardedEngine:
+    """This rank's shard of a W-way entity-sharded model."""
+
+    def __init__(self, model, n_entity, n_relation, dim, *, group=None, device=None, **kw):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        dev = torch.cuda.current_device() if device is None else device
+        self.engine = Engine(model, n_entity, n_relation, dim, device=dev,
+                             world_size=self.world, rank=self.rank, **kw)
+        self.shard = self.engine.shard
+
+    def load_tables(self, t, finalize=True):
+        self.engine.load_tables(t, finalize)
+
+    def submit(self, structure, anchors, rels, k, stream=None):
+        """Global top-k of the replicated batch: local top-k -> all-gather -> merge."""
+        td, ti = self.engine.submit(structure, anchors, rels, k, stream=stream)
+        if self.world == 1:
+            return td, ti
+        gd, gi = all_gather_topk(td, ti, self.group)
+        return self.engine.merge_topk(gd, gi, k, stream=stream)
+
+    def last_launch_count(self):
+        return self.engine.last_launch_count() + (1 if self.world > 1 else 0)
