@@ -429,6 +429,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   for (auto& l : ctx->lin) { F(l.W); F(l.W_hi); F(l.W_lo); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) { F(s->hi); F(s->lo); }
   F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->d_err); F(ctx->d_invalid);
+  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
   for (auto& r : prof_list(ctx)) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   prof_list(ctx).clear();
@@ -544,6 +545,8 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st) st = dalloc(ctx, &ctx->Q, (size_t)(Bm * 2 * ctx->qw), "Q");
   if (!st) st = dalloc(ctx, &ctx->Qt, (size_t)(nplanes * d * ctx->rpad), "Qt");
   if (!st) st = dalloc(ctx, &ctx->dist, (size_t)(ctx->bchunk * ctx->np), "dist");
+  if (!st) st = dalloc(ctx, &ctx->topk_tmp_d, (size_t)(ctx->bchunk * 4096), "top-k candidates");
+  if (!st) st = dalloc(ctx, &ctx->topk_tmp_i, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st) st = dalloc(ctx, &ctx->score_tab, (size_t)((c.model == KGQ_BETAE ? 3 : 1) * d * ctx->np), "score table");
   if (!st) st = dalloc(ctx, &ctx->d_anchor_stage, (size_t)(Bm * kMaxBranches), "staging");
   if (!st) st = dalloc(ctx, &ctx->d_rel_stage, (size_t)(Bm * kMaxBranches), "staging");
@@ -588,7 +591,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
     {
       StageTimer t(ctx, st, kStTopk);
       L += launch_topk(ctx->dist, ctx->np, nb, ctx->ns, k, ctx->e0, ctx->d_invalid + b0,
-                       topk_dist + b0 * k, topk_id + b0 * k, st);
+                       topk_dist + b0 * k, topk_id + b0 * k, ctx->topk_tmp_d, ctx->topk_tmp_i, st);
     }
     if (shard_dist)
       CK(cudaMemcpy2DAsync(shard_dist + b0 * ctx->ns, ctx->ns * sizeof(float), ctx->dist,

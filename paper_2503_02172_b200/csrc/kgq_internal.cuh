@@ -89,6 +89,8 @@ struct kgq_ctx {
   int64_t rpad = 0;
   float* dist = nullptr;                   // [bchunk, np]
   int64_t bchunk = 0;
+  float* topk_tmp_d = nullptr;             // chunked top-k candidates [<= 4096 per row]
+  int32_t* topk_tmp_i = nullptr;
   int32_t* d_err = nullptr;                // [4]: flag, row, slot, kind
   int32_t* d_invalid = nullptr;            // [max_batch]
   int32_t* d_anchor_stage = nullptr;       // kgq_submit_host staging
@@ -175,8 +177,12 @@ int launch_score(int model, int nbq, int B, int d, float cen, const float* Qt, i
                  const float* tab, int64_t np, int64_t ns, float* dist, int64_t ldd,
                  cudaStream_t st);
 // Top-k per row of dist (row length n, global id = id_base + index).
+// Rows longer than 32k entries are split into chunks (one CTA each) whose candidates
+// (tmp_d/tmp_i, <= 4096 per row) are merged by k_merge.
 int launch_topk(const float* dist, int64_t ldd, int B, int64_t n, int k, int64_t id_base,
-                const int32_t* invalid, float* out_d, int32_t* out_i, cudaStream_t st);
+                const int32_t* invalid, float* out_d, int32_t* out_i, float* tmp_d, int32_t* tmp_i,
+                cudaStream_t st);
+bool score_uses_stream(int model, int nbq, int B);
 int launch_merge(int parts, int B, int k, const float* in_d, const int32_t* in_i, float* out_d,
                  int32_t* out_i, cudaStream_t st);
 // Table preparation (finalize).

@@ -154,6 +154,102 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// ---- small-batch streaming variant (SURVEY §8(d) C5a latency regime: B*NB <= 16) ----------
+// The tiled kernel pads the query tile to 64 rows; at B <= ~16 the sweep is HBM-bound
+// (ridge ~11 queries for GQE, ~17 for BetaE-CUV), so here every thread streams 4 consecutive
+// entities of the dim-major table with 16-byte loads (a warp reads 512 contiguous bytes per
+// dim and plane) while the <= 16 query rows sit in shared memory and are read as broadcasts.
+// Per (q, e, d) it evaluates exactly the expression of k_score, in the same order, so both
+// variants return bit-identical distances.
+template <int MODEL, int NB, int QB>
+__global__ void __launch_bounds__(256)
+    k_score_stream(const float* __restrict__ Qt, int64_t rpad, const float* __restrict__ tab,
+                   int64_t np, int d, float cen, float* __restrict__ dist, int64_t ldd, int B) {
+  constexpr int NQ = Planes<MODEL>::NQ, NE = Planes<MODEL>::NE, R = QB * NB;
+  extern __shared__ __align__(16) float qs[];  // [d][NQ][R]
+  const int64_t qplane = (int64_t)d * rpad;
+  for (int i = threadIdx.x; i < d * NQ * R; i += blockDim.x) {
+    const int r = i % R, p = (i / R) % NQ, j = i / (R * NQ);
+    qs[i] = Qt[p * qplane + (int64_t)j * rpad + r];
+  }
+  __syncthreads();
+  const int64_t ngroups = np / 4;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = g * 4;
+    float acc[R][4], acc2[R][4];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[r][i] = acc2[r][i] = 0.0f;
+#pragma unroll 4
+    for (int j = 0; j < d; ++j) {
+      float e[NE][4];
+#pragma unroll
+      for (int p = 0; p < NE; ++p) {
+        const float* src = NE == 1 ? tab + (int64_t)j * np + e0 : tab + ((int64_t)j * 3 + p) * np + e0;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        e[p][0] = v.x; e[p][1] = v.y; e[p][2] = v.z; e[p][3] = v.w;
+      }
+      const float* qj = qs + j * NQ * R;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (MODEL == KGQ_GQE) {
+            acc[r][i] += fabsf(e[0][i] - qj[r]);
+          } else if (MODEL == KGQ_Q2B) {
+            const float t = fabsf(e[0][i] - qj[r]);
+            acc[r][i] += t;
+            acc2[r][i] += fminf(t, qj[R + r]);
+          } else {
+            float t = e[0][i] + qj[r];
+            t = fmaf(qj[R + r], e[1][i], t);
+            t = fmaf(qj[2 * R + r], e[2][i], t);
+            acc[r][i] += fabsf(t);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      if (b >= B) break;
+      float o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        o[i] = MODEL == KGQ_Q2B ? fmaf(-(1.0f - cen), acc2[b * NB][i], acc[b * NB][i]) : acc[b * NB][i];
+        if (NB == 2) {
+          const float o1 = MODEL == KGQ_Q2B ? fmaf(-(1.0f - cen), acc2[b * NB + 1][i], acc[b * NB + 1][i])
+                                            : acc[b * NB + 1][i];
+          o[i] = fminf(o[i], o1);
+        }
+      }
+      *reinterpret_cast<float4*>(dist + (int64_t)b * ldd + e0) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+template <int MODEL, int NB, int QB>
+void launch_stream_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d, float cen,
+                     float* dist, int64_t ldd, int B, cudaStream_t st) {
+  constexpr int NQ = Planes<MODEL>::NQ, R = QB * NB;
+  const size_t smem = (size_t)d * NQ * R * sizeof(float);
+  cudaFuncSetAttribute(k_score_stream<MODEL, NB, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t groups = np / 4;
+  const int64_t want = (groups + 255) / 256;
+  const int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+  k_score_stream<MODEL, NB, QB><<<grid, 256, smem, st>>>(Qt, rpad, tab, np, d, cen, dist, ldd, B);
+}
+
+template <int MODEL, int NB>
+void launch_stream(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d, float cen,
+                   float* dist, int64_t ldd, int B, cudaStream_t st) {
+  if (B <= 1) launch_stream_t<MODEL, NB, 1>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+  else if (B <= 2) launch_stream_t<MODEL, NB, 2>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+  else if (B <= 4) launch_stream_t<MODEL, NB, 4>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+  else launch_stream_t<MODEL, NB, (MODEL == KGQ_Q2B ? 8 / NB : 8)>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+}
+
 template <int MODEL, int NB>
 void launch_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d, float cen,
               float* dist, int64_t ldd, int B, cudaStream_t st) {
@@ -170,20 +266,28 @@ void launch_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d
 }
 }  // namespace
 
+// Small batches (<= 16 query rows; <= 8 for Q2B, which keeps two sums per pair) stream the
+// table (HBM-bound regime); larger batches use the register-tiled kernel (FP32-ALU-bound).
+bool score_uses_stream(int model, int nbq, int B) {
+  return B * nbq <= (model == KGQ_Q2B ? 8 : 16) && B <= 8;
+}
+
 int launch_score(int model, int nbq, int B, int d, float cen, const float* Qt, int64_t rpad,
                  const float* tab, int64_t np, int64_t ns, float* dist, int64_t ldd,
                  cudaStream_t st) {
   (void)ns;
+  const bool s = score_uses_stream(model, nbq, B);
+#define KGQ_SCORE(M, NB)                                                  \
+  (s ? launch_stream<M, NB>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st) \
+     : launch_t<M, NB>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st))
   if (model == KGQ_GQE) {
-    if (nbq == 2) launch_t<KGQ_GQE, 2>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
-    else launch_t<KGQ_GQE, 1>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+    if (nbq == 2) KGQ_SCORE(KGQ_GQE, 2); else KGQ_SCORE(KGQ_GQE, 1);
   } else if (model == KGQ_Q2B) {
-    if (nbq == 2) launch_t<KGQ_Q2B, 2>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
-    else launch_t<KGQ_Q2B, 1>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+    if (nbq == 2) KGQ_SCORE(KGQ_Q2B, 2); else KGQ_SCORE(KGQ_Q2B, 1);
   } else {
-    if (nbq == 2) launch_t<KGQ_BETAE, 2>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
-    else launch_t<KGQ_BETAE, 1>(Qt, rpad, tab, np, d, cen, dist, ldd, B, st);
+    if (nbq == 2) KGQ_SCORE(KGQ_BETAE, 2); else KGQ_SCORE(KGQ_BETAE, 1);
   }
+#undef KGQ_SCORE
   return 1;
 }
 

@@ -45,17 +45,28 @@ __device__ void bitonic_sort_u64(unsigned long long* v, int P) {
 }
 
 constexpr int kTopkThreads = 256;
+constexpr int64_t kTopkChunkMin = 16384;  // entries per CTA when a row is split
 
 __global__ void __launch_bounds__(kTopkThreads)
-    k_topk(const float* __restrict__ dist, int64_t ldd, int64_t n, int k, int64_t id_base,
-           const int32_t* __restrict__ invalid, float* __restrict__ od, int32_t* __restrict__ oi) {
+    k_topk(const float* __restrict__ dist, int64_t ldd, int64_t n_total, int64_t chunk, int k,
+           int64_t id_base, const int32_t* __restrict__ invalid, float* __restrict__ od,
+           int32_t* __restrict__ oi, int B) {
+  // CTA (b, c) selects the k best of row b restricted to [c*chunk, min(n, (c+1)*chunk)) and
+  // writes them at [(c*B + b)*k, ...): with one chunk that is the final [B, k] answer, with
+  // several it is the candidate list k_merge reduces (multi-CTA top-k for long rows).
   const int b = blockIdx.x;
-  const float* row = dist + (int64_t)b * ldd;
+  const int64_t c0 = (int64_t)blockIdx.y * chunk;
+  const int64_t n = (n_total - c0 < chunk ? n_total - c0 : chunk);
+  const float* row = dist + (int64_t)b * ldd + c0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  od += ((int64_t)blockIdx.y * B + b) * k;
+  oi += ((int64_t)blockIdx.y * B + b) * k;
+  const int kout = k;
+  k = (int)(n < k ? n : k);  // a short last chunk contributes all of its entries
   if (invalid && invalid[b]) {
-    for (int j = tid; j < k; j += blockDim.x) {
-      od[(int64_t)b * k + j] = __uint_as_float(0x7FFFFFFFu);
-      oi[(int64_t)b * k + j] = -1;
+    for (int j = tid; j < kout; j += blockDim.x) {
+      od[j] = __uint_as_float(0x7FFFFFFFu);
+      oi[j] = -1;
     }
     return;
   }
@@ -141,17 +152,37 @@ __global__ void __launch_bounds__(kTopkThreads)
   for (int j = k + tid; j < P; j += blockDim.x) sel[j] = ~0ull;
   __syncthreads();
   bitonic_sort_u64(sel, P);
-  for (int j = tid; j < k; j += blockDim.x) {
-    const unsigned long long v = sel[j];
-    od[(int64_t)b * k + j] = fkey_inv((uint32_t)(v >> 32));
-    oi[(int64_t)b * k + j] = (int32_t)(id_base + (int64_t)(uint32_t)(v & 0xFFFFFFFFu));
+  for (int j = tid; j < kout; j += blockDim.x) {
+    if (j < k) {
+      const unsigned long long v = sel[j];
+      od[j] = fkey_inv((uint32_t)(v >> 32));
+      oi[j] = (int32_t)(id_base + c0 + (int64_t)(uint32_t)(v & 0xFFFFFFFFu));
+    } else {  // padding of a short chunk: sorts last in k_merge
+      od[j] = __uint_as_float(0x7FFFFFFFu);
+      oi[j] = -1;
+    }
   }
 }
 
+int64_t topk_chunk(int64_t n, int k) {
+  // long rows are split so that many CTAs share a query; chunks * k must fit k_merge (4096)
+  if (n <= kTopkChunkMin * 2) return n;
+  int64_t c = kTopkChunkMin;
+  while ((n + c - 1) / c * k > 4096) c *= 2;
+  return c;
+}
+
 int launch_topk(const float* dist, int64_t ldd, int B, int64_t n, int k, int64_t id_base,
-                const int32_t* invalid, float* out_d, int32_t* out_i, cudaStream_t st) {
-  k_topk<<<B, kTopkThreads, 0, st>>>(dist, ldd, n, k, id_base, invalid, out_d, out_i);
-  return 1;
+                const int32_t* invalid, float* out_d, int32_t* out_i, float* tmp_d, int32_t* tmp_i,
+                cudaStream_t st) {
+  const int64_t chunk = topk_chunk(n, k);
+  const int nch = (int)((n + chunk - 1) / chunk);
+  if (nch == 1) {
+    k_topk<<<dim3(B, 1), kTopkThreads, 0, st>>>(dist, ldd, n, n, k, id_base, invalid, out_d, out_i, B);
+    return 1;
+  }
+  k_topk<<<dim3(B, nch), kTopkThreads, 0, st>>>(dist, ldd, n, chunk, k, id_base, invalid, tmp_d, tmp_i, B);
+  return 1 + launch_merge(nch, B, k, tmp_d, tmp_i, out_d, out_i, st);
 }
 
 // Merge parts x [B, k] candidate lists into [B, k] (a9).  ids are global; NaN rows sort last.

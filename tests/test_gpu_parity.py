@@ -204,3 +204,25 @@ def test_deterministic_repeat():
     y = e.submit("ip", dev(a), dev(r), 10, shard_dist=True)
     for u, v in zip(x, y):
         assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("model", ["gqe", "q2b", "betae"])
+def test_small_batch_stream_scorer_matches_tiled(model):
+    """B*branches <= 16 takes the streaming (HBM-regime) scorer; it evaluates the same
+    per-(q, e, d) expression in the same order as the tiled kernel -> bit-identical rows."""
+    e, m, t = engine(model)
+    N, R = SMALL["N"], SMALL["R"]
+    for s in ("1p", "2u", "ip"):
+        a, r = synth.make_queries(s, 37, N, R, seed=31)
+        big = e.submit(s, dev(a), dev(r), 10, shard_dist=True)[2].cpu()
+        for B in (1, 2, 3, 5, 8):
+            td, ti, sd = e.submit(s, dev(a[:B]), dev(r[:B]), 10, shard_dist=True)
+            assert torch.equal(sd.cpu(), big[:B]), (model, s, B)
+        run_case(model, s, B=3)
+
+
+def test_chunked_topk_long_rows():
+    """Rows > 32k entities use the multi-CTA top-k (chunks + k_merge)."""
+    for k in (10, 256):
+        run_case("gqe", "2u", N=70001, R=5, d=8, H=8, B=3, k=k, max_batch=4, max_k=256)
+    run_case("betae", "1p", N=40000, R=5, d=8, H=16, B=20, k=16, max_batch=32, max_k=16)
