@@ -18,7 +18,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -131,6 +130,54 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_c5a(args):
+    """BASELINE.json configs[4], latency regime: 2M entities, d 400, GQE and
+    BetaE, B in {1, 8}, 1p and 2u, one GPU.  Reports the scorer's table-streaming bandwidth
+    (algorithmic bytes: the shard's scoring table once per batch) against measured HBM."""
+    import torch
+    from paper_2503_02172_b200 import Engine
+    peaks, src = load_peaks()
+    N, R, d = 2_000_000, 200, 400
+    res = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for model in ("gqe", "betae"):
+        t = synth.make_tables(model, N, R, d, hidden=HID, seed=77)
+        eng = Engine(model, N, R, d, hidden=HID, max_batch=8, max_k=K)
+        eng.load_tables(t)
+        del t
+        table_bytes = (1 if model == "gqe" else 3) * d * 4 * (eng.shard[1] - eng.shard[0])
+        for s in ("1p", "2u"):
+            for B in (1, 8):
+                a, r = synth.make_queries(s, B, N, R, seed=5)
+                da, dr = torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda()
+                for _ in range(args.warmup):
+                    eng.submit(s, da, dr, K)
+                torch.cuda.synchronize()
+                eng.profile(True)
+                eng.profile_read()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                tot = 0.0
+                for _ in range(args.steps):
+                    flush.zero_()
+                    e0.record()
+                    eng.submit(s, da, dr, K)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    tot += e0.elapsed_time(e1)
+                prof = eng.profile_read()
+                eng.profile(False)
+                sc_ms = prof["score"][0] / max(1, prof["score"][1])
+                gbs = table_bytes / (sc_ms / 1e3) / 1e9
+                res[f"{model}_{s}_B{B}"] = {
+                    "ms_per_batch": tot / args.steps, "queries_per_s": B * args.steps / (tot / 1e3),
+                    "stage_ms": {k: v[0] / args.steps for k, v in prof.items()},
+                    "scorer_table_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
+                }
+        eng.close()
+    print(json.dumps({"metric": "C5a latency regime: 2M-entity scoring HBM GB/s (1 GPU)",
+                      "hbm_peak_gbs": peaks["hbm_gbs"], "peak_source": src, "results": res}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -139,7 +186,10 @@ def main():
     ap.add_argument("--impl", default="kgq", choices=["kgq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=14)
+    ap.add_argument("--workload", default="fb15k237", choices=["fb15k237", "c5a"])
     args = ap.parse_args()
+    if args.workload == "c5a":
+        return run_c5a(args)
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -164,8 +214,6 @@ def main():
     for s in STRUCTS:
         a, r = synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s))
         qs[s] = (a, r, torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda())
-    out = {s: (torch.empty((BATCH, K), device="cuda"), torch.empty((BATCH, K), dtype=torch.int32, device="cuda"))
-           for s in STRUCTS}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     launches = [0]
 
