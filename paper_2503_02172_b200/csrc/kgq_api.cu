@@ -429,7 +429,8 @@ void kgq_destroy(kgq_ctx* ctx) {
   for (auto& l : ctx->lin) { F(l.W); F(l.W_hi); F(l.W_lo); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) { F(s->hi); F(s->lo); }
   F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->d_err); F(ctx->d_invalid);
-  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i);
+  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv_hi); F(ctx->uv_lo); F(ctx->Esum);
+  F(ctx->uvsums); F(ctx->Atc.hi); F(ctx->Atc.lo); F(ctx->Ptc);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
   for (auto& r : prof_list(ctx)) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   prof_list(ctx).clear();
@@ -547,6 +548,14 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st) st = dalloc(ctx, &ctx->dist, (size_t)(ctx->bchunk * ctx->np), "dist");
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_d, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_i, (size_t)(ctx->bchunk * 4096), "top-k candidates");
+  if (!st && c.model == KGQ_BETAE) {
+    st = dalloc(ctx, &ctx->uv_hi, (size_t)(ctx->np * 2 * d), "uv table");
+    if (!st) st = dalloc(ctx, &ctx->uv_lo, (size_t)(ctx->np * 2 * d), "uv table");
+    if (!st) st = dalloc(ctx, &ctx->Esum, (size_t)ctx->np, "entity sums");
+    if (!st) st = dalloc(ctx, &ctx->uvsums, (size_t)(2 * d), "uv sums");
+    if (!st) st = alloc_split(ctx, &ctx->Atc, 2 * ctx->bchunk, 2 * d, "tc query rows");
+    if (!st) st = dalloc(ctx, &ctx->Ptc, (size_t)(2 * ctx->bchunk), "tc query sums");
+  }
   if (!st) st = dalloc(ctx, &ctx->score_tab, (size_t)((c.model == KGQ_BETAE ? 3 : 1) * d * ctx->np), "score table");
   if (!st) st = dalloc(ctx, &ctx->d_anchor_stage, (size_t)(Bm * kMaxBranches), "staging");
   if (!st) st = dalloc(ctx, &ctx->d_rel_stage, (size_t)(Bm * kMaxBranches), "staging");
@@ -556,6 +565,8 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (c.model == KGQ_BETAE) {
     launch_beta_regularize(ctx->ent, c.n_entity * ctx->ew, 0);
     launch_betae_entity_terms(ctx->ent, ctx->e0, ctx->ns, d, ctx->score_tab, ctx->np, 0);
+    launch_betae_uv_table(ctx->ent, c.n_entity, ctx->e0, ctx->ns, ctx->np, d, ctx->uvsums, ctx->uv_hi, ctx->uv_lo,
+                          ctx->Esum, 0);
   } else {
     launch_transpose_shard(ctx->ent, ctx->e0, ctx->ns, d, ctx->ew, ctx->score_tab, ctx->np, 0);
   }
@@ -578,12 +589,18 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
   }
   for (int64_t b0 = 0; b0 < B; b0 += ctx->bchunk) {
     const int nb = (int)std::min<int64_t>(ctx->bchunk, B - b0);
-    {
-      StageTimer t(ctx, st, kStPrep);
-      L += launch_score_prep(c.model, ctx->Q + b0 * P->n_out * ctx->qw, nb, P->n_out, c.dim, ctx->Qt,
-                             ctx->rpad, st);
-    }
-    {
+    const float* qb = ctx->Q + b0 * P->n_out * ctx->qw;
+    if (c.model == KGQ_BETAE && !score_uses_stream(c.model, P->n_out, nb)) {
+      // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
+      StageTimer t(ctx, st, kStScore);
+      L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
+                                 ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist,
+                                 ctx->np, st);
+    } else {
+      {
+        StageTimer t(ctx, st, kStPrep);
+        L += launch_score_prep(c.model, qb, nb, P->n_out, c.dim, ctx->Qt, ctx->rpad, st);
+      }
       StageTimer t(ctx, st, kStScore);
       L += launch_score(c.model, P->n_out, nb, c.dim, c.cen, ctx->Qt, ctx->rpad, ctx->score_tab, ctx->np,
                         ctx->ns, ctx->dist, ctx->np, st);

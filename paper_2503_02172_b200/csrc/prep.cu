@@ -15,23 +15,6 @@
 
 namespace kgq {
 
-// fp64 digamma: recurrence psi(x) = psi(x+1) - 1/x up to x >= 10, then the asymptotic
-// series ln x - 1/(2x) - sum_n B_2n / (2n x^2n) through x^-14 (truncation < 1e-16 there).
-__device__ double digamma_f64(double x) {
-  double r = 0.0;
-  while (x < 10.0) {
-    r -= 1.0 / x;
-    x += 1.0;
-  }
-  const double f = 1.0 / (x * x);
-  const double t =
-      f * (-1.0 / 12 +
-           f * (1.0 / 120 +
-                f * (-1.0 / 252 +
-                     f * (1.0 / 240 + f * (-1.0 / 132 + f * (691.0 / 32760 + f * (-1.0 / 12)))))));
-  return r + log(x) - 0.5 / x + t;
-}
-
 __device__ __forceinline__ double log_beta_f64(double a, double b) {
   return lgamma(a) + lgamma(b) - lgamma(a + b);
 }

@@ -1,0 +1,152 @@
+// Tensor-core BetaE scorer (a6 + a7 for BetaE at batch sizes past the
+// HBM ridge).
+//
+// Per dimension KL(Beta(ae,be) || Beta(aq,bq)) = L_q + C_e + aq U_e + bq V_e >= 0 (closed form
+// of the Eq. 3 densities, entity-only and query-only lgamma/digamma terms; prep.cu), and a
+// KL divergence is non-negative, so sum_d |KL_d| = sum_d KL_d exactly.  With per-dimension
+// means Ubar_d, Vbar_d (over all N entities) and u = U - Ubar, v = V - Vbar:
+//   dist(q, e) = P_q + E_e + sum_d (aq_d u_ed + bq_d v_ed)
+//   P_q = sum_d (lnB(aq_d, bq_d) + aq_d Ubar_d + bq_d Vbar_d)     (fp64, per query row)
+//   E_e = sum_d C_ed                                               (fp64, per entity, finalize)
+// The last term is a dense contraction [rows, 2d] x [2d, N] -> 3xTF32 on tcgen05 (tc_gemm.cuh).
+// Centring keeps its terms ~0.1 (|u|, |v| << |U|, |V| ~ 1), so the fp32 partial sums carry
+// ~1e-7 of sum|terms| ~ 1e-5 absolute instead of ~1e-4 for the uncentred sum, and the large,
+// cancelling P_q + E_e (~ +-800 at d = 400) are added in fp64 in the epilogue.  DNF union:
+// rows are (b, branch) = 2b + br, so the two branches of a query sit in adjacent lanes and the
+// min is one shuffle.
+#include "tc_gemm.cuh"
+
+namespace kgq {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Pass 1: per-dimension sums of U and V over all entities (means for centring).
+__global__ void k_uv_dim_sums(const float* __restrict__ ent, int64_t e0, int64_t ns, int d,
+                              double* __restrict__ sums /* [2][d] */) {
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  double su = 0.0, sv = 0.0;
+  for (int64_t e = blockIdx.x; e < ns; e += gridDim.x) {
+    const double a = ent[(e0 + e) * 2 * d + j], b = ent[(e0 + e) * 2 * d + d + j];
+    const double pab = digamma_f64(a + b);
+    su += pab - digamma_f64(a);
+    sv += pab - digamma_f64(b);
+  }
+  atomicAdd(&sums[j], su);
+  atomicAdd(&sums[d + j], sv);
+}
+
+// Pass 2: centred split table uv [np][2d] = [u; v] (hi/lo) and E_e = sum_d C_ed (fp64).
+__global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns, int64_t np, int d,
+                           int64_t n_all, const double* __restrict__ sums, float* __restrict__ uv_hi,
+                           float* __restrict__ uv_lo, double* __restrict__ Esum) {
+  const int64_t e = blockIdx.x;
+  __shared__ double red[32];
+  double c = 0.0;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float u = 0.0f, v = 0.0f;
+    if (e < ns) {
+      const double a = ent[(e0 + e) * 2 * d + j], b = ent[(e0 + e) * 2 * d + d + j];
+      const double pa = digamma_f64(a), pb = digamma_f64(b), pab = digamma_f64(a + b);
+      c += -(lgamma(a) + lgamma(b) - lgamma(a + b)) + a * pa + b * pb - (a + b) * pab;
+      u = (float)((pab - pa) - sums[j] / (double)n_all);
+      v = (float)((pab - pb) - sums[d + j] / (double)n_all);
+    }
+    store_split(uv_hi, uv_lo, e * 2 * d + j, u);
+    store_split(uv_hi, uv_lo, e * 2 * d + d + j, v);
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) Esum[e] = t;
+  }
+}
+
+// Per batch: A = split [aq; bq] rows (query embedding rows, already (b, branch) ordered) and
+// P_q in fp64.
+__global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
+                                const double* __restrict__ sums, int64_t ns, Split A,
+                                double* __restrict__ P) {
+  const int r = blockIdx.x;
+  __shared__ double red[32];
+  double p = 0.0;
+  const double inv = 1.0 / (double)ns;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const float a = q[(int64_t)r * 2 * d + j], b = q[(int64_t)r * 2 * d + d + j];
+    store_split(A.hi, A.lo, (int64_t)r * A.ld + j, a);
+    store_split(A.hi, A.lo, (int64_t)r * A.ld + d + j, b);
+    const double da = a, db = b;
+    p += lgamma(da) + lgamma(db) - lgamma(da + db) + da * sums[j] * inv + db * sums[d + j] * inv;
+  }
+  p = warp_sum(p);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) P[r] = t;
+  }
+}
+
+template <int CW, int NB>
+struct EpiBetaScore {
+  const double* P;  // [rows]
+  const double* E;  // [np]
+  float* dist;      // [rows / NB, ldd]
+  int64_t ldd;
+  int rows;
+  __device__ __forceinline__ void apply(int row, int n0, const float (&acc)[CW]) const {
+    const double p = row < rows ? P[row] : 0.0;
+    const bool store = row < rows && (NB == 1 || (row & 1) == 0);
+    float* drow = dist + (int64_t)(row / NB) * ldd + n0;
+#pragma unroll
+    for (int i = 0; i < CW; i += 4) {
+      float o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        o[t] = (float)(p + E[n0 + i + t] + (double)acc[i + t]);
+        if (NB == 2) o[t] = fminf(o[t], __shfl_xor_sync(0xffffffffu, o[t], 1));
+      }
+      if (store) *reinterpret_cast<float4*>(drow + i) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+};
+
+}  // namespace
+
+int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
+                          double* sums, float* uv_hi, float* uv_lo, double* Esum, cudaStream_t st) {
+  // centring means over ALL entities (every rank holds the full table), so that every shard
+  // uses the same u, v and a sharded run is bit-identical to a single-GPU run
+  cudaMemsetAsync(sums, 0, 2 * d * sizeof(double), st);
+  const int gx = (int)(n_all < 1024 ? n_all : 1024);
+  k_uv_dim_sums<<<dim3(gx, (d + 127) / 128), 128, 0, st>>>(ent, 0, n_all, d, sums);
+  k_uv_table<<<(unsigned)np, 128, 0, st>>>(ent, e0, ns, np, d, n_all, sums, uv_hi, uv_lo, Esum);
+  return 2;
+}
+
+int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
+                          Split A, double* P, const float* uv_hi, const float* uv_lo, const double* Esum,
+                          int64_t np, float* dist, int64_t ldd, cudaStream_t st) {
+  constexpr int BN = 128;
+  k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
+  int L = 1;
+  if (nbq == 2) {
+    EpiBetaScore<BN / 2, 2> e{P, Esum, dist, ldd, rows};
+    L += tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
+  } else {
+    EpiBetaScore<BN / 2, 1> e{P, Esum, dist, ldd, rows};
+    L += tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
+  }
+  return L;
+}
+
+}  // namespace kgq

@@ -1,0 +1,314 @@
+// tcgen05 3xTF32 GEMM core shared by the dense layers (linear_tc.cu) and the tensor-core
+// BetaE scorer (score_tc.cu).  See linear_tc.cu for the design notes.
+#pragma once
+#include <cuda.h>
+#include <stdio.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+#include "kgq_internal.cuh"
+
+namespace kgq {
+namespace tc {
+constexpr int BM = 128, BK = 32, EPI_WARPS = 8, THREADS = 64 + 32 * EPI_WARPS;  // TMA, MMA, 8 x epilogue
+
+// ---- PTX wrappers -----------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+// K-major operand tile, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;              // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+      "[%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+  static constexpr int W_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;
+  static constexpr int STAGES = BN == 128 ? 3 : 4;  // <= 227 KB of shared memory
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+  static_assert(TOTAL <= 227 * 1024, "shared memory budget");
+};
+
+// K-blocks per tensor-core partial sum.  The TMEM accumulate path truncates (measured: bias
+// ~ 0.5 ulp per MMA accumulate, rms rel. error 1.8e-5 at K = 1600 with one chain), so each
+// partial covers DRAIN*BK of K (DRAIN*3*BK/8 accumulates) and the epilogue warps add the
+// partials in fp32 round-to-nearest registers, as a sequential FFMA loop would.
+#ifndef KGQ_TC_DRAIN
+#define KGQ_TC_DRAIN 2
+#endif
+constexpr int DRAIN = KGQ_TC_DRAIN;
+
+// Generic 3xTF32 GEMM acc[m, n] = sum_k A[m, k] W[n, k] over a 128 x BN tile; the epilogue
+// policy Epi receives each epilogue thread's row and its BN fp32 sums (all 128 rows of the
+// tile, including rows >= M, so that policies may shuffle between lanes).  Each epilogue warp
+// owns 32 rows (its TMEM lane quarter) and BN/2 columns, so Epi::apply sees acc[BN/2].
+template <int BN, class Epi>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+              const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
+              int M, int N, int K, const Epi epi) {
+  using L = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  constexpr int STAGES = L::STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* accfull = empty + STAGES;   // [2] partial sum ready in TMEM buffer a
+  uint64_t* accempty = accfull + 2;     // [2] partial drained by the epilogue warps
+  uint32_t* tmem_slot = (uint32_t*)(accempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = (K + BK - 1) / BK;
+  const int ng = (nk + DRAIN - 1) / DRAIN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mAh);
+    tma_prefetch(&mAl);
+    tma_prefetch(&mWh);
+    tma_prefetch(&mWl);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&accfull[a], 1);
+      mbar_init(&accempty[a], EPI_WARPS);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // two TMEM partial accumulators: 128 lanes x 2*BN fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+        uint8_t* st = smem + s * L::STAGE_BYTES;
+        mbar_expect_tx(&full[s], L::STAGE_BYTES);
+        tma_load_2d(st, &mAh, &full[s], kb * BK, m0);
+        tma_load_2d(st + L::A_BYTES, &mAl, &full[s], kb * BK, m0);
+        tma_load_2d(st + 2 * L::A_BYTES, &mWh, &full[s], kb * BK, n0);
+        tma_load_2d(st + 2 * L::A_BYTES + L::W_BYTES, &mWl, &full[s], kb * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      // instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = 128
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const int g = kb / DRAIN, a = g & 1;
+        const bool first = (kb % DRAIN) == 0;
+        if (first && g >= 2) mbar_wait(&accempty[a], ((g >> 1) - 1) & 1);
+        mbar_wait(&full[s], (kb / STAGES) & 1);
+        fence_after();
+        const uint32_t d = tmem + (uint32_t)(a * BN);
+        const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
+        const uint32_t ah = st, al = st + L::A_BYTES;
+        const uint32_t wh = st + 2 * L::A_BYTES, wl = wh + L::W_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 32 bytes per MMA along K
+          const uint32_t off = kk * 32;
+          mma_tf32(d, umma_desc_sw128(ah + off), umma_desc_sw128(wl + off), idesc,
+                   (first && kk == 0) ? 0u : 1u);
+          mma_tf32(d, umma_desc_sw128(al + off), umma_desc_sw128(wh + off), idesc, 1u);
+          mma_tf32(d, umma_desc_sw128(ah + off), umma_desc_sw128(wh + off), idesc, 1u);
+        }
+        mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+        if ((kb % DRAIN) == DRAIN - 1 || kb == nk - 1) mma_commit(&accfull[a]);
+      }
+    }
+  } else {
+    // -------- epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4 --------
+    constexpr int CW = BN / 2;
+    const int q = warp & 3;
+    const int ch = ((warp - 2) >> 2) * CW;
+    const int row = m0 + q * 32 + lane;
+    float acc[CW];
+#pragma unroll
+    for (int i = 0; i < CW; ++i) acc[i] = 0.0f;
+    for (int g = 0; g < ng; ++g) {
+      const int a = g & 1;
+      mbar_wait(&accfull[a], (g >> 1) & 1);
+      fence_after();
+#pragma unroll
+      for (int c = 0; c < CW; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + ch + c), v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[c + i] += v[i];
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accempty[a])) : "memory");
+    }
+    epi.apply(row, n0 + ch, acc);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+  }
+}
+
+// ---- host: tensor maps (cached per buffer) -----------------------------------------------
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeFn)p;
+  });
+  return fn;
+}
+
+// rows x cols fp32 matrix with row stride ld (elements); box = box_rows x BK, 128B swizzle
+inline bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  static std::mutex mu;
+  static std::map<std::tuple<const float*, int64_t, int64_t, int64_t, int>, CUtensorMap> cache;
+  const auto key = std::make_tuple(ptr, rows, cols, ld, box_rows);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *m = it->second;
+    return true;
+  }
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(float))};
+  cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *m);
+  return true;
+}
+
+
+template <int BN, class Epi>
+int launch_tc_gemm(const Split& A, int M, const float* Wh, const float* Wl, int N, int64_t ldw, int K,
+                   const Epi& epi, cudaStream_t st) {
+  CUtensorMap mAh, mAl, mWh, mWl;
+  if (!make_map(&mAh, A.hi, M, K, A.ld, BM) || !make_map(&mAl, A.lo, M, K, A.ld, BM) ||
+      !make_map(&mWh, Wh, N, K, ldw, BN) || !make_map(&mWl, Wl, N, K, ldw, BN)) {
+    fprintf(stderr, "libkgq: cuTensorMapEncodeTiled failed\n");
+    return -1;
+  }
+  auto kern = k_tc_gemm<BN, Epi>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL);
+    attr = true;
+  }
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  kern<<<grid, THREADS, Smem<BN>::TOTAL, st>>>(mAh, mAl, mWh, mWl, M, N, K, epi);
+  return 1;
+}
+
+}  // namespace tc
+}  // namespace kgq

@@ -208,8 +208,9 @@ def test_deterministic_repeat():
 
 @pytest.mark.parametrize("model", ["gqe", "q2b", "betae"])
 def test_small_batch_stream_scorer_matches_tiled(model):
-    """B*branches <= 16 takes the streaming (HBM-regime) scorer; it evaluates the same
-    per-(q, e, d) expression in the same order as the tiled kernel -> bit-identical rows."""
+    """B*branches <= 16 takes the streaming (HBM-regime) scorer; for GQE/Q2B it evaluates the
+    same per-(q, e, d) expression in the same order as the tiled kernel -> bit-identical rows;
+    BetaE batches above 16 rows use the tensor-core scorer -> agreement within 1e-5."""
     e, m, t = engine(model)
     N, R = SMALL["N"], SMALL["R"]
     for s in ("1p", "2u", "ip"):
@@ -217,7 +218,10 @@ def test_small_batch_stream_scorer_matches_tiled(model):
         big = e.submit(s, dev(a), dev(r), 10, shard_dist=True)[2].cpu()
         for B in (1, 2, 3, 5, 8):
             td, ti, sd = e.submit(s, dev(a[:B]), dev(r[:B]), 10, shard_dist=True)
-            assert torch.equal(sd.cpu(), big[:B]), (model, s, B)
+            if model == "betae":   # large batches take the tensor-core scorer (score_tc.cu)
+                assert_dist_close(sd.cpu().numpy(), big[:B].numpy(), rel=1e-5, what=f"{s} B={B}")
+            else:
+                assert torch.equal(sd.cpu(), big[:B]), (model, s, B)
         run_case(model, s, B=3)
 
 
