@@ -282,19 +282,23 @@ def main():
         e2e_s = time.perf_counter() - t0
         e2e_v = queries / e2e_s
 
-    # ---- roofline of the dominant kernel (entity scorer): FP32-ALU bound ----------------
+    # ---- roofline of the dominant kernel: the tcgen05 3xTF32 GEMM (k_tc_gemm), which runs
+    # every dense layer of the chain (stage "dense") and the BetaE scorer contraction (stage
+    # "score").  Algorithmic work = useful fp32 FLOPs (2MNK); peak = TF32 dense peak / 3, the
+    # TF32 peak being the measured bf16 GEMM peak x the nominal tf32/bf16 ratio 1.1/2.25.
     peaks, peak_src = load_peaks()
-    score_ms, score_n = prof["score"]
-    n_union = sum(1 for s in STRUCTS if s in ("2u", "up"))
-    ops_per_step = 4.0 * BATCH * ns * DIM * (len(STRUCTS) + n_union)   # FP32 instr (lane ops)
-    achieved = ops_per_step * args.steps / (score_ms / 1e3) / 1e12
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    peak_alu = 148 * 128 * sm_mhz * 1e6 / 1e12     # T lane-instr/s at max clock
+    d_ms, d_n, d_fl = prof["dense"]
+    s_ms, s_n, s_fl = prof["score"]
+    tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
+    peak_tc = tf32 / 3.0
+    ach = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+    achieved = ach(d_fl + s_fl, d_ms + s_ms)
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "score_traffic.json")
+    tf = os.path.join(ROOT, "profiles", "tc_gemm_traffic.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get("dram_bytes_per_launch")
-    stage_share = {k: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
+    tot_ms = prof["chain"][0] + prof["prep"][0] + prof["score"][0] + prof["topk"][0]
+    stage_share = {k: round(prof[k][0] / max(1e-9, tot_ms), 4) for k in ("chain", "prep", "score", "topk", "dense")}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
@@ -304,14 +308,18 @@ def main():
             "config": dict(CONFIG, l2="flushed between timed steps (256 MiB write, untimed)",
                            parallelism=f"entity-shard x{world}" if world > 1 else "1 GPU"),
             "per_type_qps": {s: BATCH * args.steps / (per_type[s] / 1e3) for s in STRUCTS},
-            "stage_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "stage_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},  # dense is inside chain
             "stage_share": stage_share,
-            "roofline": {"kernel": "k_score<BETAE> (entity scorer)", "bound": "alu",
-                         "achieved": achieved, "peak": peak_alu, "unit": "Tinstr/s",
-                         "frac": achieved / peak_alu, "traffic": traffic,
-                         "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz ({peak_src} sm_max_mhz)",
-                         "work": "4 FP32 instr per (query, entity, dim, DNF branch)"},
-            "scorer_table_gbs": (3 * ns * DIM * 4) * score_n / (score_ms / 1e3) / 1e9,
+            "roofline": {"kernel": "k_tc_gemm (tcgen05 3xTF32: chain dense layers + BetaE scorer)",
+                         "bound": "tensor", "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tc, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16 {peaks['bf16_tflops']:.1f} x 1.1/2.25 (tf32) / 3 (3xTF32)",
+                         "work": "useful fp32 FLOPs 2MNK per GEMM launch",
+                         "launches": d_n + s_n,
+                         "parts": {"dense": {"ms_per_step": d_ms / args.steps, "tflops": ach(d_fl, d_ms),
+                                             "launches_per_step": d_n / args.steps},
+                                   "score": {"ms_per_step": s_ms / args.steps, "tflops": ach(s_fl, s_ms),
+                                             "launches_per_step": s_n / args.steps}}},
             "gpu_launches": launches[0],
             "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,

@@ -179,11 +179,13 @@ int32_t kgq_last_launch_count(const kgq_ctx* ctx);
  * (C, U, V planes).  Parity aid for the fp64 precompute. */
 kgq_status kgq_entity_terms(kgq_ctx* ctx, float* out, kgq_stream stream);
 /* Stage timing with CUDA events recorded on the launching stream (bench roofline).  Stages:
- * 0 operator chain, 1 scorer operand prep, 2 entity scorer, 3 top-k. */
+ * 0 operator chain, 1 scorer operand prep, 2 entity scorer, 3 top-k, 4 dense layers (each
+ * tcgen05 GEMM of the chain; nested inside stage 0). */
 kgq_status kgq_profile_enable(kgq_ctx* ctx, int32_t on);
-/* Summed device milliseconds ms[4] and launch-group counts n[4] since the last read;
- * synchronises on the recorded events, then resets. */
-kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n);
+/* Summed device milliseconds ms[5], timed-region counts n[5] and algorithmic work work[5]
+ * (may be NULL; dense: 2MNK FLOPs; scorer: FLOPs of the tensor-core BetaE contraction or FP32
+ * lane instructions of the SIMT scorers) since the last read; synchronises, then resets. */
+kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n, double* work);
 
 #ifdef __cplusplus
 }

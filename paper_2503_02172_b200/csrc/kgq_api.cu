@@ -108,6 +108,7 @@ struct DeviceGuard {
 struct ProfRec {
   int stage;
   cudaEvent_t a, b;
+  double work;
 };
 std::vector<ProfRec>& prof_list(kgq_ctx* ctx) {
   static thread_local std::vector<std::pair<kgq_ctx*, std::vector<ProfRec>>> lists;
@@ -121,7 +122,8 @@ struct StageTimer {
   cudaStream_t st;
   int stage;
   cudaEvent_t a = nullptr;
-  StageTimer(kgq_ctx* c, cudaStream_t s, int stg) : ctx(c), st(s), stage(stg) {
+  double work;
+  StageTimer(kgq_ctx* c, cudaStream_t s, int stg, double w = 0.0) : ctx(c), st(s), stage(stg), work(w) {
     if (!ctx->profile) return;
     cudaEventCreate(&a);
     cudaEventRecord(a, st);
@@ -131,7 +133,7 @@ struct StageTimer {
     cudaEvent_t b;
     cudaEventCreate(&b);
     cudaEventRecord(b, st);
-    prof_list(ctx).push_back({stage, a, b});
+    prof_list(ctx).push_back({stage, a, b, work});
     ctx->prof_n[stage] += 1;
   }
 };
@@ -153,6 +155,14 @@ ChainArgs chain_args(kgq_ctx* ctx, const Plan* P, int B, const int32_t* anchors,
   a.invalid = ctx->d_invalid;
   (void)B;
   return a;
+}
+
+// Every dense layer of the chain goes through here: timed as stage kStDense when profiling,
+// with 2 M N K algorithmic FLOPs.
+int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
+          int neg1, cudaStream_t st) {
+  StageTimer t(ctx, st, kStDense, 2.0 * M * (double)L.out_f * K);
+  return launch_linear(A, M, K, L, epi, out, neg0, neg1, st);
 }
 
 Split offset_split(const Split& s, int64_t rows, int64_t cols = 0) {
@@ -181,7 +191,7 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
   int K = 3 * d;
   for (int l = 0; l < ctx->cfg.n_hidden_layers; ++l) {
     const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
-    L += launch_linear(A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
+    L += dense(ctx, A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
     A = ctx->H[l & 1];
     K = lin.out_f;
   }
@@ -202,10 +212,10 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
   Split out = offset_split(ctx->S, (int64_t)br0 * B);
   const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
   if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
-    L += launch_linear(A, M, K, lo, kEpiNone, Split{ctx->T, nullptr, 2 * d}, 0, 0, st);
+    L += dense(ctx, A, M, K, lo, kEpiNone, Split{ctx->T, nullptr, 2 * d}, 0, 0, st);
     L += launch_softmax_terminal(ctx->T, 2 * d, M, 2 * d, out, 0, neg0, neg1, st);
   } else {
-    L += launch_linear(A, M, K, lo, kEpiBetaReg, out, neg0, neg1, st);
+    L += dense(ctx, A, M, K, lo, kEpiBetaReg, out, neg0, neg1, st);
   }
   for (auto& e : extra) L += launch_negate(out, e.first, e.second, 2 * d, st);
   return L;
@@ -230,16 +240,16 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
     L += launch_translate_chain(ca, ctx->ent, ctx->rel[0], ctx->rel[1], B, ctx->S, nullptr, st);
     // attention logits over centres (Q6): W2 ReLU(W1 x + b1) + b2, rows br*B + b
     const Split centres{ctx->S.hi, ctx->S.lo, ctx->S.ld};
-    L += launch_linear(centres, (int)M, d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
-    L += launch_linear(ctx->I, (int)M, d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
+    L += dense(ctx, centres, (int)M, d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
+    L += dense(ctx, ctx->I, (int)M, d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
                        Split{ctx->T, nullptr, ctx->tw}, 0, 0, st);
     const float* gate = nullptr;
     if (model == KGQ_Q2B) {  // offset gate: sigmoid(V2 mean_i ReLU(V1 o_i + c1) + c2)
       const Split offs{ctx->S.hi + d, ctx->S.lo + d, ctx->S.ld};
-      L += launch_linear(offs, (int)M, d, ctx->lin[KGQ_LAYER_OFFSET_1], kEpiRelu,
+      L += dense(ctx, offs, (int)M, d, ctx->lin[KGQ_LAYER_OFFSET_1], kEpiRelu,
                          Split{ctx->T2, nullptr, ctx->tw}, 0, 0, st);
       L += launch_branch_mean(ctx->T2, ctx->tw, nb, B, d, ctx->M, st);
-      L += launch_linear(ctx->M, B, d, ctx->lin[KGQ_LAYER_OFFSET_2], kEpiNone,
+      L += dense(ctx, ctx->M, B, d, ctx->lin[KGQ_LAYER_OFFSET_2], kEpiNone,
                          Split{ctx->T2, nullptr, ctx->tw}, 0, 0, st);
       gate = ctx->T2;
     }
@@ -284,8 +294,8 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
   }
   if (P->kind != kInter) return L + launch_state_to_q(ctx->S, P->n_out, B, 2 * d, ctx->Q, st);
   // intersection (Q6): attention over [alpha_i; beta_i] (2d -> 2d -> d), shared weights a_i
-  L += launch_linear(ctx->S, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
-  L += launch_linear(ctx->I, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
+  L += dense(ctx, ctx->S, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
+  L += dense(ctx, ctx->I, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
                      Split{ctx->T, nullptr, ctx->tw}, 0, 0, st);
   CombineArgs c{};
   c.model = model; c.nb = nb; c.B = B; c.d = d; c.ldl = ctx->tw; c.ldg = 0;
@@ -592,7 +602,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
     const float* qb = ctx->Q + b0 * P->n_out * ctx->qw;
     if (c.model == KGQ_BETAE && !score_uses_stream(c.model, P->n_out, nb)) {
       // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
-      StageTimer t(ctx, st, kStScore);
+      StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
       L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
                                  ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist,
                                  ctx->np, st);
@@ -601,7 +611,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
         StageTimer t(ctx, st, kStPrep);
         L += launch_score_prep(c.model, qb, nb, P->n_out, c.dim, ctx->Qt, ctx->rpad, st);
       }
-      StageTimer t(ctx, st, kStScore);
+      StageTimer t(ctx, st, kStScore, (c.model == KGQ_GQE ? 2.0 : 4.0) * nb * P->n_out * (double)ctx->ns * c.dim);
       L += launch_score(c.model, P->n_out, nb, c.dim, c.cen, ctx->Qt, ctx->rpad, ctx->score_tab, ctx->np,
                         ctx->ns, ctx->dist, ctx->np, st);
     }
@@ -724,17 +734,22 @@ kgq_status kgq_profile_enable(kgq_ctx* ctx, int32_t on) {
   return KGQ_OK;
 }
 
-kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n) {
+kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n, double* work) {
   if (!ctx || !ms || !n) return fail(ctx, KGQ_EINVAL, "NULL argument");
   DeviceGuard g(ctx->cfg.device);
   auto& lst = prof_list(ctx);
-  for (int i = 0; i < kStNum; ++i) { ms[i] = 0; n[i] = 0; }
+  for (int i = 0; i < kStNum; ++i) {
+    ms[i] = 0;
+    n[i] = 0;
+    if (work) work[i] = 0;
+  }
   for (auto& r : lst) {
     CK(cudaEventSynchronize(r.b), "profile event");
     float t = 0;
     cudaEventElapsedTime(&t, r.a, r.b);
     ms[r.stage] += t;
     n[r.stage] += 1;
+    if (work) work[r.stage] += r.work;
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }

@@ -60,7 +60,8 @@ struct Linear {
 enum Epi { kEpiNone = 0, kEpiRelu = 1, kEpiBetaReg = 2 };
 
 // Profiling stages (kgq_profile_* in kgq_api.cu).
-enum Stage { kStChain = 0, kStPrep = 1, kStScore = 2, kStTopk = 3, kStNum = 4 };
+// kStDense is nested inside kStChain (every dense layer of the operator chain).
+enum Stage { kStChain = 0, kStPrep = 1, kStScore = 2, kStTopk = 3, kStDense = 4, kStNum = 5 };
 
 }  // namespace kgq
 
@@ -110,6 +111,7 @@ struct kgq_ctx {
   cudaEvent_t ev[2 * kgq::kStNum] = {};
   double prof_ms[kgq::kStNum] = {};
   int64_t prof_n[kgq::kStNum] = {};
+  double prof_work[kgq::kStNum] = {};    // algorithmic work (FLOPs / lane ops) per stage
 };
 
 namespace kgq {

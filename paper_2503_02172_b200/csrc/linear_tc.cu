@@ -15,6 +15,8 @@
 //                       (+ negation) fused, split (hi/lo) or fp32 store.
 // CTA tile 128 x BN (BN = 64 or 128) x BK = 32 fp32 (one 128-byte swizzle row), 3-4 stages;
 // TMEM holds two 128 x BN partial accumulators (ping-pong between MMA and epilogue).
+#include <stdint.h>
+
 #include "tc_gemm.cuh"
 
 namespace kgq {
@@ -81,9 +83,22 @@ int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split 
                   int neg1, cudaStream_t st) {
   if (M <= 0) return 0;
   // 128-column tiles unless that leaves SMs idle
-  const int64_t tiles128 = (int64_t)((M + BM - 1) / BM) * ((L.out_f + 127) / 128);
-  if (tiles128 >= 148) return launch_bn<128>(A, M, K, L, epi, out, neg0, neg1, st);
-  return launch_bn<64>(A, M, K, L, epi, out, neg0, neg1, st);
+  // column tile: minimise waves x per-tile cost (~ BN + 64: the A tile is loaded per tile)
+  static const int kBN[4] = {32, 64, 96, 128};
+  int best = 3;
+  int64_t best_cost = INT64_MAX;
+  const int64_t mt = (M + BM - 1) / BM;
+  for (int i = 0; i < 4; ++i) {
+    const int64_t tiles = mt * ((L.out_f + kBN[i] - 1) / kBN[i]);
+    const int64_t cost = ((tiles + 147) / 148) * (kBN[i] + 64);
+    if (cost < best_cost) { best_cost = cost; best = i; }
+  }
+  switch (kBN[best]) {
+    case 32: return launch_bn<32>(A, M, K, L, epi, out, neg0, neg1, st);
+    case 64: return launch_bn<64>(A, M, K, L, epi, out, neg0, neg1, st);
+    case 96: return launch_bn<96>(A, M, K, L, epi, out, neg0, neg1, st);
+    default: return launch_bn<128>(A, M, K, L, epi, out, neg0, neg1, st);
+  }
 }
 
 }  // namespace kgq

@@ -81,6 +81,19 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
   asm volatile(
@@ -100,10 +113,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 template <int BN>
 struct Smem {
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
   static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
   static constexpr int W_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;
-  static constexpr int STAGES = BN == 128 ? 3 : 4;  // <= 227 KB of shared memory
+  static constexpr int STAGES = BN > 96 ? 3 : 4;  // <= 227 KB of shared memory
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
   static_assert(TOTAL <= 227 * 1024, "shared memory budget");
@@ -138,7 +152,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(accempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;  // M fastest: W tiles shared in time
   const int nk = (K + BK - 1) / BK;
   const int ng = (nk + DRAIN - 1) / DRAIN;
 
@@ -160,7 +174,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) {  // two TMEM partial accumulators: 128 lanes x 2*BN fp32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "n"(2 * BN));
+                 "n"(L::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
@@ -224,12 +238,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int a = g & 1;
       mbar_wait(&accfull[a], (g >> 1) & 1);
       fence_after();
+      const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + ch);
 #pragma unroll
-      for (int c = 0; c < CW; c += 32) {
+      for (int c = 0; c + 32 <= CW; c += 32) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + ch + c), v);
+        tmem_ld32(tq + c, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) acc[c + i] += v[i];
+      }
+      if constexpr (CW % 32 == 16) {
+        float v[16];
+        tmem_ld16(tq + CW - 16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[CW - 16 + i] += v[i];
       }
       fence_before();
       __syncwarp();
@@ -241,7 +262,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(L::TMEM_COLS));
   }
 }
 
@@ -305,7 +326,7 @@ int launch_tc_gemm(const Split& A, int M, const float* Wh, const float* Wl, int 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL);
     attr = true;
   }
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN);
   kern<<<grid, THREADS, Smem<BN>::TOTAL, st>>>(mAh, mAl, mWh, mWl, M, N, K, epi);
   return 1;
 }

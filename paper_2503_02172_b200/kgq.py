@@ -27,7 +27,7 @@ STATUS = {0: "KGQ_OK", 1: "KGQ_EINVAL", 2: "KGQ_ERANGE", 3: "KGQ_EUNSUPPORTED",
 LAYER_PROJ_OUT, LAYER_PROJ_HIDDEN = 0, 1
 LAYER_INTER_1, LAYER_INTER_2, LAYER_OFFSET_1, LAYER_OFFSET_2 = 16, 17, 18, 19
 REL_MAIN, REL_OFFSET = 0, 1
-STAGES = ("chain", "prep", "score", "topk")
+STAGES = ("chain", "prep", "score", "topk", "dense")
 
 # Every symbol include/kgq.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -80,7 +80,8 @@ _sig = {
     "kgq_last_launch_count": (_I32, [_P]),
     "kgq_entity_terms": (_I32, [_P, _P, _P]),
     "kgq_profile_enable": (_I32, [_P, _I32]),
-    "kgq_profile_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
+    "kgq_profile_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
+                              ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -277,7 +278,10 @@ class Engine:
         self._check(_lib.kgq_profile_enable(self._h, 1 if on else 0))
 
     def profile_read(self):
-        ms = (ctypes.c_double * 4)()
-        n = (_I64 * 4)()
-        self._check(_lib.kgq_profile_read(self._h, ms, n))
-        return {STAGES[i]: (ms[i], n[i]) for i in range(4)}
+        """{stage: (device ms, timed regions, algorithmic work)} since the last read."""
+        k = len(STAGES)
+        ms = (ctypes.c_double * k)()
+        n = (_I64 * k)()
+        w = (ctypes.c_double * k)()
+        self._check(_lib.kgq_profile_read(self._h, ms, n, w))
+        return {STAGES[i]: (ms[i], n[i], w[i]) for i in range(k)}
