@@ -32,24 +32,34 @@ struct EpiLinear {
   const float* bias;
   Split out;
   int M, N, neg0, neg1;
-  __device__ __forceinline__ void apply(int row, int n0, const float (&acc)[CW]) const {
-    if (row >= M) return;
+  __device__ __forceinline__ void apply(int row0, int lane, int n0, const float (&acc)[CW],
+                                        float* stage) const {
+    const int row = row0 + lane;
     const bool neg = row >= neg0 && row < neg1;
-    const int64_t o = (int64_t)row * out.ld + n0;
 #pragma unroll
     for (int i = 0; i < CW; ++i) {
       const int n = n0 + i;
-      if (n < N) {
-        float y = acc[i] + bias[n];
-        if (EPI == kEpiRelu) y = fmaxf(y, 0.0f);
-        if (EPI == kEpiBetaReg) {
-          y = beta_reg(y);
-          if (neg) y = 1.0f / y;
-        }
+      float y = acc[i] + (n < N ? bias[n] : 0.0f);
+      if (EPI == kEpiRelu) y = fmaxf(y, 0.0f);
+      if (EPI == kEpiBetaReg) {
+        y = beta_reg(y);
+        if (neg) y = 1.0f / y;
+      }
+      stage[lane * (CW + 1) + i] = y;
+    }
+    __syncwarp();
+    for (int r = 0; r < 32; ++r) {  // row by row: lanes write consecutive columns
+      const int rr = row0 + r;
+      if (rr >= M) break;
+      const int64_t o = (int64_t)rr * out.ld + n0;
+#pragma unroll
+      for (int c = lane; c < CW; c += 32) {
+        if (n0 + c >= N) break;
+        const float y = stage[r * (CW + 1) + c];
         if (SPLIT)
-          store_split(out.hi, out.lo, o + i, y);
+          store_split(out.hi, out.lo, o + c, y);
         else
-          out.hi[o + i] = y;
+          out.hi[o + c] = y;
       }
     }
   }
@@ -83,22 +93,9 @@ int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split 
                   int neg1, cudaStream_t st) {
   if (M <= 0) return 0;
   // 128-column tiles unless that leaves SMs idle
-  // column tile: minimise waves x per-tile cost (~ BN + 64: the A tile is loaded per tile)
-  static const int kBN[4] = {32, 64, 96, 128};
-  int best = 3;
-  int64_t best_cost = INT64_MAX;
-  const int64_t mt = (M + BM - 1) / BM;
-  for (int i = 0; i < 4; ++i) {
-    const int64_t tiles = mt * ((L.out_f + kBN[i] - 1) / kBN[i]);
-    const int64_t cost = ((tiles + 147) / 148) * (kBN[i] + 64);
-    if (cost < best_cost) { best_cost = cost; best = i; }
-  }
-  switch (kBN[best]) {
-    case 32: return launch_bn<32>(A, M, K, L, epi, out, neg0, neg1, st);
-    case 64: return launch_bn<64>(A, M, K, L, epi, out, neg0, neg1, st);
-    case 96: return launch_bn<96>(A, M, K, L, epi, out, neg0, neg1, st);
-    default: return launch_bn<128>(A, M, K, L, epi, out, neg0, neg1, st);
-  }
+  return tc::dispatch_bn(tc::choose_bn(M, L.out_f), [&](auto bn) {
+    return launch_bn<decltype(bn)::value>(A, M, K, L, epi, out, neg0, neg1, st);
+  });
 }
 
 }  // namespace kgq

@@ -12,8 +12,8 @@
 // Centring keeps its terms ~0.1 (|u|, |v| << |U|, |V| ~ 1), so the fp32 partial sums carry
 // ~1e-7 of sum|terms| ~ 1e-5 absolute instead of ~1e-4 for the uncentred sum, and the large,
 // cancelling P_q + E_e (~ +-800 at d = 400) are added in fp64 in the epilogue.  DNF union:
-// rows are (b, branch) = 2b + br, so the two branches of a query sit in adjacent lanes and the
-// min is one shuffle.
+// rows are (b, branch) = 2b + br, so the two branches of a query are adjacent rows of the
+// epilogue's staged tile and the min is taken while writing dist rows.
 #include "tc_gemm.cuh"
 
 namespace kgq {
@@ -103,19 +103,26 @@ struct EpiBetaScore {
   float* dist;      // [rows / NB, ldd]
   int64_t ldd;
   int rows;
-  __device__ __forceinline__ void apply(int row, int n0, const float (&acc)[CW]) const {
+  int64_t ncols;    // np: the last column tile may overhang it
+  __device__ __forceinline__ void apply(int row0, int lane, int n0, const float (&acc)[CW],
+                                        float* stage) const {
+    const int row = row0 + lane;
     const double p = row < rows ? P[row] : 0.0;
-    const bool store = row < rows && (NB == 1 || (row & 1) == 0);
-    float* drow = dist + (int64_t)(row / NB) * ldd + n0;
 #pragma unroll
-    for (int i = 0; i < CW; i += 4) {
-      float o[4];
+    for (int i = 0; i < CW; ++i)
+      stage[lane * (CW + 1) + i] = n0 + i < ncols ? (float)(p + E[n0 + i] + (double)acc[i]) : 0.0f;
+    __syncwarp();
+    for (int r = 0; r < 32; r += NB) {  // (b, branch) rows 2b, 2b+1 -> min; coalesced rows of dist
+      const int rr = row0 + r;
+      if (rr >= rows) break;
+      float* drow = dist + (int64_t)(rr / NB) * ldd + n0;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        o[t] = (float)(p + E[n0 + i + t] + (double)acc[i + t]);
-        if (NB == 2) o[t] = fminf(o[t], __shfl_xor_sync(0xffffffffu, o[t], 1));
+      for (int c = lane; c < CW; c += 32) {
+        if (n0 + c >= ncols) break;
+        float v = stage[r * (CW + 1) + c];
+        if (NB == 2) v = fminf(v, stage[(r + 1) * (CW + 1) + c]);
+        drow[c] = v;
       }
-      if (store) *reinterpret_cast<float4*>(drow + i) = make_float4(o[0], o[1], o[2], o[3]);
     }
   }
 };
@@ -136,17 +143,16 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
                           Split A, double* P, const float* uv_hi, const float* uv_lo, const double* Esum,
                           int64_t np, float* dist, int64_t ldd, cudaStream_t st) {
-  constexpr int BN = 128;
   k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
-  int L = 1;
-  if (nbq == 2) {
-    EpiBetaScore<BN / 2, 2> e{P, Esum, dist, ldd, rows};
-    L += tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
-  } else {
-    EpiBetaScore<BN / 2, 1> e{P, Esum, dist, ldd, rows};
-    L += tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
-  }
-  return L;
+  return 1 + tc::dispatch_bn(tc::choose_bn(rows, np), [&](auto bnc) {
+    constexpr int BN = decltype(bnc)::value;
+    if (nbq == 2) {
+      EpiBetaScore<BN / 2, 2> e{P, Esum, dist, ldd, rows, np};
+      return tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
+    }
+    EpiBetaScore<BN / 2, 1> e{P, Esum, dist, ldd, rows, np};
+    return tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
+  });
 }
 
 }  // namespace kgq

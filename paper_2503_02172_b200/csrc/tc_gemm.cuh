@@ -7,6 +7,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kgq_internal.cuh"
@@ -113,14 +114,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 template <int BN>
 struct Smem {
-  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
   static constexpr int W_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;
-  static constexpr int STAGES = BN > 96 ? 3 : 4;  // <= 227 KB of shared memory
+  static constexpr int FIT = (227 * 1024 - 2048) / STAGE_BYTES;  // stages that fit in 227 KB
+  static constexpr int STAGES = FIT > 4 ? 4 : FIT;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
   static_assert(TOTAL <= 227 * 1024, "shared memory budget");
+  static_assert(EPI_WARPS * 32 * (BN / 2 + 1) * 4 <= STAGES * STAGE_BYTES, "epilogue staging fits");
 };
 
 // K-blocks per tensor-core partial sum.  The TMEM accumulate path truncates (measured: bias
@@ -135,7 +138,9 @@ constexpr int DRAIN = KGQ_TC_DRAIN;
 // Generic 3xTF32 GEMM acc[m, n] = sum_k A[m, k] W[n, k] over a 128 x BN tile; the epilogue
 // policy Epi receives each epilogue thread's row and its BN fp32 sums (all 128 rows of the
 // tile, including rows >= M, so that policies may shuffle between lanes).  Each epilogue warp
-// owns 32 rows (its TMEM lane quarter) and BN/2 columns, so Epi::apply sees acc[BN/2].
+// owns 32 rows (its TMEM lane quarter) and BN/2 columns: Epi::apply(row0, lane, n0, acc, stage)
+// gets that warp's first row, the thread's lane (row row0 + lane), its BN/2 sums and a
+// 32 x (BN/2 + 1) fp32 shared-memory staging tile for coalesced row stores.
 template <int BN, class Epi>
 __global__ void __launch_bounds__(THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
@@ -189,11 +194,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
         uint8_t* st = smem + s * L::STAGE_BYTES;
+#ifdef KGQ_TC_DBG_NO_TMA  // perf probe only (scripts/tc_perf.cu): skip the loads
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        (void)st;
+#else
         mbar_expect_tx(&full[s], L::STAGE_BYTES);
         tma_load_2d(st, &mAh, &full[s], kb * BK, m0);
         tma_load_2d(st + L::A_BYTES, &mAl, &full[s], kb * BK, m0);
         tma_load_2d(st + 2 * L::A_BYTES, &mWh, &full[s], kb * BK, n0);
         tma_load_2d(st + 2 * L::A_BYTES + L::W_BYTES, &mWl, &full[s], kb * BK, n0);
+#endif
       }
     }
   } else if (warp == 1) {
@@ -213,6 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
         const uint32_t ah = st, al = st + L::A_BYTES;
         const uint32_t wh = st + 2 * L::A_BYTES, wl = wh + L::W_BYTES;
+#ifndef KGQ_TC_DBG_NO_MMA  // perf probe only (scripts/tc_perf.cu): skip the MMAs
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 32 bytes per MMA along K
           const uint32_t off = kk * 32;
@@ -221,6 +232,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_tf32(d, umma_desc_sw128(al + off), umma_desc_sw128(wh + off), idesc, 1u);
           mma_tf32(d, umma_desc_sw128(ah + off), umma_desc_sw128(wh + off), idesc, 1u);
         }
+#else
+        (void)d; (void)ah; (void)al; (void)wh; (void)wl; (void)idesc; (void)first;
+#endif
         mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         if ((kb % DRAIN) == DRAIN - 1 || kb == nk - 1) mma_commit(&accfull[a]);
       }
@@ -256,7 +270,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accempty[a])) : "memory");
     }
-    epi.apply(row, n0 + ch, acc);
+    // every MMA has completed (last accfull), so the pipeline buffers are free: each epilogue
+    // warp stages its 32 x CW tile there and writes rows coalesced (Epi::apply)
+    float* stage = reinterpret_cast<float*>(smem) + (warp - 2) * 32 * (CW + 1);
+    epi.apply(m0 + q * 32, lane, n0 + ch, acc, stage);
   }
   fence_before();
   __syncthreads();
@@ -304,12 +321,48 @@ inline bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t col
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return false;
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "libkgq: cuTensorMapEncodeTiled(rows %lld, cols %lld, ld %lld, box %d) = %d\n", (long long)rows,
+            (long long)cols, (long long)ld, box_rows, (int)r);
+    return false;
+  }
   if (cache.size() > 4096) cache.clear();
   cache.emplace(key, *m);
   return true;
 }
 
+
+// Column-tile width: the mainloop is bound by the L2 -> SMEM operand stream, (128 + BN) x 256 B
+// per K-block for a 128 x BN tile, so a tile costs ~ (128 + BN) and a launch ~ waves x that.
+constexpr int kTileBN[7] = {32, 64, 96, 128, 160, 192, 256};
+inline int choose_bn(int64_t M, int64_t N) {
+  const int64_t mt = (M + BM - 1) / BM;
+  int best = 0;
+  int64_t best_cost = INT64_MAX;
+  for (int i = 0; i < 7; ++i) {
+    const int64_t tiles = mt * ((N + kTileBN[i] - 1) / kTileBN[i]);
+    const int64_t cost = ((tiles + 147) / 148) * (128 + kTileBN[i]);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = i;
+    }
+  }
+  return kTileBN[best];
+}
+
+// Calls f(std::integral_constant<int, BN>{}) for the chosen tile width.
+template <class F>
+int dispatch_bn(int bn, F&& f) {
+  switch (bn) {
+    case 32: return f(std::integral_constant<int, 32>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 96: return f(std::integral_constant<int, 96>{});
+    case 128: return f(std::integral_constant<int, 128>{});
+    case 160: return f(std::integral_constant<int, 160>{});
+    case 192: return f(std::integral_constant<int, 192>{});
+    default: return f(std::integral_constant<int, 256>{});
+  }
+}
 
 template <int BN, class Epi>
 int launch_tc_gemm(const Split& A, int M, const float* Wh, const float* Wl, int N, int64_t ldw, int K,
