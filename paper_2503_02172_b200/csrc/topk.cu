@@ -4,10 +4,8 @@
 // Distances map to order-preserving uint32 keys (NaN -> max, -0 -> +0), so (key, id) packed
 // in a uint64 sorts exactly in that order.
 //
-// k_topk: one CTA per query row.  Radix select (4 passes of 8-bit digits over the row) finds
-// the k-th smallest key T and how many of the T-ties to keep; a compaction pass collects the
-// keys < T (any order) and the first ties by ascending index (block-wide ordered scan); a
-// bitonic sort of the <= 256 survivors gives the final order.
+// k_topk: one CTA per query row (or per 16k-entry chunk of a long row, the chunks then merged
+// by k_merge); warp select with per-warp thresholds (see the kernel).
 #include <stdint.h>
 
 #include "common.cuh"
@@ -45,131 +43,159 @@ __device__ void bitonic_sort_u64(unsigned long long* v, int P) {
 }
 
 constexpr int kTopkThreads = 256;
-constexpr int64_t kTopkChunkMin = 16384;  // entries per CTA when a row is split
+constexpr int64_t kTopkStage = 16384;  // entries per CTA when a row is split
 
+// Warp-cooperative ascending bitonic sort of P (power of two, >= 64) uint64 in shared memory.
+__device__ __forceinline__ void warp_bitonic_sort(unsigned long long* v, int P) {
+  const int lane = threadIdx.x & 31;
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < P / 2; i += 32) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const unsigned long long a = v[lo], b = v[hi];
+        if ((a > b) == up) {
+          v[lo] = b;
+          v[hi] = a;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// k_topk: CTA (b, c) selects the k best (distance, index) of row b restricted to
+// [c*chunk, min(n, (c+1)*chunk)) and writes them at [(c*B + b)*k, ...).  With one chunk that is
+// the final [B, k] answer; with several it is the candidate list k_merge reduces.
+// Warp select: each warp streams a contiguous slice of the chunk with coalesced loads, keeps
+// its k best packed keys (key << 32 | index: a strict total order = distance, then id) in
+// shared memory, and only elements below its current k-th best go to a 32-entry buffer; a
+// full buffer is merged by a warp bitonic sort.  In random order that is ~k ln(n/k) buffer
+// entries per warp, so almost every element costs one load and one compare.  The warps' lists
+// are then merged by one block-wide bitonic sort.
 __global__ void __launch_bounds__(kTopkThreads)
     k_topk(const float* __restrict__ dist, int64_t ldd, int64_t n_total, int64_t chunk, int k,
            int64_t id_base, const int32_t* __restrict__ invalid, float* __restrict__ od,
-           int32_t* __restrict__ oi, int B) {
-  // CTA (b, c) selects the k best of row b restricted to [c*chunk, min(n, (c+1)*chunk)) and
-  // writes them at [(c*B + b)*k, ...): with one chunk that is the final [B, k] answer, with
-  // several it is the candidate list k_merge reduces (multi-CTA top-k for long rows).
+           int32_t* __restrict__ oi, int B, int P) {
+  extern __shared__ unsigned long long wl[];  // [warps][P] lists, then the block merge area
   const int b = blockIdx.x;
   const int64_t c0 = (int64_t)blockIdx.y * chunk;
   const int64_t n = (n_total - c0 < chunk ? n_total - c0 : chunk);
   const float* row = dist + (int64_t)b * ldd + c0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int W = kTopkThreads / 32;
   od += ((int64_t)blockIdx.y * B + b) * k;
   oi += ((int64_t)blockIdx.y * B + b) * k;
-  const int kout = k;
-  k = (int)(n < k ? n : k);  // a short last chunk contributes all of its entries
   if (invalid && invalid[b]) {
-    for (int j = tid; j < kout; j += blockDim.x) {
+    for (int j = tid; j < k; j += blockDim.x) {
       od[j] = __uint_as_float(0x7FFFFFFFu);
       oi[j] = -1;
     }
     return;
   }
-  __shared__ uint32_t hist[256];
-  __shared__ uint32_t s_prefix, s_kk;
-  __shared__ unsigned long long sel[kMaxK];
-  __shared__ int s_less;
-  __shared__ int s_wsum[kTopkThreads / 32];
-
-  uint32_t prefix = 0, mask = 0, kk = (uint32_t)k;
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
-    hist[tid] = 0;
-    __syncthreads();
-    for (int64_t i = tid; i < n; i += blockDim.x) {
-      const uint32_t key = fkey(row[i]);
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    if (wid == 0) {
-      // lane owns bins [8*lane, 8*lane+8)
-      uint32_t c[8], s = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = hist[lane * 8 + j];
-        s += c[j];
-      }
-      uint32_t incl = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      uint32_t before = incl - s;
-      // the lane whose range contains the kk-th element
-      const bool mine = before < kk && kk <= incl;
-      if (mine) {
-        uint32_t cum = before;
-        for (int j = 0; j < 8; ++j) {
-          if (cum + c[j] >= kk) {
-            s_prefix = prefix | ((uint32_t)(lane * 8 + j) << shift);
-            s_kk = kk - cum;
-            break;
-          }
-          cum += c[j];
-        }
+  unsigned long long* lst = wl + wid * P;  // [0, k) sorted best, [k, k+32) buffer, rest max
+  for (int j = lane; j < P; j += 32) lst[j] = ~0ull;
+  __syncwarp();
+  unsigned long long tau = ~0ull;  // current k-th best of this warp
+  int cnt = 0;
+  auto merge = [&]() {
+    warp_bitonic_sort(lst, P);
+    for (int j = k + lane; j < P; j += 32) lst[j] = ~0ull;
+    __syncwarp();
+    tau = lst[k - 1];
+    cnt = 0;
+  };
+  constexpr int U = 8;  // loads in flight per lane (the loop is latency-bound otherwise)
+  const int64_t per = ((n + W - 1) / W + 32 * U - 1) / (32 * U) * (32 * U);
+  const int64_t w0 = (int64_t)wid * per, w1 = (w0 + per < n ? w0 + per : n);
+  // seed the list with the warp's first 32 elements, sorted in registers, so the threshold
+  // starts at their k-th best instead of +inf (saves the merges of the first pass)
+  int64_t start = w0;
+  if (k <= 32 && w0 < w1) {
+    const int64_t i = w0 + lane;
+    unsigned long long v = i < w1 ? (((unsigned long long)fkey(row[i]) << 32) | (uint32_t)i) : ~0ull;
+    for (int size = 2; size <= 32; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, stride);
+        const bool up = ((lane & size) == 0);
+        const bool lower = (lane & stride) == 0;
+        v = (lower == up) ? (v < o ? v : o) : (v > o ? v : o);
       }
     }
-    __syncthreads();
-    prefix = s_prefix;
-    kk = s_kk;
-    mask |= 255u << shift;
-    __syncthreads();
+    if (lane < k) lst[lane] = v;
+    __syncwarp();
+    tau = lst[k - 1];
+    start = w0 + 32;
   }
-  const uint32_t T = prefix;  // key of the k-th smallest; keep kk of its ties
-  const int n_less = k - (int)kk;
-  if (tid == 0) s_less = 0;
-  __syncthreads();
-  uint32_t eq_before = 0;
-  for (int64_t base = 0; base < n; base += blockDim.x) {
-    const int64_t i = base + tid;
-    const uint32_t key = i < n ? fkey(row[i]) : 0xFFFFFFFFu;
-    if (i < n && key < T) {
-      const int pos = atomicAdd(&s_less, 1);
-      sel[pos] = ((unsigned long long)key << 32) | (uint32_t)i;
+  for (int64_t base = start; base < w1; base += 32 * U) {
+    float x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 32 + lane;
+      x[u] = i < w1 ? row[i] : 0.0f;
     }
-    const bool eq = i < n && key == T;
-    const uint32_t bal = __ballot_sync(0xffffffffu, eq);
-    if (lane == 0) s_wsum[wid] = __popc(bal);
-    __syncthreads();
-    uint32_t off = 0, tot = 0;
-    for (int w = 0; w < kTopkThreads / 32; ++w) {
-      if (w < wid) off += s_wsum[w];
-      tot += s_wsum[w];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 32 + lane;
+      const unsigned long long v =
+          i < w1 ? (((unsigned long long)fkey(x[u]) << 32) | (uint32_t)i) : ~0ull;
+      const bool q = v < tau;
+      const unsigned m = __ballot_sync(0xffffffffu, q);
+      if (m) {
+        const int add = __popc(m);
+        if (cnt + add > 32) merge();
+        if (q) lst[k + cnt + __popc(m & ((1u << lane) - 1u))] = v;
+        __syncwarp();
+        cnt += add;
+        if (cnt == 32) merge();
+      }
     }
-    const uint32_t rank = eq_before + off + __popc(bal & ((1u << lane) - 1u));
-    if (eq && rank < kk) sel[n_less + rank] = ((unsigned long long)key << 32) | (uint32_t)i;
-    eq_before += tot;
-    __syncthreads();
   }
-  int P = 1;
-  while (P < k) P <<= 1;
-  for (int j = k + tid; j < P; j += blockDim.x) sel[j] = ~0ull;
+  if (cnt) merge();
   __syncthreads();
-  bitonic_sort_u64(sel, P);
-  for (int j = tid; j < kout; j += blockDim.x) {
-    if (j < k) {
-      const unsigned long long v = sel[j];
-      od[j] = fkey_inv((uint32_t)(v >> 32));
-      oi[j] = (int32_t)(id_base + c0 + (int64_t)(uint32_t)(v & 0xFFFFFFFFu));
-    } else {  // padding of a short chunk: sorts last in k_merge
+  // block merge of the W warp lists (k each)
+  unsigned long long* all = wl + W * P;
+  int Q = 1;
+  while (Q < W * k) Q <<= 1;
+  for (int j = tid; j < Q; j += blockDim.x) all[j] = j < W * k ? wl[(j / k) * P + (j % k)] : ~0ull;
+  __syncthreads();
+  bitonic_sort_u64(all, Q);
+  for (int j = tid; j < k; j += blockDim.x) {
+    const unsigned long long v = all[j];
+    const uint32_t key = (uint32_t)(v >> 32);
+    if (v == ~0ull) {  // fewer than k entries in a short chunk: padding sorts last in k_merge
       od[j] = __uint_as_float(0x7FFFFFFFu);
       oi[j] = -1;
+    } else {
+      od[j] = fkey_inv(key);
+      oi[j] = (int32_t)(id_base + c0 + (int64_t)(uint32_t)(v & 0xFFFFFFFFu));
     }
   }
 }
 
 int64_t topk_chunk(int64_t n, int k) {
   // long rows are split so that many CTAs share a query; chunks * k must fit k_merge (4096)
-  if (n <= kTopkChunkMin * 2) return n;
-  int64_t c = kTopkChunkMin;
+  if (n <= kTopkStage * 2) return n;
+  int64_t c = kTopkStage;
   while ((n + c - 1) / c * k > 4096) c *= 2;
   return c;
+}
+
+void launch_topk_kernel(dim3 grid, const float* dist, int64_t ldd, int64_t n, int64_t chunk, int k,
+                        int64_t id_base, const int32_t* invalid, float* od, int32_t* oi, int B,
+                        cudaStream_t st) {
+  int P = 64;
+  while (P < k + 32) P <<= 1;
+  int Q = 1;
+  while (Q < (kTopkThreads / 32) * k) Q <<= 1;
+  const int smem = (int)(((kTopkThreads / 32) * P + Q) * sizeof(unsigned long long));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  k_topk<<<grid, kTopkThreads, smem, st>>>(dist, ldd, n, chunk, k, id_base, invalid, od, oi, B, P);
 }
 
 int launch_topk(const float* dist, int64_t ldd, int B, int64_t n, int k, int64_t id_base,
@@ -178,10 +204,10 @@ int launch_topk(const float* dist, int64_t ldd, int B, int64_t n, int k, int64_t
   const int64_t chunk = topk_chunk(n, k);
   const int nch = (int)((n + chunk - 1) / chunk);
   if (nch == 1) {
-    k_topk<<<dim3(B, 1), kTopkThreads, 0, st>>>(dist, ldd, n, n, k, id_base, invalid, out_d, out_i, B);
+    launch_topk_kernel(dim3(B, 1), dist, ldd, n, n, k, id_base, invalid, out_d, out_i, B, st);
     return 1;
   }
-  k_topk<<<dim3(B, nch), kTopkThreads, 0, st>>>(dist, ldd, n, chunk, k, id_base, invalid, tmp_d, tmp_i, B);
+  launch_topk_kernel(dim3(B, nch), dist, ldd, n, chunk, k, id_base, invalid, tmp_d, tmp_i, B, st);
   return 1 + launch_merge(nch, B, k, tmp_d, tmp_i, out_d, out_i, st);
 }
 
