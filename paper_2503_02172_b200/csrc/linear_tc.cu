@@ -65,37 +65,30 @@ struct EpiLinear {
   }
 };
 
-template <int BN, int EPI, bool SPLIT>
-int launch_cfg(const Split& A, int M, int K, const Linear& L, Split out, int neg0, int neg1,
+template <int EPI, bool SPLIT>
+int launch_epi(const Split& A, int M, int K, const Linear& L, Split out, int neg0, int neg1,
                cudaStream_t st) {
-  EpiLinear<BN / 2, EPI, SPLIT> e{L.b, out, M, L.out_f, neg0, neg1};
-  return launch_tc_gemm<BN>(A, M, L.W_hi, L.W_lo, L.out_f, L.in_f, K, e, st);
-}
-template <int BN>
-int launch_bn(const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
-              int neg1, cudaStream_t st) {
-  const bool split = out.lo != nullptr;
-  switch (epi) {
-    case kEpiRelu:
-      return split ? launch_cfg<BN, kEpiRelu, true>(A, M, K, L, out, neg0, neg1, st)
-                   : launch_cfg<BN, kEpiRelu, false>(A, M, K, L, out, neg0, neg1, st);
-    case kEpiBetaReg:
-      return split ? launch_cfg<BN, kEpiBetaReg, true>(A, M, K, L, out, neg0, neg1, st)
-                   : launch_cfg<BN, kEpiBetaReg, false>(A, M, K, L, out, neg0, neg1, st);
-    default:
-      return split ? launch_cfg<BN, kEpiNone, true>(A, M, K, L, out, neg0, neg1, st)
-                   : launch_cfg<BN, kEpiNone, false>(A, M, K, L, out, neg0, neg1, st);
-  }
+  return tc::launch_gemm_auto(A, M, L.W_hi, L.W_lo, L.out_f, L.in_f, K, [&](auto cw) {
+    return EpiLinear<decltype(cw)::value, EPI, SPLIT>{L.b, out, M, L.out_f, neg0, neg1};
+  }, st);
 }
 }  // namespace
 
 int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
                   int neg1, cudaStream_t st) {
   if (M <= 0) return 0;
-  // 128-column tiles unless that leaves SMs idle
-  return tc::dispatch_bn(tc::choose_bn(M, L.out_f), [&](auto bn) {
-    return launch_bn<decltype(bn)::value>(A, M, K, L, epi, out, neg0, neg1, st);
-  });
+  const bool split = out.lo != nullptr;
+  switch (epi) {
+    case kEpiRelu:
+      return split ? launch_epi<kEpiRelu, true>(A, M, K, L, out, neg0, neg1, st)
+                   : launch_epi<kEpiRelu, false>(A, M, K, L, out, neg0, neg1, st);
+    case kEpiBetaReg:
+      return split ? launch_epi<kEpiBetaReg, true>(A, M, K, L, out, neg0, neg1, st)
+                   : launch_epi<kEpiBetaReg, false>(A, M, K, L, out, neg0, neg1, st);
+    default:
+      return split ? launch_epi<kEpiNone, true>(A, M, K, L, out, neg0, neg1, st)
+                   : launch_epi<kEpiNone, false>(A, M, K, L, out, neg0, neg1, st);
+  }
 }
 
 }  // namespace kgq

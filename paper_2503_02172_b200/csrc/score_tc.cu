@@ -144,15 +144,13 @@ int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double
                           Split A, double* P, const float* uv_hi, const float* uv_lo, const double* Esum,
                           int64_t np, float* dist, int64_t ldd, cudaStream_t st) {
   k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
-  return 1 + tc::dispatch_bn(tc::choose_bn(rows, np), [&](auto bnc) {
-    constexpr int BN = decltype(bnc)::value;
-    if (nbq == 2) {
-      EpiBetaScore<BN / 2, 2> e{P, Esum, dist, ldd, rows, np};
-      return tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
-    }
-    EpiBetaScore<BN / 2, 1> e{P, Esum, dist, ldd, rows, np};
-    return tc::launch_tc_gemm<BN>(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, e, st);
-  });
+  if (nbq == 2)
+    return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, [&](auto cw) {
+      return EpiBetaScore<decltype(cw)::value, 2>{P, Esum, dist, ldd, rows, np};
+    }, st);
+  return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, [&](auto cw) {
+    return EpiBetaScore<decltype(cw)::value, 1>{P, Esum, dist, ldd, rows, np};
+  }, st);
 }
 
 }  // namespace kgq

@@ -11,7 +11,7 @@ using namespace kgq;
 
 int main() {
   struct Shape { int M, N, K; };
-  for (Shape sh : {Shape{1024, 1600, 1200}, Shape{2048, 1600, 1600}, Shape{1024, 800, 1600}, Shape{3072, 1600, 1600}}) {
+  for (Shape sh : {Shape{1024, 1600, 1200}, Shape{2048, 1600, 1600}, Shape{1024, 800, 1600}, Shape{3072, 1600, 1600}, Shape{1024, 1600, 1600}, Shape{2048, 800, 1600}, Shape{2048, 800, 800}, Shape{2048, 400, 800}, Shape{1024, 14592, 800}, Shape{2048, 14592, 800}, Shape{4096, 14976, 800}}) {
     const int M = sh.M, N = sh.N, K = sh.K;
     float *x, *xh, *xl, *w, *wh, *wl, *b, *y;
     cudaMalloc(&x, (size_t)M * K * 4); cudaMalloc(&xh, (size_t)M * K * 4); cudaMalloc(&xl, (size_t)M * K * 4);
@@ -22,28 +22,33 @@ int main() {
     launch_split_copy(w, (int64_t)N * K, wh, wl, 0);
     Linear L; L.W = w; L.W_hi = wh; L.W_lo = wl; L.b = b; L.out_f = N; L.in_f = K;
     Split out{y, y + (size_t)M * N, N};
-    auto run = [&](int bn) {
-      switch (bn) {
-        case 64: launch_bn<64>(Split{xh, xl, K}, M, K, L, kEpiRelu, out, 0, 0, 0); break;
-        case 128: launch_bn<128>(Split{xh, xl, K}, M, K, L, kEpiRelu, out, 0, 0, 0); break;
-        case 256: launch_bn<256>(Split{xh, xl, K}, M, K, L, kEpiRelu, out, 0, 0, 0); break;
-        default: launch_linear(Split{xh, xl, K}, M, K, L, kEpiRelu, out, 0, 0, 0);
-      }
-    };
-    for (int bn : {0, 64, 128, 256}) {
-      for (int i = 0; i < 3; ++i) run(bn);
+    Split A{xh, xl, K};
+    auto time_it = [&](auto launch) {
+      for (int i = 0; i < 3; ++i) launch();
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaEventRecord(e0);
       const int reps = 20;
-      for (int i = 0; i < reps; ++i) run(bn);
+      for (int i = 0; i < reps; ++i) launch();
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      const double t = ms / reps;
-      const int64_t ctas = (int64_t)((M + 127) / 128) * ((N + (bn ? bn : 96) - 1) / (bn ? bn : 96));
-      printf("M=%5d N=%5d K=%5d BN=%3d (%4lld CTAs) %8.1f us  %7.1f TFLOP/s (useful fp32)  err=%s\n", M, N, K, bn,
-             (long long)ctas, t * 1e3, 2.0 * M * N * K / (t * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+      return ms / reps * 1e3;  // us
+    };
+    printf("M=%5d N=%5d K=%5d |", M, N, K);
+    for (int bn : {32, 64, 96, 128, 160, 192, 256}) {
+      const double us = tc::dispatch_bn(bn, [&](auto c) {
+        constexpr int B = decltype(c)::value;
+        return (int)(100 * time_it([&] { tc::launch_tc_gemm<B>(A, M, wh, wl, N, K, K, EpiLinear<B / 2, kEpiRelu, true>{b, out, M, N, 0, 0}, 0); }));
+      }) / 100.0;
+      printf(" 1x%d:%.1f", bn, us);
     }
+    printf(" |");
+    printf(" 2x64:%.1f", time_it([&] { tc::launch_tc_gemm2<64>(A, M, wh, wl, N, K, K, EpiLinear<32, kEpiRelu, true>{b, out, M, N, 0, 0}, 0); }));
+    printf(" 2x128:%.1f", time_it([&] { tc::launch_tc_gemm2<128>(A, M, wh, wl, N, K, K, EpiLinear<64, kEpiRelu, true>{b, out, M, N, 0, 0}, 0); }));
+    printf(" 2x192:%.1f", time_it([&] { tc::launch_tc_gemm2<192>(A, M, wh, wl, N, K, K, EpiLinear<96, kEpiRelu, true>{b, out, M, N, 0, 0}, 0); }));
+    printf(" 2x224:%.1f", time_it([&] { tc::launch_tc_gemm2<224>(A, M, wh, wl, N, K, K, EpiLinear<112, kEpiRelu, true>{b, out, M, N, 0, 0}, 0); }));
+    printf(" 2x256:%.1f", time_it([&] { tc::launch_tc_gemm2<256>(A, M, wh, wl, N, K, K, EpiLinear<128, kEpiRelu, true>{b, out, M, N, 0, 0}, 0); }));
+    printf(" | auto:%.1f\n", time_it([&] { launch_linear(A, M, K, L, kEpiRelu, out, 0, 0, 0); }));
     cudaFree(x); cudaFree(xh); cudaFree(xl); cudaFree(w); cudaFree(wh); cudaFree(wl); cudaFree(b); cudaFree(y);
   }
   return 0;
