@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -105,18 +106,6 @@ struct DeviceGuard {
 };
 
 // ---- profiling (CUDA events on the launching stream) ------------------------------------
-struct ProfRec {
-  int stage;
-  cudaEvent_t a, b;
-  double work;
-};
-std::vector<ProfRec>& prof_list(kgq_ctx* ctx) {
-  static thread_local std::vector<std::pair<kgq_ctx*, std::vector<ProfRec>>> lists;
-  for (auto& l : lists)
-    if (l.first == ctx) return l.second;
-  lists.emplace_back(ctx, std::vector<ProfRec>{});
-  return lists.back().second;
-}
 struct StageTimer {
   kgq_ctx* ctx;
   cudaStream_t st;
@@ -126,17 +115,54 @@ struct StageTimer {
   StageTimer(kgq_ctx* c, cudaStream_t s, int stg, double w = 0.0) : ctx(c), st(s), stage(stg), work(w) {
     if (!ctx->profile) return;
     cudaEventCreate(&a);
-    cudaEventRecord(a, st);
+    record(a);
+  }
+  // inside stream capture the record must be an external event-record node to be replayed
+  void record(cudaEvent_t e) {
+    if (ctx->capture_entry)
+      cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else
+      cudaEventRecord(e, st);
   }
   ~StageTimer() {
     if (!ctx->profile) return;
     cudaEvent_t b;
     cudaEventCreate(&b);
-    cudaEventRecord(b, st);
-    prof_list(ctx).push_back({stage, a, b, work});
-    ctx->prof_n[stage] += 1;
+    record(b);
+    if (ctx->capture_entry)
+      ctx->capture_entry->evs.push_back({stage, a, b, work});
+    else
+      ctx->prof_recs.push_back({stage, a, b, work});
   }
 };
+
+// Fold completed stage events into the context's accumulators.
+void harvest(kgq_ctx* ctx, std::vector<ProfRec>& recs, bool destroy) {
+  for (auto& r : recs) {
+    float t = 0;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) {
+      cudaGetLastError();  // do not leave a sticky error for the next checked call
+      t = 0;
+    }
+    ctx->prof_acc_ms[r.stage] += t;
+    ctx->prof_acc_n[r.stage] += 1;
+    ctx->prof_acc_work[r.stage] += r.work;
+    if (destroy) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  }
+  if (destroy) recs.clear();
+}
+
+void destroy_graph_entry(kgq_ctx::GraphEntry& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto& r : g.evs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g.evs.clear();
+}
 
 ChainArgs chain_args(kgq_ctx* ctx, const Plan* P, int B, const int32_t* anchors,
                      const int32_t* rels) {
@@ -159,10 +185,27 @@ ChainArgs chain_args(kgq_ctx* ctx, const Plan* P, int B, const int32_t* anchors,
 
 // Every dense layer of the chain goes through here: timed as stage kStDense when profiling,
 // with 2 M N K algorithmic FLOPs.
+// KGQ_DEBUG_LAUNCH=1: report the first failing launch (by site) on stderr.
+bool debug_launch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KGQ_DEBUG_LAUNCH");
+    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+void check_site(const char* site) {
+  if (!debug_launch()) return;
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) fprintf(stderr, "libkgq: launch error after %s: %s\n", site, cudaGetErrorString(e));
+}
+
 int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
           int neg1, cudaStream_t st) {
   StageTimer t(ctx, st, kStDense, 2.0 * M * (double)L.out_f * K);
-  return launch_linear(A, M, K, L, epi, out, neg0, neg1, st);
+  const int r = launch_linear(A, M, K, L, epi, out, neg0, neg1, st);
+  check_site("dense layer");
+  return r;
 }
 
 Split offset_split(const Split& s, int64_t rows, int64_t cols = 0) {
@@ -409,6 +452,8 @@ kgq_status kgq_create(const kgq_config* cfg, kgq_ctx** out) {
     return fail(nullptr, KGQ_EUNSUPPORTED, "libkgq is built for sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
   kgq_ctx* ctx = new kgq_ctx();
   ctx->cfg = *cfg;
+  const char* ng = getenv("KGQ_NO_GRAPHS");
+  ctx->use_graphs = !(ng && ng[0] && ng[0] != '0');
   DeviceGuard g(cfg->device);
   kgq_shard_range(cfg->n_entity, cfg->world_size, cfg->rank, &ctx->e0, &ctx->e1);
   ctx->ns = ctx->e1 - ctx->e0;
@@ -442,8 +487,9 @@ void kgq_destroy(kgq_ctx* ctx) {
   F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv_hi); F(ctx->uv_lo); F(ctx->Esum);
   F(ctx->uvsums); F(ctx->Atc.hi); F(ctx->Atc.lo); F(ctx->Ptc);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
-  for (auto& r : prof_list(ctx)) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
-  prof_list(ctx).clear();
+  for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  for (auto& r : ctx->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   delete ctx;
 }
 
@@ -597,6 +643,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
     StageTimer t(ctx, st, kStChain);
     L += run_chain(ctx, s, B, anchors, rels, st);
   }
+  check_site("operator chain");
   for (int64_t b0 = 0; b0 < B; b0 += ctx->bchunk) {
     const int nb = (int)std::min<int64_t>(ctx->bchunk, B - b0);
     const float* qb = ctx->Q + b0 * P->n_out * ctx->qw;
@@ -606,6 +653,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
       L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
                                  ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist,
                                  ctx->np, st);
+      check_site("tensor-core scorer");
     } else {
       {
         StageTimer t(ctx, st, kStPrep);
@@ -619,6 +667,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
       StageTimer t(ctx, st, kStTopk);
       L += launch_topk(ctx->dist, ctx->np, nb, ctx->ns, k, ctx->e0, ctx->d_invalid + b0,
                        topk_dist + b0 * k, topk_id + b0 * k, ctx->topk_tmp_d, ctx->topk_tmp_i, st);
+      check_site("top-k");
     }
     if (shard_dist)
       CK(cudaMemcpy2DAsync(shard_dist + b0 * ctx->ns, ctx->ns * sizeof(float), ctx->dist,
@@ -630,6 +679,72 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
   return KGQ_OK;
 }
 
+// Replays a captured CUDA graph of the whole submit (one cudaGraphLaunch instead of ~10-15
+// kernel launches) when the same (structure, batch, k, buffers) was submitted before; the
+// first call runs eagerly, the second captures.  With profiling on, the graph contains the
+// stage events; each replay's times are harvested before the next replay or at profile_read.
+static kgq_status submit_graphed(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t* anchors,
+                                 const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
+                                 cudaStream_t st) {
+  const void* key[4] = {anchors, rels, topk_dist, topk_id};
+  kgq_ctx::GraphEntry* e = nullptr;
+  for (auto& g : ctx->graphs)
+    if (g.s == s && g.B == B && g.k == k && g.prof == ctx->profile && std::equal(key, key + 4, g.ptr)) e = &g;
+  ctx->graph_clock++;
+  if (e && e->exec) {
+    e->last = ctx->graph_clock;
+    if (e->pending) harvest(ctx, e->evs, false);  // previous replay's stage times
+    CK(cudaGraphLaunch(e->exec, st), "graph launch");
+    e->pending = !e->evs.empty();
+    ctx->launches = e->launches;
+    return KGQ_OK;
+  }
+  if (!e) {
+    if (ctx->graphs.size() >= 64) {  // evict the least recently used entry
+      auto lru = std::min_element(ctx->graphs.begin(), ctx->graphs.end(),
+                                  [](const kgq_ctx::GraphEntry& a, const kgq_ctx::GraphEntry& b) { return a.last < b.last; });
+      if (lru->pending) harvest(ctx, lru->evs, false);
+      destroy_graph_entry(*lru);
+      ctx->graphs.erase(lru);
+    }
+    kgq_ctx::GraphEntry ne{s, B, k, ctx->profile, {key[0], key[1], key[2], key[3]}, nullptr, 0, 1,
+                           ctx->graph_clock, {}, false};
+    ctx->graphs.push_back(ne);
+    return submit_impl(ctx, s, B, anchors, rels, k, topk_dist, topk_id, nullptr, st);
+  }
+  e->last = ctx->graph_clock;
+  if (++e->seen < 2 || e->seen > 2) return submit_impl(ctx, s, B, anchors, rels, k, topk_dist, topk_id, nullptr, st);
+  // capture on the context's private stream, then launch on the caller's
+  if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking), "capture stream");
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+  ctx->capture_entry = e;
+  kgq_status r = submit_impl(ctx, s, B, anchors, rels, k, topk_dist, topk_id, nullptr, ctx->cap_stream);
+  ctx->capture_entry = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+  if (r != KGQ_OK || ce != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    destroy_graph_entry(*e);
+    e->seen = 3;  // never retry this key; run eagerly
+    return submit_impl(ctx, s, B, anchors, rels, k, topk_dist, topk_id, nullptr, st);
+  }
+  cudaGraphExec_t exec = nullptr;
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ce != cudaSuccess) {
+    cudaGetLastError();
+    destroy_graph_entry(*e);
+    e->seen = 3;
+    return submit_impl(ctx, s, B, anchors, rels, k, topk_dist, topk_id, nullptr, st);
+  }
+  e->exec = exec;
+  e->launches = ctx->launches;
+  CK(cudaGraphLaunch(exec, st), "graph launch");
+  e->pending = !e->evs.empty();
+  return KGQ_OK;
+}
+
 kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors, const int32_t* rels,
                       int32_t k, float* topk_dist, int32_t* topk_id, float* shard_dist, kgq_stream stream) {
   kgq_status st = check_submit(ctx, s, batch, k, true);
@@ -637,6 +752,8 @@ kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anc
   if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
   if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
   DeviceGuard g(ctx->cfg.device);
+  if (ctx->use_graphs && !shard_dist && batch <= ctx->bchunk)
+    return submit_graphed(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, (cudaStream_t)stream);
   return submit_impl(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, shard_dist, (cudaStream_t)stream);
 }
 
@@ -654,8 +771,12 @@ kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t
                      cudaMemcpyHostToDevice, cs), "anchor upload");
   CK(cudaMemcpyAsync(ctx->d_rel_stage, rels, (size_t)batch * P->n_rel * sizeof(int32_t),
                      cudaMemcpyHostToDevice, cs), "relation upload");
-  st = submit_impl(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage,
-                   ctx->d_topi_stage, nullptr, cs);
+  if (ctx->use_graphs && batch <= ctx->bchunk)
+    st = submit_graphed(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage,
+                        ctx->d_topi_stage, cs);
+  else
+    st = submit_impl(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage,
+                     ctx->d_topi_stage, nullptr, cs);
   if (st) return st;
   CK(cudaMemcpyAsync(topk_dist, ctx->d_topd_stage, (size_t)batch * k * sizeof(float), cudaMemcpyDeviceToHost, cs),
      "top-k download");
@@ -737,24 +858,19 @@ kgq_status kgq_profile_enable(kgq_ctx* ctx, int32_t on) {
 kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n, double* work) {
   if (!ctx || !ms || !n) return fail(ctx, KGQ_EINVAL, "NULL argument");
   DeviceGuard g(ctx->cfg.device);
-  auto& lst = prof_list(ctx);
+  harvest(ctx, ctx->prof_recs, true);
+  for (auto& gr : ctx->graphs)
+    if (gr.pending) {
+      harvest(ctx, gr.evs, false);
+      gr.pending = false;
+    }
   for (int i = 0; i < kStNum; ++i) {
-    ms[i] = 0;
-    n[i] = 0;
-    if (work) work[i] = 0;
+    ms[i] = ctx->prof_acc_ms[i];
+    n[i] = ctx->prof_acc_n[i];
+    if (work) work[i] = ctx->prof_acc_work[i];
+    ctx->prof_acc_ms[i] = ctx->prof_acc_work[i] = 0;
+    ctx->prof_acc_n[i] = 0;
   }
-  for (auto& r : lst) {
-    CK(cudaEventSynchronize(r.b), "profile event");
-    float t = 0;
-    cudaEventElapsedTime(&t, r.a, r.b);
-    ms[r.stage] += t;
-    n[r.stage] += 1;
-    if (work) work[r.stage] += r.work;
-    cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
-  }
-  lst.clear();
-  for (int i = 0; i < kStNum; ++i) ctx->prof_n[i] = 0;
   return KGQ_OK;
 }
 

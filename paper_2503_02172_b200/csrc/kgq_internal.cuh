@@ -59,6 +59,13 @@ struct Linear {
 
 enum Epi { kEpiNone = 0, kEpiRelu = 1, kEpiBetaReg = 2 };
 
+// A timed region: CUDA events recorded on the launching stream around one stage.
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+  double work;
+};
+
 // Profiling stages (kgq_profile_* in kgq_api.cu).
 // kStDense is nested inside kStChain (every dense layer of the operator chain).
 enum Stage { kStChain = 0, kStPrep = 1, kStScore = 2, kStTopk = 3, kStDense = 4, kStNum = 5 };
@@ -108,10 +115,28 @@ struct kgq_ctx {
 
   int launches = 0;
   bool profile = false;
-  cudaEvent_t ev[2 * kgq::kStNum] = {};
-  double prof_ms[kgq::kStNum] = {};
-  int64_t prof_n[kgq::kStNum] = {};
-  double prof_work[kgq::kStNum] = {};    // algorithmic work (FLOPs / lane ops) per stage
+  // CUDA graphs of whole submits, keyed by (structure, batch, k, caller pointers); captured on
+  // the second identical call and replayed afterwards (kgq_api.cu submit_graphed)
+  struct GraphEntry {
+    int s, B, k;
+    bool prof;  // captured with stage events (replays re-record them)
+    const void* ptr[4];
+    cudaGraphExec_t exec;
+    int launches;
+    int seen;
+    uint64_t last;
+    std::vector<kgq::ProfRec> evs;  // captured stage events (owned)
+    bool pending;                   // a replay's events have not been harvested yet
+  };
+  GraphEntry* capture_entry = nullptr;      // set while capturing: stage events go there
+  std::vector<kgq::ProfRec> prof_recs;      // eager stage events (owned until read)
+  double prof_acc_ms[kgq::kStNum] = {}, prof_acc_work[kgq::kStNum] = {};
+  int64_t prof_acc_n[kgq::kStNum] = {};
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
+  uint64_t graph_clock = 0;
+  cudaStream_t cap_stream = nullptr;
+
 };
 
 namespace kgq {

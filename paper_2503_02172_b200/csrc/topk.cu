@@ -97,13 +97,15 @@ __global__ void __launch_bounds__(kTopkThreads)
   unsigned long long* lst = wl + wid * P;  // [0, k) sorted best, [k, k+32) buffer, rest max
   for (int j = lane; j < P; j += 32) lst[j] = ~0ull;
   __syncwarp();
-  unsigned long long tau = ~0ull;  // current k-th best of this warp
+  unsigned long long tau = ~0ull;  // current k-th best of this warp (packed key)
+  float tau_f = __uint_as_float(0x7F800000u);  // its distance (+inf while the list is short)
   int cnt = 0;
   auto merge = [&]() {
     warp_bitonic_sort(lst, P);
     for (int j = k + lane; j < P; j += 32) lst[j] = ~0ull;
     __syncwarp();
     tau = lst[k - 1];
+    tau_f = tau == ~0ull ? __uint_as_float(0x7F800000u) : fkey_inv((uint32_t)(tau >> 32));
     cnt = 0;
   };
   constexpr int U = 8;  // loads in flight per lane (the loop is latency-bound otherwise)
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(kTopkThreads)
     if (lane < k) lst[lane] = v;
     __syncwarp();
     tau = lst[k - 1];
+    tau_f = tau == ~0ull ? __uint_as_float(0x7F800000u) : fkey_inv((uint32_t)(tau >> 32));
     start = w0 + 32;
   }
   for (int64_t base = start; base < w1; base += 32 * U) {
@@ -138,14 +141,15 @@ __global__ void __launch_bounds__(kTopkThreads)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * 32 + lane;
-      const unsigned long long v =
-          i < w1 ? (((unsigned long long)fkey(x[u]) << 32) | (uint32_t)i) : ~0ull;
-      const bool q = v < tau;
+      // a warp scans its slice in increasing index order, so an element equal to the current
+      // k-th best distance has a larger id than it and cannot displace it: strict < on the
+      // float is exact; keys are packed only for the rare candidates
+      const bool q = i < w1 && x[u] < tau_f;
       const unsigned m = __ballot_sync(0xffffffffu, q);
       if (m) {
         const int add = __popc(m);
         if (cnt + add > 32) merge();
-        if (q) lst[k + cnt + __popc(m & ((1u << lane) - 1u))] = v;
+        if (q) lst[k + cnt + __popc(m & ((1u << lane) - 1u))] = ((unsigned long long)fkey(x[u]) << 32) | (uint32_t)i;
         __syncwarp();
         cnt += add;
         if (cnt == 32) merge();
