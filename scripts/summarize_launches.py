@@ -11,9 +11,10 @@ def main(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name")
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         v = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("kgq::<unnamed>::", "kgq::")[:70]
