@@ -374,3 +374,35 @@ def answer(model, structure, anchors, rels, k):
     dist = model.scores(structure, anchors, rels)
     td, ti = topk(dist, k)
     return td, ti, dist
+
+
+# ----------------------------------------------------------------------------------------
+# N1: filtered ranking and MRR -- the accuracy check of RQ3,
+# KGReasoning test protocol [ext]: entities ordered by distance (logit descending), each hard
+# answer's rank counts only the NON-answer entities ranked before it ("filtered" setting);
+# ties are broken by ascending entity id (Q13), as in top-k.
+# ----------------------------------------------------------------------------------------
+def filtered_ranks(dist_row, answers, ids=None):
+    """dist_row: distances of one query to the entities `ids` (default 0..n-1); answers: all
+    answers (easy and hard) of the query.  Returns {answer: 1 + #{e not in answers:
+    (dist_e, e) < (dist_a, a)}} for every answer.  Pinned by an explicit full sort
+    (test_oracle_ranking) and the SPEC S:465-473 MRR examples."""
+    dist_row = np.asarray(dist_row, np.float64)
+    ids = np.arange(len(dist_row), dtype=np.int64) if ids is None else np.asarray(ids, np.int64)
+    pos = {int(e): i for i, e in enumerate(ids)}
+    ans = set(int(a) for a in answers)
+    keep = np.array([int(e) not in ans for e in ids])
+    d_keep, id_keep = dist_row[keep], ids[keep]
+    out = {}
+    for a in ans:
+        da = dist_row[pos[a]]
+        better = (d_keep < da) | ((d_keep == da) & (id_keep < a))
+        out[a] = 1 + int(np.count_nonzero(better))
+    return out
+
+
+def mrr_hits(ranks):
+    """ranks: filtered ranks of the hard answers of one query -> (MRR, Hits@1, Hits@3, Hits@10),
+    each a mean over those answers (KGReasoning averages per query)."""
+    r = np.asarray(list(ranks), np.float64)
+    return float(np.mean(1.0 / r)), float(np.mean(r <= 1)), float(np.mean(r <= 3)), float(np.mean(r <= 10))
