@@ -168,6 +168,24 @@ kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int
 kgq_status kgq_merge_topk(kgq_ctx* ctx, int32_t n_parts, int32_t batch, int32_t k,
                           const float* in_dist, const int32_t* in_id, float* out_dist,
                           int32_t* out_id, kgq_stream stream);
+/* N1: filtered ranking of given answers (KGReasoning test protocol behind the
+ * paper's MRR consistency check).  Query b's answer set (easy and hard, distinct
+ * global ids) is ans_id[ans_off[b] .. ans_off[b+1]) (device int32 CSR, ans_off [batch+1],
+ * n_ans = ans_off[batch], at most 2048 answers per query).  For answer a of query b:
+ *   count[a] = #{entities e of THIS shard, e not in b's answer set : (dist_e, e) < (dist_a, a)}
+ * (ties by ascending id, Q13); the filtered rank is 1 + the sum of count over all shards, and
+ * MRR / Hits@k follow on the host.  ans_dist (device fp32 [n_ans]) carries dist_a:
+ *   KGQ_RANK_LOCAL (single shard): ans_dist is written, then count.
+ *   KGQ_RANK_DIST: writes ans_dist for answers inside this shard, +inf for the others
+ *                  (min-reduce it across ranks); count is not touched.
+ *   KGQ_RANK_COUNT: reads ans_dist (the reduced one), writes count.
+ * Runs the operator chain and the scorer like kgq_submit.  A query with more than 2048
+ * answers makes kgq_check_errors() return KGQ_EINVAL. */
+enum { KGQ_RANK_LOCAL = 0, KGQ_RANK_DIST = 1, KGQ_RANK_COUNT = 2 };
+kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                            const int32_t* rels, const int32_t* ans_off, const int32_t* ans_id,
+                            int32_t n_ans, int32_t mode, float* ans_dist, int32_t* count,
+                            kgq_stream stream);
 /* Synchronise `stream`; KGQ_ERANGE (message names query row and slot) if any submit since
  * the last check saw an out-of-range id, KGQ_ECUDA on an asynchronous CUDA error. */
 kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream);

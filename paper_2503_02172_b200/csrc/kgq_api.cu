@@ -632,11 +632,34 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   return KGQ_OK;
 }
 
+// Distances of query rows [b0, b0 + nb) (chain already run) to every entity of the shard,
+// into ctx->dist rows [0, nb).  Returns the number of kernels launched.
+static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStream_t st) {
+  const kgq_config& c = ctx->cfg;
+  int L = 0;
+  const float* qb = ctx->Q + b0 * P->n_out * ctx->qw;
+  if (c.model == KGQ_BETAE && !score_uses_stream(c.model, P->n_out, nb)) {
+    // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
+    StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
+    L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
+                               ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist, ctx->np, st);
+    check_site("tensor-core scorer");
+  } else {
+    {
+      StageTimer t(ctx, st, kStPrep);
+      L += launch_score_prep(c.model, qb, nb, P->n_out, c.dim, ctx->Qt, ctx->rpad, st);
+    }
+    StageTimer t(ctx, st, kStScore, (c.model == KGQ_GQE ? 2.0 : 4.0) * nb * P->n_out * (double)ctx->ns * c.dim);
+    L += launch_score(c.model, P->n_out, nb, c.dim, c.cen, ctx->Qt, ctx->rpad, ctx->score_tab, ctx->np,
+                      ctx->ns, ctx->dist, ctx->np, st);
+  }
+  return L;
+}
+
 static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t* anchors,
                               const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
                               float* shard_dist, cudaStream_t st) {
   const Plan* P = plan_of(s);
-  const kgq_config& c = ctx->cfg;
   int L = 0;
   CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)B * sizeof(int32_t), st), "reset flags");
   {
@@ -646,23 +669,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
   check_site("operator chain");
   for (int64_t b0 = 0; b0 < B; b0 += ctx->bchunk) {
     const int nb = (int)std::min<int64_t>(ctx->bchunk, B - b0);
-    const float* qb = ctx->Q + b0 * P->n_out * ctx->qw;
-    if (c.model == KGQ_BETAE && !score_uses_stream(c.model, P->n_out, nb)) {
-      // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
-      StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
-      L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
-                                 ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist,
-                                 ctx->np, st);
-      check_site("tensor-core scorer");
-    } else {
-      {
-        StageTimer t(ctx, st, kStPrep);
-        L += launch_score_prep(c.model, qb, nb, P->n_out, c.dim, ctx->Qt, ctx->rpad, st);
-      }
-      StageTimer t(ctx, st, kStScore, (c.model == KGQ_GQE ? 2.0 : 4.0) * nb * P->n_out * (double)ctx->ns * c.dim);
-      L += launch_score(c.model, P->n_out, nb, c.dim, c.cen, ctx->Qt, ctx->rpad, ctx->score_tab, ctx->np,
-                        ctx->ns, ctx->dist, ctx->np, st);
-    }
+    L += score_rows(ctx, P, b0, nb, st);
     {
       StageTimer t(ctx, st, kStTopk);
       L += launch_topk(ctx->dist, ctx->np, nb, ctx->ns, k, ctx->e0, ctx->d_invalid + b0,
@@ -824,6 +831,10 @@ kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
   CK(cudaStreamSynchronize((cudaStream_t)stream), "stream synchronize");
   int32_t e[4];
   CK(cudaMemcpy(e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost), "error word");
+  if (e[0] == 2) {
+    CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
+    return fail(ctx, KGQ_EINVAL, "kgq_rank_answers: a query has more than %d answers", kMaxAnswers);
+  }
   if (e[0]) {
     CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
     return fail(ctx, KGQ_ERANGE, "query row %d: %s slot %d out of range", e[1], e[3] ? "relation" : "anchor",
@@ -846,6 +857,38 @@ kgq_status kgq_entity_terms(kgq_ctx* ctx, float* out, kgq_stream stream) {
                          3 * ctx->np * sizeof(float), ctx->ns * sizeof(float), d, cudaMemcpyDeviceToDevice,
                          (cudaStream_t)stream),
        "entity terms copy");
+  return KGQ_OK;
+}
+
+kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                            const int32_t* rels, const int32_t* ans_off, const int32_t* ans_id,
+                            int32_t n_ans, int32_t mode, float* ans_dist, int32_t* count,
+                            kgq_stream stream) {
+  kgq_status st = check_submit(ctx, s, batch, 0, false);
+  if (st) return st;
+  if (mode < KGQ_RANK_LOCAL || mode > KGQ_RANK_COUNT) return fail(ctx, KGQ_EINVAL, "bad rank mode %d", mode);
+  if (mode == KGQ_RANK_LOCAL && ctx->cfg.world_size > 1)
+    return fail(ctx, KGQ_EINVAL, "KGQ_RANK_LOCAL needs a single shard; use KGQ_RANK_DIST + min-reduce + KGQ_RANK_COUNT");
+  if (batch == 0 || n_ans == 0) { ctx->launches = 0; return KGQ_OK; }
+  if (!anchors || !rels || !ans_off || !ans_id || !ans_dist || (mode != KGQ_RANK_DIST && !count))
+    return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  DeviceGuard g(ctx->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const Plan* P = plan_of(s);
+  int L = 0;
+  CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)batch * sizeof(int32_t), cs), "reset flags");
+  L += run_chain(ctx, s, batch, anchors, rels, cs);
+  for (int64_t b0 = 0; b0 < batch; b0 += ctx->bchunk) {
+    const int nb = (int)std::min<int64_t>(ctx->bchunk, batch - b0);
+    L += score_rows(ctx, P, b0, nb, cs);
+    if (mode != KGQ_RANK_COUNT)
+      L += launch_answer_dist(ctx->dist, ctx->np, ctx->e0, ctx->ns, (int)b0, nb, ans_off, ans_id, ans_dist, cs);
+    if (mode != KGQ_RANK_DIST)
+      L += launch_filtered_counts(ctx->dist, ctx->np, ctx->e0, ctx->ns, (int)b0, nb, ans_off, ans_id, ans_dist,
+                                  count, ctx->d_err, cs);
+  }
+  ctx->launches = L;
+  CK(cudaGetLastError(), "rank launch");
   return KGQ_OK;
 }
 

@@ -14,6 +14,7 @@ constexpr int kMaxBranches = 3;   // 3i / 3in
 constexpr int kMaxOps = 4;        // ops per branch chain
 constexpr int kMaxLayers = 32;
 constexpr int kMaxK = 256;
+constexpr int kMaxAnswers = 2048;  // per query, kgq_rank_answers
 constexpr int kEntityPad = 128;   // scorer entity tile; shard tables are padded to it
 constexpr int kRowPad = 64;       // scorer query-row tile
 
@@ -217,6 +218,12 @@ int launch_topk(const float* dist, int64_t ldd, int B, int64_t n, int k, int64_t
                 const int32_t* invalid, float* out_d, int32_t* out_i, float* tmp_d, int32_t* tmp_i,
                 cudaStream_t st);
 bool score_uses_stream(int model, int nbq, int B);
+// N1 filtered ranking (rank.cu)
+int launch_answer_dist(const float* dist, int64_t ldd, int64_t e0, int64_t ns, int b0, int nb,
+                       const int32_t* ans_off, const int32_t* ans_id, float* ans_dist, cudaStream_t st);
+int launch_filtered_counts(const float* dist, int64_t ldd, int64_t e0, int64_t ns, int b0, int nb,
+                           const int32_t* ans_off, const int32_t* ans_id, const float* ans_dist,
+                           int32_t* count, int32_t* err, cudaStream_t st);
 // Tensor-core BetaE scorer (score_tc.cu): finalize builds the centred split table
 // uv [np][2d], E_e = sum_d C_ed (fp64) and the per-dim U/V sums; per batch it splits the
 // query rows, computes P_q (fp64) and runs the 3xTF32 GEMM with the score epilogue.

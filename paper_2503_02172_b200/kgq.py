@@ -37,8 +37,9 @@ EXPORTS = (
     "kgq_shard_end", "kgq_load_entities", "kgq_load_relations", "kgq_load_linear",
     "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_query_embedding", "kgq_merge_topk",
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
-    "kgq_profile_read",
+    "kgq_profile_read", "kgq_rank_answers",
 )
+RANK_LOCAL, RANK_DIST, RANK_COUNT = 0, 1, 2
 
 
 class KgqConfig(ctypes.Structure):
@@ -80,6 +81,7 @@ _sig = {
     "kgq_last_launch_count": (_I32, [_P]),
     "kgq_entity_terms": (_I32, [_P, _P, _P]),
     "kgq_profile_enable": (_I32, [_P, _I32]),
+    "kgq_rank_answers": (_I32, [_P, _I32, _I32, _P, _P, _P, _P, _I32, _I32, _P, _P, _P]),
     "kgq_profile_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                               ctypes.POINTER(ctypes.c_double)]),
 }
@@ -260,6 +262,24 @@ class Engine:
                                         _ptr(parts_id.contiguous()), _ptr(od), _ptr(oi),
                                         _stream(stream)))
         return od, oi
+
+    def rank_answers(self, structure, anchors, rels, ans_off, ans_id, mode=RANK_LOCAL,
+                     ans_dist=None, stream=None):
+        """N1 filtered ranking (kgq_rank_answers).  ans_off int32 [B+1], ans_id int32 [n] CUDA
+        tensors (CSR of each query's easy + hard answers).  Returns (ans_dist, count): the
+        filtered rank of answer j is 1 + count[j] (summed over shards)."""
+        import torch
+        s = structure_id(structure)
+        B = anchors.shape[0]
+        n = int(ans_id.shape[0])
+        if ans_dist is None:
+            ans_dist = torch.empty(n, dtype=torch.float32, device=anchors.device)
+        count = torch.zeros(n, dtype=torch.int32, device=anchors.device)
+        self._check(_lib.kgq_rank_answers(self._h, s, B, _ptr(anchors), _ptr(rels), _ptr(ans_off),
+                                          _ptr(ans_id), n, mode, _ptr(ans_dist),
+                                          _ptr(count) if mode != RANK_DIST else None,
+                                          _stream(stream)))
+        return ans_dist, count
 
     def check_errors(self, stream=None):
         self._check(_lib.kgq_check_errors(self._h, _stream(stream)))

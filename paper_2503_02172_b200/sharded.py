@@ -11,7 +11,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from .kgq import Engine
+from .kgq import RANK_COUNT, RANK_DIST, RANK_LOCAL, Engine
 
 
 def all_gather_topk(td: torch.Tensor, ti: torch.Tensor, group=None):
@@ -50,3 +50,36 @@ class ShardedEngine:
 
     def last_launch_count(self):
         return self.engine.last_launch_count() + (1 if self.world > 1 else 0)
+
+    def rank_answers(self, structure, anchors, rels, ans_off, ans_id, stream=None):
+        """N1 filtered ranks (1-based) of every answer across all shards: answer distances
+        from the owning shard (min-all-reduce of +inf elsewhere), then per-shard counts of
+        better non-answers, sum-all-reduced."""
+        if self.world == 1:
+            _, cnt = self.engine.rank_answers(structure, anchors, rels, ans_off, ans_id, RANK_LOCAL,
+                                              stream=stream)
+            return cnt + 1
+        ad, _ = self.engine.rank_answers(structure, anchors, rels, ans_off, ans_id, RANK_DIST,
+                                         stream=stream)
+        dist.all_reduce(ad, op=dist.ReduceOp.MIN, group=self.group)
+        _, cnt = self.engine.rank_answers(structure, anchors, rels, ans_off, ans_id, RANK_COUNT,
+                                          ans_dist=ad, stream=stream)
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=self.group)
+        return cnt + 1
+
+
+def answers_csr(answer_lists):
+    """[array of global ids per query] -> (ans_off int32 [B+1], ans_id int32 [n]) numpy."""
+    import numpy as np
+    off = np.zeros(len(answer_lists) + 1, np.int32)
+    off[1:] = np.cumsum([len(a) for a in answer_lists])
+    ids = np.concatenate([np.asarray(a, np.int32) for a in answer_lists]) if answer_lists else np.zeros(0, np.int32)
+    return off, ids.astype(np.int32)
+
+
+def mrr_hits(ranks_per_query):
+    """Mean over queries of the per-query mean of 1/rank and Hits@1/3/10 over its hard answers."""
+    import numpy as np
+    m = np.array([[np.mean(1.0 / r), np.mean(r <= 1), np.mean(r <= 3), np.mean(r <= 10)]
+                  for r in (np.asarray(x, np.float64) for x in ranks_per_query) if len(r)])
+    return dict(zip(("mrr", "hits1", "hits3", "hits10"), m.mean(0).tolist())) if len(m) else {}

@@ -87,3 +87,55 @@ def test_shard_ranges_cover_and_balance():
             rs = [kgq.shard_range(n, w, r) for r in range(w)]
             sizes = [b - a for a, b in rs]
             assert sum(sizes) == n and max(sizes) - min(sizes) <= -(-n // w)
+
+
+def _rank_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N, R, d = 157, 5, 8
+        t = synth.make_tables("q2b", N, R, d, seed=6)
+        m = O.Model("q2b", t, dim=d)
+        a, r = synth.make_queries("2u", 5, N, R, seed=2)
+        full = m.scores("2u", a, r)
+        rng = np.random.default_rng(0)
+        answers = [rng.choice(N, size=4, replace=False) for _ in range(5)]
+        lo, hi = kgq.shard_range(N, world, rank)
+        # phase 1 (KGQ_RANK_DIST): distances of the answers this shard owns, +inf elsewhere
+        ad = torch.full((5, 4), float("inf"), dtype=torch.float64)
+        for b in range(5):
+            for j, e in enumerate(answers[b]):
+                if lo <= e < hi:
+                    ad[b, j] = full[b, e]
+        dist.all_reduce(ad, op=dist.ReduceOp.MIN)
+        # phase 2 (KGQ_RANK_COUNT): better non-answers inside this shard, summed over ranks
+        cnt = torch.zeros((5, 4), dtype=torch.int64)
+        for b in range(5):
+            ans = set(int(x) for x in answers[b])
+            for j, e in enumerate(answers[b]):
+                for x in range(lo, hi):
+                    if x not in ans and (full[b, x] < ad[b, j] or (full[b, x] == ad[b, j] and x < e)):
+                        cnt[b, j] += 1
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+        ok = all(O.filtered_ranks(full[b], answers[b])[int(e)] == 1 + int(cnt[b, j])
+                 for b in range(5) for j, e in enumerate(answers[b]))
+        q.put((rank, ok))
+    except Exception as e:
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_phase_filtered_rank_protocol_over_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res

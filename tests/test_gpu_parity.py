@@ -255,3 +255,80 @@ def test_cuda_graph_replay_matches_eager(model):
         prof = e.profile_read()
         e.profile(False)
         assert prof["score"][1] >= 3 and prof["score"][0] > 0
+
+
+def _rank_bounds(ref_row, answers, rel=1e-4):
+    """Oracle filtered rank interval under the Q14 tolerance (near-ties may flip)."""
+    s_q = 1e-3 * np.median(ref_row)
+    ans = set(int(a) for a in answers)
+    keep = np.array([e not in ans for e in range(len(ref_row))])
+    d = ref_row[keep]
+    out = {}
+    for a in ans:
+        tol = rel * max(ref_row[a], s_q)
+        out[a] = (1 + int(np.sum(d < ref_row[a] - tol)), 1 + int(np.sum(d <= ref_row[a] + tol)))
+    return out
+
+
+@pytest.mark.parametrize("model", ["gqe", "q2b", "betae"])
+def test_filtered_ranks_n1(model):
+    from paper_2503_02172_b200.sharded import answers_csr
+    e, m, t = engine(model)
+    N, R = SMALL["N"], SMALL["R"]
+    rng = np.random.default_rng(5)
+    for s in ("1p", "2u", "ip"):
+        a, r = synth.make_queries(s, 37, N, R, seed=77)
+        ref = m.scores(s, a, r)
+        # answers: some of the true nearest (ranked well) + random entities
+        lists = []
+        for b in range(37):
+            near = np.argsort(ref[b])[: rng.integers(0, 4)]
+            rand = rng.choice(N, size=rng.integers(1, 6), replace=False)
+            lists.append(np.unique(np.r_[near, rand]))
+        off, ids = answers_csr(lists)
+        ad, cnt = e.rank_answers(s, dev(a), dev(r), dev(off), dev(ids))
+        e.check_errors()
+        cnt = cnt.cpu().numpy()
+        for b in range(37):
+            bounds = _rank_bounds(ref[b], lists[b])
+            exact = O.filtered_ranks(ref[b], lists[b])
+            for j in range(off[b], off[b + 1]):
+                rk = 1 + cnt[j]
+                lo, hi = bounds[int(ids[j])]
+                assert lo <= rk <= hi, (model, s, b, int(ids[j]), rk, lo, hi, exact[int(ids[j])])
+
+
+def test_filtered_ranks_planted_and_sharded():
+    from paper_2503_02172_b200.sharded import answers_csr
+    from planted import PlantedKG
+    from test_oracle_planted import planted_queries
+    from paper_2503_02172_b200.kgq import RANK_DIST, RANK_COUNT
+    kg = PlantedKG(n_entity=200, n_relation=12, dim=32, depth=4, seed=7)
+    t = synth.make_tables("gqe", kg.n, 12, 32, seed=1)
+    t["entity"], t["relation"] = kg.E.copy(), kg.R.copy()
+    full = Engine("gqe", kg.n, 12, 32, max_batch=16, max_k=8)
+    full.load_tables(t)
+    for s in ("1p", "2p", "2u", "up"):
+        a, r = planted_queries(kg, s, 12, seed=3)
+        lists = [sorted(kg.answers(s, list(a[b]), list(r[b]))) for b in range(len(a))]
+        off, ids = answers_csr(lists)
+        _, cnt = full.rank_answers(s, dev(a), dev(r), dev(off), dev(ids))
+        assert np.all(cnt.cpu().numpy() == 0), s   # every true answer has filtered rank 1
+        # the two-phase protocol over W virtual shards gives the same counts as one shard
+        rand = [np.unique(np.r_[lst, np.random.default_rng(b).choice(kg.n, 3, replace=False)])
+                for b, lst in enumerate(lists)]
+        off2, ids2 = answers_csr(rand)
+        _, c_full = full.rank_answers(s, dev(a), dev(r), dev(off2), dev(ids2))
+        for W in (2, 3):
+            shards = []
+            for rank in range(W):
+                e = Engine("gqe", kg.n, 12, 32, max_batch=16, max_k=8, world_size=W, rank=rank)
+                e.load_tables(t)
+                shards.append(e)
+            dists = [e.rank_answers(s, dev(a), dev(r), dev(off2), dev(ids2), mode=RANK_DIST)[0] for e in shards]
+            ad = torch.stack(dists).min(0).values            # the min-all-reduce
+            cnts = [e.rank_answers(s, dev(a), dev(r), dev(off2), dev(ids2), mode=RANK_COUNT, ans_dist=ad.clone())[1]
+                    for e in shards]
+            assert torch.equal(torch.stack(cnts).sum(0), c_full), (s, W)   # the sum-all-reduce
+            for e in shards:
+                e.close()
