@@ -178,6 +178,110 @@ __global__ void __launch_bounds__(kTopkThreads)
   }
 }
 
+// k_topk_reg (k <= 32): the same selection with each warp's k best held in REGISTERS, one
+// packed key per lane, sorted across lanes 0..k-1.  A candidate (distance <= the warp's k-th
+// best distance, then exact packed-key comparison, so the scan order does not matter for ties)
+// is inserted with one ballot + one shuffle: no shared memory and no sorting passes.  WPR warps
+// share one (row, chunk) task; their lists are merged by insertion at the end.  Rows are read
+// as float4 (4 entries per lane, 512 contiguous bytes per warp instruction), U loads in flight.
+// Out-of-range entries read as NaN, which never pass the filter (NaN distances sort last).
+constexpr int kRegThreads = 128;
+
+__device__ __forceinline__ void reg_insert(unsigned long long& lk, unsigned long long cand, int k,
+                                           int lane, unsigned long long& tk, float& tf) {
+  const unsigned long long up = __shfl_up_sync(0xffffffffu, lk, 1);
+  const unsigned gt = __ballot_sync(0xffffffffu, lk > cand);  // lanes >= k hold ~0 > cand
+  const int p = __ffs(gt) - 1;
+  if (lane > p) lk = up;
+  else if (lane == p) lk = cand;
+  if (lane >= k) lk = ~0ull;
+  tk = __shfl_sync(0xffffffffu, lk, k - 1);
+  tf = tk == ~0ull ? __uint_as_float(0x7F800000u) : fkey_inv((uint32_t)(tk >> 32));
+}
+
+template <int WPR>
+__global__ void __launch_bounds__(kRegThreads)
+    k_topk_reg(const float* __restrict__ dist, int64_t ldd, int64_t n_total, int64_t chunk, int k,
+               int64_t id_base, const int32_t* __restrict__ invalid, float* __restrict__ od,
+               int32_t* __restrict__ oi, int B, int tasks) {
+  constexpr int TPB = kRegThreads / 32 / WPR;  // tasks per block
+  constexpr int U = 4;
+  __shared__ unsigned long long part[kRegThreads / 32][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t = blockIdx.x * TPB + wid / WPR, sub = wid % WPR;
+  const bool live = t < tasks;
+  const int b = live ? t % B : 0, c = live ? t / B : 0;
+  const bool dead = !live || (invalid && invalid[b]);
+  const int64_t c0 = (int64_t)c * chunk;
+  const int64_t n = dead ? 0 : (n_total - c0 < chunk ? n_total - c0 : chunk);
+  const float* row = dist + (int64_t)b * ldd + c0;
+  unsigned long long lk = ~0ull, tk = ~0ull;
+  float tf = __uint_as_float(0x7F800000u);
+  const float kNaN = __uint_as_float(0x7FFFFFFFu);
+  const int64_t per = ((n + WPR - 1) / WPR + 127) / 128 * 128;
+  const int64_t w0 = (int64_t)sub * per, w1 = (w0 + per < n ? w0 + per : n);
+  const bool vec = (((uintptr_t)row) & 15) == 0;
+  for (int64_t base = w0; base < w1; base += 128 * U) {
+    float4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 128 + lane * 4;
+      if (vec && i + 4 <= w1) {
+        x[u] = __ldg(reinterpret_cast<const float4*>(row + i));
+      } else {
+        x[u].x = i < w1 ? row[i] : kNaN;
+        x[u].y = i + 1 < w1 ? row[i + 1] : kNaN;
+        x[u].z = i + 2 < w1 ? row[i + 2] : kNaN;
+        x[u].w = i + 3 < w1 ? row[i + 3] : kNaN;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float mn = fminf(fminf(x[u].x, x[u].y), fminf(x[u].z, x[u].w));
+      if (!__any_sync(0xffffffffu, mn <= tf)) continue;
+      const int64_t i0 = base + u * 128 + lane * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float xv = j == 0 ? x[u].x : j == 1 ? x[u].y : j == 2 ? x[u].z : x[u].w;
+        const unsigned long long key = ((unsigned long long)fkey(xv) << 32) | (uint32_t)(i0 + j);
+        unsigned m = __ballot_sync(0xffffffffu, xv <= tf);
+        while (m) {
+          const int src = __ffs(m) - 1;
+          const unsigned long long cand = __shfl_sync(0xffffffffu, key, src);
+          if (cand < tk) reg_insert(lk, cand, k, lane, tk, tf);
+          m &= m - 1;
+          m &= __ballot_sync(0xffffffffu, xv <= tf);
+        }
+      }
+    }
+  }
+  if (WPR > 1) {
+    part[wid][lane] = lk;
+    __syncthreads();
+    if (sub == 0) {
+      for (int w = 1; w < WPR; ++w) {
+        const unsigned long long mine = part[wid + w][lane];
+        unsigned m = __ballot_sync(0xffffffffu, lane < k && mine < tk);
+        while (m) {
+          const int src = __ffs(m) - 1;
+          const unsigned long long cand = __shfl_sync(0xffffffffu, mine, src);
+          if (cand < tk) reg_insert(lk, cand, k, lane, tk, tf);
+          m &= m - 1;
+        }
+      }
+    }
+  }
+  if (!live || sub != 0 || lane >= k) return;
+  const int64_t o = ((int64_t)c * B + b) * k + lane;
+  if (lk == ~0ull) {  // fewer than k entries (short chunk, NaN row, invalid query)
+    od[o] = kNaN;
+    oi[o] = -1;
+  } else {
+    od[o] = fkey_inv((uint32_t)(lk >> 32));
+    oi[o] = (int32_t)(id_base + c0 + (int64_t)(uint32_t)(lk & 0xFFFFFFFFu));
+  }
+}
+
 int64_t topk_chunk(int64_t n, int k) {
   // long rows are split so that many CTAs share a query; chunks * k must fit k_merge (4096)
   if (n <= kTopkStage * 2) return n;
@@ -189,6 +293,20 @@ int64_t topk_chunk(int64_t n, int k) {
 void launch_topk_kernel(dim3 grid, const float* dist, int64_t ldd, int64_t n, int64_t chunk, int k,
                         int64_t id_base, const int32_t* invalid, float* od, int32_t* oi, int B,
                         cudaStream_t st) {
+  if (k <= 32) {
+    const int tasks = (int)(grid.x * grid.y);
+    // enough warps in flight to cover memory latency: ~16 per SM
+    const int wpr = tasks >= 2048 ? 1 : tasks >= 768 ? 2 : 4;
+    const int tpb = kRegThreads / 32 / wpr;
+    const int blocks = (tasks + tpb - 1) / tpb;
+    if (wpr == 1)
+      k_topk_reg<1><<<blocks, kRegThreads, 0, st>>>(dist, ldd, n, chunk, k, id_base, invalid, od, oi, B, tasks);
+    else if (wpr == 2)
+      k_topk_reg<2><<<blocks, kRegThreads, 0, st>>>(dist, ldd, n, chunk, k, id_base, invalid, od, oi, B, tasks);
+    else
+      k_topk_reg<4><<<blocks, kRegThreads, 0, st>>>(dist, ldd, n, chunk, k, id_base, invalid, od, oi, B, tasks);
+    return;
+  }
   int P = 64;
   while (P < k + 32) P <<= 1;
   int Q = 1;
