@@ -103,10 +103,10 @@ struct kgq_ctx {
   // BetaE tensor-core scoring layout (score_tc.cu)
   float* uv_hi = nullptr;                  // [np][2d] centred (u; v), split
   float* uv_lo = nullptr;
-  double* Esum = nullptr;                  // [np]
+  float2* Esum = nullptr;                  // [np] sum_d C_ed as an fp32 (hi, lo) pair
   double* uvsums = nullptr;                // [2][d]
   kgq::Split Atc{};                        // [2*max_batch][2d] split query rows
-  double* Ptc = nullptr;                   // [2*max_batch]
+  float2* Ptc = nullptr;                   // [2*max_batch] P_q as an fp32 (hi, lo) pair
   int32_t* d_err = nullptr;                // [4]: flag, row, slot, kind
   int32_t* d_invalid = nullptr;            // [max_batch]
   int32_t* d_anchor_stage = nullptr;       // kgq_submit_host staging
@@ -228,9 +228,9 @@ int launch_filtered_counts(const float* dist, int64_t ldd, int64_t e0, int64_t n
 // uv [np][2d], E_e = sum_d C_ed (fp64) and the per-dim U/V sums; per batch it splits the
 // query rows, computes P_q (fp64) and runs the 3xTF32 GEMM with the score epilogue.
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
-                          double* sums, float* uv_hi, float* uv_lo, double* Esum, cudaStream_t st);
+                          double* sums, float* uv_hi, float* uv_lo, float2* Esum, cudaStream_t st);
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
-                          Split A, double* P, const float* uv_hi, const float* uv_lo, const double* Esum,
+                          Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
                           int64_t np, float* dist, int64_t ldd, cudaStream_t st);
 int launch_merge(int parts, int B, int k, const float* in_d, const int32_t* in_i, float* out_d,
                  int32_t* out_i, cudaStream_t st);

@@ -6,15 +6,9 @@
 //   x = x_hi + x_lo, w = w_hi + w_lo (hi = rna_tf32, lo = remainder; both exact in fp32)
 //   x w ~= x_hi w_lo + x_lo w_hi + x_hi w_hi          (x_lo w_lo, ~2^-22 relative, dropped)
 // accumulated in fp32 in TMEM.  Operands are produced already split (every producer kernel
-// writes hi/lo pairs), so the mainloop is a pure TMA -> tcgen05.mma pipeline:
-//   warp 0 / one lane : TMA producer, 4 tiles per stage (A_hi, A_lo, W_hi, W_lo), 128B swizzle
-//   warp 1 / one lane : MMA issuer, 3 x (BK/8) tcgen05.mma.kind::tf32 per stage, commit->empty
-//   warps 2-9         : epilogue; tcgen05.ld 32x32b (warp w owns TMEM lanes 32(w%4)..+31 = rows
-//                       and half of the BN columns),
-//                       partial sums added in fp32 registers, bias + ReLU / BetaE regulariser
-//                       (+ negation) fused, split (hi/lo) or fp32 store.
-// CTA tile 128 x BN (BN = 64 or 128) x BK = 32 fp32 (one 128-byte swizzle row), 3-4 stages;
-// TMEM holds two 128 x BN partial accumulators (ping-pong between MMA and epilogue).
+// writes hi/lo pairs), so the mainloop is a pure TMA -> tcgen05.mma pipeline; the GEMM core
+// (persistent CTA-pair kernel, TMA-store epilogue) is tc_gemm.cuh.  This file supplies the
+// epilogue: bias + ReLU / BetaE regulariser (+ negation) fused, split (hi/lo) or fp32 output.
 #include <stdint.h>
 
 #include "tc_gemm.cuh"
@@ -22,45 +16,28 @@
 namespace kgq {
 
 namespace {
-using tc::launch_tc_gemm;
 using tc::BM;
 
 // nn.Linear epilogue: + bias, ReLU / BetaE regulariser (clamp(y+1,.05,1e9)) with 1/x on rows
-// [neg0, neg1) (negation fused, Q5), output split (hi/lo) for a next dense layer or fp32.
-template <int CW, int EPI, bool SPLIT>
+// [neg0, neg1) (negation fused, Q5); output split (hi/lo, PLANES 2) for a next dense layer,
+// or fp32.
+template <int EPI, bool SPLIT>
 struct EpiLinear {
+  static constexpr int PLANES = SPLIT ? 2 : 1, ROWDIV = 1;
   const float* bias;
-  Split out;
-  int M, N, neg0, neg1;
-  __device__ __forceinline__ void apply(int row0, int lane, int n0, const float (&acc)[CW],
-                                        float* stage) const {
-    const int row = row0 + lane;
+  int N, neg0, neg1;
+  template <int CH>
+  __device__ __forceinline__ void chunk(int row, int n, float* v) const {
     const bool neg = row >= neg0 && row < neg1;
 #pragma unroll
-    for (int i = 0; i < CW; ++i) {
-      const int n = n0 + i;
-      float y = acc[i] + (n < N ? bias[n] : 0.0f);
+    for (int i = 0; i < CH; ++i) {
+      float y = v[i] + (n + i < N ? __ldg(bias + n + i) : 0.0f);
       if (EPI == kEpiRelu) y = fmaxf(y, 0.0f);
       if (EPI == kEpiBetaReg) {
         y = beta_reg(y);
         if (neg) y = 1.0f / y;
       }
-      stage[lane * (CW + 1) + i] = y;
-    }
-    __syncwarp();
-    for (int r = 0; r < 32; ++r) {  // row by row: lanes write consecutive columns
-      const int rr = row0 + r;
-      if (rr >= M) break;
-      const int64_t o = (int64_t)rr * out.ld + n0;
-#pragma unroll
-      for (int c = lane; c < CW; c += 32) {
-        if (n0 + c >= N) break;
-        const float y = stage[r * (CW + 1) + c];
-        if (SPLIT)
-          store_split(out.hi, out.lo, o + c, y);
-        else
-          out.hi[o + c] = y;
-      }
+      v[i] = y;
     }
   }
 };
@@ -68,9 +45,9 @@ struct EpiLinear {
 template <int EPI, bool SPLIT>
 int launch_epi(const Split& A, int M, int K, const Linear& L, Split out, int neg0, int neg1,
                cudaStream_t st) {
-  return tc::launch_gemm_auto(A, M, L.W_hi, L.W_lo, L.out_f, L.in_f, K, [&](auto cw) {
-    return EpiLinear<decltype(cw)::value, EPI, SPLIT>{L.b, out, M, L.out_f, neg0, neg1};
-  }, st);
+  const tc::OutDesc o{out.hi, out.lo, M, L.out_f, out.ld};
+  return tc::launch_gemm_auto(A, M, L.W_hi, L.W_lo, L.out_f, L.in_f, K, o,
+                              EpiLinear<EPI, SPLIT>{L.b, L.out_f, neg0, neg1}, st);
 }
 }  // namespace
 

@@ -8,6 +8,11 @@
 //   dist(q, e) = P_q + E_e + sum_d (aq_d u_ed + bq_d v_ed)
 //   P_q = sum_d (lnB(aq_d, bq_d) + aq_d Ubar_d + bq_d Vbar_d)     (fp64, per query row)
 //   E_e = sum_d C_ed                                               (fp64, per entity, finalize)
+// P_q and E_e are stored as fp32 pairs (hi = RN(x), lo = RN(x - hi)) and the epilogue forms
+// (P_hi + E_hi) + ((P_lo + E_lo) + acc) in fp32: the first sum is exact when it cancels
+// (Sterbenz; the usual case, P ~ -E) and otherwise errs by <= 2^-24 |P + E| ~ 2^-24 dist, the
+// dropped lo-lo rounding is ~2^-48 |P|, so dist carries ~1e-7 relative -- three FADDs instead
+// of fp64 adds and conversions, and no fp64 registers next to the row accumulators.
 // The last term is a dense contraction [rows, 2d] x [2d, N] -> 3xTF32 on tcgen05 (tc_gemm.cuh).
 // Centring keeps its terms ~0.1 (|u|, |v| << |U|, |V| ~ 1), so the fp32 partial sums carry
 // ~1e-7 of sum|terms| ~ 1e-5 absolute instead of ~1e-4 for the uncentred sum, and the large,
@@ -42,9 +47,14 @@ __global__ void k_uv_dim_sums(const float* __restrict__ ent, int64_t e0, int64_t
 }
 
 // Pass 2: centred split table uv [np][2d] = [u; v] (hi/lo) and E_e = sum_d C_ed (fp64).
+__device__ __forceinline__ float2 split_f64(double x) {
+  const float h = (float)x;
+  return make_float2(h, (float)(x - (double)h));
+}
+
 __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns, int64_t np, int d,
                            int64_t n_all, const double* __restrict__ sums, float* __restrict__ uv_hi,
-                           float* __restrict__ uv_lo, double* __restrict__ Esum) {
+                           float* __restrict__ uv_lo, float2* __restrict__ Esum) {
   const int64_t e = blockIdx.x;
   __shared__ double red[32];
   double c = 0.0;
@@ -66,7 +76,7 @@ __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns
   if (threadIdx.x < 32) {
     double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     t = warp_sum(t);
-    if (threadIdx.x == 0) Esum[e] = t;
+    if (threadIdx.x == 0) Esum[e] = split_f64(t);
   }
 }
 
@@ -74,7 +84,7 @@ __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns
 // P_q in fp64.
 __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
                                 const double* __restrict__ sums, int64_t ns, Split A,
-                                double* __restrict__ P) {
+                                float2* __restrict__ P) {
   const int r = blockIdx.x;
   __shared__ double red[32];
   double p = 0.0;
@@ -92,37 +102,26 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
   if (threadIdx.x < 32) {
     double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     t = warp_sum(t);
-    if (threadIdx.x == 0) P[r] = t;
+    if (threadIdx.x == 0) P[r] = split_f64(t);
   }
 }
 
-template <int CW, int NB>
+template <int NB>
 struct EpiBetaScore {
-  const double* P;  // [rows]
-  const double* E;  // [np]
-  float* dist;      // [rows / NB, ldd]
-  int64_t ldd;
+  static constexpr int PLANES = 1, ROWDIV = NB;
+  const float2* P;  // [rows] (hi, lo)
+  const float2* E;  // [np] (hi, lo); np is a multiple of 128, so pairs of columns share a bound
   int rows;
   int64_t ncols;    // np: the last column tile may overhang it
-  __device__ __forceinline__ void apply(int row0, int lane, int n0, const float (&acc)[CW],
-                                        float* stage) const {
-    const int row = row0 + lane;
-    const double p = row < rows ? P[row] : 0.0;
+  template <int CH>
+  __device__ __forceinline__ void chunk(int row, int n, float* v) const {
+    const float2 p = row < rows ? __ldg(P + row) : make_float2(0.0f, 0.0f);
 #pragma unroll
-    for (int i = 0; i < CW; ++i)
-      stage[lane * (CW + 1) + i] = n0 + i < ncols ? (float)(p + E[n0 + i] + (double)acc[i]) : 0.0f;
-    __syncwarp();
-    for (int r = 0; r < 32; r += NB) {  // (b, branch) rows 2b, 2b+1 -> min; coalesced rows of dist
-      const int rr = row0 + r;
-      if (rr >= rows) break;
-      float* drow = dist + (int64_t)(rr / NB) * ldd + n0;
-#pragma unroll
-      for (int c = lane; c < CW; c += 32) {
-        if (n0 + c >= ncols) break;
-        float v = stage[r * (CW + 1) + c];
-        if (NB == 2) v = fminf(v, stage[(r + 1) * (CW + 1) + c]);
-        drow[c] = v;
-      }
+    for (int i = 0; i < CH; i += 2) {
+      float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);  // columns n + i, n + i + 1
+      if (n + i < ncols) e = __ldg(reinterpret_cast<const float4*>(E + n + i));
+      v[i] = (p.x + e.x) + ((p.y + e.y) + v[i]);
+      v[i + 1] = (p.x + e.z) + ((p.y + e.w) + v[i + 1]);
     }
   }
 };
@@ -130,7 +129,7 @@ struct EpiBetaScore {
 }  // namespace
 
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
-                          double* sums, float* uv_hi, float* uv_lo, double* Esum, cudaStream_t st) {
+                          double* sums, float* uv_hi, float* uv_lo, float2* Esum, cudaStream_t st) {
   // centring means over ALL entities (every rank holds the full table), so that every shard
   // uses the same u, v and a sharded run is bit-identical to a single-GPU run
   cudaMemsetAsync(sums, 0, 2 * d * sizeof(double), st);
@@ -141,16 +140,16 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
 }
 
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
-                          Split A, double* P, const float* uv_hi, const float* uv_lo, const double* Esum,
+                          Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
                           int64_t np, float* dist, int64_t ldd, cudaStream_t st) {
   k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
+  // dist rows: one per query (NB = 2: min over the two DNF branch rows 2b, 2b + 1)
+  const tc::OutDesc o{dist, nullptr, rows / nbq, np, ldd};
   if (nbq == 2)
-    return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, [&](auto cw) {
-      return EpiBetaScore<decltype(cw)::value, 2>{P, Esum, dist, ldd, rows, np};
-    }, st);
-  return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, [&](auto cw) {
-    return EpiBetaScore<decltype(cw)::value, 1>{P, Esum, dist, ldd, rows, np};
-  }, st);
+    return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
+                                    EpiBetaScore<2>{P, Esum, rows, np}, st);
+  return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
+                                  EpiBetaScore<1>{P, Esum, rows, np}, st);
 }
 
 }  // namespace kgq

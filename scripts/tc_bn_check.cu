@@ -1,5 +1,6 @@
-// Correctness probe: every column-tile width of the tcgen05 GEMM core must give the same
-// y = x W^T (vs an fp64 host reference).  Not part of the library.
+// Correctness probe: every tile width of the persistent tcgen05 GEMM core, each epilogue form
+// (fp32 plane, split hi/lo planes, DNF row-pair min), ragged M / N / K, and a grid smaller
+// than the tile count (persistence), vs an fp64 host reference.  Not part of the library.
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -7,6 +8,7 @@
 
 #include "../paper_2503_02172_b200/csrc/chain.cu"
 #include "../paper_2503_02172_b200/csrc/linear_tc.cu"
+#include "../paper_2503_02172_b200/csrc/score_tc.cu"
 
 using namespace kgq;
 
@@ -14,49 +16,82 @@ int main() {
   const int M = 300, N = 520, K = 100;
   std::mt19937 g(1);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
-  std::vector<float> x((size_t)M * K), w((size_t)N * K), b(N, 0.f);
+  std::vector<float> x((size_t)M * K), w((size_t)N * K), b(N);
   for (auto& v : x) v = U(g);
   for (auto& v : w) v = U(g);
-  float *dx, *dxh, *dxl, *dw, *dwh, *dwl, *db, *dy;
-  cudaMalloc(&dx, x.size() * 4); cudaMalloc(&dxh, x.size() * 4); cudaMalloc(&dxl, x.size() * 4);
-  cudaMalloc(&dw, w.size() * 4); cudaMalloc(&dwh, w.size() * 4); cudaMalloc(&dwl, w.size() * 4);
-  cudaMalloc(&db, N * 4); cudaMalloc(&dy, (size_t)M * N * 4);
-  cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(dw, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
+  for (auto& v : b) v = U(g);
+  std::vector<double> ref((size_t)M * N), mag((size_t)M * N);
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < N; ++n) {
+      double s = 0, sa = 0;
+      for (int k = 0; k < K; ++k) {
+        s += (double)x[(size_t)m * K + k] * w[(size_t)n * K + k];
+        sa += fabs((double)x[(size_t)m * K + k] * w[(size_t)n * K + k]);
+      }
+      ref[(size_t)m * N + n] = s;
+      mag[(size_t)m * N + n] = sa + fabs(b[n]);
+    }
+  float *dxh, *dxl, *dwh, *dwl, *db, *dy;
+  float2 *dP, *dE;
+  cudaMalloc(&dxh, x.size() * 4); cudaMalloc(&dxl, x.size() * 4);
+  cudaMalloc(&dwh, w.size() * 4); cudaMalloc(&dwl, w.size() * 4);
+  cudaMalloc(&db, N * 4); cudaMalloc(&dy, (size_t)M * N * 4 * 2);
+  cudaMalloc(&dP, M * 8); cudaMalloc(&dE, 640 * 8);
+  cudaMemcpy(dxh, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dwh, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(db, b.data(), N * 4, cudaMemcpyHostToDevice);
-  launch_split_copy(dx, x.size(), dxh, dxl, 0);
-  launch_split_copy(dw, w.size(), dwh, dwl, 0);
-  Linear L; L.W = dw; L.W_hi = dwh; L.W_lo = dwl; L.b = db; L.out_f = N; L.in_f = K;
-  auto check = [&](const char* what, int bn, auto launch) {
-    cudaMemset(dy, 0, (size_t)M * N * 4);
+  cudaMemset(dP, 0, M * 8); cudaMemset(dE, 0, 640 * 8);
+  launch_split_copy(dxh, x.size(), dxh, dxl, 0);
+  launch_split_copy(dwh, w.size(), dwh, dwl, 0);
+  Split A{dxh, dxl, K};
+  int fails = 0;
+  // form 0: fp32 + bias (no activation); 1: split + bias + ReLU; 2: row-pair min (DNF union)
+  auto check = [&](const char* what, int bn, int form, auto launch) {
+    cudaMemset(dy, 0xff, (size_t)M * N * 4 * 2);  // NaN fill: every output must be written
     launch();
     cudaError_t e = cudaDeviceSynchronize();
-    std::vector<float> y((size_t)M * N);
+    std::vector<float> y((size_t)M * N * 2);
     cudaMemcpy(y.data(), dy, y.size() * 4, cudaMemcpyDeviceToHost);
-    double mx = 0; int bad = 0, fr = -1, fc = -1;
-    for (int m = 0; m < M; ++m)
+    double mx = 0;
+    int bad = 0;
+    const int rows = form == 2 ? M / 2 : M;
+    for (int m = 0; m < rows; ++m)
       for (int n = 0; n < N; ++n) {
-        double s = 0, sa = 0;
-        for (int k = 0; k < K; ++k) { s += (double)x[(size_t)m * K + k] * w[(size_t)n * K + k]; sa += fabs((double)x[(size_t)m * K + k] * w[(size_t)n * K + k]); }
-        const double r = fabs(y[(size_t)m * N + n] - s) / sa;
-        if (r > 1e-5) { if (!bad) { fr = m; fc = n; } ++bad; }
-        mx = fmax(mx, r);
+        double want, scale;
+        float got;
+        if (form == 2) {
+          want = fmin(ref[(size_t)(2 * m) * N + n], ref[(size_t)(2 * m + 1) * N + n]);
+          scale = fmax(mag[(size_t)(2 * m) * N + n], mag[(size_t)(2 * m + 1) * N + n]);
+          got = y[(size_t)m * N + n];
+        } else {
+          want = ref[(size_t)m * N + n] + b[n];
+          if (form == 1) want = fmax(want, 0.0);
+          scale = mag[(size_t)m * N + n];
+          got = y[(size_t)m * N + n];
+          if (form == 1) got += y[(size_t)M * N + (size_t)m * N + n];  // hi + lo
+        }
+        const double r = fabs((double)got - want) / scale;
+        if (!(r <= 1e-5)) ++bad;
+        if (r > mx || r != r) mx = r != r ? 1e30 : r;
       }
-    printf("%s BN=%3d max err %.3e  bad %d (first row %d col %d)  %s\n", what, bn, mx, bad, fr, fc, cudaGetErrorString(e));
+    fails += bad > 0 || e != cudaSuccess;
+    printf("%-28s BN=%3d max err %.3e (of sum|x w|)  bad %d  %s\n", what, bn, mx, bad, cudaGetErrorString(e));
   };
-  Split A{dxh, dxl, K};
-  Split out{dy, nullptr, N};
-  for (int bn : {32, 64, 96, 128, 160, 192, 256})
-    tc::dispatch_bn(bn, [&](auto c) {
-      constexpr int B = decltype(c)::value;
-      check("1-CTA", B, [&] { tc::launch_tc_gemm<B>(A, M, dwh, dwl, N, K, K, EpiLinear<B / 2, kEpiNone, false>{db, out, M, N, 0, 0}, 0); });
-      return 0;
-    });
-  check("2-CTA", 64, [&] { tc::launch_tc_gemm2<64>(A, M, dwh, dwl, N, K, K, EpiLinear<32, kEpiNone, false>{db, out, M, N, 0, 0}, 0); });
-  check("2-CTA", 128, [&] { tc::launch_tc_gemm2<128>(A, M, dwh, dwl, N, K, K, EpiLinear<64, kEpiNone, false>{db, out, M, N, 0, 0}, 0); });
-  check("2-CTA", 192, [&] { tc::launch_tc_gemm2<192>(A, M, dwh, dwl, N, K, K, EpiLinear<96, kEpiNone, false>{db, out, M, N, 0, 0}, 0); });
-  check("2-CTA", 224, [&] { tc::launch_tc_gemm2<224>(A, M, dwh, dwl, N, K, K, EpiLinear<112, kEpiNone, false>{db, out, M, N, 0, 0}, 0); });
-  check("2-CTA", 256, [&] { tc::launch_tc_gemm2<256>(A, M, dwh, dwl, N, K, K, EpiLinear<128, kEpiNone, false>{db, out, M, N, 0, 0}, 0); });
-  check("auto ", 0, [&] { launch_linear(A, M, K, L, kEpiNone, out, 0, 0, 0); });
-  return 0;
+  auto each_bn = [&](auto f) {
+    f(std::integral_constant<int, 64>{});
+    f(std::integral_constant<int, 128>{});
+    f(std::integral_constant<int, 192>{});
+    f(std::integral_constant<int, 256>{});
+  };
+  each_bn([&](auto c) {
+    constexpr int B = decltype(c)::value;
+    const tc::OutDesc o1{dy, nullptr, M, N, N}, o2{dy, dy + (size_t)M * N, M, N, N};
+    check("fp32 + bias", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0); });
+    check("split + bias + relu", B, 1, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0); });
+    check("fp32, 2 clusters (persist)", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, 2); });
+    const tc::OutDesc o3{dy, nullptr, M / 2, N, N};
+    check("row-pair min (union)", B, 2, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0); });
+  });
+  printf(fails ? "FAILED (%d)\n" : "all tile widths and epilogues OK\n", fails);
+  return fails ? 1 : 0;
 }

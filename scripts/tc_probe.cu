@@ -1,0 +1,104 @@
+// Throughput probe for the persistent tcgen05 3xTF32 GEMM core (not part of the library):
+// the C2 step's shapes -- BetaE MLP layers (M = B x branches) and the tensor-core scorer
+// (N = padded shard, K = 2d) -- timed per tile width and with the launch's own choice.
+// With -DKGQ_TC_TRACE (scripts/tc_probe.sh) it also prints per-tile phase times.
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "../paper_2503_02172_b200/csrc/chain.cu"
+#include "../paper_2503_02172_b200/csrc/linear_tc.cu"
+#include "../paper_2503_02172_b200/csrc/score_tc.cu"
+
+using namespace kgq;
+
+template <class F>
+static double time_us(F&& launch) {
+  for (int i = 0; i < 3; ++i) launch();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  const int reps = 20;
+  for (int i = 0; i < reps; ++i) launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  return ms / reps * 1e3;
+}
+
+int main() {
+  struct Shape { int M, N, K; bool score; };
+  const Shape shapes[] = {{1024, 1600, 1200, false}, {3072, 1600, 1600, false}, {2048, 800, 1600, false},
+                          {2048, 800, 800, false},   {1024, 14592, 800, true},  {2048, 14592, 800, true},
+                          {1024, 14592, 32, true},   {1024, 1600, 32, false}};
+#ifdef KGQ_TC_TRACE
+  unsigned long long* tr;
+  cudaMalloc(&tr, 8192 * 64);
+  cudaMemcpyToSymbol(tc::g_tc_trace, &tr, sizeof(tr));
+#endif
+  for (const Shape& sh : shapes) {
+    const int M = sh.M, N = sh.N, K = sh.K;
+    float *xh, *xl, *wh, *wl, *b, *y;
+    float2 *P, *E;
+    cudaMalloc(&xh, (size_t)M * K * 4); cudaMalloc(&xl, (size_t)M * K * 4);
+    cudaMalloc(&wh, (size_t)N * K * 4); cudaMalloc(&wl, (size_t)N * K * 4);
+    cudaMalloc(&b, N * 4); cudaMalloc(&y, (size_t)M * N * 4 * 2);
+    cudaMalloc(&P, M * 8); cudaMalloc(&E, N * 8);
+    std::vector<float> hx((size_t)M * K), hw((size_t)N * K);  // non-zero operands
+    for (size_t i = 0; i < hx.size(); ++i) hx[i] = (float)((i * 2654435761u) % 1000) * 1e-3f - 0.5f;
+    for (size_t i = 0; i < hw.size(); ++i) hw[i] = (float)((i * 40503u) % 1000) * 1e-3f - 0.5f;
+    cudaMemcpy(xh, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(wh, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice);
+    launch_split_copy(xh, (int64_t)M * K, xh, xl, 0);
+    launch_split_copy(wh, (int64_t)N * K, wh, wl, 0);
+    cudaMemset(b, 0, N * 4); cudaMemset(P, 0, M * 8); cudaMemset(E, 0, N * 8);
+    Split A{xh, xl, K};
+    auto run = [&](int bn) {
+      auto go = [&](auto c) {
+        constexpr int B = decltype(c)::value;
+        if (sh.score)
+          tc::launch_gemm<B>(A, M, wh, wl, N, K, K, tc::OutDesc{y, nullptr, M, N, N},
+                             EpiBetaScore<1>{P, E, M, (int64_t)N}, 0);
+        else
+          tc::launch_gemm<B>(A, M, wh, wl, N, K, K, tc::OutDesc{y, y + (size_t)M * N, M, N, N},
+                             EpiLinear<kEpiRelu, true>{b, N, 0, 0}, 0);
+      };
+      switch (bn) {
+        case 64: go(std::integral_constant<int, 64>{}); break;
+        case 128: go(std::integral_constant<int, 128>{}); break;
+        case 192: go(std::integral_constant<int, 192>{}); break;
+        default: go(std::integral_constant<int, 256>{}); break;
+      }
+    };
+    const int pick = tc::choose_bn(M, N, K);
+    printf("M=%5d N=%5d K=%5d %s |", M, N, K, sh.score ? "score " : "linear");
+    for (int bn : {64, 128, 192, 256}) printf(" %d:%.1f", bn, time_us([&] { run(bn); }));
+    const double us = time_us([&] { run(pick); });
+    printf(" | pick %d: %.1f us %.1f TFLOP/s useful\n", pick, us, 2.0 * M * N * K / us * 1e-6);
+#ifdef KGQ_TC_TRACE
+    {
+      const int tiles = ((M + 255) / 256) * ((N + pick - 1) / pick);
+      cudaMemset(tr, 0, 8192 * 64);
+      run(pick);
+      cudaDeviceSynchronize();
+      std::vector<unsigned long long> h((size_t)tiles * 8);
+      cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull, tend = 0;
+      double ph[4] = {0};
+      for (int t = 0; t < tiles; ++t) {
+        t0 = std::min(t0, h[t * 8]);
+        tend = std::max(tend, h[t * 8 + 4]);
+        for (int i = 0; i < 4; ++i) ph[i] += (double)(h[t * 8 + i + 1] - h[t * 8 + i]) * 1e-3 / tiles;
+      }
+      printf("    trace: %d tiles, span %.1f us; per tile (us): wait-first-stage %.2f mainloop %.2f "
+             "drain-tail %.2f epilogue %.2f\n", tiles, (tend - t0) * 1e-3, ph[0], ph[1], ph[2], ph[3]);
+    }
+#endif
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
+    cudaFree(xh); cudaFree(xl); cudaFree(wh); cudaFree(wl); cudaFree(b); cudaFree(y); cudaFree(P); cudaFree(E);
+  }
+  return 0;
+}

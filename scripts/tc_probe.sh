@@ -1,0 +1,16 @@
+# Build (here, CPU) or run (GPU box: `run`) the persistent tc GEMM probe and its checkers.
+cd "$(dirname "$0")"
+NVCC=/usr/local/cuda/bin/nvcc
+FL="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a --expt-relaxed-constexpr -lcuda -diag-suppress 177"
+if [ "$1" = "run" ]; then
+  echo "== bn check"; timeout 120 ./tc_bn_check
+  echo "== probe"; timeout 120 ./tc_probe_base
+  echo "== probe (no PDL)"; KGQ_NO_PDL=1 timeout 120 ./tc_probe_base
+  echo "== trace"; timeout 120 ./tc_probe_trace
+  exit 0
+fi
+$NVCC $FL tc_probe.cu -o tc_probe_base &
+$NVCC $FL -DKGQ_TC_TRACE tc_probe.cu -o tc_probe_trace &
+$NVCC $FL tc_bn_check.cu -o tc_bn_check &
+wait
+ls tc_probe_* tc_bn_check
