@@ -203,7 +203,7 @@ void check_site(const char* site) {
 int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
           int neg1, cudaStream_t st) {
   StageTimer t(ctx, st, kStDense, 2.0 * M * (double)L.out_f * K);
-  const int r = launch_linear(A, M, K, L, epi, out, neg0, neg1, st);
+  const int r = launch_linear(A, M, K, L, epi, out, neg0, neg1, &ctx->gws, st);
   check_site("dense layer");
   return r;
 }
@@ -485,7 +485,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) { F(s->hi); F(s->lo); }
   F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->d_err); F(ctx->d_invalid);
   F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv_hi); F(ctx->uv_lo); F(ctx->Esum);
-  F(ctx->uvsums); F(ctx->Atc.hi); F(ctx->Atc.lo); F(ctx->Ptc);
+  F(ctx->uvsums); F(ctx->Atc.hi); F(ctx->Atc.lo); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -612,6 +612,9 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
     if (!st) st = alloc_split(ctx, &ctx->Atc, 2 * ctx->bchunk, 2 * d, "tc query rows");
     if (!st) st = dalloc(ctx, &ctx->Ptc, (size_t)(2 * ctx->bchunk), "tc query sums");
   }
+  if (!st) st = dalloc(ctx, &ctx->gws.ws, kGemmWsFloats, "gemm split workspace");
+  if (!st) st = dalloc(ctx, &ctx->gws.cnt, (size_t)kGemmCntInts, "gemm split counters");
+  if (!st) CK(cudaMemset(ctx->gws.cnt, 0, kGemmCntInts * sizeof(int)), "gemm split counters");
   if (!st) st = dalloc(ctx, &ctx->score_tab, (size_t)((c.model == KGQ_BETAE ? 3 : 1) * d * ctx->np), "score table");
   if (!st) st = dalloc(ctx, &ctx->d_anchor_stage, (size_t)(Bm * kMaxBranches), "staging");
   if (!st) st = dalloc(ctx, &ctx->d_rel_stage, (size_t)(Bm * kMaxBranches), "staging");
@@ -642,7 +645,7 @@ static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStrea
     // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
     StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
     L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
-                               ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist, ctx->np, st);
+                               ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist, ctx->np, &ctx->gws, st);
     check_site("tensor-core scorer");
   } else {
     {

@@ -60,6 +60,15 @@ struct Linear {
 
 enum Epi { kEpiNone = 0, kEpiRelu = 1, kEpiBetaReg = 2 };
 
+// Per-context scratch of the tensor-core GEMM's split tail (tc_gemm.cuh Sched): fp32 partial
+// sums and arrival counters (zeroed once; every launch leaves them zero).
+struct GemmWs {
+  float* ws = nullptr;
+  int* cnt = nullptr;
+};
+constexpr size_t kGemmWsFloats = (size_t)74 * 256 * 256;  // <= 74 tail units of 256 x 256
+constexpr int kGemmCntInts = 74 * 16;                      // <= 74 tail tiles x 16 epilogue warps
+
 // A timed region: CUDA events recorded on the launching stream around one stage.
 struct ProfRec {
   int stage;
@@ -105,6 +114,7 @@ struct kgq_ctx {
   float* uv_lo = nullptr;
   float2* Esum = nullptr;                  // [np] sum_d C_ed as an fp32 (hi, lo) pair
   double* uvsums = nullptr;                // [2][d]
+  kgq::GemmWs gws{};                       // tensor-core GEMM split-tail scratch
   kgq::Split Atc{};                        // [2*max_batch][2d] split query rows
   float2* Ptc = nullptr;                   // [2*max_batch] P_q as an fp32 (hi, lo) pair
   int32_t* d_err = nullptr;                // [4]: flag, row, slot, kind
@@ -176,7 +186,7 @@ int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* re
 //   split output if out.lo != nullptr, else plain fp32 into out.hi.
 //   kEpiBetaReg: clamp(y+1, .05, 1e9), then 1/x on rows [neg0, neg1).
 int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split out,
-                  int neg0, int neg1, cudaStream_t st);
+                  int neg0, int neg1, const GemmWs* ws, cudaStream_t st);
 // BetaE Eq.-4 softmax terminal over rows of T (width w) -> split state rows out_row0 + r,
 // with negation on rows r in [neg0, neg1).
 int launch_softmax_terminal(const float* T, int64_t ldt, int M, int w, Split out,
@@ -231,7 +241,7 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
                           double* sums, float* uv_hi, float* uv_lo, float2* Esum, cudaStream_t st);
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
                           Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
-                          int64_t np, float* dist, int64_t ldd, cudaStream_t st);
+                          int64_t np, float* dist, int64_t ldd, const GemmWs* ws, cudaStream_t st);
 int launch_merge(int parts, int B, int k, const float* in_d, const int32_t* in_i, float* out_d,
                  int32_t* out_i, cudaStream_t st);
 // Table preparation (finalize).

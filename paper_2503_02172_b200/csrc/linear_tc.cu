@@ -26,16 +26,27 @@ struct EpiLinear {
   static constexpr int PLANES = SPLIT ? 2 : 1, ROWDIV = 1;
   const float* bias;
   int N, neg0, neg1;
+  struct Pre {
+    float b[4];  // bias of columns n0 + lane + 32 j
+    bool neg;
+  };
+  template <int CW>
+  __device__ __forceinline__ Pre prefetch(int row, int n0, int lane) const {
+    Pre p;
+#pragma unroll
+    for (int j = 0; j < CW / 32; ++j) p.b[j] = n0 + lane + 32 * j < N ? __ldg(bias + n0 + lane + 32 * j) : 0.0f;
+    p.neg = row >= neg0 && row < neg1;
+    return p;
+  }
   template <int CH>
-  __device__ __forceinline__ void chunk(int row, int n, float* v) const {
-    const bool neg = row >= neg0 && row < neg1;
+  __device__ __forceinline__ void chunk(const Pre& p, int row, int c, float* v) const {
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
-      float y = v[i] + (n + i < N ? __ldg(bias + n + i) : 0.0f);
+      float y = v[i] + __shfl_sync(0xffffffffu, p.b[(c + i) >> 5], (c + i) & 31);
       if (EPI == kEpiRelu) y = fmaxf(y, 0.0f);
       if (EPI == kEpiBetaReg) {
         y = beta_reg(y);
-        if (neg) y = 1.0f / y;
+        if (p.neg) y = 1.0f / y;
       }
       v[i] = y;
     }
@@ -44,27 +55,27 @@ struct EpiLinear {
 
 template <int EPI, bool SPLIT>
 int launch_epi(const Split& A, int M, int K, const Linear& L, Split out, int neg0, int neg1,
-               cudaStream_t st) {
+               const GemmWs* ws, cudaStream_t st) {
   const tc::OutDesc o{out.hi, out.lo, M, L.out_f, out.ld};
   return tc::launch_gemm_auto(A, M, L.W_hi, L.W_lo, L.out_f, L.in_f, K, o,
-                              EpiLinear<EPI, SPLIT>{L.b, L.out_f, neg0, neg1}, st);
+                              EpiLinear<EPI, SPLIT>{L.b, L.out_f, neg0, neg1}, ws, st);
 }
 }  // namespace
 
 int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
-                  int neg1, cudaStream_t st) {
+                  int neg1, const GemmWs* ws, cudaStream_t st) {
   if (M <= 0) return 0;
   const bool split = out.lo != nullptr;
   switch (epi) {
     case kEpiRelu:
-      return split ? launch_epi<kEpiRelu, true>(A, M, K, L, out, neg0, neg1, st)
-                   : launch_epi<kEpiRelu, false>(A, M, K, L, out, neg0, neg1, st);
+      return split ? launch_epi<kEpiRelu, true>(A, M, K, L, out, neg0, neg1, ws, st)
+                   : launch_epi<kEpiRelu, false>(A, M, K, L, out, neg0, neg1, ws, st);
     case kEpiBetaReg:
-      return split ? launch_epi<kEpiBetaReg, true>(A, M, K, L, out, neg0, neg1, st)
-                   : launch_epi<kEpiBetaReg, false>(A, M, K, L, out, neg0, neg1, st);
+      return split ? launch_epi<kEpiBetaReg, true>(A, M, K, L, out, neg0, neg1, ws, st)
+                   : launch_epi<kEpiBetaReg, false>(A, M, K, L, out, neg0, neg1, ws, st);
     default:
-      return split ? launch_epi<kEpiNone, true>(A, M, K, L, out, neg0, neg1, st)
-                   : launch_epi<kEpiNone, false>(A, M, K, L, out, neg0, neg1, st);
+      return split ? launch_epi<kEpiNone, true>(A, M, K, L, out, neg0, neg1, ws, st)
+                   : launch_epi<kEpiNone, false>(A, M, K, L, out, neg0, neg1, ws, st);
   }
 }
 

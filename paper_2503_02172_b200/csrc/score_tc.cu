@@ -110,18 +110,29 @@ template <int NB>
 struct EpiBetaScore {
   static constexpr int PLANES = 1, ROWDIV = NB;
   const float2* P;  // [rows] (hi, lo)
-  const float2* E;  // [np] (hi, lo); np is a multiple of 128, so pairs of columns share a bound
+  const float2* E;  // [np] (hi, lo)
   int rows;
   int64_t ncols;    // np: the last column tile may overhang it
-  template <int CH>
-  __device__ __forceinline__ void chunk(int row, int n, float* v) const {
-    const float2 p = row < rows ? __ldg(P + row) : make_float2(0.0f, 0.0f);
+  struct Pre {
+    float2 p;       // P of this lane's row
+    float2 e[4];    // E of columns n0 + lane + 32 j
+  };
+  template <int CW>
+  __device__ __forceinline__ Pre prefetch(int row, int n0, int lane) const {
+    Pre r;
+    r.p = row < rows ? __ldg(P + row) : make_float2(0.0f, 0.0f);
 #pragma unroll
-    for (int i = 0; i < CH; i += 2) {
-      float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);  // columns n + i, n + i + 1
-      if (n + i < ncols) e = __ldg(reinterpret_cast<const float4*>(E + n + i));
-      v[i] = (p.x + e.x) + ((p.y + e.y) + v[i]);
-      v[i + 1] = (p.x + e.z) + ((p.y + e.w) + v[i + 1]);
+    for (int j = 0; j < CW / 32; ++j)
+      r.e[j] = n0 + lane + 32 * j < ncols ? __ldg(E + n0 + lane + 32 * j) : make_float2(0.0f, 0.0f);
+    return r;
+  }
+  template <int CH>
+  __device__ __forceinline__ void chunk(const Pre& r, int row, int c, float* v) const {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const float eh = __shfl_sync(0xffffffffu, r.e[(c + i) >> 5].x, (c + i) & 31);
+      const float el = __shfl_sync(0xffffffffu, r.e[(c + i) >> 5].y, (c + i) & 31);
+      v[i] = (r.p.x + eh) + ((r.p.y + el) + v[i]);
     }
   }
 };
@@ -141,15 +152,15 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
 
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
                           Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
-                          int64_t np, float* dist, int64_t ldd, cudaStream_t st) {
+                          int64_t np, float* dist, int64_t ldd, const GemmWs* ws, cudaStream_t st) {
   k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
   // dist rows: one per query (NB = 2: min over the two DNF branch rows 2b, 2b + 1)
   const tc::OutDesc o{dist, nullptr, rows / nbq, np, ldd};
   if (nbq == 2)
     return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
-                                    EpiBetaScore<2>{P, Esum, rows, np}, st);
+                                    EpiBetaScore<2>{P, Esum, rows, np}, ws, st);
   return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
-                                  EpiBetaScore<1>{P, Esum, rows, np}, st);
+                                  EpiBetaScore<1>{P, Esum, rows, np}, ws, st);
 }
 
 }  // namespace kgq

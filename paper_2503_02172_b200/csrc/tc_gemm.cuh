@@ -27,6 +27,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -170,6 +171,7 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {  // arrive on ba
 }
 // Programmatic dependent launch: wait for the upstream grid's results / let the next grid's
 // CTAs start their setup (no-ops when the launch carries no PDL attribute).
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -212,18 +214,46 @@ struct Layout {
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "2-CTA tile: N multiple of 32 per CTA, CW multiple of 32");
 };
 
+// Work split of one launch.  Tiles [0, full) -- complete rounds over the clusters -- are
+// computed whole; each remaining (tail) tile is split into s_tail K ranges of kper K-blocks so
+// the last round fills the machine.  Every split writes its fp32 partial sums to the workspace
+// and bumps a per-(tile, epilogue warp) counter; the warp that arrives last adds the other
+// partials and runs the epilogue.  Nobody waits for another CTA, so the schedule is correct
+// whatever subset of the grid is resident.
+struct Sched {
+  int full;    // tiles computed whole
+  int s_tail;  // K splits per tail tile (1: none)
+  int kper;    // K-blocks per split
+  float* ws;   // [tail units][16 epilogue warps][BN / 8][32 lanes] float4 partial sums
+  int* cnt;    // [tail tiles][16] arrival counters (zero between launches; the last arriver resets)
+};
+__device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, int& kb0, int& kb1, int& v) {
+  if (u < sc.full) {
+    t = u; kb0 = 0; kb1 = nk; v = -1;
+    return;
+  }
+  v = u - sc.full;  // tail unit: workspace slot
+  t = sc.full + v / sc.s_tail;
+  kb0 = (v % sc.s_tail) * sc.kper;
+  kb1 = min(nk, kb0 + sc.kper);
+}
+
 // Epilogue policy concept (linear_tc.cu, score_tc.cu):
 //   static constexpr int PLANES  -- 1: fp32 output; 2: split output (hi = rna_tf32(y), lo = y - hi)
 //   static constexpr int ROWDIV  -- 1, or 2: output row r = min over tile rows 2r, 2r+1 (DNF union)
-//   template <int CH> __device__ void chunk(int row, int n, float* v) const
-//       -- v[i] (i < CH) = accumulator of (row, n + i) on entry, output value on exit
+//   struct Pre; template <int CW> __device__ Pre prefetch(int row, int n0, int lane) const
+//       -- per-tile operands (row terms, and column vectors with lane l holding columns
+//          n0 + l + 32 j), loaded before the tile's drains so their latency is hidden
+//   template <int CH> __device__ void chunk(const Pre&, int row, int c, float* v) const
+//       -- v[i] (i < CH) = accumulator of (row, n0 + c + i) on entry, output value on exit;
+//          column operands come from the prefetched registers by warp shuffle
 // Output tensor maps: plane p, box {32 / PLANES columns, 32 / ROWDIV rows}.
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
            const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
            const __grid_constant__ CUtensorMap mO0, const __grid_constant__ CUtensorMap mO1, int M, int N, int K,
-           const Epi epi) {
+           const Sched sc, const Epi epi) {
   using L = Layout<BN>;
   constexpr int STAGES = L::STAGES;
   constexpr int PLANES = Epi::PLANES, ROWDIV = Epi::ROWDIV;
@@ -243,8 +273,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int m_pairs = (M + 2 * BM - 1) / (2 * BM);
   const int ntiles = m_pairs * ((N + BN - 1) / BN);
+  const int nunits = sc.full + (ntiles - sc.full) * sc.s_tail;
   const int nk = (K + BK - 1) / BK;
-  const int ng = (nk + DRAIN - 1) / DRAIN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mAh);
@@ -280,10 +310,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs; completions counted by the leader) ----------------
       uint32_t it = 0;
-      for (int t = cluster; t < ntiles; t += nclusters) {
+      for (int u = cluster; u < nunits; u += nclusters) {
+        int t, kb0, kb1, v;
+        unit_of(u, sc, nk, t, kb0, kb1, v);
         const int m0 = (t % m_pairs) * 2 * BM + (int)rank * BM;
         const int nw = (t / m_pairs) * BN + (int)rank * (BN / 2);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
           uint8_t* st = smem + s * L::STAGE_BYTES;
@@ -302,15 +334,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)((2 * BM) >> 4) << 24);
       uint32_t it = 0, g0 = 0;
-      for (int t = cluster; t < ntiles; t += nclusters, g0 += ng) {
-        TC_TRACE(t, 0);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+      for (int u = cluster; u < nunits; u += nclusters) {
+        int t, kb0, kb1, v;
+        unit_of(u, sc, nk, t, kb0, kb1, v);
+        TC_TRACE(u, 0);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
-          const uint32_t g = g0 + kb / DRAIN, a = g & 1;
-          const bool first = (kb % DRAIN) == 0;
+          const int kr = kb - kb0;
+          const uint32_t g = g0 + kr / DRAIN, a = g & 1;
+          const bool first = (kr % DRAIN) == 0;
           if (first && g >= 2) mbar_wait(&accempty[a], ((g >> 1) - 1) & 1);
           mbar_wait(&full[s], (it / STAGES) & 1);
-          if (kb == 0) TC_TRACE(t, 1);
+          if (kr == 0) TC_TRACE(u, 1);
           fence_after();
           const uint32_t d = tmem + a * BN;
           const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
@@ -325,9 +360,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             mma_tf32_2sm(d, umma_desc_sw128(ah + off), umma_desc_sw128(wh + off), idesc, 1u);
           }
           mma_commit_2sm(&empty[s]);  // frees the smem stage (both CTAs) once these MMAs have read it
-          if ((kb % DRAIN) == DRAIN - 1 || kb == nk - 1) mma_commit_2sm(&accfull[a]);
+          if ((kr % DRAIN) == DRAIN - 1 || kb == kb1 - 1) mma_commit_2sm(&accfull[a]);
         }
-        TC_TRACE(t, 2);
+        g0 += (kb1 - kb0 + DRAIN - 1) / DRAIN;
+        TC_TRACE(u, 2);
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -337,9 +373,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint8_t* stg = smem + L::STG_OFF + (warp - EPI_WARP0) * L::BUF_BYTES;
     const uint32_t accempty_leader = mapa_shared(smem_u32(&accempty[0]), 0);
     uint32_t g0 = 0, nchunk = 0;
-    for (int t = cluster; t < ntiles; t += nclusters, g0 += ng) {
+    for (int u = cluster; u < nunits; u += nclusters) {
+      int t, kb0, kb1, v;
+      unit_of(u, sc, nk, t, kb0, kb1, v);
+      const int ng = (kb1 - kb0 + DRAIN - 1) / DRAIN;
       const int row0 = (t % m_pairs) * 2 * BM + (int)rank * BM + q * 32;
       const int n0 = (t / m_pairs) * BN + ch;
+      const auto pre = epi.template prefetch<CW>(row0 + lane, n0, lane);
       float acc[CW];
 #pragma unroll
       for (int i = 0; i < CW; ++i) acc[i] = 0.0f;
@@ -362,12 +402,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0)
           asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(accempty_leader + a * 8) : "memory");
       }
-      if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(t, 3);
+      g0 += ng;
+      if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 3);
+      if (v >= 0 && sc.s_tail > 1) {
+        // ---- split tail tile: publish this split's partial sums; the last arriver reduces ----
+        const int tt = v / sc.s_tail, slot = (int)rank * EPI_WARPS + (warp - EPI_WARP0);
+        // workspace slot of (unit, warp): [CW / 4][32 lanes] float4, so every access is 512 B
+        // contiguous per warp (row-per-lane addressing would cost one L2 request per lane)
+        float4* mine = reinterpret_cast<float4*>(sc.ws) + ((size_t)v * 2 * EPI_WARPS + slot) * 8 * CW + lane;
+#pragma unroll
+        for (int c = 0; c < CW; c += 4) __stcg(mine + c * 8, make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]));
+        fence_acq_rel_gpu();  // release: this lane's partials before the arrival count
+        __syncwarp();
+        if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 5);
+        int old = 0;
+        if (lane == 0) old = atomicAdd(&sc.cnt[tt * 2 * EPI_WARPS + slot], 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 6);
+        if (old != sc.s_tail - 1) {  // another split finishes this slice
+          if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 4);
+          continue;
+        }
+        fence_acq_rel_gpu();  // acquire: the other splits' partials after their counts
+        for (int s2 = 0; s2 < sc.s_tail; ++s2) {
+          if (s2 == v % sc.s_tail) continue;
+          const float4* other =
+              reinterpret_cast<const float4*>(sc.ws) + ((size_t)(tt * sc.s_tail + s2) * 2 * EPI_WARPS + slot) * 8 * CW + lane;
+#pragma unroll
+          for (int c = 0; c < CW; c += 4) {
+            const float4 o = __ldcg(other + c * 8);
+            acc[c] += o.x;
+            acc[c + 1] += o.y;
+            acc[c + 2] += o.z;
+            acc[c + 3] += o.w;
+          }
+        }
+        if (lane == 0) sc.cnt[tt * 2 * EPI_WARPS + slot] = 0;  // ready for the next launch
+        if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 7);
+      }
       // ---- epilogue of this tile (the MMA warp is already on the next tile's partials) ----
 #pragma unroll
       for (int c = 0; c < CW; c += CH, ++nchunk) {
         float* v = acc + c;  // in place (unrolled: stays in registers)
-        epi.template chunk<CH>(row0 + lane, n0 + c, v);
+        epi.template chunk<CH>(pre, row0 + lane, c, v);
         if (ROWDIV == 2) {
 #pragma unroll
           for (int i = 0; i < CH; ++i) v[i] = fminf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1));
@@ -399,13 +476,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
+#ifndef KGQ_TC_DBG_NO_STORE  // perf probe only: skip the output stores
         if (lane == 0) {
           tma_store_2d(&mO0, buf, n0 + c, row0 / ROWDIV);
           if (PLANES == 2) tma_store_2d(&mO1, buf + 2048, n0 + c, row0);
           bulk_commit();
         }
+#endif
       }
-      if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(t, 4);
+      if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 4);
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -485,9 +564,14 @@ inline bool pdl_enabled() {
   return v == 1;
 }
 
+// Per-context scratch of the split tail (kgq_internal.cuh GemmWs): at most kClustersMax tail
+// units of 256 x 256 fp32 and kClustersMax x 16 counters.
+static_assert(kGemmWsFloats >= (size_t)kClustersMax * 2 * BM * 256, "split-tail workspace");
+static_assert(kGemmCntInts >= kClustersMax * 2 * EPI_WARPS, "split-tail counters");
+
 template <int BN, class Epi>
 int launch_gemm(const Split& A, int M, const float* Wh, const float* Wl, int N, int64_t ldw, int K,
-                const OutDesc& o, const Epi& epi, cudaStream_t st, int max_clusters = kClustersMax) {
+                const OutDesc& o, const Epi& epi, cudaStream_t st, Sched sc, int max_clusters = kClustersMax) {
   constexpr int PLANES = Epi::PLANES, ROWDIV = Epi::ROWDIV;
   CUtensorMap mAh, mAl, mWh, mWl, mO0, mO1;
   if (!make_map(&mAh, A.hi, M, K, A.ld, BM) || !make_map(&mAl, A.lo, M, K, A.ld, BM) ||
@@ -505,7 +589,12 @@ int launch_gemm(const Split& A, int M, const float* Wh, const float* Wl, int N, 
     attr = true;
   }
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
-  const int clusters = tiles < max_clusters ? tiles : max_clusters;
+  if (sc.s_tail <= 1 || !sc.ws || !sc.cnt) {
+    sc.full = tiles;
+    sc.s_tail = 1;
+  }
+  const int units = sc.full + (tiles - sc.full) * sc.s_tail;
+  const int clusters = units < max_clusters ? units : max_clusters;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(THREADS);
@@ -516,27 +605,41 @@ int launch_gemm(const Split& A, int M, const float* Wh, const float* Wl, int N, 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, mAh, mAl, mWh, mWl, mO0, mO1, M, N, K, epi);
+  cudaLaunchKernelEx(&cfg, kern, mAh, mAl, mWh, mWl, mO0, mO1, M, N, K, sc, epi);
   return 1;
 }
 
-// Tile width per launch: a tile's mainloop costs max(operand stream, MMA) per K-block --
-// (128 + BN/2) x 256 B at ~40 B/clk per SM vs 6 BN clk of tf32 MMA per SM -- and a launch
-// costs ceil(tiles / clusters) tiles back to back plus a per-tile epilogue tail.
+// Launch plan: tile width and tail split, from a cost model in SM clocks calibrated on B200
+// (scripts/tc_probe.cu traces, profiles/r01/tc_splitk_probe.txt):
+//   * a K-block costs max(operand stream, MMA) = max((128 + BN/2) x 6.8, 6.7 BN) clk per SM
+//     ((128 + BN/2) x 256 B at ~38 B/clk vs 12 tf32 MMAs of N = BN);
+//   * complete rounds of whole tiles run back to back (their epilogues overlap the next tile);
+//   * a split tail tile costs kper K-blocks + publishing its partials (~3 us) + ~2.5 us per
+//     other split's partials added by the last arriver, + the final epilogue (~3 us).
+struct Plan {
+  int bn, full, s_tail, kper;
+};
 constexpr int kTileBN[4] = {64, 128, 192, 256};
-inline int choose_bn(int64_t M, int64_t N, int64_t K) {
+inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split) {
   const int64_t pairs_m = (M + 2 * BM - 1) / (2 * BM);
-  const int64_t nk = (K + BK - 1) / BK;
-  int best = kTileBN[0];
+  const int nk = (int)((K + BK - 1) / BK);
+  const double kEpi = 5900.0, kPublish = 5900.0, kPartial = 4900.0;  // clk
+  Plan best{kTileBN[0], 0, 1, nk};
   double best_cost = 1e300;
   for (int bn : kTileBN) {
     const int64_t tiles = pairs_m * ((N + bn - 1) / bn);
-    const int64_t rounds = (tiles + kClustersMax - 1) / kClustersMax;
-    const double kb = fmax((128.0 + bn / 2) * 256.0 / 40.0, 6.0 * bn);
-    const double cost = (double)rounds * (nk * kb + 2.0 * kb);
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = bn;
+    const int64_t full = tiles / kClustersMax * kClustersMax, tail = tiles - full;
+    const double kb = fmax((128.0 + bn / 2) * 6.8, 6.7 * bn);
+    const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, nk / 4)) : 1;
+    for (int s = 1; s <= smax; ++s) {
+      const int kper = (nk + s - 1) / s;
+      const int se = (nk + kper - 1) / kper;  // no empty split
+      const double cost = (double)(full / kClustersMax) * nk * kb + kEpi +
+                          (tail ? kper * kb + (se > 1 ? kPublish + kPartial * (se - 1) : 0.0) : 0.0);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = Plan{bn, (int)full, se, kper};
+      }
     }
   }
   return best;
@@ -544,12 +647,18 @@ inline int choose_bn(int64_t M, int64_t N, int64_t K) {
 
 template <class Epi>
 int launch_gemm_auto(const Split& A, int M, const float* Wh, const float* Wl, int N, int64_t ldw, int K,
-                     const OutDesc& o, const Epi& epi, cudaStream_t st) {
-  switch (choose_bn(M, N, K)) {
-    case 64: return launch_gemm<64>(A, M, Wh, Wl, N, ldw, K, o, epi, st);
-    case 128: return launch_gemm<128>(A, M, Wh, Wl, N, ldw, K, o, epi, st);
-    case 192: return launch_gemm<192>(A, M, Wh, Wl, N, ldw, K, o, epi, st);
-    default: return launch_gemm<256>(A, M, Wh, Wl, N, ldw, K, o, epi, st);
+                     const OutDesc& o, const Epi& epi, const GemmWs* ws, cudaStream_t st) {
+  static const bool no_split = [] {
+    const char* e = getenv("KGQ_NO_SPLITK");
+    return e && e[0] && e[0] != '0';
+  }();
+  const Plan p = plan_gemm(M, N, K, !no_split && ws != nullptr && ws->ws != nullptr);
+  const Sched sc{p.full, p.s_tail, p.kper, ws ? ws->ws : nullptr, ws ? ws->cnt : nullptr};
+  switch (p.bn) {
+    case 64: return launch_gemm<64>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
+    case 128: return launch_gemm<128>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
+    case 192: return launch_gemm<192>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
+    default: return launch_gemm<256>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
   }
 }
 

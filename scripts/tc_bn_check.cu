@@ -41,6 +41,11 @@ int main() {
   cudaMemcpy(dwh, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(db, b.data(), N * 4, cudaMemcpyHostToDevice);
   cudaMemset(dP, 0, M * 8); cudaMemset(dE, 0, 640 * 8);
+  GemmWs gws;
+  cudaMalloc(&gws.ws, kGemmWsFloats * 4);
+  cudaMalloc(&gws.cnt, kGemmCntInts * 4);
+  cudaMemset(gws.cnt, 0, kGemmCntInts * 4);
+  const tc::Sched whole{0, 1, 0, nullptr, nullptr};
   launch_split_copy(dxh, x.size(), dxh, dxl, 0);
   launch_split_copy(dwh, w.size(), dwh, dwl, 0);
   Split A{dxh, dxl, K};
@@ -86,11 +91,30 @@ int main() {
   each_bn([&](auto c) {
     constexpr int B = decltype(c)::value;
     const tc::OutDesc o1{dy, nullptr, M, N, N}, o2{dy, dy + (size_t)M * N, M, N, N};
-    check("fp32 + bias", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0); });
-    check("split + bias + relu", B, 1, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0); });
-    check("fp32, 2 clusters (persist)", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, 2); });
+    check("fp32 + bias", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, whole); });
+    check("split + bias + relu", B, 1, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0, whole); });
+    check("fp32, 2 clusters (persist)", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, whole, 2); });
     const tc::OutDesc o3{dy, nullptr, M / 2, N, N};
-    check("row-pair min (union)", B, 2, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0); });
+    check("row-pair min (union)", B, 2, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0, whole); });
+    // split tail: the last tiles (or all) split in K; K = 100 -> 4 K-blocks
+    const int tiles = ((M + 255) / 256) * ((N + B - 1) / B);
+    for (int sk : {2, 4}) {
+      const int kper = (4 + sk - 1) / sk;
+      const tc::Sched all{0, sk, kper, gws.ws, gws.cnt}, tail{tiles / 2, sk, kper, gws.ws, gws.cnt};
+      char nm[64];
+      snprintf(nm, sizeof nm, "split-K %d, every tile", sk);
+      check(nm, B, 1, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0, all); });
+      snprintf(nm, sizeof nm, "split-K %d, tail, 3 clusters", sk);
+      check(nm, B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, tail, 3); });
+      snprintf(nm, sizeof nm, "split-K %d, union rows", sk);
+      check(nm, B, 2, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0, all); });
+    }
+    // counters must be back to zero after every launch
+    std::vector<int> cnt(kGemmCntInts);
+    cudaMemcpy(cnt.data(), gws.cnt, kGemmCntInts * 4, cudaMemcpyDeviceToHost);
+    int nz = 0;
+    for (int v : cnt) nz += v != 0;
+    if (nz) { printf("BN=%d: %d split counters not reset\n", B, nz); ++fails; }
   });
   printf(fails ? "FAILED (%d)\n" : "all tile widths and epilogues OK\n", fails);
   return fails ? 1 : 0;

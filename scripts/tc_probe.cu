@@ -32,7 +32,8 @@ int main() {
   struct Shape { int M, N, K; bool score; };
   const Shape shapes[] = {{1024, 1600, 1200, false}, {3072, 1600, 1600, false}, {2048, 800, 1600, false},
                           {2048, 800, 800, false},   {1024, 14592, 800, true},  {2048, 14592, 800, true},
-                          {1024, 14592, 32, true},   {1024, 1600, 32, false}};
+                          {1024, 14592, 32, true},   {1024, 1600, 32, false}, {2048, 400, 800, false},
+                          {3072, 400, 800, false},   {1024, 800, 1600, false}, {1024, 1600, 1600, false}};
 #ifdef KGQ_TC_TRACE
   unsigned long long* tr;
   cudaMalloc(&tr, 8192 * 64);
@@ -55,15 +56,24 @@ int main() {
     launch_split_copy(wh, (int64_t)N * K, wh, wl, 0);
     cudaMemset(b, 0, N * 4); cudaMemset(P, 0, M * 8); cudaMemset(E, 0, N * 8);
     Split A{xh, xl, K};
+    static GemmWs gws;
+    if (!gws.ws) {
+      cudaMalloc(&gws.ws, kGemmWsFloats * 4);
+      cudaMalloc(&gws.cnt, kGemmCntInts * 4);
+      cudaMemset(gws.cnt, 0, kGemmCntInts * 4);
+    }
+    const tc::Plan plan = tc::plan_gemm(M, N, K, !getenv("KGQ_NO_SPLITK"));
+    const tc::Sched whole{0, 1, 0, nullptr, nullptr};
+    tc::Sched sc = whole;
     auto run = [&](int bn) {
       auto go = [&](auto c) {
         constexpr int B = decltype(c)::value;
         if (sh.score)
           tc::launch_gemm<B>(A, M, wh, wl, N, K, K, tc::OutDesc{y, nullptr, M, N, N},
-                             EpiBetaScore<1>{P, E, M, (int64_t)N}, 0);
+                             EpiBetaScore<1>{P, E, M, (int64_t)N}, 0, sc);
         else
           tc::launch_gemm<B>(A, M, wh, wl, N, K, K, tc::OutDesc{y, y + (size_t)M * N, M, N, N},
-                             EpiLinear<kEpiRelu, true>{b, N, 0, 0}, 0);
+                             EpiLinear<kEpiRelu, true>{b, N, 0, 0}, 0, sc);
       };
       switch (bn) {
         case 64: go(std::integral_constant<int, 64>{}); break;
@@ -72,14 +82,17 @@ int main() {
         default: go(std::integral_constant<int, 256>{}); break;
       }
     };
-    const int pick = tc::choose_bn(M, N, K);
+    const int pick = plan.bn;
     printf("M=%5d N=%5d K=%5d %s |", M, N, K, sh.score ? "score " : "linear");
     for (int bn : {64, 128, 192, 256}) printf(" %d:%.1f", bn, time_us([&] { run(bn); }));
+    sc = tc::Sched{plan.full, plan.s_tail, plan.kper, gws.ws, gws.cnt};
     const double us = time_us([&] { run(pick); });
-    printf(" | pick %d: %.1f us %.1f TFLOP/s useful\n", pick, us, 2.0 * M * N * K / us * 1e-6);
+    printf(" | plan %d full %d split %d: %.1f us %.1f TFLOP/s useful\n", pick, plan.full, plan.s_tail, us,
+           2.0 * M * N * K / us * 1e-6);
 #ifdef KGQ_TC_TRACE
     {
-      const int tiles = ((M + 255) / 256) * ((N + pick - 1) / pick);
+      const int tiles0 = ((M + 255) / 256) * ((N + pick - 1) / pick);
+      const int tiles = sc.s_tail > 1 ? sc.full + (tiles0 - sc.full) * sc.s_tail : tiles0;  // units
       cudaMemset(tr, 0, 8192 * 64);
       run(pick);
       cudaDeviceSynchronize();
@@ -92,8 +105,16 @@ int main() {
         tend = std::max(tend, h[t * 8 + 4]);
         for (int i = 0; i < 4; ++i) ph[i] += (double)(h[t * 8 + i + 1] - h[t * 8 + i]) * 1e-3 / tiles;
       }
-      printf("    trace: %d tiles, span %.1f us; per tile (us): wait-first-stage %.2f mainloop %.2f "
+      printf("    trace: %d units, span %.1f us; per unit (us): wait-first-stage %.2f mainloop %.2f "
              "drain-tail %.2f epilogue %.2f\n", tiles, (tend - t0) * 1e-3, ph[0], ph[1], ph[2], ph[3]);
+      if (sc.s_tail > 1)
+        for (int t = sc.full; t < tiles && t < sc.full + 6; ++t) {
+          const unsigned long long* x = &h[t * 8];
+          printf("      unit %d: start %.1f first %.1f mma-done %.1f drained %.1f published %.1f counted %.1f reduced %.1f end %.1f\n",
+                 t, (x[0] - t0) * 1e-3, (x[1] - t0) * 1e-3, (x[2] - t0) * 1e-3, (x[3] - t0) * 1e-3,
+                 x[5] ? (x[5] - t0) * 1e-3 : -1.0, x[6] ? (x[6] - t0) * 1e-3 : -1.0, x[7] ? (x[7] - t0) * 1e-3 : -1.0,
+                 (x[4] - t0) * 1e-3);
+        }
     }
 #endif
     cudaError_t e = cudaDeviceSynchronize();

@@ -7,10 +7,14 @@ if [ "$1" = "run" ]; then
   echo "== probe"; timeout 120 ./tc_probe_base
   echo "== probe (no PDL)"; KGQ_NO_PDL=1 timeout 120 ./tc_probe_base
   echo "== trace"; timeout 120 ./tc_probe_trace
+  for v in $EXTRA; do echo "== $v"; timeout 120 ./tc_probe_$v; done
   exit 0
 fi
 $NVCC $FL tc_probe.cu -o tc_probe_base &
 $NVCC $FL -DKGQ_TC_TRACE tc_probe.cu -o tc_probe_trace &
 $NVCC $FL tc_bn_check.cu -o tc_bn_check &
+declare -A DEF=([nostore]="-DKGQ_TC_TRACE -DKGQ_TC_DBG_NO_STORE" [drain3]="-DKGQ_TC_TRACE -DKGQ_TC_DRAIN=3"
+               [drain4]="-DKGQ_TC_TRACE -DKGQ_TC_DRAIN=4")
+for v in $EXTRA; do $NVCC $FL ${DEF[$v]} tc_probe.cu -o tc_probe_$v & done
 wait
 ls tc_probe_* tc_bn_check
