@@ -200,12 +200,15 @@ __device__ __forceinline__ void reg_insert(unsigned long long& lk, unsigned long
 }
 
 template <int WPR>
-__global__ void __launch_bounds__(kRegThreads)
+__global__ void __launch_bounds__(kRegThreads, 4)
     k_topk_reg(const float* __restrict__ dist, int64_t ldd, int64_t n_total, int64_t chunk, int k,
                int64_t id_base, const int32_t* __restrict__ invalid, float* __restrict__ od,
                int32_t* __restrict__ oi, int B, int tasks) {
   constexpr int TPB = kRegThreads / 32 / WPR;  // tasks per block
-  constexpr int U = 4;
+#ifndef KGQ_TOPK_U
+#define KGQ_TOPK_U 8
+#endif
+  constexpr int U = KGQ_TOPK_U;  // float4 loads in flight per lane (16 x 128 B lines per warp at 8)
   __shared__ unsigned long long part[kRegThreads / 32][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int t = blockIdx.x * TPB + wid / WPR, sub = wid % WPR;
