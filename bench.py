@@ -178,6 +178,84 @@ def run_c5a(args):
                       "hbm_peak_gbs": peaks["hbm_gbs"], "peak_source": src, "results": res}), flush=True)
 
 
+SUITE = {
+    # name: (model, N, R, d, hidden, batch, structures, note) -- BASELINE.json configs
+    "c1_gqe_toy": ("gqe", 200, 10, 32, 64, 16, ("1p", "2p", "2i"), "configs[0]: GQE toy KG, latency regime"),
+    "c3_q2b_nell995": ("q2b", 63361, 200, 400, 1600, 1024, ("1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up"),
+                       "configs[2]: Query2Box EPFO types on the NELL995 shape"),
+    "c4_betae_fb15k_neg": ("betae", 14951, 1345, 400, 1600, 4096, ("2in", "3in", "inp", "pin", "pni"),
+                           "configs[3]: BetaE negation types on the FB15k shape, batch 4096"),
+    "c5b_gqe_2m": ("gqe", 2_000_000, 200, 400, 1600, 1024, ("1p", "2u"), "configs[4], throughput regime B=1024"),
+    "c5b_betae_2m": ("betae", 2_000_000, 200, 400, 1600, 1024, ("1p", "2u"), "configs[4], throughput regime B=1024"),
+}
+
+
+def run_suite(args):
+    """One JSON line per BASELINE.json config other than the headline one: device
+    q/s with L2 flushed between steps, stage split, and the dominant kernel against its roofline
+    (SIMT scorers: FP32 lane-instructions vs 148 SMs x 128 lanes x SM clock; tensor path: useful
+    fp32 FLOPs vs the 3xTF32 peak)."""
+    import torch
+    from paper_2503_02172_b200 import Engine
+    peaks, src = load_peaks()
+    alu_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # lane-instr/s
+    tc_peak = peaks["bf16_tflops"] * (1.1 / 2.25) / 3.0
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    names = args.suite.split(",") if args.suite else list(SUITE)
+    for name in names:
+        model, N, R, d, H, B, structs, note = SUITE[name]
+        t = synth.make_tables(model, N, R, d, hidden=H, seed=SEED + 10)
+        eng = Engine(model, N, R, d, hidden=H, max_batch=B, max_k=K)
+        eng.load_tables(t)
+        del t
+        qs = {}
+        for s in structs:
+            a, r = synth.make_queries(s, B, N, R, seed=synth.query_seed(SEED + 10, s))
+            qs[s] = (torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda())
+        for _ in range(args.warmup):
+            for s in structs:
+                eng.submit(s, *qs[s], K)
+        torch.cuda.synchronize()
+        eng.check_errors()
+        eng.profile(True)
+        eng.profile_read()
+        ev = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in structs}
+        per = {s: 0.0 for s in structs}
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            for s in structs:
+                ev[s][0].record()
+                eng.submit(s, *qs[s], K)
+                ev[s][1].record()
+            torch.cuda.synchronize()
+            for s in structs:
+                per[s] += ev[s][0].elapsed_time(ev[s][1])
+        prof = eng.profile_read()
+        eng.profile(False)
+        eng.close()
+        tot = sum(per.values())
+        q = args.steps * len(structs) * B
+        st = {k: v[0] / args.steps for k, v in prof.items()}
+        sc_ms, _, sc_w = prof["score"]
+        d_ms, _, d_w = prof["dense"]
+        if model == "betae" and B > 16:
+            ach = (sc_w + d_w) / ((sc_ms + d_ms) / 1e3) / 1e12
+            roof = {"kernel": "k_gemm (tcgen05 3xTF32: dense layers + BetaE scorer)", "bound": "tensor",
+                    "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak}
+        else:
+            ach = sc_w / (sc_ms / 1e3) if sc_ms > 0 else 0.0
+            roof = {"kernel": f"k_score<{model}> (SIMT L1 / box distance)", "bound": "alu",
+                    "achieved": ach / 1e12, "peak": alu_peak / 1e12, "unit": "T lane-instr/s",
+                    "frac": ach / alu_peak}
+        print(json.dumps({"workload": name, "note": note, "model": model, "n_entity": N, "n_relation": R,
+                          "dim": d, "batch": B, "k": K, "structures": list(structs),
+                          "queries_per_s": q / (tot / 1e3), "ms_per_batch": tot / args.steps / len(structs),
+                          "per_type_qps": {s: B * args.steps / (per[s] / 1e3) for s in structs},
+                          "stage_ms_per_step": st, "roofline": roof, "peak_source": src,
+                          "l2": "flushed between steps"}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -186,10 +264,13 @@ def main():
     ap.add_argument("--impl", default="kgq", choices=["kgq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=14)
-    ap.add_argument("--workload", default="fb15k237", choices=["fb15k237", "c5a"])
+    ap.add_argument("--workload", default="fb15k237", choices=["fb15k237", "c5a", "suite"])
+    ap.add_argument("--suite", default="", help="comma list of SUITE configs (default: all)")
     args = ap.parse_args()
     if args.workload == "c5a":
         return run_c5a(args)
+    if args.workload == "suite":
+        return run_suite(args)
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
