@@ -7,6 +7,7 @@
 // k_topk: one CTA per query row (or per 16k-entry chunk of a long row, the chunks then merged
 // by k_merge); warp select with per-warp thresholds (see the kernel).
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kgq_internal.cuh"
