@@ -54,10 +54,14 @@ typedef enum { KGQ_GQE = 0, KGQ_Q2B = 1, KGQ_BETAE = 2 } kgq_model;
  *   2u  U(P(a0,r0),P(a1,r1))             up  U(P(P(a0,r0),r2),P(P(a1,r1),r2))
  *   2in I(P(a0,r0),N(P(a1,r1)))          3in I(P(a0,r0),P(a1,r1),N(P(a2,r2)))
  *   inp P(I(P(a0,r0),N(P(a1,r1))),r2)    pin I(P(P(a0,r0),r1),N(P(a1,r2)))
- *   pni I(N(P(P(a0,r0),r1)),P(a1,r2))                                                     */
+ *   pni I(N(P(P(a0,r0),r1)),P(a1,r2))
+ * De Morgan unions (BetaE only -- they use negation; KGReasoning "2u-DM",
+ * "up-DM" [ext]): the union as the negation of the intersection of the negated branches, one
+ * embedding instead of the DNF min over clauses:
+ *   2u-DM N(I(N(P(a0,r0)),N(P(a1,r1))))  up-DM P(N(I(N(P(a0,r0)),N(P(a1,r1)))),r2)          */
 typedef enum {
   KGQ_1P = 0, KGQ_2P, KGQ_3P, KGQ_2I, KGQ_3I, KGQ_PI, KGQ_IP, KGQ_2U, KGQ_UP,
-  KGQ_2IN, KGQ_3IN, KGQ_INP, KGQ_PIN, KGQ_PNI, KGQ_NUM_STRUCTURES
+  KGQ_2IN, KGQ_3IN, KGQ_INP, KGQ_PIN, KGQ_PNI, KGQ_2U_DM, KGQ_UP_DM, KGQ_NUM_STRUCTURES
 } kgq_structure;
 
 /* BetaE projection terminal: KGReasoning regulariser clamp(y+1,0.05,1e9)

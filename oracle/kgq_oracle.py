@@ -41,7 +41,7 @@ TERMINAL_REGULARIZER = "regularizer"
 TERMINAL_SOFTMAX = "softmax"
 
 STRUCTURES = ("1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up",
-              "2in", "3in", "inp", "pin", "pni")
+              "2in", "3in", "inp", "pin", "pni", "2u-DM", "up-DM")
 
 # ----------------------------------------------------------------------------------------
 # Computation plans per structure (SURVEY §8(b) slot table; Fig. 1 names P:17; Eq. 1
@@ -68,6 +68,10 @@ PLANS = {
     "inp": (P, (I, [(P, (A, 0), 0), (N, (P, (A, 1), 1))]), 2),
     "pin": (I, [(P, (P, (A, 0), 0), 1), (N, (P, (A, 1), 2))]),
     "pni": (I, [(N, (P, (P, (A, 0), 0), 1)), (P, (A, 1), 2)]),
+    # De Morgan union, U(x, y) = N(I(N(x), N(y))) -- BetaE's alternative to
+    # the DNF min (KGReasoning "2u-DM" / "up-DM" [ext]); one embedding, no top-level union.
+    "2u-DM": (N, (I, [(N, (P, (A, 0), 0)), (N, (P, (A, 1), 1))])),
+    "up-DM": (P, (N, (I, [(N, (P, (A, 0), 0)), (N, (P, (A, 1), 1))])), 2),
 }
 
 
@@ -108,7 +112,15 @@ def n_branches(s):
 
 
 def uses_negation(s):
-    return "n" in s
+    def walk(n):
+        if n[0] == N:
+            return True
+        if n[0] == P:
+            return walk(n[1])
+        if n[0] in (I, U):
+            return any(walk(c) for c in n[1])
+        return False
+    return walk(PLANS[s])
 
 
 # ----------------------------------------------------------------------------------------

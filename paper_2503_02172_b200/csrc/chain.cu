@@ -226,6 +226,10 @@ __global__ void k_attention_combine(CombineArgs c, Split S, const float* __restr
       x0 += c.rel[(int64_t)rid * d + j];
       if (c.model == KGQ_Q2B) x1 += c.rel_off[(int64_t)rid * d + j];
     }
+    if (c.negate_out) {  // De Morgan union: N(I(...)), alpha -> 1/alpha, beta -> 1/beta (Q5)
+      x0 = 1.0f / x0;
+      x1 = 1.0f / x1;
+    }
     const bool two = c.model != KGQ_GQE;
     if (out.hi) {
       store_split(out.hi, out.lo, (int64_t)b * out.ld + j, x0);

@@ -39,10 +39,13 @@ static const Plan kPlans[KGQ_NUM_STRUCTURES] = {
     /* inp */ {kInter, 2, {BR(0, 1, 0, 0, 0), BR(1, 2, 1, kOpNeg, 0)}, 1, {2, 0}, 2, 3, 1, true},
     /* pin */ {kInter, 2, {BR(0, 2, 0, 1, 0), BR(1, 2, 2, kOpNeg, 0)}, 0, {0, 0}, 2, 3, 1, true},
     /* pni */ {kInter, 2, {BR(0, 3, 0, 1, kOpNeg), BR(1, 1, 2, 0, 0)}, 0, {0, 0}, 2, 3, 1, true},
+    /* 2u-DM */ {kInter, 2, {BR(0, 2, 0, kOpNeg, 0), BR(1, 2, 1, kOpNeg, 0)}, 0, {0, 0}, 2, 2, 1, true, true},
+    /* up-DM */ {kInter, 2, {BR(0, 2, 0, kOpNeg, 0), BR(1, 2, 1, kOpNeg, 0)}, 1, {2, 0}, 2, 3, 1, true, true},
 };
 #undef BR
 static const char* kNames[KGQ_NUM_STRUCTURES] = {"1p", "2p", "3p", "2i", "3i", "pi", "ip",
-                                                 "2u", "up", "2in", "3in", "inp", "pin", "pni"};
+                                                 "2u", "up", "2in", "3in", "inp", "pin", "pni",
+                                                 "2u-DM", "up-DM"};
 const Plan* plan_of(int s) {
   return (s >= 0 && s < KGQ_NUM_STRUCTURES) ? &kPlans[s] : nullptr;
 }
@@ -343,6 +346,7 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
   CombineArgs c{};
   c.model = model; c.nb = nb; c.B = B; c.d = d; c.ldl = ctx->tw; c.ldg = 0;
   c.rels = rels; c.n_r = P->n_rel; c.n_relation = ctx->cfg.n_relation; c.post_slot = -1;
+  c.negate_out = P->neg_inter ? 1 : 0;
   c.err = ctx->d_err; c.invalid = ctx->d_invalid;
   if (P->npost == 0)
     return L + launch_attention_combine(c, ctx->S, ctx->T, nullptr, Split{nullptr, nullptr, 0}, ctx->Q, st);

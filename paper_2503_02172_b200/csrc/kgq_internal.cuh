@@ -39,6 +39,7 @@ struct Plan {
   int post[2];
   int n_anchor, n_rel, n_out;  // slot counts; n_out = DNF branches of the final embedding
   bool negation;
+  bool neg_inter;   // negate the intersection result (De Morgan unions 2u-DM, up-DM)
 };
 const Plan* plan_of(int s);
 
@@ -207,6 +208,7 @@ struct CombineArgs {
   const int32_t* rels;
   int n_r, n_relation;
   int post_slot;  // -1: none
+  int negate_out;  // BetaE: 1/x of the combined embedding (De Morgan union, N4)
   int32_t* err;
   int32_t* invalid;
 };

@@ -21,7 +21,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 ABI_VERSION = 1
 MODELS = {"gqe": 0, "q2b": 1, "betae": 2}
 STRUCTURES = ("1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up",
-              "2in", "3in", "inp", "pin", "pni")
+              "2in", "3in", "inp", "pin", "pni", "2u-DM", "up-DM")
 STATUS = {0: "KGQ_OK", 1: "KGQ_EINVAL", 2: "KGQ_ERANGE", 3: "KGQ_EUNSUPPORTED",
           4: "KGQ_ESTATE", 5: "KGQ_ENOMEM", 6: "KGQ_ECUDA"}
 LAYER_PROJ_OUT, LAYER_PROJ_HIDDEN = 0, 1

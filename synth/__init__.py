@@ -32,10 +32,13 @@ STRUCTURES = ("1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up",
               "2in", "3in", "inp", "pin", "pni")
 EPFO = STRUCTURES[:9]
 NEGATION = STRUCTURES[9:]
+#: De Morgan unions (BetaE only): not in the 14 benchmark types
+DM = ("2u-DM", "up-DM")
+ALL_STRUCTURES = STRUCTURES + DM
 N_ANCHORS = {"1p": 1, "2p": 1, "3p": 1, "2i": 2, "3i": 3, "pi": 2, "ip": 2, "2u": 2,
-             "up": 2, "2in": 2, "3in": 3, "inp": 2, "pin": 2, "pni": 2}
+             "up": 2, "2in": 2, "3in": 3, "inp": 2, "pin": 2, "pni": 2, "2u-DM": 2, "up-DM": 2}
 N_RELS = {"1p": 1, "2p": 2, "3p": 3, "2i": 2, "3i": 3, "pi": 3, "ip": 3, "2u": 2,
-          "up": 3, "2in": 2, "3in": 3, "inp": 3, "pin": 3, "pni": 3}
+          "up": 3, "2in": 2, "3in": 3, "inp": 3, "pin": 3, "pni": 3, "2u-DM": 2, "up-DM": 3}
 
 # Canonical parameter names.  nn.Linear convention: W is [out_features, in_features].
 #   betae: proj.layer1 [H,3d], proj.layer2..L [H,H], proj.layer0 [2d,H],
@@ -128,8 +131,8 @@ def _entity_block_draw(seed, n, width, lo, hi, rows):
 
 def make_queries(structure: str, batch: int, n_entity: int, n_relation: int, seed: int):
     """Uniform throughput queries: anchors int32 [B, n_a], rels int32 [B, n_r]."""
-    if structure not in STRUCTURES:
-        raise ValueError(f"unknown structure {structure!r}; valid: {', '.join(STRUCTURES)}")
+    if structure not in ALL_STRUCTURES:
+        raise ValueError(f"unknown structure {structure!r}; valid: {', '.join(ALL_STRUCTURES)}")
     rng = np.random.default_rng(seed)
     a = rng.integers(0, n_entity, size=(batch, N_ANCHORS[structure]), dtype=np.int64)
     r = rng.integers(0, n_relation, size=(batch, N_RELS[structure]), dtype=np.int64)
@@ -137,4 +140,4 @@ def make_queries(structure: str, batch: int, n_entity: int, n_relation: int, see
 
 
 def query_seed(table_seed: int, structure: str) -> int:
-    return table_seed + 1000 + STRUCTURES.index(structure)
+    return table_seed + 1000 + ALL_STRUCTURES.index(structure)

@@ -87,4 +87,5 @@ def chain_tolerance(structure, dist="kgr-init"):
     u*sum|w h|; negation 1/x maps it to a Beta parameter ~20 with relative error
     u*sum|w h|/0.05, which the attention softmax and the next projection propagate.  The
     final distances are held to the 1e-4 north-star bound regardless."""
-    return 1e-4 if (dist == "kgr-init" and "n" not in structure) else 1e-3
+    negation = "n" in structure or "DM" in structure
+    return 1e-4 if (dist == "kgr-init" and not negation) else 1e-3

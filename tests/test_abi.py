@@ -37,7 +37,7 @@ def test_structure_metadata_matches_oracle_plans():
         assert kgq.num_relations(s) == synth.N_RELS[s] == O.kgq_oracle.n_relations(s)
         assert kgq.num_branches(s) == O.kgq_oracle.n_branches(s)
         assert kgq.uses_negation(s) == O.kgq_oracle.uses_negation(s)
-    assert kgq._lib.kgq_num_anchors(14) == -1 and kgq._lib.kgq_num_anchors(-1) == -1
+    assert kgq._lib.kgq_num_anchors(len(O.STRUCTURES)) == -1 and kgq._lib.kgq_num_anchors(-1) == -1
     with pytest.raises(kgq.KgqError, match="valid: 1p"):
         kgq.structure_id("4p")
     assert kgq.embedding_width("gqe", 400) == 400

@@ -17,7 +17,7 @@ from paper_2503_02172_b200 import Engine  # noqa: E402
 
 # (name, model, N, R, d, H, B, structures) -- BASELINE.json configs[1..3]
 CONFIGS = [
-    ("betae_fb15k237", "betae", 14505, 237, 400, 1600, 1024, synth.STRUCTURES),
+    ("betae_fb15k237", "betae", 14505, 237, 400, 1600, 1024, synth.ALL_STRUCTURES),
     ("q2b_nell995", "q2b", 63361, 200, 400, 1600, 1024, synth.EPFO),
     ("betae_fb15k_neg", "betae", 14951, 1345, 400, 1600, 4096, synth.NEGATION),
 ]

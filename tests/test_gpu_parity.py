@@ -18,7 +18,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a GPU", allow_module_level=True)
 from paper_2503_02172_b200 import Engine, KgqError  # noqa: E402
 
-STRUCTS = {"gqe": synth.EPFO, "q2b": synth.EPFO, "betae": synth.STRUCTURES}
+STRUCTS = {"gqe": synth.EPFO, "q2b": synth.EPFO, "betae": synth.ALL_STRUCTURES}
 SMALL = dict(N=1000, R=20, d=40, H=96, B=37)  # ragged everywhere
 
 

@@ -301,6 +301,40 @@ def test_negation_structure_layouts():
                                m.intersect([q(0), q(1), m.negate(q(2))]), rtol=1e-13)
 
 
+def test_de_morgan_union_pins():
+    """N4 (2u-DM / up-DM, N(I(N x, N y))): identical branches reduce to 1p / 2p (intersection
+    of identical inputs returns it, negation is an involution); with zero intersection weights
+    the attention is uniform, so 2u-DM is the element-wise HARMONIC mean of the two branch
+    embeddings (1 / mean(1/x_i)) -- a closed form that a missing outer or inner negation, or an
+    arithmetic mean, fails; branch order does not matter; GQE/Q2B reject it."""
+    t = tiny_tables("betae", dist="spread")
+    m = O.Model("betae", t, dim=8)
+    a, r = synth.make_queries("up-DM", 5, 40, 6, 21)
+    p1 = lambda ai, ri: m.query_embedding("1p", a[:, [ai]], r[:, [ri]])[:, 0]
+    same_a, same_r = np.repeat(a[:, [0]], 2, 1), np.repeat(r[:, [0]], 2, 1)
+    np.testing.assert_allclose(m.query_embedding("2u-DM", same_a, same_r)[:, 0], p1(0, 0), rtol=1e-12)
+    same_r3 = np.concatenate([r[:, [0, 0]], r[:, [2]]], 1)
+    np.testing.assert_allclose(m.query_embedding("up-DM", same_a, same_r3)[:, 0],
+                               m.query_embedding("2p", a[:, [0]], r[:, [0, 2]])[:, 0], rtol=1e-12)
+    swap = m.query_embedding("2u-DM", a[:, ::-1], r[:, [1, 0]])[:, 0]
+    np.testing.assert_allclose(swap, m.query_embedding("2u-DM", a, r[:, :2])[:, 0], rtol=1e-12)
+    # up-DM = P(2u-DM, r2)
+    np.testing.assert_allclose(m.query_embedding("up-DM", a, r)[:, 0],
+                               m.project(m.query_embedding("2u-DM", a, r[:, :2])[:, 0], r[:, 2]), rtol=1e-13)
+    t0 = tiny_tables("betae", dist="spread")
+    for k in list(t0):
+        if k.startswith(("W:inter", "b:inter")):
+            t0[k][:] = 0
+    m0 = O.Model("betae", t0, dim=8)
+    x = m0.query_embedding("1p", a[:, [0]], r[:, [0]])[:, 0]
+    y = m0.query_embedding("1p", a[:, [1]], r[:, [1]])[:, 0]
+    np.testing.assert_allclose(m0.query_embedding("2u-DM", a, r[:, :2])[:, 0], 2.0 / (1.0 / x + 1.0 / y),
+                               rtol=1e-13)
+    assert O.kgq_oracle.uses_negation("2u-DM") and O.kgq_oracle.n_branches("up-DM") == 1
+    with pytest.raises(NotImplementedError):
+        O.Model("q2b", tiny_tables("q2b"), dim=8).query_embedding("2u-DM", a, r[:, :2])
+
+
 def test_slot_counts_match_synth():
     for s in O.STRUCTURES:
         assert O.kgq_oracle.n_anchors(s) == synth.N_ANCHORS[s]
