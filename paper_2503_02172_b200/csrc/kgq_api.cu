@@ -197,6 +197,14 @@ bool debug_launch() {
   }
   return v == 1;
 }
+bool topk_cmin_disabled() {  // KGQ_NO_TOPK_CMIN=1: full-row top-k (A/B and debugging)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KGQ_NO_TOPK_CMIN");
+    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
 void check_site(const char* site) {
   if (!debug_launch()) return;
   cudaError_t e = cudaPeekAtLastError();
@@ -487,7 +495,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   F(ctx->ent); F(ctx->rel[0]); F(ctx->rel[1]); F(ctx->score_tab);
   for (auto& l : ctx->lin) { F(l.W); F(l.W_hi); F(l.W_lo); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) { F(s->hi); F(s->lo); }
-  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->d_err); F(ctx->d_invalid);
+  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->d_err); F(ctx->d_invalid);
   F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv_hi); F(ctx->uv_lo); F(ctx->Esum);
   F(ctx->uvsums); F(ctx->Atc.hi); F(ctx->Atc.lo); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
@@ -606,6 +614,7 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st) st = dalloc(ctx, &ctx->Q, (size_t)(Bm * 2 * ctx->qw), "Q");
   if (!st) st = dalloc(ctx, &ctx->Qt, (size_t)(nplanes * d * ctx->rpad), "Qt");
   if (!st) st = dalloc(ctx, &ctx->dist, (size_t)(ctx->bchunk * ctx->np), "dist");
+  if (!st && c.model == KGQ_BETAE) st = dalloc(ctx, &ctx->cmin, (size_t)(ctx->bchunk * (ctx->np / 32)), "block minima");
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_d, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_i, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st && c.model == KGQ_BETAE) {
@@ -649,7 +658,8 @@ static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStrea
     // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
     StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
     L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
-                               ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist, ctx->np, &ctx->gws, st);
+                               ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist, ctx->np, ctx->cmin,
+                               ctx->np / 32, ctx->ns, &ctx->gws, st);
     check_site("tensor-core scorer");
   } else {
     {
@@ -679,8 +689,15 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
     L += score_rows(ctx, P, b0, nb, st);
     {
       StageTimer t(ctx, st, kStTopk);
-      L += launch_topk(ctx->dist, ctx->np, nb, ctx->ns, k, ctx->e0, ctx->d_invalid + b0,
-                       topk_dist + b0 * k, topk_id + b0 * k, ctx->topk_tmp_d, ctx->topk_tmp_i, st);
+      // the tensor-core scorer's epilogue wrote 32-entity block minima: pruned top-k
+      const bool blockmin = ctx->cfg.model == KGQ_BETAE && !score_uses_stream(ctx->cfg.model, P->n_out, nb) &&
+                            k <= 32 && !topk_cmin_disabled();
+      if (blockmin)
+        L += launch_topk_cmin(ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, nb, ctx->ns, k, ctx->e0,
+                              ctx->d_invalid + b0, topk_dist + b0 * k, topk_id + b0 * k, st);
+      else
+        L += launch_topk(ctx->dist, ctx->np, nb, ctx->ns, k, ctx->e0, ctx->d_invalid + b0,
+                         topk_dist + b0 * k, topk_id + b0 * k, ctx->topk_tmp_d, ctx->topk_tmp_i, st);
       check_site("top-k");
     }
     if (shard_dist)

@@ -107,6 +107,7 @@ struct kgq_ctx {
   float* Qt = nullptr;                     // scorer query operand planes [nplanes][d][rpad]
   int64_t rpad = 0;
   float* dist = nullptr;                   // [bchunk, np]
+  float* cmin = nullptr;                   // [bchunk, np / 32] block minima (tensor-core scorer)
   int64_t bchunk = 0;
   float* topk_tmp_d = nullptr;             // chunked top-k candidates [<= 4096 per row]
   int32_t* topk_tmp_i = nullptr;
@@ -243,7 +244,14 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
                           double* sums, float* uv_hi, float* uv_lo, float2* Esum, cudaStream_t st);
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
                           Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
-                          int64_t np, float* dist, int64_t ldd, const GemmWs* ws, cudaStream_t st);
+                          int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
+                          const GemmWs* ws, cudaStream_t st);
+// Top-k of dist rows using the score epilogue's 32-entity block minima cmin [B][ldc] (k <= 32):
+// tau = k-th smallest block minimum bounds the k-th best distance (k blocks each hold an
+// entry <= tau), so only blocks with minimum <= tau are scanned.  Exact (dist, id) order.
+int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
+                     int k, int64_t id_base, const int32_t* invalid, float* out_d, int32_t* out_i,
+                     cudaStream_t st);
 int launch_merge(int parts, int B, int k, const float* in_d, const int32_t* in_i, float* out_d,
                  int32_t* out_i, cudaStream_t st);
 // Table preparation (finalize).

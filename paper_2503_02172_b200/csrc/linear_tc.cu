@@ -24,6 +24,9 @@ using tc::BM;
 template <int EPI, bool SPLIT>
 struct EpiLinear {
   static constexpr int PLANES = SPLIT ? 2 : 1, ROWDIV = 1;
+  static constexpr bool CMIN = false;
+  template <int CH>
+  __device__ void chunk_min(int, int, const float*) const {}
   const float* bias;
   int N, neg0, neg1;
   struct Pre {

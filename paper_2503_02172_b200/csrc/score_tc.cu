@@ -106,13 +106,21 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
   }
 }
 
+// Score epilogue: dist = (P_hi + E_hi) + ((P_lo + E_lo) + acc), DNF min over row pairs (NB 2),
+// and, when cmin is set, the minimum of every 32-entity block of each output row over the
+// shard's real entities (columns < nvalid): cmin[row][n / 32].  The top-k reads these block
+// minima first and scans only the blocks that can hold one of the k best (k_topk_cmin).
 template <int NB>
 struct EpiBetaScore {
   static constexpr int PLANES = 1, ROWDIV = NB;
+  static constexpr bool CMIN = true;
   const float2* P;  // [rows] (hi, lo)
   const float2* E;  // [np] (hi, lo)
   int rows;
   int64_t ncols;    // np: the last column tile may overhang it
+  float* cmin = nullptr;  // [rows / NB][ldc] block minima, or nullptr
+  int64_t ldc = 0;
+  int64_t nvalid = 0;     // the shard's entity count ns (columns >= ns are padding)
   struct Pre {
     float2 p;       // P of this lane's row
     float2 e[4];    // E of columns n0 + lane + 32 j
@@ -135,6 +143,27 @@ struct EpiBetaScore {
       v[i] = (r.p.x + eh) + ((r.p.y + el) + v[i]);
     }
   }
+  template <int CH>
+  __device__ __forceinline__ void chunk_min(int row, int n, const float* v) const {
+    static_assert(CH == 32, "block minima are over 32 columns");
+    if (!cmin || (NB == 2 && (row & 1)) || row >= rows || n >= nvalid) return;
+    float m = __uint_as_float(0x7F800000u);
+    if (n + CH <= nvalid) {  // interior block: pairwise tree, no column predicates
+      float t[CH / 2];
+#pragma unroll
+      for (int i = 0; i < CH / 2; ++i) t[i] = fminf(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+      for (int w = CH / 4; w >= 1; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) t[i] = fminf(t[i], t[i + w]);
+      m = t[0];
+    } else {
+#pragma unroll
+      for (int i = 0; i < CH; ++i)
+        if (n + i < nvalid) m = fminf(m, v[i]);
+    }
+    cmin[(int64_t)(row / NB) * ldc + n / 32] = m;
+  }
 };
 
 }  // namespace
@@ -152,15 +181,16 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
 
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
                           Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
-                          int64_t np, float* dist, int64_t ldd, const GemmWs* ws, cudaStream_t st) {
+                          int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
+                          const GemmWs* ws, cudaStream_t st) {
   k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
   // dist rows: one per query (NB = 2: min over the two DNF branch rows 2b, 2b + 1)
   const tc::OutDesc o{dist, nullptr, rows / nbq, np, ldd};
   if (nbq == 2)
     return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
-                                    EpiBetaScore<2>{P, Esum, rows, np}, ws, st);
+                                    EpiBetaScore<2>{P, Esum, rows, np, cmin, ldc, nvalid}, ws, st);
   return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
-                                  EpiBetaScore<1>{P, Esum, rows, np}, ws, st);
+                                  EpiBetaScore<1>{P, Esum, rows, np, cmin, ldc, nvalid}, ws, st);
 }
 
 }  // namespace kgq

@@ -247,6 +247,8 @@ __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, 
 //   template <int CH> __device__ void chunk(const Pre&, int row, int c, float* v) const
 //       -- v[i] (i < CH) = accumulator of (row, n0 + c + i) on entry, output value on exit;
 //          column operands come from the prefetched registers by warp shuffle
+//   static constexpr bool CMIN; template <int CH> __device__ void chunk_min(int row, int n,
+//       const float* v) const -- optional side output after the row-pair min (score top-k)
 // Output tensor maps: plane p, box {32 / PLANES columns, 32 / ROWDIV rows}.
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -449,6 +451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int i = 0; i < CH; ++i) v[i] = fminf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1));
         }
+        if constexpr (Epi::CMIN) epi.template chunk_min<CH>(row0 + lane, n0 + c, v);
         uint8_t* buf = stg + (nchunk % L::NBUF) * (EPI_WARPS * L::BUF_BYTES);
         if (lane == 0) bulk_wait_read<L::NBUF - 1>();  // this buffer's previous store has read it
         __syncwarp();

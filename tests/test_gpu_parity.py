@@ -334,27 +334,29 @@ def test_filtered_ranks_planted_and_sharded():
                 e.close()
 
 
-@pytest.mark.parametrize("N,k", [(5000, 10), (5000, 32), (40000, 16)])
-def test_topk_heavy_ties(N, k):
+@pytest.mark.parametrize("N,k,model", [(5000, 10, "gqe"), (5000, 32, "gqe"), (40000, 16, "gqe"),
+                                       (5000, 10, "betae"), (3000, 32, "betae")])
+def test_topk_heavy_ties(N, k, model):
     """Q13/Q15 with massive exact ties: 7 distinct entity rows repeated over the table, so every
     query has ~N/7 entities at exactly its best distance (bit-identical: same row, same
     arithmetic).  The top-k must be those ties in ascending id order -- the filter buffer of
     the top-k kernel overflows and folds many times; N > 32k also takes the chunked path."""
-    d, R = 16, 4
+    d, R, B = 16, 4, 20   # BetaE: 20 query rows take the tensor-core scorer + block-minima top-k
     rng = np.random.default_rng(5)
-    pat = rng.uniform(-1, 1, (7, d)).astype(np.float32)
+    w = d if model == "gqe" else 2 * d
+    pat = rng.uniform(-0.9, 1, (7, w)).astype(np.float32)
     which = rng.integers(0, 7, N)
-    t = synth.make_tables("gqe", N, R, d, hidden=8, seed=3)
+    t = synth.make_tables(model, N, R, d, hidden=8, seed=3)
     t["entity"] = pat[which].copy()
-    e = Engine("gqe", N, R, d, hidden=8, max_batch=8, max_k=32)
+    e = Engine(model, N, R, d, hidden=8, max_batch=B, max_k=32)
     e.load_tables(t)
-    m = O.Model("gqe", t, dim=d)
-    a, r = synth.make_queries("1p", 8, N, R, seed=4)
+    m = O.Model(model, t, dim=d)
+    a, r = synth.make_queries("1p", B, N, R, seed=4)
     td, ti = e.submit("1p", dev(a), dev(r), k)
     e.check_errors()
     ref = m.scores("1p", a, r)
     td, ti = td.cpu().numpy(), ti.cpu().numpy()
-    for b in range(8):
+    for b in range(B):
         best = np.min(ref[b])
         ties = np.nonzero(ref[b] == best)[0]
         assert len(ties) >= k
