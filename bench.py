@@ -194,12 +194,12 @@ def run_suite(args):
     """One JSON line per BASELINE.json config other than the headline one: device
     q/s with L2 flushed between steps, stage split, and the dominant kernel against its roofline
     (SIMT scorers: FP32 lane-instructions vs 148 SMs x 128 lanes x SM clock; tensor path: useful
-    fp32 FLOPs vs the 3xTF32 peak)."""
+    fp32 FLOPs vs the bf16x3 peak = measured bf16 / 6)."""
     import torch
     from paper_2503_02172_b200 import Engine
     peaks, src = load_peaks()
     alu_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # lane-instr/s
-    tc_peak = peaks["bf16_tflops"] * (1.1 / 2.25) / 3.0
+    tc_peak = peaks["bf16_tflops"] / 6.0
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     names = args.suite.split(",") if args.suite else list(SUITE)
     for name in names:
@@ -241,7 +241,7 @@ def run_suite(args):
         d_ms, _, d_w = prof["dense"]
         if model == "betae" and B > 16:
             ach = (sc_w + d_w) / ((sc_ms + d_ms) / 1e3) / 1e12
-            roof = {"kernel": "k_gemm (tcgen05 3xTF32: dense layers + BetaE scorer)", "bound": "tensor",
+            roof = {"kernel": "k_gemm (tcgen05 bf16x3: dense layers + BetaE scorer)", "bound": "tensor",
                     "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak}
         else:
             ach = sc_w / (sc_ms / 1e3) if sc_ms > 0 else 0.0
@@ -363,15 +363,14 @@ def main():
         e2e_s = time.perf_counter() - t0
         e2e_v = queries / e2e_s
 
-    # ---- roofline of the dominant kernel: the tcgen05 3xTF32 GEMM (k_tc_gemm), which runs
-    # every dense layer of the chain (stage "dense") and the BetaE scorer contraction (stage
-    # "score").  Algorithmic work = useful fp32 FLOPs (2MNK); peak = TF32 dense peak / 3, the
-    # TF32 peak being the measured bf16 GEMM peak x the nominal tf32/bf16 ratio 1.1/2.25.
+    # ---- roofline of the dominant kernel: the tcgen05 bf16x3 GEMM (k_gemm), which runs every
+    # dense layer of the chain (stage "dense") and the BetaE scorer contraction (stage "score").
+    # Algorithmic work = useful fp32 FLOPs (2MNK); peak = measured bf16 GEMM peak / 6 (six bf16
+    # MMAs per useful fp32 multiply-add: x0w0, x0w1, x1w0, x0w2, x1w1, x2w0).
     peaks, peak_src = load_peaks()
     d_ms, d_n, d_fl = prof["dense"]
     s_ms, s_n, s_fl = prof["score"]
-    tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
-    peak_tc = tf32 / 3.0
+    peak_tc = peaks["bf16_tflops"] / 6.0
     ach = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms > 0 else 0.0
     achieved = ach(d_fl + s_fl, d_ms + s_ms)
     traffic = None
@@ -391,10 +390,10 @@ def main():
             "per_type_qps": {s: BATCH * args.steps / (per_type[s] / 1e3) for s in STRUCTS},
             "stage_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},  # dense is inside chain
             "stage_share": stage_share,
-            "roofline": {"kernel": "k_tc_gemm (tcgen05 3xTF32: chain dense layers + BetaE scorer)",
+            "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",
                          "bound": "tensor", "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
                          "frac": achieved / peak_tc, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16 {peaks['bf16_tflops']:.1f} x 1.1/2.25 (tf32) / 3 (3xTF32)",
+                         "peak_source": f"{peak_src} bf16 {peaks['bf16_tflops']:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
                          "work": "useful fp32 FLOPs 2MNK per GEMM launch",
                          "launches": d_n + s_n,
                          "parts": {"dense": {"ms_per_step": d_ms / args.steps, "tflops": ach(d_fl, d_ms),

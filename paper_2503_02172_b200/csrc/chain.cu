@@ -49,10 +49,10 @@ __global__ void k_translate_chain(ChainArgs a, const float* __restrict__ ent,
       c += rel[(int64_t)rid[o] * d + j];
       if (q2b) off += rel_off[(int64_t)rid[o] * d + j];
     }
-    if (out.hi) {
+    if (out.valid()) {
       const int64_t row = (int64_t)br * B + b;
-      store_split(out.hi, out.lo, row * out.ld + j, c);
-      if (q2b) store_split(out.hi, out.lo, row * out.ld + d + j, off);
+      store_split(out, row * out.ld + j, c);
+      if (q2b) store_split(out, row * out.ld + q2b_off(d) + j, off);
     } else {
       float* dst = q + ((int64_t)b * a.nb + br) * w;
       dst[j] = c;
@@ -88,11 +88,11 @@ __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
   const int64_t zrow = ((int64_t)gi * B + b) * z.ld;
   const int64_t srow = (g.src_row[gi] + b) * src.ld;
   for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
-    float x = from_anchor ? ent[(int64_t)aid * 2 * d + j] : load_split(src.hi, src.lo, srow + j);
-    store_split(z.hi, z.lo, zrow + j, x);
+    float x = from_anchor ? ent[(int64_t)aid * 2 * d + j] : load_split(src, srow + j);
+    store_split(z, zrow + j, x);
   }
   for (int j = threadIdx.x; j < d; j += blockDim.x)
-    store_split(z.hi, z.lo, zrow + 2 * d + j, rel[(int64_t)rid * d + j]);
+    store_split(z, zrow + 2 * d + j, rel[(int64_t)rid * d + j]);
 }
 
 int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
@@ -137,7 +137,7 @@ __global__ void k_softmax_terminal(const float* __restrict__ T, int64_t ldt, int
   for (int j = threadIdx.x; j < w; j += blockDim.x) {
     float y = fmaxf(expf(t[j] - m) * inv, 1e-6f);
     if (neg) y = 1.0f / y;
-    store_split(out.hi, out.lo, (out_row0 + r) * out.ld + j, y);
+    store_split(out, (out_row0 + r) * out.ld + j, y);
   }
 }
 
@@ -154,7 +154,7 @@ __global__ void k_negate(Split x, int64_t r0, int64_t nrows, int w) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = r0 + i / w, j = i % w;
     const int64_t o = r * x.ld + j;
-    store_split(x.hi, x.lo, o, 1.0f / load_split(x.hi, x.lo, o));
+    store_split(x, o, 1.0f / load_split(x, o));
   }
 }
 
@@ -172,7 +172,7 @@ __global__ void k_branch_mean(const float* __restrict__ T, int64_t ldt, int nb, 
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     float s = 0.0f;
     for (int i = 0; i < nb; ++i) s += T[((int64_t)i * B + b) * ldt + j];
-    store_split(out.hi, out.lo, (int64_t)b * out.ld + j, s / (float)nb);
+    store_split(out, (int64_t)b * out.ld + j, s / (float)nb);
   }
 }
 
@@ -214,9 +214,9 @@ __global__ void k_attention_combine(CombineArgs c, Split S, const float* __restr
     for (int i = 0; i < nb; ++i) {
       const int64_t row = ((int64_t)i * B + b) * S.ld;
       const float a = l[i] * inv;
-      x0 += a * load_split(S.hi, S.lo, row + j);
-      if (c.model == KGQ_BETAE) x1 += a * load_split(S.hi, S.lo, row + d + j);
-      if (c.model == KGQ_Q2B) omin = fminf(omin, load_split(S.hi, S.lo, row + d + j));
+      x0 += a * load_split(S, row + j);
+      if (c.model == KGQ_BETAE) x1 += a * load_split(S, row + d + j);
+      if (c.model == KGQ_Q2B) omin = fminf(omin, load_split(S, row + q2b_off(d) + j));
     }
     if (c.model == KGQ_Q2B) {
       const float g = gate[(int64_t)b * c.ldg + j];
@@ -231,9 +231,9 @@ __global__ void k_attention_combine(CombineArgs c, Split S, const float* __restr
       x1 = 1.0f / x1;
     }
     const bool two = c.model != KGQ_GQE;
-    if (out.hi) {
-      store_split(out.hi, out.lo, (int64_t)b * out.ld + j, x0);
-      if (two) store_split(out.hi, out.lo, (int64_t)b * out.ld + d + j, x1);
+    if (out.valid()) {
+      store_split(out, (int64_t)b * out.ld + j, x0);
+      if (two) store_split(out, (int64_t)b * out.ld + d + j, x1);
     } else {
       float* dst = q + (int64_t)b * (two ? 2 * d : d);
       dst[j] = x0;
@@ -252,7 +252,7 @@ int launch_attention_combine(const CombineArgs& c, Split S, const float* logits,
 __global__ void k_state_to_q(Split S, int nb, int B, int w, float* __restrict__ q) {
   const int b = blockIdx.x, br = blockIdx.y;
   for (int j = threadIdx.x; j < w; j += blockDim.x)
-    q[((int64_t)b * nb + br) * w + j] = load_split(S.hi, S.lo, ((int64_t)br * B + b) * S.ld + j);
+    q[((int64_t)b * nb + br) * w + j] = load_split(S, ((int64_t)br * B + b) * S.ld + j);
 }
 
 int launch_state_to_q(Split S, int nb, int B, int w, float* q, cudaStream_t st) {
@@ -261,14 +261,27 @@ int launch_state_to_q(Split S, int nb, int B, int w, float* q, cudaStream_t st) 
 }
 
 // ---- split copy (weights -> tensor-core operands) --------------------------------------
-__global__ void k_split_copy(const float* __restrict__ src, int64_t n, float* hi, float* lo) {
+__global__ void k_split_copy(const float* __restrict__ src, int64_t n, Split dst) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    store_split(hi, lo, i, src[i]);
+    store_split(dst, i, src[i]);
 }
 
-int launch_split_copy(const float* src, int64_t n, float* hi, float* lo, cudaStream_t st) {
-  k_split_copy<<<1024, 256, 0, st>>>(src, n, hi, lo);
+int launch_split_copy(const float* src, int64_t n, Split dst, cudaStream_t st) {
+  k_split_copy<<<1024, 256, 0, st>>>(src, n, dst);
+  return 1;
+}
+
+// row-major [rows, cols] fp32 -> split planes with row stride dst.ld (>= cols)
+__global__ void k_split_copy_rows(const float* __restrict__ src, int64_t rows, int cols, Split dst) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    store_split(dst, (i / cols) * dst.ld + i % cols, src[i]);
+}
+
+int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st) {
+  k_split_copy_rows<<<1024, 256, 0, st>>>(src, rows, cols, dst);
   return 1;
 }
 

@@ -1,26 +1,54 @@
 // Small device helpers shared by the kernels of libkgq.so.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace kgq {
 
-// fp32 -> tf32 (round to nearest, ties away) kept in an fp32 container (low 13 bits zero).
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// fp32 tensor held as three bf16 planes, the operand format of the tensor-core GEMMs
+// (tc_gemm.cuh, bf16x3): b0 = RN_bf16(x), b1 = RN_bf16(x - b0), b2 = RN_bf16(x - b0 - b1).
+// Each remainder is exact in fp32 and the last one has <= 8 significant bits, so
+// b0 + b1 + b2 == x exactly (bf16 keeps fp32's exponent range).  6 bytes per element.
+struct Split {
+  __nv_bfloat16* b0 = nullptr;
+  __nv_bfloat16* b1 = nullptr;
+  __nv_bfloat16* b2 = nullptr;
+  int64_t ld = 0;  // row stride in elements (all three planes)
+  __host__ __device__ __nv_bfloat16* plane(int p) const { return p == 0 ? b0 : p == 1 ? b1 : b2; }
+  __host__ __device__ bool valid() const { return b0 != nullptr; }
+  // the view starting at (row, col): same planes, shifted
+  __host__ __device__ Split at(int64_t row, int64_t col = 0) const {
+    const int64_t o = row * ld + col;
+    return Split{b0 + o, b1 + o, b2 + o, ld};
+  }
+};
+
+// Column of the offset half in a Q2B split state [centre | offset]: 8-element (16-byte) aligned
+// so that the offset half is itself a TMA-addressable GEMM operand.
+__host__ __device__ constexpr int q2b_off(int d) { return (d + 7) & ~7; }
+
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& a, __nv_bfloat16& b, __nv_bfloat16& c) {
+  a = __float2bfloat16_rn(x);
+  const float r = x - __bfloat162float(a);
+  b = __float2bfloat16_rn(r);
+  c = __float2bfloat16_rn(r - __bfloat162float(b));
+}
+__device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
+  return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
 }
 
-// Store x as the split pair (hi, lo): hi = rna_tf32(x), lo = x - hi (exact in fp32).
-__device__ __forceinline__ void store_split(float* hi, float* lo, int64_t i, float x) {
-  float h = tf32_rna(x);
-  hi[i] = h;
-  lo[i] = x - h;
+// Store x at element i of the split tensor (all three planes).
+__device__ __forceinline__ void store_split(const Split& s, int64_t i, float x) {
+  __nv_bfloat16 a, b, c;
+  split3(x, a, b, c);
+  s.b0[i] = a;
+  s.b1[i] = b;
+  s.b2[i] = c;
 }
 
-__device__ __forceinline__ float load_split(const float* hi, const float* lo, int64_t i) {
-  return hi[i] + lo[i];
+__device__ __forceinline__ float load_split(const Split& s, int64_t i) {
+  return (__bfloat162float(s.b0[i]) + __bfloat162float(s.b1[i])) + __bfloat162float(s.b2[i]);
 }
 
 // Record the first out-of-range id: err = {flag, row, slot, kind(0 anchor, 1 relation)}.

@@ -86,11 +86,16 @@ kgq_status dalloc(kgq_ctx* ctx, T** p, size_t n, const char* what) {
   return KGQ_OK;
 }
 
+// Three bf16 planes of [rows, ld] in one allocation (freed through b0); ld = w rounded up to 8
+// elements so every row starts 16-byte aligned (TMA operand maps).
 kgq_status alloc_split(kgq_ctx* ctx, Split* s, int64_t rows, int64_t w, const char* what) {
-  s->ld = w;
-  kgq_status st = dalloc(ctx, &s->hi, (size_t)(rows * w), what);
+  s->ld = (w + 7) / 8 * 8;
+  const size_t plane = (size_t)(rows * s->ld);
+  kgq_status st = dalloc(ctx, &s->b0, 3 * plane, what);
   if (st) return st;
-  return dalloc(ctx, &s->lo, (size_t)(rows * w), what);
+  s->b1 = s->b0 + plane;
+  s->b2 = s->b1 + plane;
+  return KGQ_OK;
 }
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -211,16 +216,20 @@ void check_site(const char* site) {
   if (e != cudaSuccess) fprintf(stderr, "libkgq: launch error after %s: %s\n", site, cudaGetErrorString(e));
 }
 
-int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
+// dense layer into a split (bf16x3) state, or into an fp32 buffer [M, ld]
+int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, const Split& out, int neg0,
           int neg1, cudaStream_t st) {
   StageTimer t(ctx, st, kStDense, 2.0 * M * (double)L.out_f * K);
-  const int r = launch_linear(A, M, K, L, epi, out, neg0, neg1, &ctx->gws, st);
+  const int r = launch_linear(A, M, K, L, epi, out, nullptr, 0, neg0, neg1, &ctx->gws, st);
   check_site("dense layer");
   return r;
 }
-
-Split offset_split(const Split& s, int64_t rows, int64_t cols = 0) {
-  return Split{s.hi + rows * s.ld + cols, s.lo + rows * s.ld + cols, s.ld};
+int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, float* out, int64_t ld,
+          cudaStream_t st) {
+  StageTimer t(ctx, st, kStDense, 2.0 * M * (double)L.out_f * K);
+  const int r = launch_linear(A, M, K, L, epi, Split{}, out, ld, 0, 0, &ctx->gws, st);
+  check_site("dense layer");
+  return r;
 }
 
 // BetaE: one projection hop (Eq. 4 MLP) for the contiguous branch run [br0, br0+n) of rows
@@ -263,10 +272,10 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
       extra.emplace_back(r0, r1);
     }
   }
-  Split out = offset_split(ctx->S, (int64_t)br0 * B);
+  Split out = ctx->S.at((int64_t)br0 * B);
   const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
   if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
-    L += dense(ctx, A, M, K, lo, kEpiNone, Split{ctx->T, nullptr, 2 * d}, 0, 0, st);
+    L += dense(ctx, A, M, K, lo, kEpiNone, ctx->T, 2 * d, st);
     L += launch_softmax_terminal(ctx->T, 2 * d, M, 2 * d, out, 0, neg0, neg1, st);
   } else {
     L += dense(ctx, A, M, K, lo, kEpiBetaReg, out, neg0, neg1, st);
@@ -288,23 +297,19 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
 
   if (model != KGQ_BETAE) {
     if (P->kind != kInter) {
-      return launch_translate_chain(ca, ctx->ent, ctx->rel[0], ctx->rel[1], B, Split{nullptr, nullptr, 0},
-                                    ctx->Q, st);
+      return launch_translate_chain(ca, ctx->ent, ctx->rel[0], ctx->rel[1], B, Split{}, ctx->Q, st);
     }
     L += launch_translate_chain(ca, ctx->ent, ctx->rel[0], ctx->rel[1], B, ctx->S, nullptr, st);
     // attention logits over centres (Q6): W2 ReLU(W1 x + b1) + b2, rows br*B + b
-    const Split centres{ctx->S.hi, ctx->S.lo, ctx->S.ld};
+    const Split centres = ctx->S;
     L += dense(ctx, centres, (int)M, d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
-    L += dense(ctx, ctx->I, (int)M, d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
-                       Split{ctx->T, nullptr, ctx->tw}, 0, 0, st);
+    L += dense(ctx, ctx->I, (int)M, d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone, ctx->T, ctx->tw, st);
     const float* gate = nullptr;
     if (model == KGQ_Q2B) {  // offset gate: sigmoid(V2 mean_i ReLU(V1 o_i + c1) + c2)
-      const Split offs{ctx->S.hi + d, ctx->S.lo + d, ctx->S.ld};
-      L += dense(ctx, offs, (int)M, d, ctx->lin[KGQ_LAYER_OFFSET_1], kEpiRelu,
-                         Split{ctx->T2, nullptr, ctx->tw}, 0, 0, st);
+      const Split offs = ctx->S.at(0, q2b_off(d));  // offsets start 16-byte aligned (common.cuh)
+      L += dense(ctx, offs, (int)M, d, ctx->lin[KGQ_LAYER_OFFSET_1], kEpiRelu, ctx->T2, ctx->tw, st);
       L += launch_branch_mean(ctx->T2, ctx->tw, nb, B, d, ctx->M, st);
-      L += dense(ctx, ctx->M, B, d, ctx->lin[KGQ_LAYER_OFFSET_2], kEpiNone,
-                         Split{ctx->T2, nullptr, ctx->tw}, 0, 0, st);
+      L += dense(ctx, ctx->M, B, d, ctx->lin[KGQ_LAYER_OFFSET_2], kEpiNone, ctx->T2, ctx->tw, st);
       gate = ctx->T2;
     }
     CombineArgs c{};
@@ -312,7 +317,7 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
     c.rel = ctx->rel[0]; c.rel_off = ctx->rel[1]; c.rels = rels; c.n_r = P->n_rel;
     c.n_relation = ctx->cfg.n_relation; c.post_slot = P->npost ? P->post[0] : -1;
     c.err = ctx->d_err; c.invalid = ctx->d_invalid;
-    L += launch_attention_combine(c, ctx->S, ctx->T, gate, Split{nullptr, nullptr, 0}, ctx->Q, st);
+    L += launch_attention_combine(c, ctx->S, ctx->T, gate, Split{}, ctx->Q, st);
     return L;
   }
 
@@ -349,15 +354,14 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
   if (P->kind != kInter) return L + launch_state_to_q(ctx->S, P->n_out, B, 2 * d, ctx->Q, st);
   // intersection (Q6): attention over [alpha_i; beta_i] (2d -> 2d -> d), shared weights a_i
   L += dense(ctx, ctx->S, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
-  L += dense(ctx, ctx->I, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone,
-                     Split{ctx->T, nullptr, ctx->tw}, 0, 0, st);
+  L += dense(ctx, ctx->I, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone, ctx->T, ctx->tw, st);
   CombineArgs c{};
   c.model = model; c.nb = nb; c.B = B; c.d = d; c.ldl = ctx->tw; c.ldg = 0;
   c.rels = rels; c.n_r = P->n_rel; c.n_relation = ctx->cfg.n_relation; c.post_slot = -1;
   c.negate_out = P->neg_inter ? 1 : 0;
   c.err = ctx->d_err; c.invalid = ctx->d_invalid;
   if (P->npost == 0)
-    return L + launch_attention_combine(c, ctx->S, ctx->T, nullptr, Split{nullptr, nullptr, 0}, ctx->Q, st);
+    return L + launch_attention_combine(c, ctx->S, ctx->T, nullptr, Split{}, ctx->Q, st);
   L += launch_attention_combine(c, ctx->S, ctx->T, nullptr, ctx->M, nullptr, st);
   // post projections (ip, inp): MLP hops on the combined state, result in S rows [0, B)
   int pproj[kMaxBranches][kMaxOps] = {};
@@ -493,11 +497,11 @@ void kgq_destroy(kgq_ctx* ctx) {
   cudaDeviceSynchronize();
   auto F = [](void* p) { if (p) cudaFree(p); };
   F(ctx->ent); F(ctx->rel[0]); F(ctx->rel[1]); F(ctx->score_tab);
-  for (auto& l : ctx->lin) { F(l.W); F(l.W_hi); F(l.W_lo); F(l.b); }
-  for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) { F(s->hi); F(s->lo); }
+  for (auto& l : ctx->lin) { F(l.W); F(l.Wsp.b0); F(l.b); }
+  for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) F(s->b0);
   F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->d_err); F(ctx->d_invalid);
-  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv_hi); F(ctx->uv_lo); F(ctx->Esum);
-  F(ctx->uvsums); F(ctx->Atc.hi); F(ctx->Atc.lo); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
+  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum);
+  F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -559,8 +563,7 @@ kgq_status kgq_load_linear(kgq_ctx* ctx, int32_t id, const float* W, const float
   kgq_status st = KGQ_OK;
   if (!L.W) {
     if (!st) st = dalloc(ctx, &L.W, n, "linear W");
-    if (!st) st = dalloc(ctx, &L.W_hi, n, "linear W_hi");
-    if (!st) st = dalloc(ctx, &L.W_lo, n, "linear W_lo");
+    if (!st) st = alloc_split(ctx, &L.Wsp, out_f, in_f, "linear W (bf16x3)");
     if (!st) st = dalloc(ctx, &L.b, (size_t)out_f, "linear b");
     if (st) return st;
   }
@@ -568,7 +571,7 @@ kgq_status kgq_load_linear(kgq_ctx* ctx, int32_t id, const float* W, const float
   L.in_f = in_f;
   CK(cudaMemcpy(L.W, W, n * sizeof(float), cudaMemcpyHostToDevice), "linear W upload");
   CK(cudaMemcpy(L.b, b, (size_t)out_f * sizeof(float), cudaMemcpyHostToDevice), "linear b upload");
-  launch_split_copy(L.W, (int64_t)n, L.W_hi, L.W_lo, 0);
+  launch_split_copy_rows(L.W, out_f, in_f, L.Wsp, 0);
   CK(cudaDeviceSynchronize(), "linear split");
   return KGQ_OK;
 }
@@ -601,7 +604,9 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   ctx->bchunk = std::max<int64_t>(1, std::min<int64_t>(Bm, budget / (ctx->np * 4)));
   kgq_status st = KGQ_OK;
   const int iw = c.model == KGQ_BETAE ? 2 * d : d;
-  if (!st) st = alloc_split(ctx, &ctx->S, ctx->rows_max, ctx->qw, "state S");
+  // Q2B states hold [centre | offset] with the offset half at a 16-byte aligned column
+  const int64_t sw = c.model == KGQ_Q2B ? q2b_off(d) + d : ctx->qw;
+  if (!st) st = alloc_split(ctx, &ctx->S, ctx->rows_max, sw, "state S");
   if (!st) st = alloc_split(ctx, &ctx->I, ctx->rows_max, iw, "intersection hidden");
   if (!st) st = alloc_split(ctx, &ctx->M, Bm, ctx->qw, "combined state");
   if (!st && c.model == KGQ_BETAE) {
@@ -618,8 +623,7 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_d, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_i, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st && c.model == KGQ_BETAE) {
-    st = dalloc(ctx, &ctx->uv_hi, (size_t)(ctx->np * 2 * d), "uv table");
-    if (!st) st = dalloc(ctx, &ctx->uv_lo, (size_t)(ctx->np * 2 * d), "uv table");
+    st = alloc_split(ctx, &ctx->uv, ctx->np, 2 * d, "uv table");
     if (!st) st = dalloc(ctx, &ctx->Esum, (size_t)ctx->np, "entity sums");
     if (!st) st = dalloc(ctx, &ctx->uvsums, (size_t)(2 * d), "uv sums");
     if (!st) st = alloc_split(ctx, &ctx->Atc, 2 * ctx->bchunk, 2 * d, "tc query rows");
@@ -637,7 +641,7 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (c.model == KGQ_BETAE) {
     launch_beta_regularize(ctx->ent, c.n_entity * ctx->ew, 0);
     launch_betae_entity_terms(ctx->ent, ctx->e0, ctx->ns, d, ctx->score_tab, ctx->np, 0);
-    launch_betae_uv_table(ctx->ent, c.n_entity, ctx->e0, ctx->ns, ctx->np, d, ctx->uvsums, ctx->uv_hi, ctx->uv_lo,
+    launch_betae_uv_table(ctx->ent, c.n_entity, ctx->e0, ctx->ns, ctx->np, d, ctx->uvsums, ctx->uv,
                           ctx->Esum, 0);
   } else {
     launch_transpose_shard(ctx->ent, ctx->e0, ctx->ns, d, ctx->ew, ctx->score_tab, ctx->np, 0);
@@ -658,7 +662,7 @@ static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStrea
     // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
     StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
     L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
-                               ctx->Ptc, ctx->uv_hi, ctx->uv_lo, ctx->Esum, ctx->np, ctx->dist, ctx->np, ctx->cmin,
+                               ctx->Ptc, ctx->uv, ctx->Esum, ctx->np, ctx->dist, ctx->np, ctx->cmin,
                                ctx->np / 32, ctx->ns, &ctx->gws, st);
     check_site("tensor-core scorer");
   } else {

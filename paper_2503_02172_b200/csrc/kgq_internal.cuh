@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/kgq.h"
+#include "common.cuh"
 
 namespace kgq {
 
@@ -43,18 +44,9 @@ struct Plan {
 };
 const Plan* plan_of(int s);
 
-// fp32 tensor split into (hi = rna_tf32(x), lo = x - hi) with hi + lo == x exactly.
-// Every activation that feeds a dense layer is kept in this form (3xTF32 operands).
-struct Split {
-  float* hi;
-  float* lo;
-  int64_t ld;  // row stride in elements
-};
-
 struct Linear {
   float* W = nullptr;     // [out, in] fp32
-  float* W_hi = nullptr;  // split copies for the tensor-core path
-  float* W_lo = nullptr;
+  Split Wsp{};            // bf16x3 planes of W for the tensor-core path (ld = in)
   float* b = nullptr;     // [out]
   int out_f = 0, in_f = 0;
 };
@@ -112,8 +104,7 @@ struct kgq_ctx {
   float* topk_tmp_d = nullptr;             // chunked top-k candidates [<= 4096 per row]
   int32_t* topk_tmp_i = nullptr;
   // BetaE tensor-core scoring layout (score_tc.cu)
-  float* uv_hi = nullptr;                  // [np][2d] centred (u; v), split
-  float* uv_lo = nullptr;
+  kgq::Split uv{};                         // [np][2d] centred (u; v), bf16x3
   float2* Esum = nullptr;                  // [np] sum_d C_ed as an fp32 (hi, lo) pair
   double* uvsums = nullptr;                // [2][d]
   kgq::GemmWs gws{};                       // tensor-core GEMM split-tail scratch
@@ -185,10 +176,10 @@ struct MlpGroup {
 int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
                            const MlpGroup& g, Split src, Split z, cudaStream_t st);
 // Dense layer: out = epi(A W^T + b) for rows [0, M), A given as split (K columns).
-//   split output if out.lo != nullptr, else plain fp32 into out.hi.
+//   split (bf16x3) output into out_sp if out_sp.valid(), else fp32 into out_f32 (row stride ld_f32).
 //   kEpiBetaReg: clamp(y+1, .05, 1e9), then 1/x on rows [neg0, neg1).
-int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split out,
-                  int neg0, int neg1, const GemmWs* ws, cudaStream_t st);
+int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, const Split& out_sp,
+                  float* out_f32, int64_t ld_f32, int neg0, int neg1, const GemmWs* ws, cudaStream_t st);
 // BetaE Eq.-4 softmax terminal over rows of T (width w) -> split state rows out_row0 + r,
 // with negation on rows r in [neg0, neg1).
 int launch_softmax_terminal(const float* T, int64_t ldt, int M, int w, Split out,
@@ -241,9 +232,9 @@ int launch_filtered_counts(const float* dist, int64_t ldd, int64_t e0, int64_t n
 // uv [np][2d], E_e = sum_d C_ed (fp64) and the per-dim U/V sums; per batch it splits the
 // query rows, computes P_q (fp64) and runs the 3xTF32 GEMM with the score epilogue.
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
-                          double* sums, float* uv_hi, float* uv_lo, float2* Esum, cudaStream_t st);
+                          double* sums, Split uv, float2* Esum, cudaStream_t st);
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
-                          Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
+                          Split A, float2* P, const Split& uv, const float2* Esum,
                           int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
                           const GemmWs* ws, cudaStream_t st);
 // Top-k of dist rows using the score epilogue's 32-entity block minima cmin [B][ldc] (k <= 32):
@@ -260,5 +251,6 @@ int launch_transpose_shard(const float* ent, int64_t e0, int64_t ns, int d, int 
                            int64_t np, cudaStream_t st);
 int launch_betae_entity_terms(const float* ent, int64_t e0, int64_t ns, int d, float* tab,
                               int64_t np, cudaStream_t st);
-int launch_split_copy(const float* src, int64_t n, float* hi, float* lo, cudaStream_t st);
+int launch_split_copy(const float* src, int64_t n, Split dst, cudaStream_t st);
+int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st);
 }  // namespace kgq

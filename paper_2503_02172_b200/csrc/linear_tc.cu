@@ -2,13 +2,14 @@
 //
 // Used by the BetaE projection MLP (Eq. 4) and the intersection attention nets
 // -- the only dense contractions on the path.  B200 has no fp32-input MMA,
-// and single-pass TF32 misses the 1e-4 parity bound (SURVEY §0 finding 5), so this is 3xTF32:
-//   x = x_hi + x_lo, w = w_hi + w_lo (hi = rna_tf32, lo = remainder; both exact in fp32)
-//   x w ~= x_hi w_lo + x_lo w_hi + x_hi w_hi          (x_lo w_lo, ~2^-22 relative, dropped)
-// accumulated in fp32 in TMEM.  Operands are produced already split (every producer kernel
-// writes hi/lo pairs), so the mainloop is a pure TMA -> tcgen05.mma pipeline; the GEMM core
-// (persistent CTA-pair kernel, TMA-store epilogue) is tc_gemm.cuh.  This file supplies the
-// epilogue: bias + ReLU / BetaE regulariser (+ negation) fused, split (hi/lo) or fp32 output.
+// and single-pass TF32 / BF16 miss the 1e-4 parity bound (SURVEY §0 finding 5), so operands are
+// held as three bf16 planes x = x0 + x1 + x2 (exact, common.cuh Split) and
+//   x w ~= x0 w0 + x0 w1 + x1 w0 + x0 w2 + x1 w1 + x2 w0     (dropped terms <= 2^-23 |x w|)
+// accumulated in fp32 in TMEM (bf16x3, tc_gemm.cuh).  Operands are produced already split (every
+// producer kernel writes the three planes), so the mainloop is a pure TMA -> tcgen05.mma
+// pipeline; the GEMM core (persistent CTA-pair kernel, TMA-store epilogue) is tc_gemm.cuh.  This
+// file supplies the epilogue: bias + ReLU / BetaE regulariser (+ negation) fused, split
+// (bf16x3) or fp32 output.
 #include <stdint.h>
 
 #include "tc_gemm.cuh"
@@ -19,11 +20,11 @@ namespace {
 using tc::BM;
 
 // nn.Linear epilogue: + bias, ReLU / BetaE regulariser (clamp(y+1,.05,1e9)) with 1/x on rows
-// [neg0, neg1) (negation fused, Q5); output split (hi/lo, PLANES 2) for a next dense layer,
+// [neg0, neg1) (negation fused, Q5); output split (bf16x3, PLANES 3) for a next dense layer,
 // or fp32.
 template <int EPI, bool SPLIT>
 struct EpiLinear {
-  static constexpr int PLANES = SPLIT ? 2 : 1, ROWDIV = 1;
+  static constexpr int PLANES = SPLIT ? 3 : 1, ROWDIV = 1;
   static constexpr bool CMIN = false;
   template <int CH>
   __device__ void chunk_min(int, int, const float*) const {}
@@ -57,29 +58,25 @@ struct EpiLinear {
 };
 
 template <int EPI, bool SPLIT>
-int launch_epi(const Split& A, int M, int K, const Linear& L, Split out, int neg0, int neg1,
-               const GemmWs* ws, cudaStream_t st) {
-  const tc::OutDesc o{out.hi, out.lo, M, L.out_f, out.ld};
-  return tc::launch_gemm_auto(A, M, L.W_hi, L.W_lo, L.out_f, L.in_f, K, o,
-                              EpiLinear<EPI, SPLIT>{L.b, L.out_f, neg0, neg1}, ws, st);
+int launch_epi(const Split& A, int M, int K, const Linear& L, const Split& out_sp, float* out_f32, int64_t ld_f32,
+               int neg0, int neg1, const GemmWs* ws, cudaStream_t st) {
+  const tc::OutDesc o{out_f32, ld_f32, out_sp, M, L.out_f};
+  return tc::launch_gemm_auto(A, M, L.Wsp, L.out_f, K, o, EpiLinear<EPI, SPLIT>{L.b, L.out_f, neg0, neg1}, ws, st);
 }
 }  // namespace
 
-int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, Split out, int neg0,
-                  int neg1, const GemmWs* ws, cudaStream_t st) {
+int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, const Split& out_sp, float* out_f32,
+                  int64_t ld_f32, int neg0, int neg1, const GemmWs* ws, cudaStream_t st) {
   if (M <= 0) return 0;
-  const bool split = out.lo != nullptr;
+  const bool split = out_sp.valid();
+#define KGQ_EPI(E) (split ? launch_epi<E, true>(A, M, K, L, out_sp, out_f32, ld_f32, neg0, neg1, ws, st) \
+                          : launch_epi<E, false>(A, M, K, L, out_sp, out_f32, ld_f32, neg0, neg1, ws, st))
   switch (epi) {
-    case kEpiRelu:
-      return split ? launch_epi<kEpiRelu, true>(A, M, K, L, out, neg0, neg1, ws, st)
-                   : launch_epi<kEpiRelu, false>(A, M, K, L, out, neg0, neg1, ws, st);
-    case kEpiBetaReg:
-      return split ? launch_epi<kEpiBetaReg, true>(A, M, K, L, out, neg0, neg1, ws, st)
-                   : launch_epi<kEpiBetaReg, false>(A, M, K, L, out, neg0, neg1, ws, st);
-    default:
-      return split ? launch_epi<kEpiNone, true>(A, M, K, L, out, neg0, neg1, ws, st)
-                   : launch_epi<kEpiNone, false>(A, M, K, L, out, neg0, neg1, ws, st);
+    case kEpiRelu: return KGQ_EPI(kEpiRelu);
+    case kEpiBetaReg: return KGQ_EPI(kEpiBetaReg);
+    default: return KGQ_EPI(kEpiNone);
   }
+#undef KGQ_EPI
 }
 
 }  // namespace kgq

@@ -13,7 +13,7 @@
 // (Sterbenz; the usual case, P ~ -E) and otherwise errs by <= 2^-24 |P + E| ~ 2^-24 dist, the
 // dropped lo-lo rounding is ~2^-48 |P|, so dist carries ~1e-7 relative -- three FADDs instead
 // of fp64 adds and conversions, and no fp64 registers next to the row accumulators.
-// The last term is a dense contraction [rows, 2d] x [2d, N] -> 3xTF32 on tcgen05 (tc_gemm.cuh).
+// The last term is a dense contraction [rows, 2d] x [2d, N] -> bf16x3 on tcgen05 (tc_gemm.cuh).
 // Centring keeps its terms ~0.1 (|u|, |v| << |U|, |V| ~ 1), so the fp32 partial sums carry
 // ~1e-7 of sum|terms| ~ 1e-5 absolute instead of ~1e-4 for the uncentred sum, and the large,
 // cancelling P_q + E_e (~ +-800 at d = 400) are added in fp64 in the epilogue.  DNF union:
@@ -53,8 +53,8 @@ __device__ __forceinline__ float2 split_f64(double x) {
 }
 
 __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns, int64_t np, int d,
-                           int64_t n_all, const double* __restrict__ sums, float* __restrict__ uv_hi,
-                           float* __restrict__ uv_lo, float2* __restrict__ Esum) {
+                           int64_t n_all, const double* __restrict__ sums, Split uv,
+                           float2* __restrict__ Esum) {
   const int64_t e = blockIdx.x;
   __shared__ double red[32];
   double c = 0.0;
@@ -67,8 +67,8 @@ __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns
       u = (float)((pab - pa) - sums[j] / (double)n_all);
       v = (float)((pab - pb) - sums[d + j] / (double)n_all);
     }
-    store_split(uv_hi, uv_lo, e * 2 * d + j, u);
-    store_split(uv_hi, uv_lo, e * 2 * d + d + j, v);
+    store_split(uv, e * 2 * d + j, u);
+    store_split(uv, e * 2 * d + d + j, v);
   }
   c = warp_sum(c);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
@@ -91,8 +91,8 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
   const double inv = 1.0 / (double)ns;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     const float a = q[(int64_t)r * 2 * d + j], b = q[(int64_t)r * 2 * d + d + j];
-    store_split(A.hi, A.lo, (int64_t)r * A.ld + j, a);
-    store_split(A.hi, A.lo, (int64_t)r * A.ld + d + j, b);
+    store_split(A, (int64_t)r * A.ld + j, a);
+    store_split(A, (int64_t)r * A.ld + d + j, b);
     const double da = a, db = b;
     p += lgamma(da) + lgamma(db) - lgamma(da + db) + da * sums[j] * inv + db * sums[d + j] * inv;
   }
@@ -169,27 +169,27 @@ struct EpiBetaScore {
 }  // namespace
 
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
-                          double* sums, float* uv_hi, float* uv_lo, float2* Esum, cudaStream_t st) {
+                          double* sums, Split uv, float2* Esum, cudaStream_t st) {
   // centring means over ALL entities (every rank holds the full table), so that every shard
   // uses the same u, v and a sharded run is bit-identical to a single-GPU run
   cudaMemsetAsync(sums, 0, 2 * d * sizeof(double), st);
   const int gx = (int)(n_all < 1024 ? n_all : 1024);
   k_uv_dim_sums<<<dim3(gx, (d + 127) / 128), 128, 0, st>>>(ent, 0, n_all, d, sums);
-  k_uv_table<<<(unsigned)np, 128, 0, st>>>(ent, e0, ns, np, d, n_all, sums, uv_hi, uv_lo, Esum);
+  k_uv_table<<<(unsigned)np, 128, 0, st>>>(ent, e0, ns, np, d, n_all, sums, uv, Esum);
   return 2;
 }
 
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
-                          Split A, float2* P, const float* uv_hi, const float* uv_lo, const float2* Esum,
+                          Split A, float2* P, const Split& uv, const float2* Esum,
                           int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
                           const GemmWs* ws, cudaStream_t st) {
   k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
   // dist rows: one per query (NB = 2: min over the two DNF branch rows 2b, 2b + 1)
-  const tc::OutDesc o{dist, nullptr, rows / nbq, np, ldd};
+  const tc::OutDesc o{dist, ldd, Split{}, rows / nbq, np};
   if (nbq == 2)
-    return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
+    return 1 + tc::launch_gemm_auto(A, rows, uv, (int)np, 2 * d, o,
                                     EpiBetaScore<2>{P, Esum, rows, np, cmin, ldc, nvalid}, ws, st);
-  return 1 + tc::launch_gemm_auto(A, rows, uv_hi, uv_lo, (int)np, 2 * d, 2 * d, o,
+  return 1 + tc::launch_gemm_auto(A, rows, uv, (int)np, 2 * d, o,
                                   EpiBetaScore<1>{P, Esum, rows, np, cmin, ldc, nvalid}, ws, st);
 }
 

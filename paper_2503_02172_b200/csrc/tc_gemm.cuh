@@ -1,12 +1,15 @@
 // tcgen05 3xTF32 GEMM core shared by the dense layers (linear_tc.cu) and the tensor-core
 // BetaE scorer (score_tc.cu).
 //
-// acc[m, n] = sum_k A[m, k] W[n, k] in 3xTF32 (x w ~= x_hi w_lo + x_lo w_hi + x_hi w_hi, hi/lo
-// split operands produced by every upstream kernel), persistent and CTA-pair based:
+// acc[m, n] = sum_k A[m, k] W[n, k] in bf16x3: every fp32 operand is held as three bf16 planes
+// x = x0 + x1 + x2 (exact; written by every upstream kernel, common.cuh), and
+//   x w ~= x0 w0 + x0 w1 + x1 w0 + x0 w2 + x1 w1 + x2 w0      (dropped terms <= 2^-23 |x w|)
+// on tcgen05.mma.kind::f16 (bf16 inputs, fp32 accumulation; 6 bf16 MMAs = the tensor time of 3
+// tf32 ones, 6 operand bytes per element instead of 3xTF32's 8), persistent, CTA-pair based:
 //   * a cluster of two CTAs (one TPC) computes 256 x BN output tiles with
 //     tcgen05.mma.cta_group::2 (M 256, N BN, K 8), each CTA staging its own 128 rows of A and
-//     half (BN/2 rows) of the W tile by TMA (128-byte swizzle, OOB zero fill), so per CTA the
-//     operand stream is (128 + BN/2) x 256 B per 32-deep K-block;
+//     half (BN/2 rows) of the W tile by TMA (64-byte swizzle, OOB zero fill), so per CTA the
+//     operand stream is (128 + BN/2) x 192 B per 32-deep K-block;
 //   * the grid is at most one cluster per TPC (74 on B200) and loops over tiles (M fastest,
 //     so concurrently running clusters read the same W tiles out of L2);
 //   * warp 0 lane 0 = TMA producer, warp 1 lane 0 (leader CTA) = MMA issuer, warps 2-9 =
@@ -17,13 +20,14 @@
 //   * the epilogue of tile t (bias / activation / split / score terms, Epi::chunk) overlaps
 //     the first partials of tile t+1, and writes through a swizzled shared-memory staging tile
 //     and TMA bulk tensor stores (cp.async.bulk.tensor shared -> global; the tensor map clips
-//     the ragged M / N edges);
+//     the ragged M / N edges; split outputs are written as the three bf16 planes);
 //   * launched with programmatic dependent launch: barrier init, TMEM allocation and tensor-map
 //     prefetch overlap the upstream kernel's tail (griddepcontrol.wait before the first load).
 // Measured (profiles/r01/tc_trace_*.txt): the non-persistent predecessor spent 6-14 us per tile
 // in a per-element STG epilogue and ~3 us in per-CTA setup; this layout hides both.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -67,6 +71,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait for a phase that is typically far away (epilogue warps waiting for a whole partial,
+// the producer waiting for a free stage): poll with a nanosleep back-off so that idle warps do
+// not take issue slots from the single MMA-issuing thread on the same SM sub-partition.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) break;
+#ifndef KGQ_TC_NO_BACKOFF
+    __nanosleep(64);
+#endif
+  }
+}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -76,14 +102,14 @@ __device__ __forceinline__ void fence_after() {
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
-// K-major operand tile, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+// K-major bf16 operand tile, 64-byte swizzle: rows of 32 bf16 = 64 B, 8-row atoms 512 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
   d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;              // SBO: 8 rows x 128 B
+  d |= (uint64_t)(512 >> 4) << 32;               // SBO: 8 rows x 64 B
   d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+  d |= (uint64_t)4 << 61;                        // SWIZZLE_64B
   return d;
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -151,13 +177,13 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                              uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
@@ -200,17 +226,19 @@ constexpr int DRAIN = KGQ_TC_DRAIN;
 template <int BN>
 struct Layout {
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int A_BYTES = BM * BK * 4;         // 16 KB
-  static constexpr int W_BYTES = (BN / 2) * BK * 4;   // this CTA's half of the W tile
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;
+  static constexpr int A_BYTES = BM * BK * 2;         // one bf16 plane of A: 8 KB
+  static constexpr int W_BYTES = (BN / 2) * BK * 2;   // one plane of this CTA's half of the W tile
+  static constexpr int STAGE_BYTES = 3 * A_BYTES + 3 * W_BYTES;
   static constexpr int BUF_BYTES = 4096;
   static constexpr int BUDGET = 227 * 1024 - 1024 - 256;  // minus alignment slack and barriers
-  static constexpr int STAGES = (BUDGET - EPI_WARPS * BUF_BYTES) / STAGE_BYTES >= 4 ? 4 : 3;
+  static constexpr int FIT = (BUDGET - EPI_WARPS * BUF_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = FIT > 6 ? 6 : FIT;
   static constexpr int NBUF = BUDGET - STAGES * STAGE_BYTES >= 2 * EPI_WARPS * BUF_BYTES ? 2 : 1;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = STG_OFF + NBUF * EPI_WARPS * BUF_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
   static_assert(TOTAL <= 227 * 1024, "shared memory budget");
+  static_assert(STAGES >= 3, "pipeline depth");
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "2-CTA tile: N multiple of 32 per CTA, CW multiple of 32");
 };
 
@@ -239,7 +267,7 @@ __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, 
 }
 
 // Epilogue policy concept (linear_tc.cu, score_tc.cu):
-//   static constexpr int PLANES  -- 1: fp32 output; 2: split output (hi = rna_tf32(y), lo = y - hi)
+//   static constexpr int PLANES  -- 1: fp32 output; 3: split output (three bf16 planes, exact)
 //   static constexpr int ROWDIV  -- 1, or 2: output row r = min over tile rows 2r, 2r+1 (DNF union)
 //   struct Pre; template <int CW> __device__ Pre prefetch(int row, int n0, int lane) const
 //       -- per-tile operands (row terms, and column vectors with lane l holding columns
@@ -249,18 +277,20 @@ __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, 
 //          column operands come from the prefetched registers by warp shuffle
 //   static constexpr bool CMIN; template <int CH> __device__ void chunk_min(int row, int n,
 //       const float* v) const -- optional side output after the row-pair min (score top-k)
-// Output tensor maps: plane p, box {32 / PLANES columns, 32 / ROWDIV rows}.
+// Output tensor maps: PLANES 1: fp32, box {32 columns, 32 / ROWDIV rows}, 128-byte swizzle;
+// PLANES 3: bf16 plane p, box {16 columns, 32 rows}, 32-byte swizzle.
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
            const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
-           const __grid_constant__ CUtensorMap mO0, const __grid_constant__ CUtensorMap mO1, int M, int N, int K,
-           const Sched sc, const Epi epi) {
+           const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mW2,
+           const __grid_constant__ CUtensorMap mO0, const __grid_constant__ CUtensorMap mO1,
+           const __grid_constant__ CUtensorMap mO2, int M, int N, int K, const Sched sc, const Epi epi) {
   using L = Layout<BN>;
   constexpr int STAGES = L::STAGES;
   constexpr int PLANES = Epi::PLANES, ROWDIV = Epi::ROWDIV;
   constexpr int CW = BN / 2;            // columns per epilogue warp
-  constexpr int CH = 32 / PLANES;       // columns per staged chunk
+  constexpr int CH = PLANES == 1 ? 32 : 16;  // columns per staged chunk
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
@@ -281,12 +311,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mAh);
     tma_prefetch(&mAl);
+    tma_prefetch(&mA2);
     tma_prefetch(&mWh);
     tma_prefetch(&mWl);
+    tma_prefetch(&mW2);
     tma_prefetch(&mO0);
-    if (PLANES == 2) tma_prefetch(&mO1);
+    if (PLANES == 3) {
+      tma_prefetch(&mO1);
+      tma_prefetch(&mO2);
+    }
     for (int s = 0; s < STAGES; ++s) {
+#ifdef KGQ_TC_DBG_NO_TMA
+      mbar_init(&full[s], 2);
+#else
       mbar_init(&full[s], 1);
+#endif
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -319,21 +358,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int nw = (t / m_pairs) * BN + (int)rank * (BN / 2);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          if (it >= STAGES) mbar_wait_backoff(&empty[s], ((it / STAGES) - 1) & 1);
           uint8_t* st = smem + s * L::STAGE_BYTES;
           const uint32_t lb = mapa_shared(smem_u32(&full[s]), 0);
+#ifdef KGQ_TC_DBG_NO_TMA  // perf probe only: no operand loads, each CTA arrives on the leader's barrier
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(lb) : "memory");
+          (void)st;
+          continue;
+#endif
           if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
           tma_load_2d_2sm(st, &mAh, lb, kb * BK, m0);
           tma_load_2d_2sm(st + L::A_BYTES, &mAl, lb, kb * BK, m0);
-          tma_load_2d_2sm(st + 2 * L::A_BYTES, &mWh, lb, kb * BK, nw);
-          tma_load_2d_2sm(st + 2 * L::A_BYTES + L::W_BYTES, &mWl, lb, kb * BK, nw);
+          tma_load_2d_2sm(st + 2 * L::A_BYTES, &mA2, lb, kb * BK, m0);
+          tma_load_2d_2sm(st + 3 * L::A_BYTES, &mWh, lb, kb * BK, nw);
+          tma_load_2d_2sm(st + 3 * L::A_BYTES + L::W_BYTES, &mWl, lb, kb * BK, nw);
+          tma_load_2d_2sm(st + 3 * L::A_BYTES + 2 * L::W_BYTES, &mW2, lb, kb * BK, nw);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader only): M = 256 over the pair, N = BN ----------------
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+      // instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 256 over the pair
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)((2 * BM) >> 4) << 24);
       uint32_t it = 0, g0 = 0;
       for (int u = cluster; u < nunits; u += nclusters) {
@@ -351,15 +398,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           fence_after();
           const uint32_t d = tmem + a * BN;
           const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
-          const uint32_t ah = st, al = st + L::A_BYTES;
-          const uint32_t wh = st + 2 * L::A_BYTES, wl = wh + L::W_BYTES;
+          const uint32_t a0 = st, a1 = st + L::A_BYTES, a2 = st + 2 * L::A_BYTES;
+          const uint32_t w0 = st + 3 * L::A_BYTES, w1 = w0 + L::W_BYTES, w2 = w1 + L::W_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 32 bytes per MMA along K
+          for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 32 bytes per MMA along K
             const uint32_t off = kk * 32;
-            mma_tf32_2sm(d, umma_desc_sw128(ah + off), umma_desc_sw128(wl + off), idesc,
+            // small terms first; x0 w0 last
+            mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w2 + off), idesc,
                          (first && kk == 0) ? 0u : 1u);
-            mma_tf32_2sm(d, umma_desc_sw128(al + off), umma_desc_sw128(wh + off), idesc, 1u);
-            mma_tf32_2sm(d, umma_desc_sw128(ah + off), umma_desc_sw128(wh + off), idesc, 1u);
+            mma_bf16_2sm(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w1 + off), idesc, 1u);
+            mma_bf16_2sm(d, umma_desc_sw64(a2 + off), umma_desc_sw64(w0 + off), idesc, 1u);
+            mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w1 + off), idesc, 1u);
+            mma_bf16_2sm(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w0 + off), idesc, 1u);
+            mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w0 + off), idesc, 1u);
           }
           mma_commit_2sm(&empty[s]);  // frees the smem stage (both CTAs) once these MMAs have read it
           if ((kr % DRAIN) == DRAIN - 1 || kb == kb1 - 1) mma_commit_2sm(&accfull[a]);
@@ -387,9 +438,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int i = 0; i < CW; ++i) acc[i] = 0.0f;
       for (int gi = 0; gi < ng; ++gi) {
         const uint32_t g = g0 + gi, a = g & 1;
-        mbar_wait(&accfull[a], (g >> 1) & 1);
+        mbar_wait_backoff(&accfull[a], (g >> 1) & 1);
         fence_after();
         const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + a * BN + ch;
+#ifndef KGQ_TC_DBG_NO_DRAIN  // perf probe only: skip the TMEM reads
 #pragma unroll
         for (int c = 0; c < CW; c += 16) {  // x16 loads: few live temporaries next to acc[CW]
           float v[16];
@@ -397,6 +449,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
         }
+#else
+        (void)tq;
+#endif
         fence_before();
         __syncwarp();
         // default .release.cta semantics: the TMEM reads are complete (tcgen05.wait::ld) and
@@ -464,17 +519,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
         } else {
+          // 16 columns -> three bf16 planes of 32 rows x 32 B (1 KB each), 32-byte swizzle:
+          // 16-byte chunk c of row r at r * 32 + ((c ^ ((r >> 2) & 1)) << 4)
+          uint32_t q0[8], q1[8], q2[8];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float h[4], l[4];
+          for (int i = 0; i < 8; ++i) {
+            __nv_bfloat16 x0, x1, x2, y0, y1, y2;
+            split3(v[2 * i], x0, x1, x2);
+            split3(v[2 * i + 1], y0, y1, y2);
+            q0[i] = pack_bf16(x0, y0);
+            q1[i] = pack_bf16(x1, y1);
+            q2[i] = pack_bf16(x2, y2);
+          }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              h[e] = tf32_rna(v[4 * j + e]);
-              l[e] = v[4 * j + e] - h[e];
-            }
-            const int o = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
-            *reinterpret_cast<float4*>(buf + o) = make_float4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<float4*>(buf + 2048 + o) = make_float4(l[0], l[1], l[2], l[3]);
+          for (int c = 0; c < 2; ++c) {
+            const int o = lane * 32 + ((c ^ ((lane >> 2) & 1)) << 4);
+            *reinterpret_cast<uint4*>(buf + o) = make_uint4(q0[4 * c], q0[4 * c + 1], q0[4 * c + 2], q0[4 * c + 3]);
+            *reinterpret_cast<uint4*>(buf + 1024 + o) = make_uint4(q1[4 * c], q1[4 * c + 1], q1[4 * c + 2], q1[4 * c + 3]);
+            *reinterpret_cast<uint4*>(buf + 2048 + o) = make_uint4(q2[4 * c], q2[4 * c + 1], q2[4 * c + 2], q2[4 * c + 3]);
           }
         }
         fence_proxy_async_smem();
@@ -482,7 +544,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifndef KGQ_TC_DBG_NO_STORE  // perf probe only: skip the output stores
         if (lane == 0) {
           tma_store_2d(&mO0, buf, n0 + c, row0 / ROWDIV);
-          if (PLANES == 2) tma_store_2d(&mO1, buf + 2048, n0 + c, row0);
+          if (PLANES == 3) {
+            tma_store_2d(&mO1, buf + 1024, n0 + c, row0);
+            tma_store_2d(&mO2, buf + 2048, n0 + c, row0);
+          }
           bulk_commit();
         }
 #endif
@@ -517,13 +582,12 @@ inline EncodeFn encode_fn() {
   return fn;
 }
 
-// rows x cols fp32 matrix with row stride ld (elements); box = box_rows x box_cols, swizzled
-// (128 B for 32-column boxes, 64 B for 16-column boxes)
-inline bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
-                     int box_cols = BK) {
+// rows x cols matrix (fp32 or bf16) with row stride ld (elements); box = box_rows x box_cols
+inline bool make_map(CUtensorMap* m, const void* ptr, bool bf16, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows, int box_cols, CUtensorMapSwizzle sw) {
   static std::mutex mu;
-  static std::map<std::tuple<const float*, int64_t, int64_t, int64_t, int, int>, CUtensorMap> cache;
-  const auto key = std::make_tuple(ptr, rows, cols, ld, box_rows, box_cols);
+  static std::map<std::tuple<const void*, int64_t, int64_t, int64_t, int, int, int>, CUtensorMap> cache;
+  const auto key = std::make_tuple(ptr, rows, cols, ld, box_rows, box_cols * (bf16 ? -1 : 1), (int)sw);
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -532,13 +596,13 @@ inline bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t col
   }
   EncodeFn fn = encode_fn();
   if (!fn) return false;
+  const size_t es = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(float))};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapSwizzle sw = box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     fprintf(stderr, "libkgq: cuTensorMapEncodeTiled(rows %lld, cols %lld, ld %lld, box %dx%d) = %d\n",
@@ -549,13 +613,19 @@ inline bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t col
   cache.emplace(key, *m);
   return true;
 }
+// bf16 operand plane: box rows x 32 columns (64 B), 64-byte swizzle (umma_desc_sw64)
+inline bool make_operand_map(CUtensorMap* m, const __nv_bfloat16* p, int64_t rows, int64_t cols, int64_t ld,
+                             int box_rows) {
+  return make_map(m, p, true, rows, cols, ld, box_rows, BK, CU_TENSOR_MAP_SWIZZLE_64B);
+}
 
-// Output of a GEMM launch: plane pointers (plane 1 only for PLANES == 2), [rows, cols] with
-// row stride ld, rows = M / ROWDIV.
+// Output of a GEMM launch: rows x cols (rows = M / ROWDIV), either fp32 (f32, row stride ld;
+// PLANES 1) or the three bf16 planes of a Split (PLANES 3).
 struct OutDesc {
-  float* p0;
-  float* p1;
-  int64_t rows, cols, ld;
+  float* f32;
+  int64_t ld;
+  Split sp;
+  int64_t rows, cols;
 };
 
 inline bool pdl_enabled() {
@@ -573,18 +643,27 @@ static_assert(kGemmWsFloats >= (size_t)kClustersMax * 2 * BM * 256, "split-tail 
 static_assert(kGemmCntInts >= kClustersMax * 2 * EPI_WARPS, "split-tail counters");
 
 template <int BN, class Epi>
-int launch_gemm(const Split& A, int M, const float* Wh, const float* Wl, int N, int64_t ldw, int K,
-                const OutDesc& o, const Epi& epi, cudaStream_t st, Sched sc, int max_clusters = kClustersMax) {
+int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDesc& o, const Epi& epi,
+                cudaStream_t st, Sched sc, int max_clusters = kClustersMax) {
   constexpr int PLANES = Epi::PLANES, ROWDIV = Epi::ROWDIV;
-  CUtensorMap mAh, mAl, mWh, mWl, mO0, mO1;
-  if (!make_map(&mAh, A.hi, M, K, A.ld, BM) || !make_map(&mAl, A.lo, M, K, A.ld, BM) ||
-      !make_map(&mWh, Wh, N, K, ldw, BN / 2) || !make_map(&mWl, Wl, N, K, ldw, BN / 2) ||
-      !make_map(&mO0, o.p0, o.rows, o.cols, o.ld, 32 / ROWDIV, 32 / PLANES) ||
-      (PLANES == 2 && !make_map(&mO1, o.p1, o.rows, o.cols, o.ld, 32 / ROWDIV, 32 / PLANES))) {
+  static_assert(PLANES == 1 || PLANES == 3, "fp32 or bf16x3 output");
+  CUtensorMap mA[3], mW[3], mO[3];
+  bool ok = true;
+  for (int p = 0; p < 3; ++p) {
+    ok = ok && make_operand_map(&mA[p], A.plane(p), M, K, A.ld, BM);
+    ok = ok && make_operand_map(&mW[p], W.plane(p), N, K, W.ld, BN / 2);
+  }
+  if (PLANES == 1) {
+    ok = ok && make_map(&mO[0], o.f32, false, o.rows, o.cols, o.ld, 32 / ROWDIV, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    mO[1] = mO[2] = mO[0];
+  } else {
+    for (int p = 0; p < 3; ++p)
+      ok = ok && make_map(&mO[p], o.sp.plane(p), true, o.rows, o.cols, o.sp.ld, 32, 16, CU_TENSOR_MAP_SWIZZLE_32B);
+  }
+  if (!ok) {
     fprintf(stderr, "libkgq: cuTensorMapEncodeTiled failed\n");
     return -1;
   }
-  if (PLANES == 1) mO1 = mO0;
   auto kern = k_gemm<BN, Epi>;
   static bool attr = false;
   if (!attr) {
@@ -608,14 +687,14 @@ int launch_gemm(const Split& A, int M, const float* Wh, const float* Wl, int N, 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, mAh, mAl, mWh, mWl, mO0, mO1, M, N, K, sc, epi);
+  cudaLaunchKernelEx(&cfg, kern, mA[0], mA[1], mW[0], mW[1], mA[2], mW[2], mO[0], mO[1], mO[2], M, N, K, sc, epi);
   return 1;
 }
 
 // Launch plan: tile width and tail split, from a cost model in SM clocks calibrated on B200
 // (scripts/tc_probe.cu traces, profiles/r01/tc_splitk_probe.txt):
-//   * a K-block costs max(operand stream, MMA) = max((128 + BN/2) x 6.8, 6.7 BN) clk per SM
-//     ((128 + BN/2) x 256 B at ~38 B/clk vs 12 tf32 MMAs of N = BN);
+//   * a K-block costs max(operand stream, MMA) = max((128 + BN/2) x 5.1, 6.7 BN) clk per SM
+//     ((128 + BN/2) x 192 B at ~38 B/clk vs 12 bf16 MMAs of N = BN);
 //   * complete rounds of whole tiles run back to back (their epilogues overlap the next tile);
 //   * a split tail tile costs kper K-blocks + publishing its partials (~3 us) + ~2.5 us per
 //     other split's partials added by the last arriver, + the final epilogue (~3 us).
@@ -632,7 +711,7 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split) {
   for (int bn : kTileBN) {
     const int64_t tiles = pairs_m * ((N + bn - 1) / bn);
     const int64_t full = tiles / kClustersMax * kClustersMax, tail = tiles - full;
-    const double kb = fmax((128.0 + bn / 2) * 6.8, 6.7 * bn);
+    const double kb = fmax((128.0 + bn / 2) * 5.1, 6.7 * bn);
     const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, nk / 4)) : 1;
     for (int s = 1; s <= smax; ++s) {
       const int kper = (nk + s - 1) / s;
@@ -649,8 +728,8 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split) {
 }
 
 template <class Epi>
-int launch_gemm_auto(const Split& A, int M, const float* Wh, const float* Wl, int N, int64_t ldw, int K,
-                     const OutDesc& o, const Epi& epi, const GemmWs* ws, cudaStream_t st) {
+int launch_gemm_auto(const Split& A, int M, const Split& W, int N, int K, const OutDesc& o, const Epi& epi,
+                     const GemmWs* ws, cudaStream_t st) {
   static const bool no_split = [] {
     const char* e = getenv("KGQ_NO_SPLITK");
     return e && e[0] && e[0] != '0';
@@ -658,10 +737,10 @@ int launch_gemm_auto(const Split& A, int M, const float* Wh, const float* Wl, in
   const Plan p = plan_gemm(M, N, K, !no_split && ws != nullptr && ws->ws != nullptr);
   const Sched sc{p.full, p.s_tail, p.kper, ws ? ws->ws : nullptr, ws ? ws->cnt : nullptr};
   switch (p.bn) {
-    case 64: return launch_gemm<64>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
-    case 128: return launch_gemm<128>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
-    case 192: return launch_gemm<192>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
-    default: return launch_gemm<256>(A, M, Wh, Wl, N, ldw, K, o, epi, st, sc);
+    case 64: return launch_gemm<64>(A, M, W, N, K, o, epi, st, sc);
+    case 128: return launch_gemm<128>(A, M, W, N, K, o, epi, st, sc);
+    case 192: return launch_gemm<192>(A, M, W, N, K, o, epi, st, sc);
+    default: return launch_gemm<256>(A, M, W, N, K, o, epi, st, sc);
   }
 }
 

@@ -2,6 +2,8 @@
 // (fp32 plane, split hi/lo planes, DNF row-pair min), ragged M / N / K, and a grid smaller
 // than the tile count (persistence), vs an fp64 host reference.  Not part of the library.
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <cstdio>
 #include <random>
 #include <vector>
@@ -12,8 +14,8 @@
 
 using namespace kgq;
 
-int main() {
-  const int M = 300, N = 520, K = 100;
+int main(int argc, char** argv) {
+  const int M = 300, N = 520, K = argc > 1 ? atoi(argv[1]) : 100;
   std::mt19937 g(1);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
   std::vector<float> x((size_t)M * K), w((size_t)N * K), b(N);
@@ -31,35 +33,47 @@ int main() {
       ref[(size_t)m * N + n] = s;
       mag[(size_t)m * N + n] = sa + fabs(b[n]);
     }
-  float *dxh, *dxl, *dwh, *dwl, *db, *dy;
+  float *dx, *dw, *db, *dy;
   float2 *dP, *dE;
-  cudaMalloc(&dxh, x.size() * 4); cudaMalloc(&dxl, x.size() * 4);
-  cudaMalloc(&dwh, w.size() * 4); cudaMalloc(&dwl, w.size() * 4);
+  cudaMalloc(&dx, x.size() * 4); cudaMalloc(&dw, w.size() * 4);
   cudaMalloc(&db, N * 4); cudaMalloc(&dy, (size_t)M * N * 4 * 2);
   cudaMalloc(&dP, M * 8); cudaMalloc(&dE, 640 * 8);
-  cudaMemcpy(dxh, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(dwh, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dw, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(db, b.data(), N * 4, cudaMemcpyHostToDevice);
   cudaMemset(dP, 0, M * 8); cudaMemset(dE, 0, 640 * 8);
+  auto mk = [](int64_t rows, int64_t cols) {
+    Split s;
+    s.ld = (cols + 7) / 8 * 8;
+    cudaMalloc(&s.b0, 3 * rows * s.ld * 2);
+    s.b1 = s.b0 + rows * s.ld;
+    s.b2 = s.b1 + rows * s.ld;
+    return s;
+  };
+  Split A = mk(M, K), Wsp = mk(N, K), Ysp = mk(M, N);
+  launch_split_copy_rows(dx, M, K, A, 0);
+  launch_split_copy_rows(dw, N, K, Wsp, 0);
   GemmWs gws;
   cudaMalloc(&gws.ws, kGemmWsFloats * 4);
   cudaMalloc(&gws.cnt, kGemmCntInts * 4);
   cudaMemset(gws.cnt, 0, kGemmCntInts * 4);
   const tc::Sched whole{0, 1, 0, nullptr, nullptr};
-  launch_split_copy(dxh, x.size(), dxh, dxl, 0);
-  launch_split_copy(dwh, w.size(), dwh, dwl, 0);
-  Split A{dxh, dxl, K};
   int fails = 0;
-  // form 0: fp32 + bias (no activation); 1: split + bias + ReLU; 2: row-pair min (DNF union)
+  // form 0: fp32 + bias (no activation); 1: split (bf16x3) + bias + ReLU; 2: row-pair min (DNF union)
+  std::vector<uint16_t> hb(3 * (size_t)M * Ysp.ld);
+  auto bf = [](uint16_t u) { uint32_t v = (uint32_t)u << 16; float f; memcpy(&f, &v, 4); return f; };
   auto check = [&](const char* what, int bn, int form, auto launch) {
     cudaMemset(dy, 0xff, (size_t)M * N * 4 * 2);  // NaN fill: every output must be written
+    cudaMemset(Ysp.b0, 0xff, hb.size() * 2);
     launch();
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<float> y((size_t)M * N * 2);
     cudaMemcpy(y.data(), dy, y.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hb.data(), Ysp.b0, hb.size() * 2, cudaMemcpyDeviceToHost);
     double mx = 0;
     int bad = 0;
     const int rows = form == 2 ? M / 2 : M;
+    const size_t pl = (size_t)M * Ysp.ld;
     for (int m = 0; m < rows; ++m)
       for (int n = 0; n < N; ++n) {
         double want, scale;
@@ -72,11 +86,15 @@ int main() {
           want = ref[(size_t)m * N + n] + b[n];
           if (form == 1) want = fmax(want, 0.0);
           scale = mag[(size_t)m * N + n];
-          got = y[(size_t)m * N + n];
-          if (form == 1) got += y[(size_t)M * N + (size_t)m * N + n];  // hi + lo
+          if (form == 1) {  // three bf16 planes, exact sum
+            const size_t o = (size_t)m * Ysp.ld + n;
+            got = (bf(hb[o]) + bf(hb[pl + o])) + bf(hb[2 * pl + o]);
+          } else {
+            got = y[(size_t)m * N + n];
+          }
         }
         const double r = fabs((double)got - want) / scale;
-        if (!(r <= 1e-5)) ++bad;
+        if (!(r <= 1e-6)) ++bad;
         if (r > mx || r != r) mx = r != r ? 1e30 : r;
       }
     fails += bad > 0 || e != cudaSuccess;
@@ -90,24 +108,24 @@ int main() {
   };
   each_bn([&](auto c) {
     constexpr int B = decltype(c)::value;
-    const tc::OutDesc o1{dy, nullptr, M, N, N}, o2{dy, dy + (size_t)M * N, M, N, N};
-    check("fp32 + bias", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, whole); });
-    check("split + bias + relu", B, 1, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0, whole); });
-    check("fp32, 2 clusters (persist)", B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, whole, 2); });
-    const tc::OutDesc o3{dy, nullptr, M / 2, N, N};
-    check("row-pair min (union)", B, 2, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0, whole); });
+    const tc::OutDesc o1{dy, N, Split{}, M, N}, o2{nullptr, 0, Ysp, M, N};
+    check("fp32 + bias", B, 0, [&] { tc::launch_gemm<B>(A, M, Wsp, N, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, whole); });
+    check("split + bias + relu", B, 1, [&] { tc::launch_gemm<B>(A, M, Wsp, N, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0, whole); });
+    check("fp32, 2 clusters (persist)", B, 0, [&] { tc::launch_gemm<B>(A, M, Wsp, N, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, whole, 2); });
+    const tc::OutDesc o3{dy, N, Split{}, M / 2, N};
+    check("row-pair min (union)", B, 2, [&] { tc::launch_gemm<B>(A, M, Wsp, N, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0, whole); });
     // split tail: the last tiles (or all) split in K; K = 100 -> 4 K-blocks
     const int tiles = ((M + 255) / 256) * ((N + B - 1) / B);
     for (int sk : {2, 4}) {
-      const int kper = (4 + sk - 1) / sk;
+      const int nkb = (K + 31) / 32, kper = (nkb + sk - 1) / sk;
       const tc::Sched all{0, sk, kper, gws.ws, gws.cnt}, tail{tiles / 2, sk, kper, gws.ws, gws.cnt};
       char nm[64];
       snprintf(nm, sizeof nm, "split-K %d, every tile", sk);
-      check(nm, B, 1, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0, all); });
+      check(nm, B, 1, [&] { tc::launch_gemm<B>(A, M, Wsp, N, K, o2, EpiLinear<kEpiRelu, true>{db, N, 0, 0}, 0, all); });
       snprintf(nm, sizeof nm, "split-K %d, tail, 3 clusters", sk);
-      check(nm, B, 0, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, tail, 3); });
+      check(nm, B, 0, [&] { tc::launch_gemm<B>(A, M, Wsp, N, K, o1, EpiLinear<kEpiNone, false>{db, N, 0, 0}, 0, tail, 3); });
       snprintf(nm, sizeof nm, "split-K %d, union rows", sk);
-      check(nm, B, 2, [&] { tc::launch_gemm<B>(A, M, dwh, dwl, N, K, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0, all); });
+      check(nm, B, 2, [&] { tc::launch_gemm<B>(A, M, Wsp, N, K, o3, EpiBetaScore<2>{dP, dE, M, 640}, 0, all); });
     }
     // counters must be back to zero after every launch
     std::vector<int> cnt(kGemmCntInts);

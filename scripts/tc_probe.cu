@@ -41,21 +41,28 @@ int main() {
 #endif
   for (const Shape& sh : shapes) {
     const int M = sh.M, N = sh.N, K = sh.K;
-    float *xh, *xl, *wh, *wl, *b, *y;
+    float *xf, *wf, *b, *y;
     float2 *P, *E;
-    cudaMalloc(&xh, (size_t)M * K * 4); cudaMalloc(&xl, (size_t)M * K * 4);
-    cudaMalloc(&wh, (size_t)N * K * 4); cudaMalloc(&wl, (size_t)N * K * 4);
-    cudaMalloc(&b, N * 4); cudaMalloc(&y, (size_t)M * N * 4 * 2);
+    cudaMalloc(&xf, (size_t)M * K * 4); cudaMalloc(&wf, (size_t)N * K * 4);
+    cudaMalloc(&b, N * 4); cudaMalloc(&y, (size_t)M * N * 4);
     cudaMalloc(&P, M * 8); cudaMalloc(&E, N * 8);
     std::vector<float> hx((size_t)M * K), hw((size_t)N * K);  // non-zero operands
     for (size_t i = 0; i < hx.size(); ++i) hx[i] = (float)((i * 2654435761u) % 1000) * 1e-3f - 0.5f;
     for (size_t i = 0; i < hw.size(); ++i) hw[i] = (float)((i * 40503u) % 1000) * 1e-3f - 0.5f;
-    cudaMemcpy(xh, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(wh, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice);
-    launch_split_copy(xh, (int64_t)M * K, xh, xl, 0);
-    launch_split_copy(wh, (int64_t)N * K, wh, wl, 0);
+    cudaMemcpy(xf, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(wf, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice);
+    auto mk = [](int64_t rows, int64_t cols) {
+      Split s;
+      s.ld = (cols + 7) / 8 * 8;
+      cudaMalloc(&s.b0, 3 * rows * s.ld * 2);
+      s.b1 = s.b0 + rows * s.ld;
+      s.b2 = s.b1 + rows * s.ld;
+      return s;
+    };
+    Split A = mk(M, K), Wsp = mk(N, K), Ysp = mk(M, N);
+    launch_split_copy_rows(xf, M, K, A, 0);
+    launch_split_copy_rows(wf, N, K, Wsp, 0);
     cudaMemset(b, 0, N * 4); cudaMemset(P, 0, M * 8); cudaMemset(E, 0, N * 8);
-    Split A{xh, xl, K};
     static GemmWs gws;
     if (!gws.ws) {
       cudaMalloc(&gws.ws, kGemmWsFloats * 4);
@@ -69,10 +76,10 @@ int main() {
       auto go = [&](auto c) {
         constexpr int B = decltype(c)::value;
         if (sh.score)
-          tc::launch_gemm<B>(A, M, wh, wl, N, K, K, tc::OutDesc{y, nullptr, M, N, N},
+          tc::launch_gemm<B>(A, M, Wsp, N, K, tc::OutDesc{y, N, Split{}, M, N},
                              EpiBetaScore<1>{P, E, M, (int64_t)N}, 0, sc);
         else
-          tc::launch_gemm<B>(A, M, wh, wl, N, K, K, tc::OutDesc{y, y + (size_t)M * N, M, N, N},
+          tc::launch_gemm<B>(A, M, Wsp, N, K, tc::OutDesc{nullptr, 0, Ysp, M, N},
                              EpiLinear<kEpiRelu, true>{b, N, 0, 0}, 0, sc);
       };
       switch (bn) {
@@ -119,7 +126,8 @@ int main() {
 #endif
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
-    cudaFree(xh); cudaFree(xl); cudaFree(wh); cudaFree(wl); cudaFree(b); cudaFree(y); cudaFree(P); cudaFree(E);
+    cudaFree(xf); cudaFree(wf); cudaFree(A.b0); cudaFree(Wsp.b0); cudaFree(Ysp.b0); cudaFree(b); cudaFree(y);
+    cudaFree(P); cudaFree(E);
   }
   return 0;
 }
