@@ -286,48 +286,53 @@ __global__ void __launch_bounds__(kRegThreads, 4)
   }
 }
 
-// k_topk_cmin (k <= 32): one warp per query row, using the score epilogue's minima of
-// 32-entity blocks.  Pass 1 finds an upper bound tau of the k-th best distance from the block
-// minima; the k best entries lie in blocks whose minimum is <= tau.  Pass 2 scans only those blocks (one coalesced 128-byte load each,
-// eight in flight), skipping any whose minimum already exceeds the tightened k-th best, and
-// inserts entries in exact (distance, id) order.  Reads ~n/32 + ~k x 32 values per row instead
-// of n (C2: 14,505 -> ~800).
+// k_topk_cmin (k <= 32): one CTA of four warps per query row, using the score epilogue's
+// minima of 32-entity blocks.  Warp w owns a quarter of the blocks.  Pass 1: each lane takes
+// the minimum over its blocks; the k-th smallest of a warp's 32 lane minima comes from k
+// distinct blocks, each holding an entry <= it, so it bounds the row's k-th best distance from
+// above, and tau = the smallest of the four warps' bounds is one too (for i.i.d. block minima it
+// selects ~1.1 k blocks).  Pass 2: the warps load only the blocks whose minimum is <= tau (one
+// coalesced 128-byte load each, eight in flight) and append every entry <= tau -- a superset of
+// the k best, ties included -- to a shared list (ballot compaction, typically 10-30 entries);
+// one block-wide bitonic sort of the packed (distance, id) keys gives the exact top-k.  If more
+// than kCandCap entries tie below tau (adversarial ties), warp 0 falls back to a register-list
+// scan of the same blocks.  Reads ~n/32 + ~k x 32 values per row instead of n.
 constexpr int kCminWarps = 4;
+constexpr int kCandCap = 256;
 
 __global__ void __launch_bounds__(32 * kCminWarps)
     k_topk_cmin(const float* __restrict__ dist, int64_t ldd, const float* __restrict__ cmin, int64_t ldc,
                 int64_t n, int k, int64_t id_base, const int32_t* __restrict__ invalid,
                 float* __restrict__ od, int32_t* __restrict__ oi, int B) {
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * kCminWarps + (threadIdx.x >> 5);
-  if (b >= B) return;
+  __shared__ float wtau[kCminWarps];
+  __shared__ unsigned long long cand[kCandCap];
+  __shared__ int ncand;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int b = blockIdx.x;
   const float kNaN = __uint_as_float(0x7FFFFFFFu), kInf = __uint_as_float(0x7F800000u);
   od += (int64_t)b * k;
   oi += (int64_t)b * k;
   if (invalid && invalid[b]) {
-    if (lane < k) {
+    if (wid == 0 && lane < k) {
       od[lane] = kNaN;
       oi[lane] = -1;
     }
     return;
   }
+  if (threadIdx.x == 0) ncand = 0;
   const int64_t nblk = (n + 31) / 32;
+  const int64_t per = (nblk + kCminWarps - 1) / kCminWarps;
+  const int64_t j0w = (int64_t)wid * per, j1w = j0w + per < nblk ? j0w + per : nblk;
   const float* cm = cmin + (int64_t)b * ldc;
   const float* row = dist + (int64_t)b * ldd;
-  unsigned long long lk = ~0ull, tk = ~0ull;
-  float tf = kInf;
-  // ---- pass 1: tau = the k-th smallest of the 32 lane minima (each lane's minimum over its
-  // blocks j = lane mod 32).  k distinct lanes -> k distinct blocks each holding an entry
-  // <= tau, so tau bounds the k-th best distance from above; for i.i.d. block minima it
-  // selects ~1.1 k blocks (vs exactly k for the k-th smallest block minimum) at the cost of
-  // one warp sort instead of ~k ln(n/32k) serial register insertions.
+  // ---- pass 1: warp bound = k-th smallest lane minimum over this warp's blocks ----
   float lmin = kInf;
-  for (int64_t g0 = 0; g0 < nblk; g0 += 32 * 8) {
+  for (int64_t g0 = j0w; g0 < j1w; g0 += 32 * 8) {
     float xs[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int64_t j = g0 + u * 32 + lane;
-      xs[u] = j < nblk ? cm[j] : kInf;
+      xs[u] = j < j1w ? cm[j] : kInf;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) lmin = fminf(lmin, xs[u]);
@@ -339,50 +344,92 @@ __global__ void __launch_bounds__(32 * kCminWarps)
       const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
       v = (lower == up) ? fminf(v, o) : fmaxf(v, o);
     }
-  const float tau = __shfl_sync(0xffffffffu, v, k - 1);  // +inf if fewer than k lanes hold blocks
-  // ---- pass 2: scan the blocks whose minimum is <= tau; only entries <= tau can be among
-  // the k best, so the filter starts at tau instead of +inf ----
-  for (int64_t j0 = 0; j0 < nblk; j0 += 32) {
-    const float x = j0 + lane < nblk ? cm[j0 + lane] : kNaN;
+  if (lane == k - 1) wtau[wid] = v;  // +inf if fewer than k lanes hold blocks
+  __syncthreads();
+  float tau = wtau[0];
+#pragma unroll
+  for (int w = 1; w < kCminWarps; ++w) tau = fminf(tau, wtau[w]);
+  // ---- pass 2: every entry <= tau of the blocks whose minimum is <= tau -> shared list ----
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t g0 = j0w; g0 < j1w; g0 += 32) {
+    const float x = g0 + lane < j1w ? cm[g0 + lane] : kNaN;
     unsigned sel = __ballot_sync(0xffffffffu, x <= tau);
     while (sel) {
       int blk[8];
-      float v[8];
-      int nsel = 0;
+      float vv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {  // up to eight blocks' loads in flight
         blk[u] = -1;
-        v[u] = kNaN;
+        vv[u] = kNaN;
         if (sel) {
           const int o = __ffs(sel) - 1;
           sel &= sel - 1;
-          if (__shfl_sync(0xffffffffu, x, o) <= fminf(tf, tau)) {  // block min vs the tightened bound
-            blk[u] = (int)(j0 + o);
-            const int64_t i = (int64_t)blk[u] * 32 + lane;
-            v[u] = i < n ? row[i] : kNaN;
-            ++nsel;
-          }
+          blk[u] = (int)(g0 + o);
+          const int64_t i = (int64_t)blk[u] * 32 + lane;
+          vv[u] = i < n ? row[i] : kNaN;
         }
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if (blk[u] < 0) continue;
-        const int64_t i = (int64_t)blk[u] * 32 + lane;
-        const unsigned long long key = ((unsigned long long)fkey(v[u]) << 32) | (uint32_t)i;
-        unsigned m = __ballot_sync(0xffffffffu, v[u] <= fminf(tf, tau));
-        while (m) {
-          const int src = __ffs(m) - 1;
-          const unsigned long long cand = __shfl_sync(0xffffffffu, key, src);
-          if (cand < tk) reg_insert(lk, cand, k, lane, tk, tf);
-          m &= m - 1;
-          m &= __ballot_sync(0xffffffffu, v[u] <= fminf(tf, tau));
-        }
+        const bool pass = vv[u] <= tau;
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (!m) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&ncand, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const int slot = base + __popc(m & lt);
+        if (pass && slot < kCandCap)
+          cand[slot] = ((unsigned long long)fkey(vv[u]) << 32) | (uint32_t)((int64_t)blk[u] * 32 + lane);
       }
-      (void)nsel;
+    }
+  }
+  __syncthreads();
+  const int nc = ncand;
+  if (nc <= kCandCap) {
+    int P = 32;
+    while (P < nc) P <<= 1;
+    for (int t = nc + threadIdx.x; t < P; t += blockDim.x) cand[t] = ~0ull;
+    __syncthreads();
+    bitonic_sort_u64(cand, P);
+    if (threadIdx.x < k) {
+      const unsigned long long key = cand[threadIdx.x];
+      if (key == ~0ull) {  // fewer than k entries
+        od[threadIdx.x] = kNaN;
+        oi[threadIdx.x] = -1;
+      } else {
+        od[threadIdx.x] = fkey_inv((uint32_t)(key >> 32));
+        oi[threadIdx.x] = (int32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
+      }
+    }
+    return;
+  }
+  // ---- overflow (more than kCandCap entries <= tau): register-list scan by warp 0 ----
+  if (wid != 0) return;
+  unsigned long long lk = ~0ull, tk = ~0ull;
+  float tf = kInf;
+  for (int64_t g0 = 0; g0 < nblk; g0 += 32) {
+    const float x = g0 + lane < nblk ? cm[g0 + lane] : kNaN;
+    unsigned sel = __ballot_sync(0xffffffffu, x <= tau);
+    while (sel) {
+      const int o = __ffs(sel) - 1;
+      sel &= sel - 1;
+      if (__shfl_sync(0xffffffffu, x, o) > fminf(tf, tau)) continue;
+      const int64_t i = (g0 + o) * 32 + lane;
+      const float vi = i < n ? row[i] : kNaN;
+      const unsigned long long key = ((unsigned long long)fkey(vi) << 32) | (uint32_t)i;
+      unsigned m = __ballot_sync(0xffffffffu, vi <= fminf(tf, tau));
+      while (m) {
+        const int src = __ffs(m) - 1;
+        const unsigned long long c = __shfl_sync(0xffffffffu, key, src);
+        if (c < tk) reg_insert(lk, c, k, lane, tk, tf);
+        m &= m - 1;
+        m &= __ballot_sync(0xffffffffu, vi <= fminf(tf, tau));
+      }
     }
   }
   if (lane >= k) return;
-  if (lk == ~0ull) {  // fewer than k entries
+  if (lk == ~0ull) {
     od[lane] = kNaN;
     oi[lane] = -1;
   } else {
@@ -394,8 +441,7 @@ __global__ void __launch_bounds__(32 * kCminWarps)
 int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                      int k, int64_t id_base, const int32_t* invalid, float* out_d, int32_t* out_i,
                      cudaStream_t st) {
-  k_topk_cmin<<<(B + kCminWarps - 1) / kCminWarps, 32 * kCminWarps, 0, st>>>(dist, ldd, cmin, ldc, n, k, id_base,
-                                                                             invalid, out_d, out_i, B);
+  k_topk_cmin<<<B, 32 * kCminWarps, 0, st>>>(dist, ldd, cmin, ldc, n, k, id_base, invalid, out_d, out_i, B);
   return 1;
 }
 
