@@ -73,7 +73,7 @@ int launch_translate_chain(const ChainArgs& a, const float* ent, const float* re
 // Group row g*B + b of Z; source = regularised anchor row or split state row.
 __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
                                   const float* __restrict__ rel, int B, MlpGroup g, Split src,
-                                  Split z) {
+                                  Split z, int with_rel) {
   const int b = blockIdx.x;
   const int gi = blockIdx.y;
   const int d = a.d;
@@ -91,14 +91,37 @@ __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
     float x = from_anchor ? ent[(int64_t)aid * 2 * d + j] : load_split(src, srow + j);
     store_split(z, zrow + j, x);
   }
-  for (int j = threadIdx.x; j < d; j += blockDim.x)
-    store_split(z, zrow + 2 * d + j, rel[(int64_t)rid * d + j]);
+  if (with_rel)
+    for (int j = threadIdx.x; j < d; j += blockDim.x)
+      store_split(z, zrow + 2 * d + j, rel[(int64_t)rid * d + j]);
 }
 
 int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
-                           const MlpGroup& g, Split src, Split z, cudaStream_t st) {
+                           const MlpGroup& g, Split src, Split z, cudaStream_t st, bool with_rel) {
   dim3 grid(B, g.n);
-  k_betae_mlp_input<<<grid, 128, 0, st>>>(a, ent, rel, B, g, src, z);
+  k_betae_mlp_input<<<grid, 128, 0, st>>>(a, ent, rel, B, g, src, z, with_rel ? 1 : 0);
+  return 1;
+}
+
+// ---- relation term of the first projection layer: RW[r, n] = sum_k W[n, col0 + k] R[r, k] ----
+// fp64 accumulation, once per table load (finalize).  Block (r, 128 outputs); R[r] staged in smem.
+__global__ void k_relation_term(const float* __restrict__ R, int d, const float* __restrict__ W, int64_t ldw,
+                                int col0, int H, float* __restrict__ RW) {
+  extern __shared__ double rr[];
+  const int r = blockIdx.x;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) rr[k] = R[(int64_t)r * d + k];
+  __syncthreads();
+  const int n = blockIdx.y * blockDim.x + threadIdx.x;
+  if (n >= H) return;
+  const float* w = W + (int64_t)n * ldw + col0;
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) s += (double)w[k] * rr[k];
+  RW[(int64_t)r * H + n] = (float)s;
+}
+
+int launch_relation_term(const float* R, int n_relation, int d, const float* W, int64_t ldw, int col0, int H,
+                         float* RW, cudaStream_t st) {
+  k_relation_term<<<dim3(n_relation, (H + 127) / 128), 128, d * sizeof(double), st>>>(R, d, W, ldw, col0, H, RW);
   return 1;
 }
 
@@ -272,16 +295,16 @@ int launch_split_copy(const float* src, int64_t n, Split dst, cudaStream_t st) {
   return 1;
 }
 
-// row-major [rows, cols] fp32 -> split planes with row stride dst.ld (>= cols)
-__global__ void k_split_copy_rows(const float* __restrict__ src, int64_t rows, int cols, Split dst) {
+// [rows, cols] fp32 with row stride lds -> split planes with row stride dst.ld (>= cols)
+__global__ void k_split_copy_rows(const float* __restrict__ src, int64_t lds, int64_t rows, int cols, Split dst) {
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    store_split(dst, (i / cols) * dst.ld + i % cols, src[i]);
+    store_split(dst, (i / cols) * dst.ld + i % cols, src[(i / cols) * lds + i % cols]);
 }
 
-int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st) {
-  k_split_copy_rows<<<1024, 256, 0, st>>>(src, rows, cols, dst);
+int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st, int64_t lds) {
+  k_split_copy_rows<<<1024, 256, 0, st>>>(src, lds > 0 ? lds : cols, rows, cols, dst);
   return 1;
 }
 

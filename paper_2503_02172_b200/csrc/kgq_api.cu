@@ -202,6 +202,14 @@ bool debug_launch() {
   }
   return v == 1;
 }
+bool relterm_disabled() {  // KGQ_NO_RELTERM=1: first projection layer on the assembled [x; R[r]] input
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KGQ_NO_RELTERM");
+    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
 bool topk_cmin_disabled() {  // KGQ_NO_TOPK_CMIN=1: full-row top-k (A/B and debugging)
   static int v = -1;
   if (v < 0) {
@@ -248,11 +256,42 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
     g.src_row[gi] = src_row0 < 0 ? (int64_t)br * B : src_row0 + (int64_t)gi * B;
   }
   int L = 0;
-  L += launch_betae_mlp_input(ca, ctx->ent, ctx->rel[0], B, g, src_state, ctx->Z, st);
   const int M = n * B;
   Split A = ctx->Z;
   int K = 3 * d;
-  for (int l = 0; l < ctx->cfg.n_hidden_layers; ++l) {
+  int l0 = 0;
+  if (ctx->RW) {
+    // first layer with the relation input factored out (RelTerm): K = 2d straight from the state
+    // rows (contiguous run) or from the gathered anchor rows; accumulators start at RW[r]
+    if (src_row0 < 0) {
+      L += launch_betae_mlp_input(ca, ctx->ent, ctx->rel[0], B, g, src_state, ctx->Z, st, false);
+      A = ctx->Z;
+    } else {
+      A = src_state.at(src_row0);
+    }
+    RelTerm rt;
+    rt.RW = ctx->RW;
+    rt.ldrw = ctx->cfg.hidden;
+    rt.M = M;
+    rt.B = B;
+    rt.rels = ca.rels;
+    rt.n_r = ca.n_r;
+    rt.n_relation = ca.n_relation;
+    for (int gi = 0; gi < n; ++gi) rt.rel_slot[gi] = g.rel_slot[gi];
+    rt.err = ca.err;
+    rt.invalid = ca.invalid;
+    {
+      StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
+      L += launch_linear_rel(A, M, 2 * d, ctx->lin1x, rt, ctx->H[0], &ctx->gws, st);
+      check_site("dense layer (relation term)");
+    }
+    A = ctx->H[0];
+    K = ctx->lin1x.out_f;
+    l0 = 1;
+  } else {
+    L += launch_betae_mlp_input(ca, ctx->ent, ctx->rel[0], B, g, src_state, ctx->Z, st);
+  }
+  for (int l = l0; l < ctx->cfg.n_hidden_layers; ++l) {
     const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
     L += dense(ctx, A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
     A = ctx->H[l & 1];
@@ -500,7 +539,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   for (auto& l : ctx->lin) { F(l.W); F(l.Wsp.b0); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) F(s->b0);
   F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->d_err); F(ctx->d_invalid);
-  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum);
+  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum); F(ctx->lin1x.Wsp.b0); F(ctx->RW);
   F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
@@ -638,6 +677,21 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st) st = dalloc(ctx, &ctx->d_topd_stage, (size_t)(Bm * c.max_k), "staging");
   if (!st) st = dalloc(ctx, &ctx->d_topi_stage, (size_t)(Bm * c.max_k), "staging");
   if (st) return st;
+  if (c.model == KGQ_BETAE && !relterm_disabled()) {
+    // first projection layer with the relation input factored out (RelTerm, kgq_internal.cuh);
+    // recomputed at every finalize (tables or weights may have been reloaded)
+    const Linear& l1 = ctx->lin[KGQ_LAYER_PROJ_HIDDEN];
+    if (!ctx->RW) {
+      st = alloc_split(ctx, &ctx->lin1x.Wsp, l1.out_f, 2 * d, "layer-1 state weights");
+      if (!st) st = dalloc(ctx, &ctx->RW, (size_t)c.n_relation * l1.out_f, "relation term");
+      if (st) return st;
+    }
+    ctx->lin1x.b = l1.b;
+    ctx->lin1x.out_f = l1.out_f;
+    ctx->lin1x.in_f = 2 * d;
+    launch_split_copy_rows(l1.W, l1.out_f, 2 * d, ctx->lin1x.Wsp, 0, l1.in_f);
+    launch_relation_term(ctx->rel[0], c.n_relation, d, l1.W, l1.in_f, 2 * d, l1.out_f, ctx->RW, 0);
+  }
   if (c.model == KGQ_BETAE) {
     launch_beta_regularize(ctx->ent, c.n_entity * ctx->ew, 0);
     launch_betae_entity_terms(ctx->ent, ctx->e0, ctx->ns, d, ctx->score_tab, ctx->np, 0);

@@ -105,6 +105,8 @@ struct kgq_ctx {
   int32_t* topk_tmp_i = nullptr;
   // BetaE tensor-core scoring layout (score_tc.cu)
   kgq::Split uv{};                         // [np][2d] centred (u; v), bf16x3
+  kgq::Linear lin1x{};                     // BetaE first projection layer, state columns W1[:, :2d]
+  float* RW = nullptr;                     // [n_relation, H] relation term R W1[:, 2d:]^T (fp64 -> fp32)
   float2* Esum = nullptr;                  // [np] sum_d C_ed as an fp32 (hi, lo) pair
   double* uvsums = nullptr;                // [2][d]
   kgq::GemmWs gws{};                       // tensor-core GEMM split-tail scratch
@@ -174,12 +176,31 @@ struct MlpGroup {
   int64_t src_row[kMaxBranches];
 };
 int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
-                           const MlpGroup& g, Split src, Split z, cudaStream_t st);
+                           const MlpGroup& g, Split src, Split z, cudaStream_t st, bool with_rel = true);
 // Dense layer: out = epi(A W^T + b) for rows [0, M), A given as split (K columns).
 //   split (bf16x3) output into out_sp if out_sp.valid(), else fp32 into out_f32 (row stride ld_f32).
 //   kEpiBetaReg: clamp(y+1, .05, 1e9), then 1/x on rows [neg0, neg1).
 int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, const Split& out_sp,
                   float* out_f32, int64_t ld_f32, int neg0, int neg1, const GemmWs* ws, cudaStream_t st);
+// First BetaE projection layer with the relation input factored out of Eq. 4's z = [x; R[r]]:
+// W1 z + b1 = W1[:, :2d] x + (R W1[:, 2d:]^T)[r] + b1.  RW = R W1[:, 2d:]^T is precomputed once in
+// fp64 at finalize ([R, H] fp32); the GEMM runs with K = 2d on the state rows directly and its
+// accumulators start at RW[r] of each row (EpiLinear<.., REL> init), r range-checked there.
+struct RelTerm {
+  const float* RW = nullptr;  // [n_relation, ldrw]
+  int64_t ldrw = 0;
+  int M = 0, B = 0;           // rows = group member gi * B + query b
+  const int32_t* rels = nullptr;
+  int n_r = 0, n_relation = 0;
+  int rel_slot[kMaxBranches] = {0, 0, 0};
+  int32_t* err = nullptr;
+  int32_t* invalid = nullptr;
+};
+int launch_linear_rel(const Split& A, int M, int K, const Linear& L, const RelTerm& rt, const Split& out,
+                      const GemmWs* ws, cudaStream_t st);
+// RW[r, n] = sum_k W[n, col0 + k] R[r, k] (k < d) in fp64 -> fp32
+int launch_relation_term(const float* R, int n_relation, int d, const float* W, int64_t ldw, int col0, int H,
+                         float* RW, cudaStream_t st);
 // BetaE Eq.-4 softmax terminal over rows of T (width w) -> split state rows out_row0 + r,
 // with negation on rows r in [neg0, neg1).
 int launch_softmax_terminal(const float* T, int64_t ldt, int M, int w, Split out,
@@ -252,5 +273,5 @@ int launch_transpose_shard(const float* ent, int64_t e0, int64_t ns, int d, int 
 int launch_betae_entity_terms(const float* ent, int64_t e0, int64_t ns, int d, float* tab,
                               int64_t np, cudaStream_t st);
 int launch_split_copy(const float* src, int64_t n, Split dst, cudaStream_t st);
-int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st);
+int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st, int64_t lds = 0);
 }  // namespace kgq

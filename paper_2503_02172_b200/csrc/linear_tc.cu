@@ -22,14 +22,44 @@ using tc::BM;
 // nn.Linear epilogue: + bias, ReLU / BetaE regulariser (clamp(y+1,.05,1e9)) with 1/x on rows
 // [neg0, neg1) (negation fused, Q5); output split (bf16x3, PLANES 3) for a next dense layer,
 // or fp32.
-template <int EPI, bool SPLIT>
+// REL: first BetaE projection layer with the relation input factored out (RelTerm below): the
+// accumulator of row (group gi, query b) starts at RW[r] for r = rels[b, rel_slot[gi]].
+template <int EPI, bool SPLIT, bool REL = false>
 struct EpiLinear {
   static constexpr int PLANES = SPLIT ? 3 : 1, ROWDIV = 1;
-  static constexpr bool CMIN = false;
+  static constexpr bool CMIN = false, INIT = REL;
   template <int CH>
   __device__ void chunk_min(int, int, const float*) const {}
   const float* bias;
   int N, neg0, neg1;
+  RelTerm rt;
+  template <int CW>
+  __device__ __forceinline__ void init(int row, int n0, float* acc) const {
+    if (row >= rt.M) return;
+    const int gi = row / rt.B, b = row - gi * rt.B;
+    const int slot = rt.rel_slot[gi];
+    int r = rt.rels[(int64_t)b * rt.n_r + slot];
+    if (r < 0 || r >= rt.n_relation) {  // kgq.h: out-of-range id -> NaN row, KGQ_ERANGE
+      if (atomicCAS(&rt.err[0], 0, 1) == 0) {
+        rt.err[1] = b;
+        rt.err[2] = slot;
+        rt.err[3] = 1;
+      }
+      rt.invalid[b] = 1;
+      r = 0;
+    }
+    const float* w = rt.RW + (int64_t)r * rt.ldrw + n0;
+#pragma unroll
+    for (int i = 0; i < CW; i += 4) {
+      if (n0 + i + 4 <= N) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(w + i));
+        acc[i] = v.x;
+        acc[i + 1] = v.y;
+        acc[i + 2] = v.z;
+        acc[i + 3] = v.w;
+      }
+    }
+  }
   struct Pre {
     float b[4];  // bias of columns n0 + lane + 32 j
     bool neg;
@@ -61,9 +91,18 @@ template <int EPI, bool SPLIT>
 int launch_epi(const Split& A, int M, int K, const Linear& L, const Split& out_sp, float* out_f32, int64_t ld_f32,
                int neg0, int neg1, const GemmWs* ws, cudaStream_t st) {
   const tc::OutDesc o{out_f32, ld_f32, out_sp, M, L.out_f};
-  return tc::launch_gemm_auto(A, M, L.Wsp, L.out_f, K, o, EpiLinear<EPI, SPLIT>{L.b, L.out_f, neg0, neg1}, ws, st);
+  return tc::launch_gemm_auto(A, M, L.Wsp, L.out_f, K, o, EpiLinear<EPI, SPLIT>{L.b, L.out_f, neg0, neg1, RelTerm{}},
+                              ws, st);
 }
 }  // namespace
+
+int launch_linear_rel(const Split& A, int M, int K, const Linear& L, const RelTerm& rt, const Split& out,
+                      const GemmWs* ws, cudaStream_t st) {
+  if (M <= 0) return 0;
+  const tc::OutDesc o{nullptr, 0, out, M, L.out_f};
+  return tc::launch_gemm_auto(A, M, L.Wsp, L.out_f, K, o, EpiLinear<kEpiRelu, true, true>{L.b, L.out_f, 0, 0, rt},
+                              ws, st);
+}
 
 int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, const Split& out_sp, float* out_f32,
                   int64_t ld_f32, int neg0, int neg1, const GemmWs* ws, cudaStream_t st) {

@@ -113,7 +113,9 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
 template <int NB>
 struct EpiBetaScore {
   static constexpr int PLANES = 1, ROWDIV = NB;
-  static constexpr bool CMIN = true;
+  static constexpr bool CMIN = true, INIT = false;
+  template <int CW>
+  __device__ void init(int, int, float*) const {}
   const float2* P;  // [rows] (hi, lo)
   const float2* E;  // [np] (hi, lo)
   int rows;

@@ -277,6 +277,8 @@ __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, 
 //          column operands come from the prefetched registers by warp shuffle
 //   static constexpr bool CMIN; template <int CH> __device__ void chunk_min(int row, int n,
 //       const float* v) const -- optional side output after the row-pair min (score top-k)
+//   static constexpr bool INIT; template <int CW> __device__ void init(int row, int n0,
+//       float* acc) const -- optional initial accumulator values (relation term of layer 1)
 // Output tensor maps: PLANES 1: fp32, box {32 columns, 32 / ROWDIV rows}, 128-byte swizzle;
 // PLANES 3: bf16 plane p, box {16 columns, 32 rows}, 32-byte swizzle.
 template <int BN, class Epi>
@@ -436,6 +438,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       float acc[CW];
 #pragma unroll
       for (int i = 0; i < CW; ++i) acc[i] = 0.0f;
+      // optional per-(row, column) initial value, added once (by the split holding K-block 0);
+      // loaded here so its latency hides under the first partial's MMAs
+      if constexpr (Epi::INIT)
+        if (kb0 == 0) epi.template init<CW>(row0 + lane, n0, acc);
       for (int gi = 0; gi < ng; ++gi) {
         const uint32_t g = g0 + gi, a = g & 1;
         mbar_wait_backoff(&accfull[a], (g >> 1) & 1);

@@ -363,3 +363,24 @@ def test_topk_heavy_ties(N, k, model):
         np.testing.assert_array_equal(ti[b], ties[:k], err_msg=f"row {b}: tied ids not ascending")
         assert np.all(td[b] == td[b][0])
     e.close()
+
+
+def test_betae_out_of_range_relation_at_later_hop():
+    """The first projection layer range-checks relation ids in its GEMM epilogue (relation
+    term factored out): a bad hop-1 relation must still give KGQ_ERANGE and a
+    NaN / -1 row, leaving the other rows exact."""
+    e, m, t = engine("betae")
+    a, r = synth.make_queries("3p", 20, SMALL["N"], SMALL["R"], seed=17)
+    bad = r.copy()
+    bad[3, 1] = SMALL["R"]
+    bad[7, 2] = -5
+    td, ti = e.submit("3p", dev(a), dev(bad), 5)
+    with pytest.raises(KgqError, match="ERANGE"):
+        e.check_errors()
+    e.check_errors()
+    td, ti = td.cpu().numpy(), ti.cpu().numpy()
+    assert np.all(np.isnan(td[[3, 7]])) and np.all(ti[[3, 7]] == -1)
+    ok = [b for b in range(20) if b not in (3, 7)]
+    ref = m.scores("3p", a[ok], r[ok])
+    for j, b in enumerate(ok):
+        assert_topk_ok(td[b], ti[b], ref[j], 5)
