@@ -15,8 +15,8 @@
 //   * warp 0 lane 0 = TMA producer, warp 1 lane 0 (leader CTA) = MMA issuer, warps 2-9 =
 //     epilogue.  The MMA accumulates DRAIN K-blocks into one of two TMEM partials (ping-pong)
 //     and the epilogue warps add the partials in fp32 round-to-nearest registers: the TMEM
-//     accumulate path truncates (measured: 1.8e-5 of sum|x w| over one K = 1600 chain, vs
-//     8e-7 with DRAIN = 2; profiles/r01/tc_gemm_accuracy.txt);
+//     accumulate path truncates (3xTF32 era: 1.8e-5 of sum|x w| over one K = 1600 chain vs 8e-7
+//     with 2-K-block partials, profiles/r01/tc_gemm_accuracy.txt; bf16x3 with DRAIN = 8: 2.7e-7);
 //   * the epilogue of tile t (bias / activation / split / score terms, Epi::chunk) overlaps
 //     the first partials of tile t+1, and writes through a swizzled shared-memory staging tile
 //     and TMA bulk tensor stores (cp.async.bulk.tensor shared -> global; the tensor map clips
@@ -214,8 +214,11 @@ __device__ unsigned long long* g_tc_trace;
 #endif
 
 // K-blocks per TMEM partial (see header comment).
+// 8 for bf16x3: 2.7e-7 of sum|x w| at K = 1600 (DRAIN 2: 7.3e-8, 4: 1.4e-7, 16: 5.3e-7;
+// scripts/tc_bn_check.cu 1600) and 5-8% faster mainloops than DRAIN 2 -- a longer partial
+// hides the accumulator hand-off (MMA commit -> epilogue drain -> accempty) better.
 #ifndef KGQ_TC_DRAIN
-#define KGQ_TC_DRAIN 2
+#define KGQ_TC_DRAIN 8
 #endif
 constexpr int DRAIN = KGQ_TC_DRAIN;
 

@@ -16,7 +16,8 @@ $NVCC $FL tc_bn_check.cu -o tc_bn_check &
 declare -A DEF=([nostore]="-DKGQ_TC_TRACE -DKGQ_TC_DBG_NO_STORE" [drain3]="-DKGQ_TC_TRACE -DKGQ_TC_DRAIN=3"
                [drain4]="-DKGQ_TC_TRACE -DKGQ_TC_DRAIN=4" [nobackoff]="-DKGQ_TC_NO_BACKOFF" [notma]="-DKGQ_TC_DBG_NO_TMA"
                [notma_nodrain]="-DKGQ_TC_DBG_NO_TMA -DKGQ_TC_DBG_NO_DRAIN" [notma_nostore]="-DKGQ_TC_DBG_NO_TMA -DKGQ_TC_DBG_NO_STORE"
-               [notma_nodrain_nostore]="-DKGQ_TC_DBG_NO_TMA -DKGQ_TC_DBG_NO_DRAIN -DKGQ_TC_DBG_NO_STORE")
+               [notma_nodrain_nostore]="-DKGQ_TC_DBG_NO_TMA -DKGQ_TC_DBG_NO_DRAIN -DKGQ_TC_DBG_NO_STORE"
+               [drain8]="-DKGQ_TC_DRAIN=8")
 $NVCC $FL -DKGQ_TC_DRAIN=4 tc_bn_check.cu -o tc_bn_check_drain4 &
 for v in $EXTRA; do $NVCC $FL ${DEF[$v]} tc_probe.cu -o tc_probe_$v & done
 wait
