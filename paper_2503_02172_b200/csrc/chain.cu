@@ -26,6 +26,7 @@ __global__ void k_translate_chain(ChainArgs a, const float* __restrict__ ent,
                                   const float* __restrict__ rel,
                                   const float* __restrict__ rel_off, int B, Split out,
                                   float* __restrict__ q) {
+  pdl_grid_sync();
   const int b = blockIdx.x;
   const int br = blockIdx.y;
   const BranchPlan& P = a.br[br];
@@ -65,7 +66,7 @@ int launch_translate_chain(const ChainArgs& a, const float* ent, const float* re
                            const float* rel_off, int B, Split out_split, float* out_q,
                            cudaStream_t st) {
   dim3 grid(B, a.nb);
-  k_translate_chain<<<grid, 128, 0, st>>>(a, ent, rel, rel_off, B, out_split, out_q);
+  launch_pdl(k_translate_chain, grid, dim3(128), 0, st, a, ent, rel, rel_off, B, out_split, out_q);
   return 1;
 }
 
@@ -74,6 +75,7 @@ int launch_translate_chain(const ChainArgs& a, const float* ent, const float* re
 __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
                                   const float* __restrict__ rel, int B, MlpGroup g, Split src,
                                   Split z, int with_rel) {
+  pdl_grid_sync();
   const int b = blockIdx.x;
   const int gi = blockIdx.y;
   const int d = a.d;
@@ -99,7 +101,7 @@ __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
 int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
                            const MlpGroup& g, Split src, Split z, cudaStream_t st, bool with_rel) {
   dim3 grid(B, g.n);
-  k_betae_mlp_input<<<grid, 128, 0, st>>>(a, ent, rel, B, g, src, z, with_rel ? 1 : 0);
+  launch_pdl(k_betae_mlp_input, grid, dim3(128), 0, st, a, ent, rel, B, g, src, z, with_rel ? 1 : 0);
   return 1;
 }
 
@@ -128,6 +130,7 @@ int launch_relation_term(const float* R, int n_relation, int d, const float* W, 
 // ---- BetaE Eq.-4 literal terminal: softmax over the 2d outputs, max(., 1e-6) -----------
 __global__ void k_softmax_terminal(const float* __restrict__ T, int64_t ldt, int w, Split out,
                                    int64_t out_row0, int neg0, int neg1) {
+  pdl_grid_sync();
   const int r = blockIdx.x;
   const float* t = T + (int64_t)r * ldt;
   __shared__ float red[32];
@@ -166,12 +169,13 @@ __global__ void k_softmax_terminal(const float* __restrict__ T, int64_t ldt, int
 
 int launch_softmax_terminal(const float* T, int64_t ldt, int M, int w, Split out,
                             int64_t out_row0, int neg0, int neg1, cudaStream_t st) {
-  k_softmax_terminal<<<M, 256, 0, st>>>(T, ldt, w, out, out_row0, neg0, neg1);
+  launch_pdl(k_softmax_terminal, dim3(M), dim3(256), 0, st, T, ldt, w, out, out_row0, neg0, neg1);
   return 1;
 }
 
 // ---- negation (Q5): alpha -> 1/alpha, beta -> 1/beta, in place on split rows -----------
 __global__ void k_negate(Split x, int64_t r0, int64_t nrows, int w) {
+  pdl_grid_sync();
   const int64_t n = nrows * w;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -184,13 +188,14 @@ __global__ void k_negate(Split x, int64_t r0, int64_t nrows, int w) {
 int launch_negate(Split x, int64_t r0, int64_t r1, int w, cudaStream_t st) {
   const int64_t n = (r1 - r0) * w;
   const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-  k_negate<<<blocks, 256, 0, st>>>(x, r0, r1 - r0, w);
+  launch_pdl(k_negate, dim3(blocks), dim3(256), 0, st, x, r0, r1 - r0, w);
   return 1;
 }
 
 // ---- Q2B offset gate input: mean over branches of ReLU(V1 o_i + c1) --------------------
 __global__ void k_branch_mean(const float* __restrict__ T, int64_t ldt, int nb, int B, int d,
                               Split out) {
+  pdl_grid_sync();
   const int b = blockIdx.x;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     float s = 0.0f;
@@ -201,7 +206,7 @@ __global__ void k_branch_mean(const float* __restrict__ T, int64_t ldt, int nb, 
 
 int launch_branch_mean(const float* T, int64_t ldt, int nb, int B, int d, Split out,
                        cudaStream_t st) {
-  k_branch_mean<<<B, 128, 0, st>>>(T, ldt, nb, B, d, out);
+  launch_pdl(k_branch_mean, dim3(B), dim3(128), 0, st, T, ldt, nb, B, d, out);
   return 1;
 }
 
@@ -212,6 +217,7 @@ int launch_branch_mean(const float* T, int64_t ldt, int nb, int B, int d, Split 
 __global__ void k_attention_combine(CombineArgs c, Split S, const float* __restrict__ logits,
                                     const float* __restrict__ gate, Split out,
                                     float* __restrict__ q) {
+  pdl_grid_sync();
   const int b = blockIdx.x;
   const int d = c.d;
   const int B = c.B;
@@ -267,19 +273,20 @@ __global__ void k_attention_combine(CombineArgs c, Split S, const float* __restr
 
 int launch_attention_combine(const CombineArgs& c, Split S, const float* logits,
                              const float* gate, Split out_split, float* out_q, cudaStream_t st) {
-  k_attention_combine<<<c.B, 128, 0, st>>>(c, S, logits, gate, out_split, out_q);
+  launch_pdl(k_attention_combine, dim3(c.B), dim3(128), 0, st, c, S, logits, gate, out_split, out_q);
   return 1;
 }
 
 // ---- split state rows -> q[b, br, :] ---------------------------------------------------
 __global__ void k_state_to_q(Split S, int nb, int B, int w, float* __restrict__ q) {
+  pdl_grid_sync();
   const int b = blockIdx.x, br = blockIdx.y;
   for (int j = threadIdx.x; j < w; j += blockDim.x)
     q[((int64_t)b * nb + br) * w + j] = load_split(S, ((int64_t)br * B + b) * S.ld + j);
 }
 
 int launch_state_to_q(Split S, int nb, int B, int w, float* q, cudaStream_t st) {
-  k_state_to_q<<<dim3(B, nb), 128, 0, st>>>(S, nb, B, w, q);
+  launch_pdl(k_state_to_q, dim3(B, nb), dim3(128), 0, st, S, nb, B, w, q);
   return 1;
 }
 

@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
+
+#include <utility>
 #include <stdint.h>
 
 namespace kgq {
@@ -23,6 +26,39 @@ struct Split {
     return Split{b0 + o, b1 + o, b2 + o, ld};
   }
 };
+
+// Programmatic dependent launch (PDL): every hot-path kernel is launched with programmatic
+// stream serialization, waits for its predecessor's results with griddepcontrol.wait before
+// reading them and lets its successor start launching right away (griddepcontrol.
+// launch_dependents), so kernel launch latency overlaps the predecessor's tail.  Both are
+// no-ops for a kernel launched without the attribute.  KGQ_NO_PDL=1 disables the attribute.
+__device__ __forceinline__ void pdl_grid_sync() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KGQ_NO_PDL");
+    v = (e && e[0] && e[0] != '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Column of the offset half in a Q2B split state [centre | offset]: 8-element (16-byte) aligned
 // so that the offset half is itself a TMA-addressable GEMM operand.

@@ -85,6 +85,7 @@ __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns
 __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
                                 const double* __restrict__ sums, int64_t ns, Split A,
                                 float2* __restrict__ P) {
+  pdl_grid_sync();
   const int r = blockIdx.x;
   __shared__ double red[32];
   double p = 0.0;
@@ -185,7 +186,7 @@ int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double
                           Split A, float2* P, const Split& uv, const float2* Esum,
                           int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
                           const GemmWs* ws, cudaStream_t st) {
-  k_score_prep_tc<<<rows, 128, 0, st>>>(q, rows, d, sums, ns, A, P);
+  launch_pdl(k_score_prep_tc, dim3(rows), dim3(128), 0, st, q, rows, d, sums, ns, A, P);
   // dist rows: one per query (NB = 2: min over the two DNF branch rows 2b, 2b + 1)
   const tc::OutDesc o{dist, ldd, Split{}, rows / nbq, np};
   if (nbq == 2)

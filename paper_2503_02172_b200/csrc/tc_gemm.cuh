@@ -637,14 +637,6 @@ struct OutDesc {
   int64_t rows, cols;
 };
 
-inline bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("KGQ_NO_PDL");
-    v = (e && e[0] && e[0] != '0') ? 0 : 1;
-  }
-  return v == 1;
-}
 
 // Per-context scratch of the split tail (kgq_internal.cuh GemmWs): at most kClustersMax tail
 // units of 256 x 256 fp32 and kClustersMax x 16 counters.

@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(32 * kCminWarps)
     k_topk_cmin(const float* __restrict__ dist, int64_t ldd, const float* __restrict__ cmin, int64_t ldc,
                 int64_t n, int k, int64_t id_base, const int32_t* __restrict__ invalid,
                 float* __restrict__ od, int32_t* __restrict__ oi, int B) {
+  pdl_grid_sync();
   __shared__ float wtau[kCminWarps];
   __shared__ unsigned long long cand[kCandCap];
   __shared__ int ncand;
@@ -441,7 +442,8 @@ __global__ void __launch_bounds__(32 * kCminWarps)
 int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                      int k, int64_t id_base, const int32_t* invalid, float* out_d, int32_t* out_i,
                      cudaStream_t st) {
-  k_topk_cmin<<<B, 32 * kCminWarps, 0, st>>>(dist, ldd, cmin, ldc, n, k, id_base, invalid, out_d, out_i, B);
+  launch_pdl(k_topk_cmin, dim3(B), dim3(32 * kCminWarps), 0, st, dist, ldd, cmin, ldc, n, k, id_base, invalid, out_d,
+             out_i, B);
   return 1;
 }
 
