@@ -264,6 +264,7 @@ def main():
     ap.add_argument("--impl", default="kgq", choices=["kgq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=14)
+    ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-structure submit measurement")
     ap.add_argument("--workload", default="fb15k237", choices=["fb15k237", "c5a", "suite"])
     ap.add_argument("--suite", default="", help="comma list of SUITE configs (default: all)")
     args = ap.parse_args()
@@ -346,6 +347,32 @@ def main():
     queries = args.steps * len(STRUCTS) * BATCH
     value = queries / (total_ms / 1e3)
 
+    # ---- the same step as ONE mixed-structure submit (kgq_submit_mixed):
+    # every projection hop of all 14 types' branches is one MLP, one scorer and one top-k ----
+    mixed = None
+    if world == 1 and not args.no_mixed:
+        from paper_2503_02172_b200 import Engine
+        meng = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH * len(STRUCTS), max_k=K, device=local)
+        meng.load_tables(t)
+        groups = [(s, qs[s][2].int(), qs[s][3].int()) for s in STRUCTS]
+        for _ in range(args.warmup):
+            meng.submit_mixed(groups, K)
+        torch.cuda.synchronize()
+        meng.check_errors()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        mt = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0.record()
+            meng.submit_mixed(groups, K)
+            e1.record()
+            torch.cuda.synchronize()
+            mt += e0.elapsed_time(e1)
+        mixed = {"value": queries / (mt / 1e3), "unit": "queries/s", "ms_per_step": mt / args.steps,
+                 "how": "one kgq_submit_mixed per step with the same 14 x 1024 queries (L2 flushed between steps)"}
+        meng.close()
+
     # ---- end to end through the public API with host buffers (pinned) ----------------
     pin = {s: (torch.from_numpy(qs[s][0]).pin_memory(), torch.from_numpy(qs[s][1]).pin_memory()) for s in STRUCTS}
     hout = (torch.empty((BATCH, K)).pin_memory(), torch.empty((BATCH, K), dtype=torch.int32).pin_memory())
@@ -401,6 +428,7 @@ def main():
                                    "score": {"ms_per_step": s_ms / args.steps, "tflops": ach(s_fl, s_ms),
                                              "launches_per_step": s_n / args.steps}}},
             "gpu_launches": launches[0],
+            "mixed_submit": mixed,
             "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "how": "kgq_submit_host per type from pinned host buffers, wall clock"},

@@ -162,6 +162,17 @@ kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anc
 kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
                            const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
                            kgq_stream stream);
+/* Mixed-structure batch: n_groups groups, group i = batches[i] queries of
+ * structure structures[i] (host arrays).  anchors / rels: device int32, the groups' [B_i, n_a(s_i)]
+ * and [B_i, n_r(s_i)] blocks concatenated in group order; topk_dist / topk_id: device
+ * [sum B_i, k], rows in the same order.  Sum B_i <= max_batch.  BetaE runs the groups
+ * level-synchronously (each projection hop of all groups' branches is one MLP, all
+ * intersections one attention GEMM pair, one scorer and one top-k for all queries); GQE / Q2B
+ * (and BetaE with k > 32) run group by group.  Same results and error behaviour as one
+ * kgq_submit per group (global query index in error reports). */
+kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures, const int32_t* batches,
+                            const int32_t* anchors, const int32_t* rels, int32_t k, float* topk_dist,
+                            int32_t* topk_id, kgq_stream stream);
 /* Operator chain only (parity aid): device out fp32 [batch, kgq_num_branches(s),
  * kgq_embedding_width(model, d)]. */
 kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,

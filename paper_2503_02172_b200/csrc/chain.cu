@@ -105,6 +105,66 @@ int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* re
   return 1;
 }
 
+// ---- mixed-structure batches: hop gather / scatter over row blocks (MixSegs) ----------------
+__device__ __forceinline__ int mix_seg_of(const MixSegs& sg, int row) {
+  int i = 0;
+  while (i + 1 < sg.n && sg.s[i + 1].dst0 <= row) ++i;
+  return i;
+}
+
+__global__ void k_mix_gather(MixSegs sg, const float* __restrict__ ent, Split S, Split Mst, Split Z,
+                             int32_t* __restrict__ rid, int d, int64_t n_entity, int n_relation,
+                             int32_t* err, int32_t* invalid) {
+  pdl_grid_sync();
+  const int row = blockIdx.x;
+  const MixSeg& g = sg.s[mix_seg_of(sg, row)];
+  const int b = row - g.dst0, q = g.q0 + b;
+  int r = g.rels[(int64_t)b * g.n_r + g.rslot];
+  if (r < 0 || r >= n_relation) {
+    if (threadIdx.x == 0) report_range(err, invalid, q, g.rslot, 1);
+    r = 0;
+  }
+  if (threadIdx.x == 0) rid[row] = r;
+  const int64_t zrow = (int64_t)row * Z.ld;
+  if (g.kind == 0) {
+    int a = g.anchors[(int64_t)b * g.n_a + g.aslot];
+    if (a < 0 || a >= n_entity) {
+      if (threadIdx.x == 0) report_range(err, invalid, q, g.aslot, 0);
+      a = 0;
+    }
+    for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) store_split(Z, zrow + j, ent[(int64_t)a * 2 * d + j]);
+  } else {
+    const Split& src = g.kind == 1 ? S : Mst;
+    const int64_t srow = (g.src0 + b) * src.ld;
+    for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) store_split(Z, zrow + j, load_split(src, srow + j));
+  }
+}
+
+int launch_mix_gather(const MixSegs& sg, int M, const float* ent, Split S, Split Mst, Split Z, int32_t* rid, int d,
+                      int64_t n_entity, int n_relation, int32_t* err, int32_t* invalid, cudaStream_t st) {
+  if (M <= 0) return 0;
+  launch_pdl(k_mix_gather, dim3(M), dim3(128), 0, st, sg, ent, S, Mst, Z, rid, d, n_entity, n_relation, err, invalid);
+  return 1;
+}
+
+__global__ void k_mix_scatter(MixSegs sg, Split src, Split S, int w) {
+  pdl_grid_sync();
+  const int row = blockIdx.x;
+  const MixSeg& g = sg.s[mix_seg_of(sg, row)];
+  const int64_t o = (g.src0 + row - g.dst0) * S.ld, i = (int64_t)row * src.ld;
+  for (int j = threadIdx.x; j < w; j += blockDim.x) {
+    S.b0[o + j] = src.b0[i + j];
+    S.b1[o + j] = src.b1[i + j];
+    S.b2[o + j] = src.b2[i + j];
+  }
+}
+
+int launch_mix_scatter(const MixSegs& sg, int M, Split src, Split S, int w, cudaStream_t st) {
+  if (M <= 0) return 0;
+  launch_pdl(k_mix_scatter, dim3(M), dim3(128), 0, st, sg, src, S, w);
+  return 1;
+}
+
 // ---- relation term of the first projection layer: RW[r, n] = sum_k W[n, col0 + k] R[r, k] ----
 // fp64 accumulation, once per table load (finalize).  Block (r, 128 outputs); R[r] staged in smem.
 __global__ void k_relation_term(const float* __restrict__ R, int d, const float* __restrict__ W, int64_t ldw,

@@ -540,6 +540,9 @@ void kgq_destroy(kgq_ctx* ctx) {
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) F(s->b0);
   F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->d_err); F(ctx->d_invalid);
   F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum); F(ctx->lin1x.Wsp.b0); F(ctx->RW);
+  F(ctx->mix_rid); F(ctx->mix_map);
+  if (ctx->mix_map_host) cudaFreeHost(ctx->mix_map_host);
+  if (ctx->mix_map_ev) cudaEventDestroy(ctx->mix_map_ev);
   F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
@@ -844,6 +847,293 @@ kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anc
   if (ctx->use_graphs && !shard_dist && batch <= ctx->bchunk)
     return submit_graphed(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, (cudaStream_t)stream);
   return submit_impl(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, shard_dist, (cudaStream_t)stream);
+}
+
+// ---- mixed-structure batches ---------------------------------------------
+// Several (structure, batch) groups in one call.  BetaE runs level-synchronously: every
+// projection hop of every group's branches (and then every post-intersection hop) is ONE MLP
+// over all their rows, the intersections of all groups are one pair of attention GEMMs, and the
+// scorer and the top-k run once over all queries -- the dense layers see M = sum of the groups'
+// branch rows instead of one structure's.  GQE / Q2B (cheap translation chains) submit group by
+// group.  Rows of S: intersection groups' branch blocks first (contiguous attention input),
+// then the others; hop batches are gathered into Z, run through the MLP into I and scattered
+// back; final query embeddings stay in S (branch 0 block, union: blocks 0 and 1).
+namespace {
+struct MixGroup {
+  int s, B, q0;
+  const Plan* P;
+  const int32_t* anchors;
+  const int32_t* rels;
+  int nb, maxh;
+  int nproj[kMaxBranches];
+  int proj[kMaxBranches][kMaxOps];
+  bool neg_after[kMaxBranches][kMaxOps];
+  int64_t srow[kMaxBranches];
+};
+}  // namespace
+
+// one MLP over a hop batch (segments already describe the batch rows); negated rows are last
+static int mix_mlp(kgq_ctx* ctx, const MixSegs& sg, int M, int neg0, cudaStream_t st) {
+  const int d = ctx->cfg.dim;
+  int L = 0;
+  L += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,
+                         ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
+  RelTerm rt;
+  rt.RW = ctx->RW;
+  rt.ldrw = ctx->cfg.hidden;
+  rt.M = M;
+  rt.rid = ctx->mix_rid;
+  {
+    StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
+    L += launch_linear_rel(ctx->Z, M, 2 * d, ctx->lin1x, rt, ctx->H[0], &ctx->gws, st);
+  }
+  Split A = ctx->H[0];
+  int K = ctx->lin1x.out_f;
+  for (int l = 1; l < ctx->cfg.n_hidden_layers; ++l) {
+    const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
+    L += dense(ctx, A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
+    A = ctx->H[l & 1];
+    K = lin.out_f;
+  }
+  const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
+  if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
+    L += dense(ctx, A, M, K, lo, kEpiNone, ctx->T, 2 * d, st);
+    L += launch_softmax_terminal(ctx->T, 2 * d, M, 2 * d, ctx->I, 0, neg0, M, st);
+  } else {
+    L += dense(ctx, A, M, K, lo, kEpiBetaReg, ctx->I, neg0, M, st);
+  }
+  L += launch_mix_scatter(sg, M, ctx->I, ctx->S, 2 * d, st);
+  check_site("mixed hop");
+  return L;
+}
+
+static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int32_t k, float* topk_dist,
+                              int32_t* topk_id, cudaStream_t st) {
+  const int d = ctx->cfg.dim;
+  int L = 0;
+  CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)Q * sizeof(int32_t), st), "reset flags");
+  // S layout: intersection groups first
+  int64_t cur = 0, inter_rows = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (auto& g : G)
+      if ((g.P->kind == kInter) == (pass == 0))
+        for (int br = 0; br < g.nb; ++br) {
+          g.srow[br] = cur;
+          cur += g.B;
+          if (pass == 0) inter_rows += g.B;
+        }
+  {
+    StageTimer t(ctx, st, kStChain);
+    // ---- branch hops ----
+    int maxh = 0;
+    for (auto& g : G) maxh = std::max(maxh, g.maxh);
+    for (int h = 0; h < maxh; ++h) {
+      MixSegs sg;
+      int M = 0, neg0 = 0;
+      for (int negpass = 0; negpass < 2; ++negpass) {
+        if (negpass == 1) neg0 = M;
+        for (auto& g : G)
+          for (int br = 0; br < g.nb; ++br) {
+            if (g.nproj[br] <= h || g.neg_after[br][h] != (negpass == 1)) continue;
+            if (sg.n == kMaxMixSegs) return fail(ctx, KGQ_EINVAL, "mixed submit: too many groups");
+            MixSeg& m = sg.s[sg.n++];
+            m.dst0 = M; m.B = g.B; m.q0 = g.q0;
+            m.kind = h == 0 ? 0 : 1;
+            m.src0 = g.srow[br];
+            m.anchors = g.anchors; m.n_a = g.P->n_anchor; m.aslot = g.P->br[br].anchor;
+            m.rels = g.rels; m.n_r = g.P->n_rel; m.rslot = g.proj[br][h];
+            M += g.B;
+          }
+      }
+      // scatter targets: the same blocks' S rows (src0 already = srow)
+      L += mix_mlp(ctx, sg, M, neg0, st);
+    }
+    // ---- intersections: one attention GEMM pair over every intersection group's branch rows ----
+    if (inter_rows > 0) {
+      L += dense(ctx, ctx->S, (int)inter_rows, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
+      L += dense(ctx, ctx->I, (int)inter_rows, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone, ctx->T, ctx->tw, st);
+      for (auto& g : G) {
+        if (g.P->kind != kInter) continue;
+        CombineArgs c{};
+        c.model = KGQ_BETAE; c.nb = g.nb; c.B = g.B; c.d = d; c.ldl = ctx->tw; c.ldg = 0;
+        c.rels = g.rels; c.n_r = g.P->n_rel; c.n_relation = ctx->cfg.n_relation; c.post_slot = -1;
+        c.negate_out = g.P->neg_inter ? 1 : 0;
+        c.err = ctx->d_err; c.invalid = ctx->d_invalid + g.q0;
+        const Split out = g.P->npost ? ctx->M.at(g.q0) : ctx->S.at(g.srow[0]);
+        L += launch_attention_combine(c, ctx->S.at(g.srow[0]), ctx->T + g.srow[0] * ctx->tw, nullptr, out, nullptr, st);
+      }
+      // ---- post-intersection projections (ip, inp, up-DM) ----
+      int maxpost = 0;
+      for (auto& g : G) maxpost = std::max(maxpost, g.P->kind == kInter ? g.P->npost : 0);
+      for (int p = 0; p < maxpost; ++p) {
+        MixSegs sg;
+        int M = 0;
+        for (auto& g : G) {
+          if (g.P->kind != kInter || g.P->npost <= p) continue;
+          MixSeg& m = sg.s[sg.n++];
+          m.dst0 = M; m.B = g.B; m.q0 = g.q0;
+          m.kind = p == 0 ? 2 : 1;
+          m.src0 = p == 0 ? g.q0 : g.srow[0];
+          m.anchors = g.anchors; m.n_a = g.P->n_anchor; m.aslot = 0;
+          m.rels = g.rels; m.n_r = g.P->n_rel; m.rslot = g.P->post[p];
+          M += g.B;
+        }
+        // the hop's output goes to the group's branch-0 block; src0 of the scatter = srow[0]
+        MixSegs out = sg;
+        for (int i = 0; i < out.n; ++i) out.s[i].src0 = 0;
+        int gi = 0;
+        for (auto& g : G)
+          if (g.P->kind == kInter && g.P->npost > p) out.s[gi++].src0 = g.srow[0];
+        int Lh = 0;
+        Lh += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,
+                                ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
+        // reuse mix_mlp's layers without its gather/scatter: run them here
+        RelTerm rt;
+        rt.RW = ctx->RW; rt.ldrw = ctx->cfg.hidden; rt.M = M; rt.rid = ctx->mix_rid;
+        {
+          StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
+          Lh += launch_linear_rel(ctx->Z, M, 2 * d, ctx->lin1x, rt, ctx->H[0], &ctx->gws, st);
+        }
+        Split A = ctx->H[0];
+        int K = ctx->lin1x.out_f;
+        for (int l = 1; l < ctx->cfg.n_hidden_layers; ++l) {
+          const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
+          Lh += dense(ctx, A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
+          A = ctx->H[l & 1];
+          K = lin.out_f;
+        }
+        const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
+        if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
+          Lh += dense(ctx, A, M, K, lo, kEpiNone, ctx->T, 2 * d, st);
+          Lh += launch_softmax_terminal(ctx->T, 2 * d, M, 2 * d, ctx->I, 0, M, M, st);
+        } else {
+          Lh += dense(ctx, A, M, K, lo, kEpiBetaReg, ctx->I, M, M, st);
+        }
+        Lh += launch_mix_scatter(out, M, ctx->I, ctx->S, 2 * d, st);
+        L += Lh;
+      }
+    }
+  }
+  // ---- score rows: single-embedding groups first (query order), then the DNF-union groups
+  // (rows 2b + branch); out_row maps every dist row back to its global query index ----
+  int R1 = 0, R2 = 0;
+  for (auto& g : G) (g.P->n_out == 1 ? R1 : R2) += g.B * g.P->n_out;
+  const int Q1 = R1, Q2 = R2 / 2;
+  if (ctx->mix_map_ev) CK(cudaEventSynchronize(ctx->mix_map_ev), "mixed staging");
+  int64_t* srcrow = ctx->mix_map_host;
+  int64_t* outrow = ctx->mix_map_host + (R1 + R2);  // stored as int64 pairs of int32 below
+  int32_t* outrow32 = reinterpret_cast<int32_t*>(outrow);
+  {
+    int r = 0, o = 0;
+    for (auto& g : G)
+      if (g.P->n_out == 1)
+        for (int b = 0; b < g.B; ++b) {
+          srcrow[r++] = g.srow[0] + b;
+          outrow32[o++] = g.q0 + b;
+        }
+    for (auto& g : G)
+      if (g.P->n_out == 2)
+        for (int b = 0; b < g.B; ++b) {
+          srcrow[r++] = g.srow[0] + b;
+          srcrow[r++] = g.srow[1] + b;
+          outrow32[o++] = g.q0 + b;
+        }
+  }
+  const size_t map_bytes = (size_t)(R1 + R2) * sizeof(int64_t) + (size_t)(Q1 + Q2) * sizeof(int32_t);
+  CK(cudaMemcpyAsync(ctx->mix_map, ctx->mix_map_host, map_bytes, cudaMemcpyHostToDevice, st), "mixed map upload");
+  CK(cudaEventRecord(ctx->mix_map_ev, st), "mixed staging");
+  const int64_t* d_srcrow = ctx->mix_map;
+  const int32_t* d_outrow = reinterpret_cast<const int32_t*>(ctx->mix_map + (R1 + R2));
+  {
+    StageTimer t(ctx, st, kStScore, 2.0 * (R1 + R2) * (double)ctx->ns * 2 * d);
+    L += launch_mix_score_prep(d_srcrow, ctx->S, R1 + R2, d, ctx->uvsums, ctx->cfg.n_entity, ctx->Atc, ctx->Ptc, st);
+    L += launch_score_tc_gemm(R1, 1, d, ctx->Atc, ctx->Ptc, ctx->uv, ctx->Esum, ctx->np, ctx->dist, ctx->np,
+                              ctx->cmin, ctx->np / 32, ctx->ns, &ctx->gws, st);
+    L += launch_score_tc_gemm(R2, 2, d, ctx->Atc.at(R1), ctx->Ptc + R1, ctx->uv, ctx->Esum, ctx->np,
+                              ctx->dist + (int64_t)Q1 * ctx->np, ctx->np, ctx->cmin + (int64_t)Q1 * (ctx->np / 32),
+                              ctx->np / 32, ctx->ns, &ctx->gws, st);
+    check_site("mixed scorer");
+  }
+  {
+    StageTimer t(ctx, st, kStTopk);
+    L += launch_topk_cmin_map(ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, Q1 + Q2, ctx->ns, k, ctx->e0,
+                              ctx->d_invalid, d_outrow, topk_dist, topk_id, st);
+    check_site("mixed top-k");
+  }
+  ctx->launches = L;
+  CK(cudaGetLastError(), "mixed submit launch");
+  return KGQ_OK;
+}
+
+kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures, const int32_t* batches,
+                            const int32_t* anchors, const int32_t* rels, int32_t k, float* topk_dist,
+                            int32_t* topk_id, kgq_stream stream) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (n_groups < 0 || (n_groups > 0 && (!structures || !batches)))
+    return fail(ctx, KGQ_EINVAL, "mixed submit: bad group arrays");
+  int64_t Q = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    kgq_status st = check_submit(ctx, structures[i], batches[i], k, true);
+    if (st) return st;
+    Q += batches[i];
+  }
+  if (Q > ctx->cfg.max_batch)
+    return fail(ctx, KGQ_EINVAL, "mixed submit: %lld queries > max_batch %d", (long long)Q, ctx->cfg.max_batch);
+  if (Q == 0) { ctx->launches = 0; return KGQ_OK; }
+  if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  DeviceGuard dg(ctx->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  std::vector<MixGroup> G;
+  int64_t ao = 0, ro = 0, q0 = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    MixGroup g{};
+    g.s = structures[i];
+    g.B = batches[i];
+    g.q0 = (int)q0;
+    g.P = plan_of(g.s);
+    g.anchors = anchors + ao;
+    g.rels = rels + ro;
+    ao += (int64_t)g.B * g.P->n_anchor;
+    ro += (int64_t)g.B * g.P->n_rel;
+    q0 += g.B;
+    g.nb = g.P->nbranch;
+    for (int br = 0; br < g.nb; ++br) {
+      g.nproj[br] = 0;
+      for (int o = 0; o < g.P->br[br].nops; ++o) {
+        const int op = g.P->br[br].ops[o];
+        if (op == kOpNeg) {
+          g.neg_after[br][g.nproj[br] - 1] = true;
+        } else {
+          g.proj[br][g.nproj[br]] = op;
+          g.neg_after[br][g.nproj[br]] = false;
+          g.nproj[br]++;
+        }
+      }
+      g.maxh = std::max(g.maxh, g.nproj[br]);
+    }
+    if (g.B > 0) G.push_back(g);
+  }
+  const bool batched = ctx->cfg.model == KGQ_BETAE && ctx->RW && k <= 32 && Q <= ctx->bchunk &&
+                       !score_uses_stream(KGQ_BETAE, 1, (int)Q) && (int)G.size() * kMaxBranches <= kMaxMixSegs;
+  if (!batched) {  // group by group through the single-structure path
+    int L = 0;
+    for (auto& g : G) {
+      kgq_status st = submit_impl(ctx, g.s, g.B, g.anchors, g.rels, k, topk_dist + (int64_t)g.q0 * k,
+                                  topk_id + (int64_t)g.q0 * k, nullptr, cs);
+      if (st) return st;
+      L += ctx->launches;
+    }
+    ctx->launches = L;
+    return KGQ_OK;
+  }
+  if (!ctx->mix_rid) {
+    kgq_status st = dalloc(ctx, &ctx->mix_rid, (size_t)ctx->rows_max, "mixed relation ids");
+    if (!st) st = dalloc(ctx, &ctx->mix_map, (size_t)(3 * ctx->cfg.max_batch), "mixed row map");
+    if (st) return st;
+    CK(cudaMallocHost((void**)&ctx->mix_map_host, (size_t)(3 * ctx->cfg.max_batch) * sizeof(int64_t)), "mixed staging");
+    CK(cudaEventCreateWithFlags(&ctx->mix_map_ev, cudaEventDisableTiming), "mixed staging");
+  }
+  return mixed_betae(ctx, G, (int)Q, k, topk_dist, topk_id, cs);
 }
 
 kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,

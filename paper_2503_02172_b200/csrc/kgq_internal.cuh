@@ -107,6 +107,10 @@ struct kgq_ctx {
   kgq::Split uv{};                         // [np][2d] centred (u; v), bf16x3
   kgq::Linear lin1x{};                     // BetaE first projection layer, state columns W1[:, :2d]
   float* RW = nullptr;                     // [n_relation, H] relation term R W1[:, 2d:]^T (fp64 -> fp32)
+  int32_t* mix_rid = nullptr;              // mixed batches: per-row relation ids of a hop batch [rows_max]
+  int64_t* mix_map = nullptr;              // mixed batches: score-row source rows [2 max_batch] + output rows
+  int64_t* mix_map_host = nullptr;         // pinned staging of mix_map
+  cudaEvent_t mix_map_ev = nullptr;        // staging reuse guard
   float2* Esum = nullptr;                  // [np] sum_d C_ed as an fp32 (hi, lo) pair
   double* uvsums = nullptr;                // [2][d]
   kgq::GemmWs gws{};                       // tensor-core GEMM split-tail scratch
@@ -188,6 +192,7 @@ int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, const 
 // accumulators start at RW[r] of each row (EpiLinear<.., REL> init), r range-checked there.
 struct RelTerm {
   const float* RW = nullptr;  // [n_relation, ldrw]
+  const int32_t* rid = nullptr;  // optional per-row relation id (already range-checked)
   int64_t ldrw = 0;
   int M = 0, B = 0;           // rows = group member gi * B + query b
   const int32_t* rels = nullptr;
@@ -198,6 +203,39 @@ struct RelTerm {
 };
 int launch_linear_rel(const Split& A, int M, int K, const Linear& L, const RelTerm& rt, const Split& out,
                       const GemmWs* ws, cudaStream_t st);
+// ---- mixed-structure batches (kgq_submit_mixed) ----------------------------
+// One block of B query rows inside a batched hop: rows [dst0, dst0 + B) of the batch come from
+// anchor slot aslot (kind 0), state rows src0 + b of S (kind 1) or of the combined state Mst
+// (kind 2); relation slot rslot; global query index q0 + b (error reporting, invalid flags).
+struct MixSeg {
+  int32_t dst0, B, q0, kind;
+  int64_t src0;
+  const int32_t* anchors;
+  int32_t n_a, aslot;
+  const int32_t* rels;
+  int32_t n_r, rslot;
+};
+constexpr int kMaxMixSegs = 48;
+struct MixSegs {
+  int32_t n = 0;
+  MixSeg s[kMaxMixSegs];
+};
+// batch rows -> Z [rows, 2d] split (state / regularised anchor rows) and rid[row] (checked)
+int launch_mix_gather(const MixSegs& sg, int M, const float* ent, Split S, Split Mst, Split Z, int32_t* rid, int d,
+                      int64_t n_entity, int n_relation, int32_t* err, int32_t* invalid, cudaStream_t st);
+// batch rows [dst0 + b] of src -> S rows src0 + b (width w)
+int launch_mix_scatter(const MixSegs& sg, int M, Split src, Split S, int w, cudaStream_t st);
+// score rows r: A[r] = S[srcrow[r]] (split copy) and P_q (fp64, as k_score_prep_tc)
+int launch_mix_score_prep(const int64_t* srcrow, Split S, int rows, int d, const double* sums, int64_t ns,
+                          Split A, float2* P, cudaStream_t st);
+// tensor-core score GEMM only (A and P prepared): dist rows = rows / nbq
+int launch_score_tc_gemm(int rows, int nbq, int d, Split A, const float2* P, const Split& uv, const float2* Esum,
+                         int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
+                         const GemmWs* ws, cudaStream_t st);
+// block-minima top-k with an output row map (out_row[b] = output / invalid-flag row of dist row b)
+int launch_topk_cmin_map(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
+                         int k, int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d,
+                         int32_t* out_i, cudaStream_t st);
 // RW[r, n] = sum_k W[n, col0 + k] R[r, k] (k < d) in fp64 -> fp32
 int launch_relation_term(const float* R, int n_relation, int d, const float* W, int64_t ldw, int col0, int H,
                          float* RW, cudaStream_t st);

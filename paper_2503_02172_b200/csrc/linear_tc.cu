@@ -36,17 +36,22 @@ struct EpiLinear {
   template <int CW>
   __device__ __forceinline__ void init(int row, int n0, float* acc) const {
     if (row >= rt.M) return;
-    const int gi = row / rt.B, b = row - gi * rt.B;
-    const int slot = rt.rel_slot[gi];
-    int r = rt.rels[(int64_t)b * rt.n_r + slot];
-    if (r < 0 || r >= rt.n_relation) {  // kgq.h: out-of-range id -> NaN row, KGQ_ERANGE
-      if (atomicCAS(&rt.err[0], 0, 1) == 0) {
-        rt.err[1] = b;
-        rt.err[2] = slot;
-        rt.err[3] = 1;
+    int r;
+    if (rt.rid) {
+      r = rt.rid[row];  // mixed batches: looked up and range-checked by the gather
+    } else {
+      const int gi = row / rt.B, b = row - gi * rt.B;
+      const int slot = rt.rel_slot[gi];
+      r = rt.rels[(int64_t)b * rt.n_r + slot];
+      if (r < 0 || r >= rt.n_relation) {  // kgq.h: out-of-range id -> NaN row, KGQ_ERANGE
+        if (atomicCAS(&rt.err[0], 0, 1) == 0) {
+          rt.err[1] = b;
+          rt.err[2] = slot;
+          rt.err[3] = 1;
+        }
+        rt.invalid[b] = 1;
+        r = 0;
       }
-      rt.invalid[b] = 1;
-      r = 0;
     }
     const float* w = rt.RW + (int64_t)r * rt.ldrw + n0;
 #pragma unroll

@@ -111,6 +111,32 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
 // and, when cmin is set, the minimum of every 32-entity block of each output row over the
 // shard's real entities (columns < nvalid): cmin[row][n / 32].  The top-k reads these block
 // minima first and scans only the blocks that can hold one of the k best (k_topk_cmin).
+// Mixed batches: score row r is the split state row srcrow[r] of S (no fp32 round trip).
+__global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, int d,
+                                 const double* __restrict__ sums, int64_t ns, Split A, float2* __restrict__ P) {
+  pdl_grid_sync();
+  const int r = blockIdx.x;
+  __shared__ double red[32];
+  double p = 0.0;
+  const double inv = 1.0 / (double)ns;
+  const int64_t s0 = srcrow[r] * S.ld, a0 = (int64_t)r * A.ld;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const float a = load_split(S, s0 + j), b = load_split(S, s0 + d + j);
+    store_split(A, a0 + j, a);
+    store_split(A, a0 + d + j, b);
+    const double da = a, db = b;
+    p += lgamma(da) + lgamma(db) - lgamma(da + db) + da * sums[j] * inv + db * sums[d + j] * inv;
+  }
+  p = warp_sum(p);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) P[r] = split_f64(t);
+  }
+}
+
 template <int NB>
 struct EpiBetaScore {
   static constexpr int PLANES = 1, ROWDIV = NB;
@@ -180,6 +206,25 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
   k_uv_dim_sums<<<dim3(gx, (d + 127) / 128), 128, 0, st>>>(ent, 0, n_all, d, sums);
   k_uv_table<<<(unsigned)np, 128, 0, st>>>(ent, e0, ns, np, d, n_all, sums, uv, Esum);
   return 2;
+}
+
+int launch_mix_score_prep(const int64_t* srcrow, Split S, int rows, int d, const double* sums, int64_t ns,
+                          Split A, float2* P, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  launch_pdl(k_mix_score_prep, dim3(rows), dim3(128), 0, st, srcrow, S, d, sums, ns, A, P);
+  return 1;
+}
+
+int launch_score_tc_gemm(int rows, int nbq, int d, Split A, const float2* P, const Split& uv, const float2* Esum,
+                         int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
+                         const GemmWs* ws, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  const tc::OutDesc o{dist, ldd, Split{}, rows / nbq, np};
+  if (nbq == 2)
+    return tc::launch_gemm_auto(A, rows, uv, (int)np, 2 * d, o, EpiBetaScore<2>{P, Esum, rows, np, cmin, ldc, nvalid},
+                                ws, st);
+  return tc::launch_gemm_auto(A, rows, uv, (int)np, 2 * d, o, EpiBetaScore<1>{P, Esum, rows, np, cmin, ldc, nvalid},
+                              ws, st);
 }
 
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,

@@ -303,17 +303,18 @@ constexpr int kCandCap = 256;
 __global__ void __launch_bounds__(32 * kCminWarps)
     k_topk_cmin(const float* __restrict__ dist, int64_t ldd, const float* __restrict__ cmin, int64_t ldc,
                 int64_t n, int k, int64_t id_base, const int32_t* __restrict__ invalid,
-                float* __restrict__ od, int32_t* __restrict__ oi, int B) {
+                const int32_t* __restrict__ out_row, float* __restrict__ od, int32_t* __restrict__ oi, int B) {
   pdl_grid_sync();
   __shared__ float wtau[kCminWarps];
   __shared__ unsigned long long cand[kCandCap];
   __shared__ int ncand;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int b = blockIdx.x;
+  const int ob = out_row ? out_row[b] : b;  // output / invalid-flag row (mixed batches)
   const float kNaN = __uint_as_float(0x7FFFFFFFu), kInf = __uint_as_float(0x7F800000u);
-  od += (int64_t)b * k;
-  oi += (int64_t)b * k;
-  if (invalid && invalid[b]) {
+  od += (int64_t)ob * k;
+  oi += (int64_t)ob * k;
+  if (invalid && invalid[ob]) {
     if (wid == 0 && lane < k) {
       od[lane] = kNaN;
       oi[lane] = -1;
@@ -442,8 +443,17 @@ __global__ void __launch_bounds__(32 * kCminWarps)
 int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                      int k, int64_t id_base, const int32_t* invalid, float* out_d, int32_t* out_i,
                      cudaStream_t st) {
-  launch_pdl(k_topk_cmin, dim3(B), dim3(32 * kCminWarps), 0, st, dist, ldd, cmin, ldc, n, k, id_base, invalid, out_d,
-             out_i, B);
+  launch_pdl(k_topk_cmin, dim3(B), dim3(32 * kCminWarps), 0, st, dist, ldd, cmin, ldc, n, k, id_base, invalid,
+             (const int32_t*)nullptr, out_d, out_i, B);
+  return 1;
+}
+
+int launch_topk_cmin_map(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
+                         int k, int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d,
+                         int32_t* out_i, cudaStream_t st) {
+  if (B <= 0) return 0;
+  launch_pdl(k_topk_cmin, dim3(B), dim3(32 * kCminWarps), 0, st, dist, ldd, cmin, ldc, n, k, id_base, invalid,
+             out_row, out_d, out_i, B);
   return 1;
 }
 

@@ -35,7 +35,7 @@ EXPORTS = (
     "kgq_num_relations", "kgq_num_branches", "kgq_uses_negation", "kgq_structure_name",
     "kgq_structure_from_name", "kgq_embedding_width", "kgq_shard_range", "kgq_shard_begin",
     "kgq_shard_end", "kgq_load_entities", "kgq_load_relations", "kgq_load_linear",
-    "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_query_embedding", "kgq_merge_topk",
+    "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_submit_mixed", "kgq_query_embedding", "kgq_merge_topk",
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
     "kgq_profile_read", "kgq_rank_answers",
 )
@@ -75,6 +75,7 @@ _sig = {
     "kgq_finalize": (_I32, [_P]),
     "kgq_submit": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P]),
     "kgq_submit_host": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
+    "kgq_submit_mixed": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P]),
     "kgq_query_embedding": (_I32, [_P, _I32, _I32, _P, _P, _P, _P]),
     "kgq_merge_topk": (_I32, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
     "kgq_check_errors": (_I32, [_P, _P]),
@@ -225,6 +226,27 @@ class Engine:
         self._check(_lib.kgq_submit(self._h, s, B, _ptr(anchors), _ptr(rels), k, _ptr(td),
                                     _ptr(ti), _ptr(sd), _stream(stream)))
         return (td, ti, sd) if shard_dist else (td, ti)
+
+    def submit_mixed(self, groups, k, *, out=None, stream=None):
+        """Mixed-structure batch (kgq_submit_mixed): groups = [(structure, anchors, rels), ...]
+        with int32 CUDA tensors [B_i, n_a] / [B_i, n_r].  Returns (dist, ids) CUDA tensors
+        [sum B_i, k], rows in group order."""
+        import torch
+        ss = (ctypes.c_int32 * len(groups))(*[structure_id(g[0]) for g in groups])
+        bs = (ctypes.c_int32 * len(groups))(*[int(g[1].shape[0]) for g in groups])
+        dev = groups[0][1].device if groups else torch.device("cuda")
+        a = torch.cat([g[1].reshape(-1) for g in groups]) if groups else torch.empty(0, dtype=torch.int32, device=dev)
+        r = torch.cat([g[2].reshape(-1) for g in groups]) if groups else torch.empty(0, dtype=torch.int32, device=dev)
+        Q = sum(int(g[1].shape[0]) for g in groups)
+        if out is None:
+            td = torch.empty((Q, k), dtype=torch.float32, device=dev)
+            ti = torch.empty((Q, k), dtype=torch.int32, device=dev)
+        else:
+            td, ti = out
+        self._keep = (a, r)  # the launch is asynchronous: keep the concatenated inputs alive
+        self._check(_lib.kgq_submit_mixed(self._h, len(groups), ss, bs, _ptr(a), _ptr(r), k, _ptr(td),
+                                          _ptr(ti), _stream(stream)))
+        return td, ti
 
     def submit_host(self, structure, anchors: np.ndarray, rels: np.ndarray, k: int,
                     out=None, stream=None):

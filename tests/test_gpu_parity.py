@@ -384,3 +384,60 @@ def test_betae_out_of_range_relation_at_later_hop():
     ref = m.scores("3p", a[ok], r[ok])
     for j, b in enumerate(ok):
         assert_topk_ok(td[b], ti[b], ref[j], 5)
+
+
+@pytest.mark.parametrize("model", ["betae", "gqe"])
+def test_mixed_structure_batch(model):
+    """kgq_submit_mixed: several structures in one call.  BetaE runs them
+    level-synchronously (hops of all groups batched into one MLP, one scorer, one top-k), GQE
+    group by group; every group's rows must match the oracle like a plain submit."""
+    e, m, t = engine(model, max_batch=256)
+    N, R = SMALL["N"], SMALL["R"]
+    structs = STRUCTS[model]
+    groups, refs = [], []
+    for i, s in enumerate(structs):
+        B = 5 + (i * 7) % 11   # ragged group sizes
+        a, r = synth.make_queries(s, B, N, R, seed=100 + i)
+        groups.append((s, dev(a.astype(np.int32)), dev(r.astype(np.int32))))
+        refs.append(m.scores(s, a, r))
+    td, ti = e.submit_mixed(groups, 10)
+    e.check_errors()
+    td, ti = td.cpu().numpy(), ti.cpu().numpy()
+    q = 0
+    for (s, a, _), ref in zip(groups, refs):
+        for b in range(a.shape[0]):
+            assert_topk_ok(td[q + b], ti[q + b], ref[b], 10, what=f"mixed {model} {s} row {b}")
+        q += a.shape[0]
+    assert q == td.shape[0]
+
+
+def test_mixed_batch_out_of_range_and_equivalence():
+    """A bad relation id in one group flags exactly that query (global index); the other rows
+    agree with one kgq_submit per group (same arithmetic, different batching: 1e-5)."""
+    e, m, t = engine("betae", max_batch=256)
+    N, R = SMALL["N"], SMALL["R"]
+    groups = []
+    for i, s in enumerate(("3p", "2u", "ip", "pni", "up-DM")):
+        a, r = synth.make_queries(s, 12, N, R, seed=200 + i)
+        if s == "ip":
+            r = r.copy()
+            r[4, 2] = R + 3   # post-intersection hop relation out of range
+        groups.append((s, dev(a.astype(np.int32)), dev(r.astype(np.int32))))
+    td, ti = e.submit_mixed(groups, 8)
+    with pytest.raises(KgqError, match="ERANGE"):
+        e.check_errors()
+    e.check_errors()
+    td, ti = td.cpu().numpy(), ti.cpu().numpy()
+    bad = 2 * 12 + 4
+    assert np.all(np.isnan(td[bad])) and np.all(ti[bad] == -1)
+    q = 0
+    for s, a, r in groups:
+        sd, si = e.submit(s, a, r, 8)
+        sd, si = sd.cpu().numpy(), si.cpu().numpy()
+        for b in range(12):
+            if q + b == bad:
+                continue
+            np.testing.assert_allclose(td[q + b], sd[b], rtol=1e-5, err_msg=f"{s} row {b}")
+        q += 12
+    with pytest.raises(KgqError, match="ERANGE"):  # the per-group "ip" submit re-flags the bad id
+        e.check_errors()
