@@ -48,6 +48,15 @@ class ShardedEngine:
         gd, gi = all_gather_topk(td, ti, self.group)
         return self.engine.merge_topk(gd, gi, k, stream=stream)
 
+    def submit_mixed(self, groups, k, stream=None):
+        """Mixed-structure batch (kgq_submit_mixed) -> global top-k: the local [sum B_i, k]
+        lists are all-gathered and merged exactly like a single-structure submit."""
+        td, ti = self.engine.submit_mixed(groups, k, stream=stream)
+        if self.world == 1:
+            return td, ti
+        gd, gi = all_gather_topk(td, ti, self.group)
+        return self.engine.merge_topk(gd, gi, k, stream=stream)
+
     def last_launch_count(self):
         return self.engine.last_launch_count() + (1 if self.world > 1 else 0)
 

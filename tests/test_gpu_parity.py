@@ -441,3 +441,28 @@ def test_mixed_batch_out_of_range_and_equivalence():
         q += 12
     with pytest.raises(KgqError, match="ERANGE"):  # the per-group "ip" submit re-flags the bad id
         e.check_errors()
+
+
+def test_virtual_shards_mixed_batch():
+    """kgq_submit_mixed on W entity shards + kgq_merge_topk == one shard, bit for bit."""
+    N, R, d = 1000, 20, 40
+    t = synth.make_tables("betae", N, R, d, hidden=96, seed=5)
+    groups = []
+    for i, s in enumerate(("2p", "up", "3in", "ip", "2u-DM")):
+        a, r = synth.make_queries(s, 9 + i, N, R, seed=40 + i)
+        groups.append((s, dev(a.astype(np.int32)), dev(r.astype(np.int32))))
+    full = Engine("betae", N, R, d, hidden=96, max_batch=128, max_k=32)
+    full.load_tables(t)
+    fd, fi = full.submit_mixed(groups, 12)
+    for W in (2, 3):
+        parts = []
+        for rank in range(W):
+            e = Engine("betae", N, R, d, hidden=96, max_batch=128, max_k=32, world_size=W, rank=rank)
+            e.load_tables(t)
+            parts.append(e.submit_mixed(groups, 12))
+            torch.cuda.synchronize()
+            e.close()
+        md, mi = full.merge_topk(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]), 12)
+        assert torch.equal(mi, fi), W
+        assert torch.equal(md, fd), W
+    full.close()
