@@ -102,6 +102,32 @@ __device__ __forceinline__ float beta_reg(float y) {  // Q2/Q12: clamp(y + 1, 0.
   return fminf(fmaxf(y + 1.0f, 0.05f), 1e9f);
 }
 
+// ln Gamma(y) for y >= 8 by the Stirling series through y^-13 (the first dropped term is
+// < 1e-15 there): (y - 1/2) ln y - y + ln(2 pi)/2 + sum_k B_2k / (2k (2k-1) y^(2k-1)).
+__device__ __forceinline__ double lgamma_stirling8(double y) {
+  const double r = 1.0 / y, z = r * r;
+  const double s = r * (1.0 / 12 + z * (-1.0 / 360 + z * (1.0 / 1260 + z * (-1.0 / 1680 +
+                   z * (1.0 / 1188 + z * (-691.0 / 360360 + z * (1.0 / 156)))))));
+  return (y - 0.5) * log(y) - y + 0.91893853320467274178 + s;
+}
+// Shift x > 0 up to y = x + n >= 8: ln Gamma(x) = ln Gamma(y) - ln(x (x+1) ... (x+n-1)); the
+// product is returned in *p (multiplied into it), y as the result.
+__device__ __forceinline__ double lgamma_shift8(double x, double* p) {
+  while (x < 8.0) {
+    *p *= x;
+    x += 1.0;
+  }
+  return x;
+}
+// ln B(a, b) = ln Gamma(a) + ln Gamma(b) - ln Gamma(a + b) for a, b > 0 (Eq. 3): three
+// Stirling evaluations and ONE log of the combined shift products -- ~4x fewer instructions
+// than three libdevice lgamma calls (the query-side P_q precompute of the tensor-core scorer).
+__device__ __forceinline__ double lnbeta_f64(double a, double b) {
+  double pa = 1.0, pb = 1.0, pab = 1.0;
+  const double ya = lgamma_shift8(a, &pa), yb = lgamma_shift8(b, &pb), yab = lgamma_shift8(a + b, &pab);
+  return lgamma_stirling8(ya) + lgamma_stirling8(yb) - lgamma_stirling8(yab) + log(pab / (pa * pb));
+}
+
 // fp64 digamma: recurrence psi(x) = psi(x+1) - 1/x up to x >= 10, then the asymptotic
 // series ln x - 1/(2x) - sum_n B_2n / (2n x^2n) through x^-14 (truncation < 1e-16 there).
 __device__ __forceinline__ double digamma_f64(double x) {

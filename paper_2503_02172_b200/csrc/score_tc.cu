@@ -95,7 +95,7 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
     store_split(A, (int64_t)r * A.ld + j, a);
     store_split(A, (int64_t)r * A.ld + d + j, b);
     const double da = a, db = b;
-    p += lgamma(da) + lgamma(db) - lgamma(da + db) + da * sums[j] * inv + db * sums[d + j] * inv;
+    p += lnbeta_f64(da, db) + da * sums[j] * inv + db * sums[d + j] * inv;
   }
   p = warp_sum(p);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
@@ -125,7 +125,7 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
     store_split(A, a0 + j, a);
     store_split(A, a0 + d + j, b);
     const double da = a, db = b;
-    p += lgamma(da) + lgamma(db) - lgamma(da + db) + da * sums[j] * inv + db * sums[d + j] * inv;
+    p += lnbeta_f64(da, db) + da * sums[j] * inv + db * sums[d + j] * inv;
   }
   p = warp_sum(p);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
