@@ -27,7 +27,7 @@ using tc::BM;
 template <int EPI, bool SPLIT, bool REL = false>
 struct EpiLinear {
   static constexpr int PLANES = SPLIT ? 3 : 1, ROWDIV = 1;
-  static constexpr bool CMIN = false, INIT = REL;
+  static constexpr bool CMIN = false, INIT = REL, STREAM_OUT = false;
   template <int CH>
   __device__ void chunk_min(int, int, const float*) const {}
   const float* bias;

@@ -140,7 +140,7 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
 template <int NB>
 struct EpiBetaScore {
   static constexpr int PLANES = 1, ROWDIV = NB;
-  static constexpr bool CMIN = true, INIT = false;
+  static constexpr bool CMIN = true, INIT = false, STREAM_OUT = true;
   template <int CW>
   __device__ void init(int, int, float*) const {}
   const float2* P;  // [rows] (hi, lo)

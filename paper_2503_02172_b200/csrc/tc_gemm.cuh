@@ -168,6 +168,16 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// TMA store with an L2 evict-first policy: streaming outputs (the scorer's distance block,
+// 60 MB per C2 batch, of which the top-k reads ~3%) must not push the weights and the entity
+// table out of L2.
+__device__ __forceinline__ void tma_store_2d_evict_first(const CUtensorMap* map, const void* src, int c0, int c1) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -552,7 +562,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         __syncwarp();
 #ifndef KGQ_TC_DBG_NO_STORE  // perf probe only: skip the output stores
         if (lane == 0) {
-          tma_store_2d(&mO0, buf, n0 + c, row0 / ROWDIV);
+          if (Epi::STREAM_OUT)
+            tma_store_2d_evict_first(&mO0, buf, n0 + c, row0 / ROWDIV);
+          else
+            tma_store_2d(&mO0, buf, n0 + c, row0 / ROWDIV);
           if (PLANES == 3) {
             tma_store_2d(&mO1, buf + 1024, n0 + c, row0);
             tma_store_2d(&mO2, buf + 2048, n0 + c, row0);
