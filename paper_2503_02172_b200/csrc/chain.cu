@@ -133,10 +133,23 @@ __global__ void k_mix_gather(MixSegs sg, const float* __restrict__ ent, Split S,
       a = 0;
     }
     for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) store_split(Z, zrow + j, ent[(int64_t)a * 2 * d + j]);
-  } else {
+  } else {  // split -> split: a plane-wise copy, 16-byte vectors when aligned
     const Split& src = g.kind == 1 ? S : Mst;
     const int64_t srow = (g.src0 + b) * src.ld;
-    for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) store_split(Z, zrow + j, load_split(src, srow + j));
+    if (((2 * d) & 7) == 0) {
+      const int nv = (2 * d) >> 3;
+      for (int p = 0; p < 3; ++p) {
+        const uint4* sp = reinterpret_cast<const uint4*>(src.plane(p) + srow);
+        uint4* dp = reinterpret_cast<uint4*>(Z.plane(p) + zrow);
+        for (int j = threadIdx.x; j < nv; j += blockDim.x) dp[j] = sp[j];
+      }
+    } else {
+      for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+        Z.b0[zrow + j] = src.b0[srow + j];
+        Z.b1[zrow + j] = src.b1[srow + j];
+        Z.b2[zrow + j] = src.b2[srow + j];
+      }
+    }
   }
 }
 
@@ -152,6 +165,15 @@ __global__ void k_mix_scatter(MixSegs sg, Split src, Split S, int w) {
   const int row = blockIdx.x;
   const MixSeg& g = sg.s[mix_seg_of(sg, row)];
   const int64_t o = (g.src0 + row - g.dst0) * S.ld, i = (int64_t)row * src.ld;
+  if ((w & 7) == 0) {  // 16-byte vectors (row starts are 16-byte aligned: ld % 8 == 0)
+    const int nv = w >> 3;
+    for (int p = 0; p < 3; ++p) {
+      const uint4* sp = reinterpret_cast<const uint4*>(src.plane(p) + i);
+      uint4* dp = reinterpret_cast<uint4*>(S.plane(p) + o);
+      for (int j = threadIdx.x; j < nv; j += blockDim.x) dp[j] = sp[j];
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < w; j += blockDim.x) {
     S.b0[o + j] = src.b0[i + j];
     S.b1[o + j] = src.b1[i + j];
@@ -274,11 +296,9 @@ int launch_branch_mean(const float* T, int64_t ldt, int nb, int B, int d, Split 
 // GQE: x = state[:, :d].  BetaE: the same a_i weights alpha (cols [0,d)) and beta ([d,2d)).
 // Q2B: centre as GQE; offset o = min_i o_i * sigmoid(G) (gate logits G [B, d]).
 // Post projection (ip): + R[r] on the centre (GQE/Q2B; Q2B offset + R_o[r]).
-__global__ void k_attention_combine(CombineArgs c, Split S, const float* __restrict__ logits,
-                                    const float* __restrict__ gate, Split out,
-                                    float* __restrict__ q) {
-  pdl_grid_sync();
-  const int b = blockIdx.x;
+__device__ __forceinline__ void combine_query(const CombineArgs& c, const Split& S, const float* __restrict__ logits,
+                                              const float* __restrict__ gate, const Split& out,
+                                              float* __restrict__ q, int b) {
   const int d = c.d;
   const int B = c.B;
   const int nb = c.nb;
@@ -329,6 +349,33 @@ __global__ void k_attention_combine(CombineArgs c, Split S, const float* __restr
       if (two) dst[d + j] = x1;
     }
   }
+}
+
+__global__ void k_attention_combine(CombineArgs c, Split S, const float* __restrict__ logits,
+                                    const float* __restrict__ gate, Split out,
+                                    float* __restrict__ q) {
+  pdl_grid_sync();
+  combine_query(c, S, logits, gate, out, q, blockIdx.x);
+}
+
+// Mixed batches: the attention combine of every intersection group in one launch.  Block i is
+// query i of the concatenation of the groups (MixCombine::q_begin prefix).
+__global__ void k_mix_combine(MixCombine mc, Split S, const float* __restrict__ logits, int64_t ldl, Split Mst) {
+  pdl_grid_sync();
+  const int i = blockIdx.x;
+  int g = 0;
+  while (g + 1 < mc.n && mc.g[g + 1].q_begin <= i) ++g;
+  const MixCombine::Group& G = mc.g[g];
+  const Split src = S.at(G.srow0);
+  const Split out = G.to_m ? Mst.at(G.q0) : src;
+  combine_query(G.c, src, logits + G.srow0 * ldl, nullptr, out, nullptr, i - G.q_begin);
+}
+
+int launch_mix_combine(const MixCombine& mc, int total, Split S, const float* logits, int64_t ldl, Split Mst,
+                       cudaStream_t st) {
+  if (total <= 0) return 0;
+  launch_pdl(k_mix_combine, dim3(total), dim3(128), 0, st, mc, S, logits, ldl, Mst);
+  return 1;
 }
 
 int launch_attention_combine(const CombineArgs& c, Split S, const float* logits,

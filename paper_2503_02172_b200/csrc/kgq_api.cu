@@ -952,16 +952,24 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
     if (inter_rows > 0) {
       L += dense(ctx, ctx->S, (int)inter_rows, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
       L += dense(ctx, ctx->I, (int)inter_rows, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone, ctx->T, ctx->tw, st);
+      MixCombine mc;
+      int total = 0;
       for (auto& g : G) {
         if (g.P->kind != kInter) continue;
-        CombineArgs c{};
+        MixCombine::Group& mg = mc.g[mc.n++];
+        CombineArgs& c = mg.c;
+        c = CombineArgs{};
         c.model = KGQ_BETAE; c.nb = g.nb; c.B = g.B; c.d = d; c.ldl = ctx->tw; c.ldg = 0;
         c.rels = g.rels; c.n_r = g.P->n_rel; c.n_relation = ctx->cfg.n_relation; c.post_slot = -1;
         c.negate_out = g.P->neg_inter ? 1 : 0;
         c.err = ctx->d_err; c.invalid = ctx->d_invalid + g.q0;
-        const Split out = g.P->npost ? ctx->M.at(g.q0) : ctx->S.at(g.srow[0]);
-        L += launch_attention_combine(c, ctx->S.at(g.srow[0]), ctx->T + g.srow[0] * ctx->tw, nullptr, out, nullptr, st);
+        mg.q_begin = total;
+        mg.q0 = g.q0;
+        mg.srow0 = g.srow[0];
+        mg.to_m = g.P->npost ? 1 : 0;
+        total += g.B;
       }
+      L += launch_mix_combine(mc, total, ctx->S, ctx->T, ctx->tw, ctx->M, st);
       // ---- post-intersection projections (ip, inp, up-DM) ----
       int maxpost = 0;
       for (auto& g : G) maxpost = std::max(maxpost, g.P->kind == kInter ? g.P->npost : 0);

@@ -265,6 +265,21 @@ struct CombineArgs {
 };
 int launch_attention_combine(const CombineArgs& c, Split S, const float* logits,
                              const float* gate, Split out_split, float* out_q, cudaStream_t st);
+// attention combine of every intersection group in one launch (blocks = queries of all groups)
+struct MixCombine {
+  struct Group {
+    CombineArgs c;   // per-group args (B, nb, negate_out, err / invalid at the group's queries)
+    int32_t q_begin; // first block of this group
+    int32_t q0;      // global query index (row of the combined state Mst when to_m)
+    int64_t srow0;   // S (and logits) row of the group's branch-0 block
+    int32_t to_m;    // 1: write the combined state to Mst rows q0.. (post projections follow);
+                     // 0: in place into the branch-0 block
+  };
+  int32_t n = 0;
+  Group g[16];
+};
+int launch_mix_combine(const MixCombine& mc, int total, Split S, const float* logits, int64_t ldl, Split Mst,
+                       cudaStream_t st);
 // Copy split state rows (b, branch br) to fp32 q[b, br, :].
 int launch_state_to_q(Split S, int nb, int B, int w, float* q, cudaStream_t st);
 // Scorer operands: query planes (k-major) from q[B, nbq, qw].
