@@ -362,6 +362,8 @@ def main():
         torch.cuda.synchronize()
         meng.check_errors()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        meng.profile(True)
+        meng.profile_read()
         mt = 0.0
         for _ in range(args.steps):
             flush.zero_()
@@ -370,7 +372,16 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             mt += e0.elapsed_time(e1)
+        mp = meng.profile_read()
+        meng.profile(False)
+        pk, _ = load_peaks()
+        mfl, mms = mp["dense"][2] + mp["score"][2], mp["dense"][0] + mp["score"][0]
+        mach = mfl / (mms / 1e3) / 1e12 if mms > 0 else 0.0
         mixed = {"value": queries / (mt / 1e3), "unit": "queries/s", "ms_per_step": mt / args.steps,
+                 "stage_ms_per_step": {k: v[0] / args.steps for k, v in mp.items()},
+                 "roofline": {"kernel": "k_gemm (tcgen05 bf16x3)", "bound": "tensor", "achieved": mach,
+                              "peak": pk["bf16_tflops"] / 6.0, "unit": "TFLOP/s",
+                              "frac": mach / (pk["bf16_tflops"] / 6.0)},
                  "how": "one kgq_submit_mixed per step with the same 14 x 1024 queries (L2 flushed between steps)"}
         meng.close()
 
