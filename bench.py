@@ -265,6 +265,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=14)
     ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-structure submit measurement")
+    ap.add_argument("--merge", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 cross-shard top-k exchange: NCCL all-gather + merge kernel (default) or the "
+                         "all-gather fused into the top-k over symmetric peer memory (N2)")
     ap.add_argument("--workload", default="fb15k237", choices=["fb15k237", "c5a", "suite"])
     ap.add_argument("--suite", default="", help="comma list of SUITE configs (default: all)")
     args = ap.parse_args()
@@ -287,7 +290,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t = synth.make_tables("betae", N_ENT, N_REL, DIM, hidden=HID, seed=SEED)
-    seng = ShardedEngine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K, device=local)
+    seng = ShardedEngine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K, device=local,
+                         merge=args.merge)
     seng.load_tables(t)
     eng = seng.engine
     ns = eng.shard[1] - eng.shard[0]
@@ -425,7 +429,8 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": dict(CONFIG, l2="flushed between timed steps (256 MiB write, untimed)",
-                           parallelism=f"entity-shard x{world}" if world > 1 else "1 GPU"),
+                           parallelism=f"entity-shard x{world}" if world > 1 else "1 GPU",
+                           merge=seng.merge_mode if world > 1 else None),
             "per_type_qps": {s: BATCH * args.steps / (per_type[s] / 1e3) for s in STRUCTS},
             "stage_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},  # dense is inside chain
             "stage_share": stage_share,

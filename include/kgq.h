@@ -183,6 +183,29 @@ kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int
 kgq_status kgq_merge_topk(kgq_ctx* ctx, int32_t n_parts, int32_t batch, int32_t k,
                           const float* in_dist, const int32_t* in_id, float* out_dist,
                           int32_t* out_id, kgq_stream stream);
+/* N2: the all-gather of a9 fused into the top-k kernel over peer memory
+ * (NVLink P2P on a multi-GPU node; any device memory for virtual shards on one GPU).
+ *   kgq_peer_bytes: size of the per-rank peer buffer for `world` ranks (-1 on bad arguments):
+ *     flag uint32 [2][world][max_batch] (256-byte padded), then key uint64
+ *     [2][world][max_batch][max_k] = (order key of dist << 32) | global id.
+ *   kgq_set_peers: registers the device pointers (host array of `world` entries; each
+ *     256-byte aligned, kgq_peer_bytes long, e.g. one symmetric-memory allocation per rank)
+ *     of every rank's buffer, this context being `rank`; zero-fills its own buffer and its
+ *     epoch (call on every rank, then barrier, before the next submit).  world = 0 turns the
+ *     push off.  Invalidates captured submit graphs.
+ *   With peers set, every kgq_submit / kgq_submit_host / kgq_submit_mixed starts a new epoch
+ *   and its top-k writes each output row's k keys into slot (epoch & 1, rank, row) of EVERY
+ *   rank's buffer, then releases the row's flag (= epoch) at system scope.  The local
+ *   topk_dist / topk_id outputs are written as before.
+ *   kgq_merge_peers: waits (acquire, per row) for all ranks' pushes of the current epoch and
+ *     writes the merged global top-k (dist, id ascending; NaN sorts last with id -1) to device
+ *     out_dist / out_id [batch, k].  Every rank must issue the same sequence of submits.  A
+ *     rank that has not published a row within KGQ_PEER_TIMEOUT_MS (default 10000) is
+ *     treated as empty and kgq_check_errors then returns KGQ_ESTATE naming it (no hang). */
+int64_t kgq_peer_bytes(const kgq_ctx* ctx, int32_t world);
+kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const* peer_bufs);
+kgq_status kgq_merge_peers(kgq_ctx* ctx, int32_t batch, int32_t k, float* out_dist, int32_t* out_id,
+                           kgq_stream stream);
 /* N1: filtered ranking of given answers (KGReasoning test protocol behind the
  * paper's MRR consistency check).  Query b's answer set (easy and hard, distinct
  * global ids) is ans_id[ans_off[b] .. ans_off[b+1]) (device int32 CSR, ans_off [batch+1],

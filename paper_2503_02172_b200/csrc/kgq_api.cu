@@ -544,7 +544,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   if (ctx->mix_map_host) cudaFreeHost(ctx->mix_map_host);
   if (ctx->mix_map_ev) cudaEventDestroy(ctx->mix_map_ev);
   F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
-  F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage);
+  F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage); F(ctx->d_epoch);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (auto& r : ctx->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -739,6 +739,7 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
                               float* shard_dist, cudaStream_t st) {
   const Plan* P = plan_of(s);
   int L = 0;
+  const bool push = ctx->peers.on() && ctx->push_row0 >= 0;  // N2: fused all-gather of the top-k
   CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)B * sizeof(int32_t), st), "reset flags");
   {
     StageTimer t(ctx, st, kStChain);
@@ -753,12 +754,19 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
       // the tensor-core scorer's epilogue wrote 32-entity block minima: pruned top-k
       const bool blockmin = ctx->cfg.model == KGQ_BETAE && !score_uses_stream(ctx->cfg.model, P->n_out, nb) &&
                             k <= 32 && !topk_cmin_disabled();
-      if (blockmin)
+      PeerPush pp{};
+      if (push) {
+        pp = ctx->peers;
+        pp.row0 = ctx->push_row0 + (int)b0;
+      }
+      if (blockmin) {
         L += launch_topk_cmin(ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, nb, ctx->ns, k, ctx->e0,
-                              ctx->d_invalid + b0, topk_dist + b0 * k, topk_id + b0 * k, st);
-      else
+                              ctx->d_invalid + b0, topk_dist + b0 * k, topk_id + b0 * k, st, pp);
+      } else {
         L += launch_topk(ctx->dist, ctx->np, nb, ctx->ns, k, ctx->e0, ctx->d_invalid + b0,
                          topk_dist + b0 * k, topk_id + b0 * k, ctx->topk_tmp_d, ctx->topk_tmp_i, st);
+        if (push) L += launch_peer_push(pp, nb, k, topk_dist + b0 * k, topk_id + b0 * k, st);
+      }
       check_site("top-k");
     }
     if (shard_dist)
@@ -844,6 +852,7 @@ kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anc
   if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
   if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
   DeviceGuard g(ctx->cfg.device);
+  ctx->push_row0 = ctx->peers.on() ? 0 : -1;
   if (ctx->use_graphs && !shard_dist && batch <= ctx->bchunk)
     return submit_graphed(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, (cudaStream_t)stream);
   return submit_impl(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, shard_dist, (cudaStream_t)stream);
@@ -1064,8 +1073,10 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
   }
   {
     StageTimer t(ctx, st, kStTopk);
+    PeerPush pp{};
+    if (ctx->peers.on()) pp = ctx->peers;  // N2: rows pushed by output row (row0 = 0)
     L += launch_topk_cmin_map(ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, Q1 + Q2, ctx->ns, k, ctx->e0,
-                              ctx->d_invalid, d_outrow, topk_dist, topk_id, st);
+                              ctx->d_invalid, d_outrow, topk_dist, topk_id, st, pp);
     check_site("mixed top-k");
   }
   ctx->launches = L;
@@ -1123,9 +1134,10 @@ kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* struc
   }
   const bool batched = ctx->cfg.model == KGQ_BETAE && ctx->RW && k <= 32 && Q <= ctx->bchunk &&
                        !score_uses_stream(KGQ_BETAE, 1, (int)Q) && (int)G.size() * kMaxBranches <= kMaxMixSegs;
-  if (!batched) {  // group by group through the single-structure path
+  if (!batched) {  // group by group through the single-structure path (one epoch: rows by q0)
     int L = 0;
     for (auto& g : G) {
+      ctx->push_row0 = ctx->peers.on() ? g.q0 : -1;
       kgq_status st = submit_impl(ctx, g.s, g.B, g.anchors, g.rels, k, topk_dist + (int64_t)g.q0 * k,
                                   topk_id + (int64_t)g.q0 * k, nullptr, cs);
       if (st) return st;
@@ -1158,6 +1170,7 @@ kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t
                      cudaMemcpyHostToDevice, cs), "anchor upload");
   CK(cudaMemcpyAsync(ctx->d_rel_stage, rels, (size_t)batch * P->n_rel * sizeof(int32_t),
                      cudaMemcpyHostToDevice, cs), "relation upload");
+  ctx->push_row0 = ctx->peers.on() ? 0 : -1;
   if (ctx->use_graphs && batch <= ctx->bchunk)
     st = submit_graphed(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage,
                         ctx->d_topi_stage, cs);
@@ -1215,11 +1228,87 @@ kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
     CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
     return fail(ctx, KGQ_EINVAL, "kgq_rank_answers: a query has more than %d answers", kMaxAnswers);
   }
+  if (e[0] == 3) {
+    CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
+    return fail(ctx, KGQ_ESTATE, "kgq_merge_peers: rank %d did not publish row %d within %lld ms", e[2], e[1],
+                ctx->peer_timeout_ns / 1000000);
+  }
   if (e[0]) {
     CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
     return fail(ctx, KGQ_ERANGE, "query row %d: %s slot %d out of range", e[1], e[3] ? "relation" : "anchor",
                 e[2]);
   }
+  return KGQ_OK;
+}
+
+// ---- N2: fused top-k all-gather over peer memory (peer.cuh) --------------------------------
+static int64_t peer_flag_bytes(const kgq_ctx* ctx, int world) {
+  return ((int64_t)2 * world * ctx->cfg.max_batch * (int64_t)sizeof(uint32_t) + 255) / 256 * 256;
+}
+
+int64_t kgq_peer_bytes(const kgq_ctx* ctx, int32_t world) {
+  if (!ctx || world < 1 || world > kMaxPeers) return -1;
+  return peer_flag_bytes(ctx, world) +
+         (int64_t)2 * world * ctx->cfg.max_batch * (int64_t)ctx->cfg.max_k * (int64_t)sizeof(unsigned long long);
+}
+
+kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const* peer_bufs) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  DeviceGuard g(ctx->cfg.device);
+  for (auto& gr : ctx->graphs) {  // captured submits bake in the old push arguments
+    if (gr.pending) harvest(ctx, gr.evs, false);
+    destroy_graph_entry(gr);
+  }
+  ctx->graphs.clear();
+  if (world == 0) {
+    ctx->peers = PeerPush{};
+    return KGQ_OK;
+  }
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return fail(ctx, KGQ_EINVAL, "kgq_set_peers: rank %d / world %d (1 <= world <= %d)", rank, world, kMaxPeers);
+  if (!peer_bufs) return fail(ctx, KGQ_EINVAL, "kgq_set_peers: peer_bufs is NULL");
+  for (int p = 0; p < world; ++p)
+    if (!peer_bufs[p] || ((uintptr_t)peer_bufs[p] & 255))
+      return fail(ctx, KGQ_EINVAL, "kgq_set_peers: buffer of rank %d is NULL or not 256-byte aligned", p);
+  if (!ctx->d_epoch) {
+    kgq_status st = dalloc(ctx, &ctx->d_epoch, 2, "peer epoch");
+    if (st) return st;
+  }
+  const char* to = getenv("KGQ_PEER_TIMEOUT_MS");
+  if (to && atoll(to) > 0) ctx->peer_timeout_ns = atoll(to) * 1000000LL;
+  PeerPush pp{};
+  pp.world = world;
+  pp.rank = rank;
+  pp.max_rows = ctx->cfg.max_batch;
+  pp.max_k = ctx->cfg.max_k;
+  pp.epoch = ctx->d_epoch;
+  const int64_t fb = peer_flag_bytes(ctx, world);
+  for (int p = 0; p < world; ++p) {
+    pp.flag[p] = static_cast<uint32_t*>(peer_bufs[p]);
+    pp.key[p] = reinterpret_cast<unsigned long long*>(static_cast<char*>(peer_bufs[p]) + fb);
+  }
+  CK(cudaMemset(peer_bufs[rank], 0, (size_t)kgq_peer_bytes(ctx, world)), "peer buffer reset");
+  const uint32_t ep0[2] = {1u, 0u};
+  CK(cudaMemcpy(ctx->d_epoch, ep0, sizeof ep0, cudaMemcpyHostToDevice), "peer epoch reset");
+  CK(cudaDeviceSynchronize(), "kgq_set_peers");
+  ctx->peers = pp;
+  return KGQ_OK;
+}
+
+kgq_status kgq_merge_peers(kgq_ctx* ctx, int32_t batch, int32_t k, float* out_dist, int32_t* out_id,
+                           kgq_stream stream) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (!ctx->peers.on()) return fail(ctx, KGQ_ESTATE, "kgq_merge_peers: no peers registered (kgq_set_peers)");
+  if (batch < 0 || batch > ctx->cfg.max_batch) return fail(ctx, KGQ_EINVAL, "batch %d outside [0, max_batch]", batch);
+  if (k < 1 || k > ctx->cfg.max_k) return fail(ctx, KGQ_EINVAL, "k %d outside [1, max_k=%d]", k, ctx->cfg.max_k);
+  if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
+  if (!out_dist || !out_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  DeviceGuard g(ctx->cfg.device);
+  PeerPush pp = ctx->peers;
+  pp.row0 = 0;
+  ctx->launches = launch_peer_merge(pp, batch, k, out_dist, out_id, ctx->d_err, ctx->peer_timeout_ns,
+                                    (cudaStream_t)stream);
+  CK(cudaGetLastError(), "kgq_merge_peers launch");
   return KGQ_OK;
 }
 

@@ -8,6 +8,7 @@
 
 #include "../../include/kgq.h"
 #include "common.cuh"
+#include "peer.cuh"
 
 namespace kgq {
 
@@ -146,6 +147,11 @@ struct kgq_ctx {
   bool use_graphs = true;
   uint64_t graph_clock = 0;
   cudaStream_t cap_stream = nullptr;
+  // N2: fused top-k all-gather over peer memory (kgq_set_peers); peers.world == 0: off
+  kgq::PeerPush peers{};
+  uint32_t* d_epoch = nullptr;             // [2]: epoch, merge CTA counter
+  int push_row0 = -1;      // set by the entry points: output-row offset of submit_impl's pushes (-1: none)
+  long long peer_timeout_ns = 10000000000LL;  // KGQ_PEER_TIMEOUT_MS
 
 };
 
@@ -235,7 +241,7 @@ int launch_score_tc_gemm(int rows, int nbq, int d, Split A, const float2* P, con
 // block-minima top-k with an output row map (out_row[b] = output / invalid-flag row of dist row b)
 int launch_topk_cmin_map(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                          int k, int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d,
-                         int32_t* out_i, cudaStream_t st);
+                         int32_t* out_i, cudaStream_t st, const PeerPush& pp);
 // RW[r, n] = sum_k W[n, col0 + k] R[r, k] (k < d) in fp64 -> fp32
 int launch_relation_term(const float* R, int n_relation, int d, const float* W, int64_t ldw, int col0, int H,
                          float* RW, cudaStream_t st);
@@ -316,7 +322,12 @@ int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double
 // entry <= tau), so only blocks with minimum <= tau are scanned.  Exact (dist, id) order.
 int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                      int k, int64_t id_base, const int32_t* invalid, float* out_d, int32_t* out_i,
-                     cudaStream_t st);
+                     cudaStream_t st, const PeerPush& pp);
+// N2 (peer.cuh): push of finished output rows [0, B) of (out_d, out_i) (top-k paths without
+// the fused push); the waiting merge (advances the epoch; epoch[1] is its CTA counter).
+int launch_peer_push(const PeerPush& pp, int B, int k, const float* out_d, const int32_t* out_i, cudaStream_t st);
+int launch_peer_merge(const PeerPush& pp, int B, int k, float* out_d, int32_t* out_i, int32_t* err,
+                      long long timeout_ns, cudaStream_t st);
 int launch_merge(int parts, int B, int k, const float* in_d, const int32_t* in_i, float* out_d,
                  int32_t* out_i, cudaStream_t st);
 // Table preparation (finalize).

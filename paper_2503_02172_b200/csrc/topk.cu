@@ -303,7 +303,8 @@ constexpr int kCandCap = 256;
 __global__ void __launch_bounds__(32 * kCminWarps)
     k_topk_cmin(const float* __restrict__ dist, int64_t ldd, const float* __restrict__ cmin, int64_t ldc,
                 int64_t n, int k, int64_t id_base, const int32_t* __restrict__ invalid,
-                const int32_t* __restrict__ out_row, float* __restrict__ od, int32_t* __restrict__ oi, int B) {
+                const int32_t* __restrict__ out_row, float* __restrict__ od, int32_t* __restrict__ oi, int B,
+                const PeerPush pp) {
   pdl_grid_sync();
   __shared__ float wtau[kCminWarps];
   __shared__ unsigned long long cand[kCandCap];
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(32 * kCminWarps)
       od[lane] = kNaN;
       oi[lane] = -1;
     }
+    if (wid == 0 && pp.on()) peer_push_warp(pp, ob, k, ~0ull, lane);  // N2: fused all-gather
     return;
   }
   if (threadIdx.x == 0) ncand = 0;
@@ -394,16 +396,20 @@ __global__ void __launch_bounds__(32 * kCminWarps)
     for (int t = nc + threadIdx.x; t < P; t += blockDim.x) cand[t] = ~0ull;
     __syncthreads();
     bitonic_sort_u64(cand, P);
+    unsigned long long gk = ~0ull;  // (key, global id) of output j = threadIdx.x
     if (threadIdx.x < k) {
       const unsigned long long key = cand[threadIdx.x];
       if (key == ~0ull) {  // fewer than k entries
         od[threadIdx.x] = kNaN;
         oi[threadIdx.x] = -1;
       } else {
+        const uint32_t gid = (uint32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
         od[threadIdx.x] = fkey_inv((uint32_t)(key >> 32));
-        oi[threadIdx.x] = (int32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
+        oi[threadIdx.x] = (int32_t)gid;
+        gk = (key & 0xFFFFFFFF00000000ull) | gid;
       }
     }
+    if (wid == 0 && pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
     return;
   }
   // ---- overflow (more than kCandCap entries <= tau): register-list scan by warp 0 ----
@@ -430,30 +436,35 @@ __global__ void __launch_bounds__(32 * kCminWarps)
       }
     }
   }
-  if (lane >= k) return;
-  if (lk == ~0ull) {
-    od[lane] = kNaN;
-    oi[lane] = -1;
-  } else {
-    od[lane] = fkey_inv((uint32_t)(lk >> 32));
-    oi[lane] = (int32_t)(id_base + (int64_t)(uint32_t)(lk & 0xFFFFFFFFu));
+  unsigned long long gk = ~0ull;
+  if (lane < k) {
+    if (lk == ~0ull) {
+      od[lane] = kNaN;
+      oi[lane] = -1;
+    } else {
+      const uint32_t gid = (uint32_t)(id_base + (int64_t)(uint32_t)(lk & 0xFFFFFFFFu));
+      od[lane] = fkey_inv((uint32_t)(lk >> 32));
+      oi[lane] = (int32_t)gid;
+      gk = (lk & 0xFFFFFFFF00000000ull) | gid;
+    }
   }
+  if (pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
 }
 
 int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                      int k, int64_t id_base, const int32_t* invalid, float* out_d, int32_t* out_i,
-                     cudaStream_t st) {
+                     cudaStream_t st, const PeerPush& pp) {
   launch_pdl(k_topk_cmin, dim3(B), dim3(32 * kCminWarps), 0, st, dist, ldd, cmin, ldc, n, k, id_base, invalid,
-             (const int32_t*)nullptr, out_d, out_i, B);
+             (const int32_t*)nullptr, out_d, out_i, B, pp);
   return 1;
 }
 
 int launch_topk_cmin_map(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                          int k, int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d,
-                         int32_t* out_i, cudaStream_t st) {
+                         int32_t* out_i, cudaStream_t st, const PeerPush& pp) {
   if (B <= 0) return 0;
   launch_pdl(k_topk_cmin, dim3(B), dim3(32 * kCminWarps), 0, st, dist, ldd, cmin, ldc, n, k, id_base, invalid,
-             out_row, out_d, out_i, B);
+             out_row, out_d, out_i, B, pp);
   return 1;
 }
 

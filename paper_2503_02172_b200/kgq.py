@@ -37,7 +37,7 @@ EXPORTS = (
     "kgq_shard_end", "kgq_load_entities", "kgq_load_relations", "kgq_load_linear",
     "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_submit_mixed", "kgq_query_embedding", "kgq_merge_topk",
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
-    "kgq_profile_read", "kgq_rank_answers",
+    "kgq_profile_read", "kgq_rank_answers", "kgq_peer_bytes", "kgq_set_peers", "kgq_merge_peers",
 )
 RANK_LOCAL, RANK_DIST, RANK_COUNT = 0, 1, 2
 
@@ -83,6 +83,9 @@ _sig = {
     "kgq_entity_terms": (_I32, [_P, _P, _P]),
     "kgq_profile_enable": (_I32, [_P, _I32]),
     "kgq_rank_answers": (_I32, [_P, _I32, _I32, _P, _P, _P, _P, _I32, _I32, _P, _P, _P]),
+    "kgq_peer_bytes": (_I64, [_P, _I32]),
+    "kgq_set_peers": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),
+    "kgq_merge_peers": (_I32, [_P, _I32, _I32, _P, _P, _P]),
     "kgq_profile_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                               ctypes.POINTER(ctypes.c_double)]),
 }
@@ -284,6 +287,31 @@ class Engine:
                                         _ptr(parts_id.contiguous()), _ptr(od), _ptr(oi),
                                         _stream(stream)))
         return od, oi
+
+    # ---- N2: fused top-k all-gather over peer memory (kgq_set_peers / kgq_merge_peers) ----
+    def peer_bytes(self, world):
+        """Size in bytes of this context's per-rank peer buffer for `world` ranks."""
+        n = int(_lib.kgq_peer_bytes(self._h, world))
+        if n < 0:
+            raise KgqError(-1, f"kgq_peer_bytes: bad world {world}")
+        return n
+
+    def set_peers(self, rank, world, ptrs):
+        """Registers every rank's peer buffer (device addresses, this context = rank); world 0
+        turns the push off."""
+        arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[int(p) for p in ptrs])
+        self._check(_lib.kgq_set_peers(self._h, rank, world, arr if world else None))
+
+    def merge_peers(self, batch, k, out=None, stream=None):
+        """Waits for every rank's push of the current submit and merges: (dist, ids) [batch, k]."""
+        import torch
+        if out is None:
+            td = torch.empty((batch, k), dtype=torch.float32, device=f"cuda:{self.device}")
+            ti = torch.empty((batch, k), dtype=torch.int32, device=f"cuda:{self.device}")
+        else:
+            td, ti = out
+        self._check(_lib.kgq_merge_peers(self._h, batch, k, _ptr(td), _ptr(ti), _stream(stream)))
+        return td, ti
 
     def rank_answers(self, structure, anchors, rels, ans_off, ans_id, mode=RANK_LOCAL,
                      ans_dist=None, stream=None):

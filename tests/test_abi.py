@@ -71,3 +71,13 @@ def test_create_rejects_bad_config_without_crashing():
 def test_sass_is_sm100a():
     out = os.popen(f"cuobjdump -lelf {kgq.LIB_PATH} 2>&1").read()
     assert "sm_100a" in out
+
+
+def test_peer_entry_points_validate_without_a_gpu():
+    """N2 host-side argument handling: NULL context, and the ShardedEngine merge switch."""
+    assert kgq._lib.kgq_peer_bytes(None, 2) == -1
+    assert kgq._lib.kgq_set_peers(None, 0, 2, None) == 1  # KGQ_EINVAL
+    assert kgq._lib.kgq_merge_peers(None, 4, 5, None, None, None) == 1
+    from paper_2503_02172_b200.sharded import ShardedEngine
+    with pytest.raises(ValueError, match="merge"):
+        ShardedEngine("betae", 100, 5, 8, merge="allreduce")
