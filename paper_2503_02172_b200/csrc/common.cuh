@@ -102,30 +102,65 @@ __device__ __forceinline__ float beta_reg(float y) {  // Q2/Q12: clamp(y + 1, 0.
   return fminf(fmaxf(y + 1.0f, 0.05f), 1e9f);
 }
 
-// ln Gamma(y) for y >= 8 by the Stirling series through y^-13 (the first dropped term is
-// < 1e-15 there): (y - 1/2) ln y - y + ln(2 pi)/2 + sum_k B_2k / (2k (2k-1) y^(2k-1)).
-__device__ __forceinline__ double lgamma_stirling8(double y) {
-  const double r = 1.0 / y, z = r * r;
-  const double s = r * (1.0 / 12 + z * (-1.0 / 360 + z * (1.0 / 1260 + z * (-1.0 / 1680 +
-                   z * (1.0 / 1188 + z * (-691.0 / 360360 + z * (1.0 / 156)))))));
-  return (y - 0.5) * log(y) - y + 0.91893853320467274178 + s;
+// fp64 reciprocal: fp32 seed + two Newton steps (2^-23 -> 2^-46 -> ~2^-92: within an ulp);
+// x normal and inside the fp32 range
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r = (double)__frcp_rn((float)x);
+  r = r * (2.0 - x * r);
+  r = r * (2.0 - x * r);
+  return r;
 }
-// Shift x > 0 up to y = x + n >= 8: ln Gamma(x) = ln Gamma(y) - ln(x (x+1) ... (x+n-1)); the
-// product is returned in *p (multiplied into it), y as the result.
-__device__ __forceinline__ double lgamma_shift8(double x, double* p) {
-  while (x < 8.0) {
-    *p *= x;
-    x += 1.0;
+// fp64 natural log for normal x > 0 without libdevice's special-case handling: x = 2^e m,
+// m in [sqrt(1/2), sqrt(2)), ln m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, odd series
+// through s^19 (truncation < 4e-16 relative).
+__device__ __forceinline__ double log_pos(double x) {
+  int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  int e = (hi >> 20) - 1023;
+  hi = (hi & 0x000FFFFF) | 0x3FF00000;
+  double m = __hiloint2double(hi, lo);
+  if (m > 1.4142135623730951) {
+    m *= 0.5;
+    e += 1;
   }
-  return x;
+  const double f = m - 1.0, den = m + 1.0;
+  const double r = rcp_nr(den);
+  double sq = f * r;
+  sq = sq + r * (f - sq * den);  // residual correction of the quotient
+  const double z = sq * sq;
+  const double p = 1.0 / 3 + z * (1.0 / 5 + z * (1.0 / 7 + z * (1.0 / 9 + z * (1.0 / 11 + z * (1.0 / 13 +
+                   z * (1.0 / 15 + z * (1.0 / 17 + z * (1.0 / 19))))))));
+  return (double)e * 0.69314718055994530942 + (2.0 * sq + 2.0 * sq * z * p);
 }
-// ln B(a, b) = ln Gamma(a) + ln Gamma(b) - ln Gamma(a + b) for a, b > 0 (Eq. 3): three
-// Stirling evaluations and ONE log of the combined shift products -- ~4x fewer instructions
-// than three libdevice lgamma calls (the query-side P_q precompute of the tensor-core scorer).
+// ln B(a, b) = ln Gamma(a) + ln Gamma(b) - ln Gamma(a + b) for a, b > 0 (Eq. 3), the
+// query-side P_q precompute of the tensor-core scorer.  ln Gamma(y) for y >= 8 by Stirling:
+// (y - 1/2) ln y - y + ln(2 pi)/2 + sum_k B_2k / (2k (2k-1) y^(2k-1)).  Branch-free: every argument x is shifted
+// by exactly 8 (y = x + 8 >= 8, ln Gamma(x) = ln Gamma(y) - ln(x (x+1) ... (x+7))), Stirling's
+// series at y through y^-9 (truncation <= 691/360360 y^-11 ~ 2e-13 at y = 8), one reciprocal for
+// the three series, and ONE log of the combined shift-product ratio.  Against libdevice lgamma:
+// scripts/lnb_check.cu (same ~1e-5 relative cancellation limit when one argument is > 1e8 and
+// the other O(0.1), where the libdevice formula loses the same digits).
 __device__ __forceinline__ double lnbeta_f64(double a, double b) {
-  double pa = 1.0, pb = 1.0, pab = 1.0;
-  const double ya = lgamma_shift8(a, &pa), yb = lgamma_shift8(b, &pb), yab = lgamma_shift8(a + b, &pab);
-  return lgamma_stirling8(ya) + lgamma_stirling8(yb) - lgamma_stirling8(yab) + log(pab / (pa * pb));
+  const double c = a + b;
+  double pa = a, pb = b, pc = c;
+#pragma unroll
+  for (int i = 1; i < 8; ++i) {
+    pa *= a + i;
+    pb *= b + i;
+    pc *= c + i;
+  }
+  const double ya = a + 8.0, yb = b + 8.0, yc = c + 8.0;
+  const double yab = ya * yb;
+  const double rall = rcp_nr(yab * yc);  // <= (2e9 + 8)^3: inside the fp32 seed range
+  const double ra = rall * yb * yc, rb = rall * ya * yc, rc = rall * yab;
+  auto ser = [](double r) {
+    const double z = r * r;
+    return r * (1.0 / 12 + z * (-1.0 / 360 + z * (1.0 / 1260 + z * (-1.0 / 1680 + z * (1.0 / 1188)))));
+  };
+  const double pab = pa * pb;
+  const double ratio = pab < 1e30 ? pc * rcp_nr(pab) : pc / pab;
+  return (ya - 0.5) * log_pos(ya) + (yb - 0.5) * log_pos(yb) - (yc - 0.5) * log_pos(yc) - ya - yb + yc +
+         0.91893853320467274178 + ser(ra) + ser(rb) - ser(rc) + log_pos(ratio);
 }
 
 // fp64 digamma: recurrence psi(x) = psi(x+1) - 1/x up to x >= 10, then the asymptotic

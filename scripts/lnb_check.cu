@@ -32,7 +32,7 @@ int main() {
       if (rel > mxr) mxr = rel;
       if (e > mx) mx = e;
     }
-    printf("lnbeta_f64 vs libdevice lgamma, (a, b) log-uniform in [0.01, %g]: max |diff| %.3e, max |diff|/max(1,|lnB|) %.3e\n",
+    printf("lnbeta_f64 (shift-8, log_pos) vs libdevice lgamma, (a, b) log-uniform in [0.01, %g]: max |diff| %.3e, max |diff|/max(1,|lnB|) %.3e\n",
            h ? 1e9 : 1e4, mx, mxr);
   }
   return 0;
