@@ -71,37 +71,63 @@ int launch_translate_chain(const ChainArgs& a, const float* ent, const float* re
 }
 
 // ---- BetaE MLP input: z = [alpha; beta; R[r]] (Eq. 4 var_S with the relation, Q3) -------
-// Group row g*B + b of Z; source = regularised anchor row or split state row.
+// Group row g*B + b of Z; source = regularised anchor row or split state row.  One warp per
+// row, 16-byte loads and 8-byte plane stores (d % 4 == 0 and every row stride % 8 == 0, so
+// rows are 16-byte aligned).
+__device__ __forceinline__ void store_split4(const Split& z, int64_t i, float4 x) {
+  __nv_bfloat16 a[4], b[4], c[4];
+  split3(x.x, a[0], b[0], c[0]);
+  split3(x.y, a[1], b[1], c[1]);
+  split3(x.z, a[2], b[2], c[2]);
+  split3(x.w, a[3], b[3], c[3]);
+  *reinterpret_cast<uint2*>(z.b0 + i) = make_uint2(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]));
+  *reinterpret_cast<uint2*>(z.b1 + i) = make_uint2(pack_bf16(b[0], b[1]), pack_bf16(b[2], b[3]));
+  *reinterpret_cast<uint2*>(z.b2 + i) = make_uint2(pack_bf16(c[0], c[1]), pack_bf16(c[2], c[3]));
+}
+constexpr int kMlpInRows = 4;  // rows (warps) per block
 __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
                                   const float* __restrict__ rel, int B, MlpGroup g, Split src,
                                   Split z, int with_rel) {
   pdl_grid_sync();
-  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kMlpInRows + (threadIdx.x >> 5);
   const int gi = blockIdx.y;
+  if (b >= B) return;
   const int d = a.d;
   const int rslot = g.rel_slot[gi];
-  const int rid = checked_id(a.rels[(int64_t)b * a.n_r + rslot], a.n_relation, a.err,
-                             a.invalid, b, rslot, 1);
-  int aid = 0;
-  const bool from_anchor = g.anchor_slot[gi] >= 0;
-  if (from_anchor)
-    aid = checked_id(a.anchors[(int64_t)b * a.n_a + g.anchor_slot[gi]], a.n_entity, a.err,
-                     a.invalid, b, g.anchor_slot[gi], 0);
-  const int64_t zrow = ((int64_t)gi * B + b) * z.ld;
-  const int64_t srow = (g.src_row[gi] + b) * src.ld;
-  for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
-    float x = from_anchor ? ent[(int64_t)aid * 2 * d + j] : load_split(src, srow + j);
-    store_split(z, zrow + j, x);
+  int rid = a.rels[(int64_t)b * a.n_r + rslot];
+  if (rid < 0 || rid >= a.n_relation) {
+    if (lane == 0) report_range(a.err, a.invalid, b, rslot, 1);
+    rid = 0;
   }
-  if (with_rel)
-    for (int j = threadIdx.x; j < d; j += blockDim.x)
-      store_split(z, zrow + 2 * d + j, rel[(int64_t)rid * d + j]);
+  const int aslot = g.anchor_slot[gi];
+  const int64_t zrow = ((int64_t)gi * B + b) * z.ld;
+  if (aslot >= 0) {
+    int aid = a.anchors[(int64_t)b * a.n_a + aslot];
+    if (aid < 0 || aid >= a.n_entity) {
+      if (lane == 0) report_range(a.err, a.invalid, b, aslot, 0);
+      aid = 0;
+    }
+    const float4* er = reinterpret_cast<const float4*>(ent + (int64_t)aid * 2 * d);
+    for (int j = lane; j < (2 * d) / 4; j += 32) store_split4(z, zrow + 4 * j, __ldg(er + j));
+  } else {  // split -> split: plane copies (exact)
+    const int64_t srow = (g.src_row[gi] + b) * src.ld;
+    for (int p = 0; p < 3; ++p) {
+      const uint2* sp = reinterpret_cast<const uint2*>(src.plane(p) + srow);
+      uint2* dp = reinterpret_cast<uint2*>(z.plane(p) + zrow);
+      for (int j = lane; j < (2 * d) / 4; j += 32) dp[j] = sp[j];
+    }
+  }
+  if (with_rel) {
+    const float4* rr = reinterpret_cast<const float4*>(rel + (int64_t)rid * d);
+    for (int j = lane; j < d / 4; j += 32) store_split4(z, zrow + 2 * d + 4 * j, __ldg(rr + j));
+  }
 }
 
 int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* rel, int B,
                            const MlpGroup& g, Split src, Split z, cudaStream_t st, bool with_rel) {
-  dim3 grid(B, g.n);
-  launch_pdl(k_betae_mlp_input, grid, dim3(128), 0, st, a, ent, rel, B, g, src, z, with_rel ? 1 : 0);
+  dim3 grid((B + kMlpInRows - 1) / kMlpInRows, g.n);
+  launch_pdl(k_betae_mlp_input, grid, dim3(32 * kMlpInRows), 0, st, a, ent, rel, B, g, src, z, with_rel ? 1 : 0);
   return 1;
 }
 

@@ -15,3 +15,11 @@ da, dr = torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda()
 for _ in range(4):
     e.submit(s, da, dr, K)
 torch.cuda.synchronize()
+if len(sys.argv) > 2 and sys.argv[2] == "time":
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        e.submit(s, da, dr, K)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{s}: {e0.elapsed_time(e1) * 1e3 / 20:.1f} us per submit (graph replay, warm L2), launches {e.last_launch_count()}")
