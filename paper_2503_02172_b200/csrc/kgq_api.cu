@@ -325,7 +325,7 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
 
 // Operator chain for one batch: writes ctx->Q [B, n_out, qw].
 int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t* rels,
-              cudaStream_t st) {
+              cudaStream_t st, bool want_q = true) {
   const Plan* P = plan_of(s);
   const int model = ctx->cfg.model;
   const int d = ctx->cfg.dim;
@@ -390,7 +390,7 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
       br = e;
     }
   }
-  if (P->kind != kInter) return L + launch_state_to_q(ctx->S, P->n_out, B, 2 * d, ctx->Q, st);
+  if (P->kind != kInter) return want_q ? L + launch_state_to_q(ctx->S, P->n_out, B, 2 * d, ctx->Q, st) : L;
   // intersection (Q6): attention over [alpha_i; beta_i] (2d -> 2d -> d), shared weights a_i
   L += dense(ctx, ctx->S, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
   L += dense(ctx, ctx->I, (int)M, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone, ctx->T, ctx->tw, st);
@@ -412,7 +412,17 @@ int run_chain(kgq_ctx* ctx, int s, int B, const int32_t* anchors, const int32_t*
     L += betae_hop(ctx, cb, B, p, 0, 1, pproj, pneg, src, 0, st);
     src = ctx->S;
   }
-  return L + launch_state_to_q(ctx->S, 1, B, 2 * d, ctx->Q, st);
+  return want_q ? L + launch_state_to_q(ctx->S, 1, B, 2 * d, ctx->Q, st) : L;
+}
+
+// True when every chunk of a BetaE batch of B queries is scored on the tensor cores and the
+// chain's final state stays in the split state rows S (no intersection as the last operator):
+// the scorer's prep then reads S directly and the chain skips the fp32 Q copy.
+static bool q_in_state(const kgq_ctx* ctx, const Plan* P, int B) {
+  if (ctx->cfg.model != KGQ_BETAE || (P->kind == kInter && P->npost == 0)) return false;
+  for (int64_t b0 = 0; b0 < B; b0 += ctx->bchunk)
+    if (score_uses_stream(KGQ_BETAE, P->n_out, (int)std::min<int64_t>(ctx->bchunk, B - b0))) return false;
+  return true;
 }
 
 kgq_status check_submit(kgq_ctx* ctx, int32_t s, int32_t batch, int32_t k, bool need_k) {
@@ -711,11 +721,19 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
 
 // Distances of query rows [b0, b0 + nb) (chain already run) to every entity of the shard,
 // into ctx->dist rows [0, nb).  Returns the number of kernels launched.
-static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStream_t st) {
+static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStream_t st, int B = 0,
+                      bool from_state = false) {
   const kgq_config& c = ctx->cfg;
   int L = 0;
   const float* qb = ctx->Q + b0 * P->n_out * ctx->qw;
-  if (c.model == KGQ_BETAE && !score_uses_stream(c.model, P->n_out, nb)) {
+  if (from_state) {  // BetaE, query state still in S (q_in_state): prep straight from the split rows
+    StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
+    L += launch_mix_score_prep(nullptr, ctx->S, nb * P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc, ctx->Ptc,
+                               st, B, b0, P->n_out);
+    L += launch_score_tc_gemm(nb * P->n_out, P->n_out, c.dim, ctx->Atc, ctx->Ptc, ctx->uv, ctx->Esum, ctx->np,
+                              ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, ctx->ns, &ctx->gws, st);
+    check_site("tensor-core scorer");
+  } else if (c.model == KGQ_BETAE && !score_uses_stream(c.model, P->n_out, nb)) {
     // past the HBM ridge BetaE scoring is a dense contraction: tensor cores (score_tc.cu)
     StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
     L += launch_score_betae_tc(qb, nb * P->n_out, P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc,
@@ -741,14 +759,15 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
   int L = 0;
   const bool push = ctx->peers.on() && ctx->push_row0 >= 0;  // N2: fused all-gather of the top-k
   CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)B * sizeof(int32_t), st), "reset flags");
+  const bool from_state = q_in_state(ctx, P, B);
   {
     StageTimer t(ctx, st, kStChain);
-    L += run_chain(ctx, s, B, anchors, rels, st);
+    L += run_chain(ctx, s, B, anchors, rels, st, !from_state);
   }
   check_site("operator chain");
   for (int64_t b0 = 0; b0 < B; b0 += ctx->bchunk) {
     const int nb = (int)std::min<int64_t>(ctx->bchunk, B - b0);
-    L += score_rows(ctx, P, b0, nb, st);
+    L += score_rows(ctx, P, b0, nb, st, B, from_state);
     {
       StageTimer t(ctx, st, kStTopk);
       // the tensor-core scorer's epilogue wrote 32-entity block minima: pruned top-k
@@ -1346,10 +1365,11 @@ kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_
   const Plan* P = plan_of(s);
   int L = 0;
   CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)batch * sizeof(int32_t), cs), "reset flags");
-  L += run_chain(ctx, s, batch, anchors, rels, cs);
+  const bool from_state = q_in_state(ctx, P, batch);
+  L += run_chain(ctx, s, batch, anchors, rels, cs, !from_state);
   for (int64_t b0 = 0; b0 < batch; b0 += ctx->bchunk) {
     const int nb = (int)std::min<int64_t>(ctx->bchunk, batch - b0);
-    L += score_rows(ctx, P, b0, nb, cs);
+    L += score_rows(ctx, P, b0, nb, cs, batch, from_state);
     if (mode != KGQ_RANK_COUNT)
       L += launch_answer_dist(ctx->dist, ctx->np, ctx->e0, ctx->ns, (int)b0, nb, ans_off, ans_id, ans_dist, cs);
     if (mode != KGQ_RANK_DIST)

@@ -231,9 +231,10 @@ int launch_mix_gather(const MixSegs& sg, int M, const float* ent, Split S, Split
                       int64_t n_entity, int n_relation, int32_t* err, int32_t* invalid, cudaStream_t st);
 // batch rows [dst0 + b] of src -> S rows src0 + b (width w)
 int launch_mix_scatter(const MixSegs& sg, int M, Split src, Split S, int w, cudaStream_t st);
-// score rows r: A[r] = S[srcrow[r]] (split copy) and P_q (fp64, as k_score_prep_tc)
+// score rows r: A[r] = S[srcrow[r]] (split copy) and P_q (fp64, as k_score_prep_tc); srcrow
+// nullptr: row r of a single-structure chunk = state row (r % nout) * B + b0 + r / nout
 int launch_mix_score_prep(const int64_t* srcrow, Split S, int rows, int d, const double* sums, int64_t ns,
-                          Split A, float2* P, cudaStream_t st);
+                          Split A, float2* P, cudaStream_t st, int64_t B = 0, int64_t b0 = 0, int nout = 1);
 // tensor-core score GEMM only (A and P prepared): dist rows = rows / nbq
 int launch_score_tc_gemm(int rows, int nbq, int d, Split A, const float2* P, const Split& uv, const float2* Esum,
                          int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,

@@ -112,14 +112,18 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
 // shard's real entities (columns < nvalid): cmin[row][n / 32].  The top-k reads these block
 // minima first and scans only the blocks that can hold one of the k best (k_topk_cmin).
 // Mixed batches: score row r is the split state row srcrow[r] of S (no fp32 round trip).
+// Single-structure submits (srcrow == nullptr): score row r of the chunk starting at query b0 is
+// branch r % nout of query b0 + r / nout, i.e. state row (r % nout) * B + b0 + r / nout.
 __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, int d,
-                                 const double* __restrict__ sums, int64_t ns, Split A, float2* __restrict__ P) {
+                                 const double* __restrict__ sums, int64_t ns, Split A, float2* __restrict__ P,
+                                 int64_t B, int64_t b0, int nout) {
   pdl_grid_sync();
   const int r = blockIdx.x;
   __shared__ double red[32];
   double p = 0.0;
   const double inv = 1.0 / (double)ns;
-  const int64_t s0 = srcrow[r] * S.ld, a0 = (int64_t)r * A.ld;
+  const int64_t srow = srcrow ? srcrow[r] : (int64_t)(r % nout) * B + b0 + r / nout;
+  const int64_t s0 = srow * S.ld, a0 = (int64_t)r * A.ld;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     const float a = load_split(S, s0 + j), b = load_split(S, s0 + d + j);
     store_split(A, a0 + j, a);
@@ -209,9 +213,9 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
 }
 
 int launch_mix_score_prep(const int64_t* srcrow, Split S, int rows, int d, const double* sums, int64_t ns,
-                          Split A, float2* P, cudaStream_t st) {
+                          Split A, float2* P, cudaStream_t st, int64_t B, int64_t b0, int nout) {
   if (rows <= 0) return 0;
-  launch_pdl(k_mix_score_prep, dim3(rows), dim3(128), 0, st, srcrow, S, d, sums, ns, A, P);
+  launch_pdl(k_mix_score_prep, dim3(rows), dim3(128), 0, st, srcrow, S, d, sums, ns, A, P, B, b0, nout);
   return 1;
 }
 
