@@ -322,6 +322,17 @@ int launch_branch_mean(const float* T, int64_t ldt, int nb, int B, int d, Split 
 // GQE: x = state[:, :d].  BetaE: the same a_i weights alpha (cols [0,d)) and beta ([d,2d)).
 // Q2B: centre as GQE; offset o = min_i o_i * sigmoid(G) (gate logits G [B, d]).
 // Post projection (ip): + R[r] on the centre (GQE/Q2B; Q2B offset + R_o[r]).
+__device__ __forceinline__ float4 load_split4(const Split& s, int64_t i) {  // i % 4 == 0
+  const uint2 a = *reinterpret_cast<const uint2*>(s.b0 + i);
+  const uint2 b = *reinterpret_cast<const uint2*>(s.b1 + i);
+  const uint2 c = *reinterpret_cast<const uint2*>(s.b2 + i);
+  auto lo = [](uint32_t u) { return __uint_as_float(u << 16); };
+  auto hi = [](uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); };
+  return make_float4((lo(a.x) + lo(b.x)) + lo(c.x), (hi(a.x) + hi(b.x)) + hi(c.x),
+                     (lo(a.y) + lo(b.y)) + lo(c.y), (hi(a.y) + hi(b.y)) + hi(c.y));
+}
+// One query per block; each thread owns 4 consecutive dimensions (d % 4 == 0, all row strides
+// % 8 == 0: 16-byte logit / gate / relation loads, 8-byte plane loads and stores).
 __device__ __forceinline__ void combine_query(const CombineArgs& c, const Split& S, const float* __restrict__ logits,
                                               const float* __restrict__ gate, const Split& out,
                                               float* __restrict__ q, int b) {
@@ -332,47 +343,83 @@ __device__ __forceinline__ void combine_query(const CombineArgs& c, const Split&
   if (c.post_slot >= 0)
     rid = checked_id(c.rels[(int64_t)b * c.n_r + c.post_slot], c.n_relation, c.err, c.invalid,
                      b, c.post_slot, 1);
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float l[kMaxBranches];
-    float m = -INFINITY;
-    for (int i = 0; i < nb; ++i) {
-      l[i] = logits[((int64_t)i * B + b) * c.ldl + j];
-      m = fmaxf(m, l[i]);
+  for (int j = 4 * threadIdx.x; j < d; j += 4 * blockDim.x) {
+    float l[kMaxBranches][4];
+    float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int i = 0; i < kMaxBranches; ++i) {  // unrolled: l stays in registers
+      if (i >= nb) break;
+      const float4 v = *reinterpret_cast<const float4*>(logits + ((int64_t)i * B + b) * c.ldl + j);
+      l[i][0] = v.x; l[i][1] = v.y; l[i][2] = v.z; l[i][3] = v.w;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m[u] = fmaxf(m[u], l[i][u]);
     }
-    float s = 0.0f;
-    for (int i = 0; i < nb; ++i) {
-      l[i] = expf(l[i] - m);
-      s += l[i];
-    }
-    const float inv = 1.0f / s;
-    float x0 = 0.0f, x1 = 0.0f, omin = INFINITY;
-    for (int i = 0; i < nb; ++i) {
+    float sum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int i = 0; i < kMaxBranches; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i >= nb) break;
+        l[i][u] = expf(l[i][u] - m[u]);
+        sum[u] += l[i][u];
+      }
+    float inv[4], x0[4] = {0.0f, 0.0f, 0.0f, 0.0f}, x1[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float omin[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) inv[u] = 1.0f / sum[u];
+#pragma unroll
+    for (int i = 0; i < kMaxBranches; ++i) {
+      if (i >= nb) break;
       const int64_t row = ((int64_t)i * B + b) * S.ld;
-      const float a = l[i] * inv;
-      x0 += a * load_split(S, row + j);
-      if (c.model == KGQ_BETAE) x1 += a * load_split(S, row + d + j);
-      if (c.model == KGQ_Q2B) omin = fminf(omin, load_split(S, row + q2b_off(d) + j));
+      const float4 s0 = load_split4(S, row + j);
+      const float v0[4] = {s0.x, s0.y, s0.z, s0.w};
+      float v1[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (c.model == KGQ_BETAE) {
+        const float4 s1 = load_split4(S, row + d + j);
+        v1[0] = s1.x; v1[1] = s1.y; v1[2] = s1.z; v1[3] = s1.w;
+      }
+      if (c.model == KGQ_Q2B) {
+        const float4 o = load_split4(S, row + q2b_off(d) + j);
+        const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) omin[u] = fminf(omin[u], ov[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = l[i][u] * inv[u];
+        x0[u] += a * v0[u];
+        if (c.model == KGQ_BETAE) x1[u] += a * v1[u];
+      }
     }
     if (c.model == KGQ_Q2B) {
-      const float g = gate[(int64_t)b * c.ldg + j];
-      x1 = omin * (1.0f / (1.0f + expf(-g)));
+      const float4 g = *reinterpret_cast<const float4*>(gate + (int64_t)b * c.ldg + j);
+      const float gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x1[u] = omin[u] * (1.0f / (1.0f + expf(-gv[u])));
     }
     if (c.post_slot >= 0) {
-      x0 += c.rel[(int64_t)rid * d + j];
-      if (c.model == KGQ_Q2B) x1 += c.rel_off[(int64_t)rid * d + j];
+      const float4 r0 = *reinterpret_cast<const float4*>(c.rel + (int64_t)rid * d + j);
+      x0[0] += r0.x; x0[1] += r0.y; x0[2] += r0.z; x0[3] += r0.w;
+      if (c.model == KGQ_Q2B) {
+        const float4 r1 = *reinterpret_cast<const float4*>(c.rel_off + (int64_t)rid * d + j);
+        x1[0] += r1.x; x1[1] += r1.y; x1[2] += r1.z; x1[3] += r1.w;
+      }
     }
     if (c.negate_out) {  // De Morgan union: N(I(...)), alpha -> 1/alpha, beta -> 1/beta (Q5)
-      x0 = 1.0f / x0;
-      x1 = 1.0f / x1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = 1.0f / x0[u];
+        x1[u] = 1.0f / x1[u];
+      }
     }
     const bool two = c.model != KGQ_GQE;
     if (out.valid()) {
-      store_split(out, (int64_t)b * out.ld + j, x0);
-      if (two) store_split(out, (int64_t)b * out.ld + d + j, x1);
+      store_split4(out, (int64_t)b * out.ld + j, make_float4(x0[0], x0[1], x0[2], x0[3]));
+      if (two) store_split4(out, (int64_t)b * out.ld + d + j, make_float4(x1[0], x1[1], x1[2], x1[3]));
     } else {
       float* dst = q + (int64_t)b * (two ? 2 * d : d);
-      dst[j] = x0;
-      if (two) dst[d + j] = x1;
+      *reinterpret_cast<float4*>(dst + j) = make_float4(x0[0], x0[1], x0[2], x0[3]);
+      if (two) *reinterpret_cast<float4*>(dst + d + j) = make_float4(x1[0], x1[1], x1[2], x1[3]);
     }
   }
 }

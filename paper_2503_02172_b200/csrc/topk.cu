@@ -391,25 +391,47 @@ __global__ void __launch_bounds__(32 * kCminWarps)
   __syncthreads();
   const int nc = ncand;
   if (nc <= kCandCap) {
-    int P = 32;
-    while (P < nc) P <<= 1;
-    for (int t = nc + threadIdx.x; t < P; t += blockDim.x) cand[t] = ~0ull;
-    __syncthreads();
-    bitonic_sort_u64(cand, P);
-    unsigned long long gk = ~0ull;  // (key, global id) of output j = threadIdx.x
-    if (threadIdx.x < k) {
-      const unsigned long long key = cand[threadIdx.x];
+    // k smallest of <= 256 distinct (key, id) candidates by warp 0: each lane keeps up to 8 in
+    // registers; k rounds of warp arg-min, the owner drops its winner (no block-wide sort)
+    if (wid != 0) return;
+    unsigned long long v[kCandCap / 32];
+#pragma unroll
+    for (int m = 0; m < kCandCap / 32; ++m) v[m] = lane + 32 * m < nc ? cand[lane + 32 * m] : ~0ull;
+    unsigned long long mine = ~0ull;
+#pragma unroll
+    for (int m = 0; m < kCandCap / 32; ++m) mine = v[m] < mine ? v[m] : mine;
+    unsigned long long key = ~0ull;  // output j = lane
+    for (int j = 0; j < k; ++j) {
+      unsigned long long w = mine;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, w, o);
+        w = t < w ? t : w;
+      }
+      if (lane == j) key = w;
+      if (w == ~0ull) break;  // fewer than k candidates: the rest stay empty
+      if (mine == w) {        // keys are unique (ids): exactly one lane owns w
+        mine = ~0ull;
+#pragma unroll
+        for (int m = 0; m < kCandCap / 32; ++m) {
+          if (v[m] == w) v[m] = ~0ull;
+          mine = v[m] < mine ? v[m] : mine;
+        }
+      }
+    }
+    unsigned long long gk = ~0ull;  // (key, global id) of output j = lane
+    if (lane < k) {
       if (key == ~0ull) {  // fewer than k entries
-        od[threadIdx.x] = kNaN;
-        oi[threadIdx.x] = -1;
+        od[lane] = kNaN;
+        oi[lane] = -1;
       } else {
         const uint32_t gid = (uint32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
-        od[threadIdx.x] = fkey_inv((uint32_t)(key >> 32));
-        oi[threadIdx.x] = (int32_t)gid;
+        od[lane] = fkey_inv((uint32_t)(key >> 32));
+        oi[lane] = (int32_t)gid;
         gk = (key & 0xFFFFFFFF00000000ull) | gid;
       }
     }
-    if (wid == 0 && pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
+    if (pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
     return;
   }
   // ---- overflow (more than kCandCap entries <= tau): register-list scan by warp 0 ----
