@@ -716,16 +716,29 @@ struct Plan {
   int bn, full, s_tail, kper;
 };
 constexpr int kTileBN[4] = {64, 128, 192, 256};
+struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN, KGQ_GEMM_KB128
+  int force_bn = 0;
+  double kb128 = 0.0;
+  PlanKnobs() {
+    const char* e = getenv("KGQ_GEMM_BN");
+    if (e) force_bn = atoi(e);
+    e = getenv("KGQ_GEMM_KB128");
+    if (e) kb128 = atof(e);
+  }
+};
 inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split) {
+  static const PlanKnobs knobs;
   const int64_t pairs_m = (M + 2 * BM - 1) / (2 * BM);
   const int nk = (int)((K + BK - 1) / BK);
   const double kEpi = 5900.0, kPublish = 5900.0, kPartial = 4900.0;  // clk
   Plan best{kTileBN[0], 0, 1, nk};
   double best_cost = 1e300;
   for (int bn : kTileBN) {
+    if (knobs.force_bn && bn != knobs.force_bn) continue;
     const int64_t tiles = pairs_m * ((N + bn - 1) / bn);
     const int64_t full = tiles / kClustersMax * kClustersMax, tail = tiles - full;
-    const double kb = fmax((128.0 + bn / 2) * 5.1, 6.7 * bn);
+    double kb = fmax((128.0 + bn / 2) * 5.1, 6.7 * bn);
+    if (bn == 128 && knobs.kb128 > 0) kb = knobs.kb128;
     const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, nk / 4)) : 1;
     for (int s = 1; s <= smax; ++s) {
       const int kper = (nk + s - 1) / s;
