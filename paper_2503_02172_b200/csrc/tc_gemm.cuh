@@ -236,7 +236,7 @@ constexpr int DRAIN = KGQ_TC_DRAIN;
 // epilogue warp owns NBUF x 4 KB holding a 32-row chunk of its columns in the 128-byte
 // (1 plane, 32 columns) or 64-byte (2 planes, 16 columns each) swizzled layout of the output
 // tensor map's box -- then the barriers.
-template <int BN>
+template <int BN, bool NBUF2 = false>
 struct Layout {
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int A_BYTES = BM * BK * 2;         // one bf16 plane of A: 8 KB
@@ -245,7 +245,12 @@ struct Layout {
   static constexpr int BUF_BYTES = 4096;
   static constexpr int BUDGET = 227 * 1024 - 1024 - 256;  // minus alignment slack and barriers
   static constexpr int FIT = (BUDGET - EPI_WARPS * BUF_BYTES) / STAGE_BYTES;
-  static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+  // NBUF2 (split-output dense layers, short one-wave launches): double-buffered epilogue
+  // staging -- a chunk's st.shared does not wait for the previous chunk's TMA store to drain the
+  // buffer -- at the price of one operand stage (C2: dense -1%; the long score GEMM keeps its
+  // stages, where the extra stage is worth more)
+  static constexpr int FIT2 = (BUDGET - 2 * EPI_WARPS * BUF_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = NBUF2 && FIT2 >= 3 ? (FIT2 > 6 ? 6 : FIT2) : (FIT > 6 ? 6 : FIT);
   static constexpr int NBUF = BUDGET - STAGES * STAGE_BYTES >= 2 * EPI_WARPS * BUF_BYTES ? 2 : 1;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = STG_OFF + NBUF * EPI_WARPS * BUF_BYTES;
@@ -301,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
            const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mW2,
            const __grid_constant__ CUtensorMap mO0, const __grid_constant__ CUtensorMap mO1,
            const __grid_constant__ CUtensorMap mO2, int M, int N, int K, const Sched sc, const Epi epi) {
-  using L = Layout<BN>;
+  using L = Layout<BN, Epi::PLANES == 3>;
   constexpr int STAGES = L::STAGES;
   constexpr int PLANES = Epi::PLANES, ROWDIV = Epi::ROWDIV;
   constexpr int CW = BN / 2;            // columns per epilogue warp
@@ -681,7 +686,7 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   auto kern = k_gemm<BN, Epi>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<BN>::TOTAL);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<BN, Epi::PLANES == 3>::TOTAL);
     attr = true;
   }
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
@@ -694,7 +699,7 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = Layout<BN>::TOTAL;
+  cfg.dynamicSmemBytes = Layout<BN, Epi::PLANES == 3>::TOTAL;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
