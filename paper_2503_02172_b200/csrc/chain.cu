@@ -75,14 +75,12 @@ int launch_translate_chain(const ChainArgs& a, const float* ent, const float* re
 // row, 16-byte loads and 8-byte plane stores (d % 4 == 0 and every row stride % 8 == 0, so
 // rows are 16-byte aligned).
 __device__ __forceinline__ void store_split4(const Split& z, int64_t i, float4 x) {
-  __nv_bfloat16 a[4], b[4], c[4];
-  split3(x.x, a[0], b[0], c[0]);
-  split3(x.y, a[1], b[1], c[1]);
-  split3(x.z, a[2], b[2], c[2]);
-  split3(x.w, a[3], b[3], c[3]);
-  *reinterpret_cast<uint2*>(z.b0 + i) = make_uint2(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]));
-  *reinterpret_cast<uint2*>(z.b1 + i) = make_uint2(pack_bf16(b[0], b[1]), pack_bf16(b[2], b[3]));
-  *reinterpret_cast<uint2*>(z.b2 + i) = make_uint2(pack_bf16(c[0], c[1]), pack_bf16(c[2], c[3]));
+  uint32_t a0, b0, c0, a1, b1, c1;
+  split3_pair(x.x, x.y, a0, b0, c0);
+  split3_pair(x.z, x.w, a1, b1, c1);
+  *reinterpret_cast<uint2*>(z.b0 + i) = make_uint2(a0, a1);
+  *reinterpret_cast<uint2*>(z.b1 + i) = make_uint2(b0, b1);
+  *reinterpret_cast<uint2*>(z.b2 + i) = make_uint2(c0, c1);
 }
 constexpr int kMlpInRows = 4;  // rows (warps) per block
 __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,

@@ -73,6 +73,21 @@ __device__ __forceinline__ void split3(float x, __nv_bfloat16& a, __nv_bfloat16&
 __device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
   return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
 }
+// split3 of two values at once with packed conversions (one F2FP per plane pair): q0/q1/q2 =
+// the (x, y) bf16 pairs of planes 0/1/2, x in the low half -- bit-identical to
+// pack_bf16(split3(x), split3(y)) plane by plane.
+__device__ __forceinline__ void split3_pair(float x, float y, uint32_t& q0, uint32_t& q1, uint32_t& q2) {
+  auto pk = [](float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  };
+  auto lo = [](uint32_t u) { return __uint_as_float(u << 16); };
+  auto hi = [](uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); };
+  q0 = pk(x, y);
+  const float rx = x - lo(q0), ry = y - hi(q0);
+  q1 = pk(rx, ry);
+  q2 = pk(rx - lo(q1), ry - hi(q1));
+}
 
 // Store x at element i of the split tensor (all three planes).
 __device__ __forceinline__ void store_split(const Split& s, int64_t i, float x) {

@@ -547,14 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // 16-byte chunk c of row r at r * 32 + ((c ^ ((r >> 2) & 1)) << 4)
           uint32_t q0[8], q1[8], q2[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            __nv_bfloat16 x0, x1, x2, y0, y1, y2;
-            split3(v[2 * i], x0, x1, x2);
-            split3(v[2 * i + 1], y0, y1, y2);
-            q0[i] = pack_bf16(x0, y0);
-            q1[i] = pack_bf16(x1, y1);
-            q2[i] = pack_bf16(x2, y2);
-          }
+          for (int i = 0; i < 8; ++i) split3_pair(v[2 * i], v[2 * i + 1], q0[i], q1[i], q2[i]);
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int o = lane * 32 + ((c ^ ((lane >> 2) & 1)) << 4);
