@@ -73,7 +73,7 @@ struct EpiLinear {
   __device__ __forceinline__ Pre prefetch(int row, int n0, int lane) const {
     Pre p;
 #pragma unroll
-    for (int j = 0; j < CW / 32; ++j) p.b[j] = n0 + lane + 32 * j < N ? __ldg(bias + n0 + lane + 32 * j) : 0.0f;
+    for (int j = 0; j < (CW + 31) / 32; ++j) p.b[j] = n0 + lane + 32 * j < N ? __ldg(bias + n0 + lane + 32 * j) : 0.0f;
     p.neg = row >= neg0 && row < neg1;
     return p;
   }

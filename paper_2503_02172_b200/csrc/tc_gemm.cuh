@@ -257,7 +257,7 @@ struct Layout {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
   static_assert(TOTAL <= 227 * 1024, "shared memory budget");
   static_assert(STAGES >= 3, "pipeline depth");
-  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "2-CTA tile: N multiple of 32 per CTA, CW multiple of 32");
+  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "2-CTA tile: N multiple of 16 per CTA, CW multiple of 16");
 };
 
 // Work split of one launch.  Tiles [0, full) -- complete rounds over the clusters -- are
@@ -311,6 +311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   constexpr int PLANES = Epi::PLANES, ROWDIV = Epi::ROWDIV;
   constexpr int CW = BN / 2;            // columns per epilogue warp
   constexpr int CH = PLANES == 1 ? 32 : 16;  // columns per staged chunk
+  static_assert(CW % CH == 0, "fp32 outputs (32-column chunks) need BN % 64 == 0");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
@@ -713,18 +714,22 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
 struct Plan {
   int bn, full, s_tail, kper;
 };
-constexpr int kTileBN[4] = {64, 128, 192, 256};
+// 160 (split-output dense layers only: 16-column chunks) tiles N = 800 / 1600 exactly
+constexpr int kTileBN[5] = {64, 128, 160, 192, 256};
 struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN, KGQ_GEMM_KB128
   int force_bn = 0;
   double kb128 = 0.0;
+  bool no160 = false;
   PlanKnobs() {
+    const char* n = getenv("KGQ_GEMM_NO160");
+    no160 = n && n[0] && n[0] != '0';
     const char* e = getenv("KGQ_GEMM_BN");
     if (e) force_bn = atoi(e);
     e = getenv("KGQ_GEMM_KB128");
     if (e) kb128 = atof(e);
   }
 };
-inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split) {
+inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allow160) {
   static const PlanKnobs knobs;
   const int64_t pairs_m = (M + 2 * BM - 1) / (2 * BM);
   const int nk = (int)((K + BK - 1) / BK);
@@ -733,10 +738,12 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split) {
   double best_cost = 1e300;
   for (int bn : kTileBN) {
     if (knobs.force_bn && bn != knobs.force_bn) continue;
+    if (bn == 160 && (!allow160 || knobs.no160)) continue;
     const int64_t tiles = pairs_m * ((N + bn - 1) / bn);
     const int64_t full = tiles / kClustersMax * kClustersMax, tail = tiles - full;
     double kb = fmax((128.0 + bn / 2) * 5.1, 6.7 * bn);
     if (bn == 128 && knobs.kb128 > 0) kb = knobs.kb128;
+    if (bn == 160) kb *= 1.03;  // measured: only worth it when it saves whole tiles (N = 800)
     const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, nk / 4)) : 1;
     for (int s = 1; s <= smax; ++s) {
       const int kper = (nk + s - 1) / s;
@@ -759,11 +766,14 @@ int launch_gemm_auto(const Split& A, int M, const Split& W, int N, int K, const 
     const char* e = getenv("KGQ_NO_SPLITK");
     return e && e[0] && e[0] != '0';
   }();
-  const Plan p = plan_gemm(M, N, K, !no_split && ws != nullptr && ws->ws != nullptr);
+  const Plan p = plan_gemm(M, N, K, !no_split && ws != nullptr && ws->ws != nullptr, Epi::PLANES == 3);
   const Sched sc{p.full, p.s_tail, p.kper, ws ? ws->ws : nullptr, ws ? ws->cnt : nullptr};
   switch (p.bn) {
     case 64: return launch_gemm<64>(A, M, W, N, K, o, epi, st, sc);
     case 128: return launch_gemm<128>(A, M, W, N, K, o, epi, st, sc);
+    case 160:
+      if constexpr (Epi::PLANES == 3) return launch_gemm<160>(A, M, W, N, K, o, epi, st, sc);
+      return -1;  // not planned for fp32 outputs
     case 192: return launch_gemm<192>(A, M, W, N, K, o, epi, st, sc);
     default: return launch_gemm<256>(A, M, W, N, K, o, epi, st, sc);
   }

@@ -69,13 +69,16 @@ int main() {
       cudaMalloc(&gws.cnt, kGemmCntInts * 4);
       cudaMemset(gws.cnt, 0, kGemmCntInts * 4);
     }
-    const tc::Plan plan = tc::plan_gemm(M, N, K, !getenv("KGQ_NO_SPLITK"));
+    const tc::Plan plan = tc::plan_gemm(M, N, K, !getenv("KGQ_NO_SPLITK"), !sh.score);
     const tc::Sched whole{0, 1, 0, nullptr, nullptr};
     tc::Sched sc = whole;
     auto run = [&](int bn) {
       auto go = [&](auto c) {
         constexpr int B = decltype(c)::value;
-        if (sh.score)
+        if constexpr (B % 64 != 0) {
+          tc::launch_gemm<B>(A, M, Wsp, N, K, tc::OutDesc{nullptr, 0, Ysp, M, N},
+                             EpiLinear<kEpiRelu, true>{b, N, 0, 0}, 0, sc);
+        } else if (sh.score)
           tc::launch_gemm<B>(A, M, Wsp, N, K, tc::OutDesc{y, N, Split{}, M, N},
                              EpiBetaScore<1>{P, E, M, (int64_t)N}, 0, sc);
         else
@@ -85,13 +88,15 @@ int main() {
       switch (bn) {
         case 64: go(std::integral_constant<int, 64>{}); break;
         case 128: go(std::integral_constant<int, 128>{}); break;
+        case 160: go(std::integral_constant<int, 160>{}); break;
         case 192: go(std::integral_constant<int, 192>{}); break;
         default: go(std::integral_constant<int, 256>{}); break;
       }
     };
     const int pick = plan.bn;
     printf("M=%5d N=%5d K=%5d %s |", M, N, K, sh.score ? "score " : "linear");
-    for (int bn : {64, 128, 192, 256}) printf(" %d:%.1f", bn, time_us([&] { run(bn); }));
+    for (int bn : {64, 128, 160, 192, 256})
+      if (bn % 64 == 0 || !sh.score) printf(" %d:%.1f", bn, time_us([&] { run(bn); }));
     sc = tc::Sched{plan.full, plan.s_tail, plan.kper, gws.ws, gws.cnt};
     const double us = time_us([&] { run(pick); });
     printf(" | plan %d full %d split %d: %.1f us %.1f TFLOP/s useful\n", pick, plan.full, plan.s_tail, us,
