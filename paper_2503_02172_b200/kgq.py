@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkgq.so")
+LIB_PATH = os.environ.get("KGQ_LIB_PATH") or os.path.join(_HERE, "libkgq.so")  # override: A/B builds only
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
                       " (or `make -C paper_2503_02172_b200/csrc`)")
