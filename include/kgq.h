@@ -162,6 +162,14 @@ kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anc
 kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
                            const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
                            kgq_stream stream);
+/* kgq_submit_host without the final synchronisation: the copies and kernels are enqueued on
+ * `stream` and the call returns; topk_dist / topk_id are valid (and anchors / rels may be
+ * reused) once the stream has been synchronised.  With pinned host buffers consecutive calls
+ * overlap the host turnaround with the previous submit's kernels; calls on one context are
+ * ordered by the stream (the staging buffers are reused in stream order). */
+kgq_status kgq_submit_host_async(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                                 const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
+                                 kgq_stream stream);
 /* Mixed-structure batch: n_groups groups, group i = batches[i] queries of
  * structure structures[i] (host arrays).  anchors / rels: device int32, the groups' [B_i, n_a(s_i)]
  * and [B_i, n_r(s_i)] blocks concatenated in group order; topk_dist / topk_id: device

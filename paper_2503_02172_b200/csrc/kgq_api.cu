@@ -1178,6 +1178,15 @@ kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* struc
 kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
                            const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
                            kgq_stream stream) {
+  kgq_status st = kgq_submit_host_async(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, stream);
+  if (st || batch == 0) return st;
+  CK(cudaStreamSynchronize((cudaStream_t)stream), "submit_host sync");
+  return KGQ_OK;
+}
+
+kgq_status kgq_submit_host_async(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
+                                 const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
+                                 kgq_stream stream) {
   kgq_status st = check_submit(ctx, s, batch, k, true);
   if (st) return st;
   if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
@@ -1201,7 +1210,6 @@ kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t
      "top-k download");
   CK(cudaMemcpyAsync(topk_id, ctx->d_topi_stage, (size_t)batch * k * sizeof(int32_t), cudaMemcpyDeviceToHost, cs),
      "top-k download");
-  CK(cudaStreamSynchronize(cs), "submit_host sync");
   return KGQ_OK;
 }
 

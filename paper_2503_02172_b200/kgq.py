@@ -35,7 +35,7 @@ EXPORTS = (
     "kgq_num_relations", "kgq_num_branches", "kgq_uses_negation", "kgq_structure_name",
     "kgq_structure_from_name", "kgq_embedding_width", "kgq_shard_range", "kgq_shard_begin",
     "kgq_shard_end", "kgq_load_entities", "kgq_load_relations", "kgq_load_linear",
-    "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_submit_mixed", "kgq_query_embedding", "kgq_merge_topk",
+    "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_submit_host_async", "kgq_submit_mixed", "kgq_query_embedding", "kgq_merge_topk",
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
     "kgq_profile_read", "kgq_rank_answers", "kgq_peer_bytes", "kgq_set_peers", "kgq_merge_peers",
 )
@@ -75,6 +75,7 @@ _sig = {
     "kgq_finalize": (_I32, [_P]),
     "kgq_submit": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P]),
     "kgq_submit_host": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
+    "kgq_submit_host_async": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
     "kgq_submit_mixed": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P]),
     "kgq_query_embedding": (_I32, [_P, _I32, _I32, _P, _P, _P, _P]),
     "kgq_merge_topk": (_I32, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
@@ -252,8 +253,10 @@ class Engine:
         return td, ti
 
     def submit_host(self, structure, anchors: np.ndarray, rels: np.ndarray, k: int,
-                    out=None, stream=None):
-        """End-to-end call with host buffers (H2D + path + D2H inside the library)."""
+                    out=None, stream=None, sync=True):
+        """End-to-end call with host buffers (H2D + path + D2H inside the library).  sync=False
+        (kgq_submit_host_async): returns after enqueueing; the outputs are valid after the
+        stream is synchronised (use pinned buffers for overlap)."""
         s = structure_id(structure)
         anchors = np.ascontiguousarray(anchors, dtype=np.int32)
         rels = np.ascontiguousarray(rels, dtype=np.int32)
@@ -263,8 +266,9 @@ class Engine:
             ti = np.empty((B, k), np.int32)
         else:
             td, ti = out
-        self._check(_lib.kgq_submit_host(self._h, s, B, anchors.ctypes.data, rels.ctypes.data, k,
-                                         td.ctypes.data, ti.ctypes.data, _stream(stream)))
+        fn = _lib.kgq_submit_host if sync else _lib.kgq_submit_host_async
+        self._check(fn(self._h, s, B, anchors.ctypes.data, rels.ctypes.data, k,
+                       td.ctypes.data, ti.ctypes.data, _stream(stream)))
         return td, ti
 
     def query_embedding(self, structure, anchors, rels, stream=None):

@@ -195,6 +195,21 @@ def test_submit_host_matches_device_path():
     np.testing.assert_array_equal(hi, di.cpu().numpy())
     np.testing.assert_array_equal(hd, dd.cpu().numpy())
     assert e.last_launch_count() > 0
+    # async variant: several structures enqueued back to back (pinned buffers), one sync
+    outs = {}
+    for s in ("inp", "2u", "3in"):
+        a2, r2 = synth.make_queries(s, 20, SMALL["N"], SMALL["R"], seed=11)
+        pa = torch.from_numpy(a2.astype(np.int32)).pin_memory()
+        pr = torch.from_numpy(r2.astype(np.int32)).pin_memory()
+        od = torch.empty((20, 7)).pin_memory()
+        oi = torch.empty((20, 7), dtype=torch.int32).pin_memory()
+        e.submit_host(s, pa.numpy(), pr.numpy(), 7, out=(od.numpy(), oi.numpy()), sync=False)
+        outs[s] = (a2, r2, pa, pr, od, oi)
+    torch.cuda.synchronize()
+    for s, (a2, r2, pa, pr, od, oi) in outs.items():
+        dd, di = e.submit(s, dev(a2), dev(r2), 7)
+        np.testing.assert_array_equal(oi.numpy(), di.cpu().numpy())
+        np.testing.assert_array_equal(od.numpy(), dd.cpu().numpy())
 
 
 def test_deterministic_repeat():
