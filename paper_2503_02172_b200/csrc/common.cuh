@@ -31,17 +31,28 @@ struct Split {
 // stream serialization, waits for its predecessor's results with griddepcontrol.wait before
 // reading them and lets its successor start launching right away (griddepcontrol.
 // launch_dependents), so kernel launch latency overlaps the predecessor's tail.  Both are
-// no-ops for a kernel launched without the attribute.  KGQ_NO_PDL=1 disables the attribute.
+// no-ops for a kernel launched without the attribute (the default, see pdl_env).
 __device__ __forceinline__ void pdl_grid_sync() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-inline bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("KGQ_NO_PDL");
-    v = (e && e[0] && e[0] != '0') ? 0 : 1;
-  }
+// OFF by default (KGQ_PDL=1 turns it on, KGQ_PDL_SMALL / KGQ_PDL_GEMM = 0|1 per kernel class):
+// measured on C2 (graph replays, no stage events) PDL costs 2.5% -- a PDL-launched persistent
+// GEMM gets its clusters placed as the predecessor's CTAs drain, and with static round-robin
+// units a late cluster finishes its units late; the early-launched small kernels' CTAs also
+// take SM slots the predecessor's later CTAs need.  No-PDL 3.01M q/s vs 2.93M.
+inline int pdl_env(const char* specific) {
+  const char* f = getenv(specific);
+  if (f && f[0]) return f[0] == '1' ? 1 : 0;
+  const char* e = getenv("KGQ_PDL");
+  return e && e[0] == '1' ? 1 : 0;
+}
+inline bool pdl_enabled() {  // small kernels (launch_pdl)
+  static const int v = pdl_env("KGQ_PDL_SMALL");
+  return v == 1;
+}
+inline bool pdl_gemm_enabled() {  // the persistent GEMM (tc_gemm.cuh launch_gemm)
+  static const int v = pdl_env("KGQ_PDL_GEMM");
   return v == 1;
 }
 template <typename... KArgs, typename... Args>

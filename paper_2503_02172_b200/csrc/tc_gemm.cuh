@@ -699,7 +699,7 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_gemm_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kern, mA[0], mA[1], mW[0], mW[1], mA[2], mW[2], mO[0], mO[1], mO[2], M, N, K, sc, epi);
   return 1;
 }

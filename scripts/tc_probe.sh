@@ -5,7 +5,7 @@ FL="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a --expt-relaxed-conste
 if [ "$1" = "run" ]; then
   echo "== bn check"; timeout 120 ./tc_bn_check
   echo "== probe"; timeout 120 ./tc_probe_base
-  echo "== probe (no PDL)"; KGQ_NO_PDL=1 timeout 120 ./tc_probe_base
+  echo "== probe (PDL)"; KGQ_PDL=1 timeout 120 ./tc_probe_base
   echo "== trace"; timeout 120 ./tc_probe_trace
   for v in $EXTRA; do echo "== $v"; timeout 120 ./tc_probe_$v; done
   exit 0
