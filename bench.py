@@ -153,17 +153,25 @@ def run_c5a(args):
                 for _ in range(args.warmup):
                     eng.submit(s, da, dr, K)
                 torch.cuda.synchronize()
-                eng.profile(True)
-                eng.profile_read()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                tot = 0.0
-                for _ in range(args.steps):
-                    flush.zero_()
-                    e0.record()
-                    eng.submit(s, da, dr, K)
-                    e1.record()
-                    torch.cuda.synchronize()
-                    tot += e0.elapsed_time(e1)
+
+                def c5a_steps():
+                    tt = 0.0
+                    for _ in range(args.steps):
+                        flush.zero_()
+                        e0.record()
+                        eng.submit(s, da, dr, K)
+                        e1.record()
+                        torch.cuda.synchronize()
+                        tt += e0.elapsed_time(e1)
+                    return tt
+                tot = c5a_steps()  # headline: no stage events
+                eng.profile(True)  # second pass: scorer time
+                eng.submit(s, da, dr, K)
+                eng.submit(s, da, dr, K)
+                torch.cuda.synchronize()
+                eng.profile_read()
+                c5a_steps()
                 prof = eng.profile_read()
                 eng.profile(False)
                 sc_ms = prof["score"][0] / max(1, prof["score"][1])
@@ -217,20 +225,29 @@ def run_suite(args):
                 eng.submit(s, *qs[s], K)
         torch.cuda.synchronize()
         eng.check_errors()
-        eng.profile(True)
-        eng.profile_read()
         ev = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in structs}
-        per = {s: 0.0 for s in structs}
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            for s in structs:
-                ev[s][0].record()
-                eng.submit(s, *qs[s], K)
-                ev[s][1].record()
-            torch.cuda.synchronize()
-            for s in structs:
-                per[s] += ev[s][0].elapsed_time(ev[s][1])
+
+        def suite_steps():
+            per = {s: 0.0 for s in structs}
+            for _ in range(args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                for s in structs:
+                    ev[s][0].record()
+                    eng.submit(s, *qs[s], K)
+                    ev[s][1].record()
+                torch.cuda.synchronize()
+                for s in structs:
+                    per[s] += ev[s][0].elapsed_time(ev[s][1])
+            return per
+        per = suite_steps()  # headline: no stage events
+        eng.profile(True)    # second pass: stage split + scorer / GEMM times
+        for s in structs:    # capture the profiled graphs before the pass
+            eng.submit(s, *qs[s], K)
+            eng.submit(s, *qs[s], K)
+        torch.cuda.synchronize()
+        eng.profile_read()
+        suite_steps()
         prof = eng.profile_read()
         eng.profile(False)
         eng.close()
