@@ -498,7 +498,7 @@ def main():
             "stage_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()},  # dense is inside chain
             "stage_pass": {"ms_per_step": sum(prof_step_ms) / prof_steps,
                            "how": "stage split and roofline from a second pass of the same steps with the "
-                                  "library's stage events on (they split the PDL chains: slower than the "
+                                  "library's stage events on (their event nodes sit between the captured kernels: slower than the "
                                   "headline pass, which runs without them)"},
             "stage_share": stage_share,
             "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",

@@ -36,23 +36,24 @@ __device__ __forceinline__ void pdl_grid_sync() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-// OFF by default (KGQ_PDL=1 turns it on, KGQ_PDL_SMALL / KGQ_PDL_GEMM = 0|1 per kernel class):
-// measured on C2 (graph replays, no stage events) PDL costs 2.5% -- a PDL-launched persistent
-// GEMM gets its clusters placed as the predecessor's CTAs drain, and with static round-robin
-// units a late cluster finishes its units late; the early-launched small kernels' CTAs also
-// take SM slots the predecessor's later CTAs need.  No-PDL 3.01M q/s vs 2.93M.
-inline int pdl_env(const char* specific) {
+// Defaults from same-box measurements (KGQ_PDL = 0|1 sets both classes, KGQ_PDL_SMALL /
+// KGQ_PDL_GEMM = 0|1 one class): ON for the persistent GEMM -- neutral in the per-type graph
+// replays, +8% for the eagerly launched mixed-structure submit (3.41M -> 3.68M q/s) -- and OFF for
+// the small kernels, whose early-launched CTAs take SM slots the predecessor still needs
+// (per-type C2 -2.6% with them on).
+inline int pdl_env(const char* specific, int dflt) {
   const char* f = getenv(specific);
   if (f && f[0]) return f[0] == '1' ? 1 : 0;
   const char* e = getenv("KGQ_PDL");
-  return e && e[0] == '1' ? 1 : 0;
+  if (e && e[0]) return e[0] == '1' ? 1 : 0;
+  return dflt;
 }
 inline bool pdl_enabled() {  // small kernels (launch_pdl)
-  static const int v = pdl_env("KGQ_PDL_SMALL");
+  static const int v = pdl_env("KGQ_PDL_SMALL", 0);
   return v == 1;
 }
 inline bool pdl_gemm_enabled() {  // the persistent GEMM (tc_gemm.cuh launch_gemm)
-  static const int v = pdl_env("KGQ_PDL_GEMM");
+  static const int v = pdl_env("KGQ_PDL_GEMM", 1);
   return v == 1;
 }
 template <typename... KArgs, typename... Args>
