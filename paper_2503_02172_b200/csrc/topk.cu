@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(32 * kCminWarps)
   pdl_grid_sync();
   __shared__ float wtau[kCminWarps];
   __shared__ unsigned long long cand[kCandCap];
+  __shared__ int blist[kCminWarps][kCandCap];  // per warp: qualifying block ids
   __shared__ int ncand;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int b = blockIdx.x;
@@ -354,38 +355,44 @@ __global__ void __launch_bounds__(32 * kCminWarps)
 #pragma unroll
   for (int w = 1; w < kCminWarps; ++w) tau = fminf(tau, wtau[w]);
   // ---- pass 2: every entry <= tau of the blocks whose minimum is <= tau -> shared list ----
+  // first compact this warp's qualifying block ids (ballot + prefix count), then load them
+  // eight at a time: no load slots are spent on unselected blocks
   const unsigned lt = (1u << lane) - 1u;
+  int* bl = blist[wid];
+  int nsel = 0;
   for (int64_t g0 = j0w; g0 < j1w; g0 += 32) {
     const float x = g0 + lane < j1w ? cm[g0 + lane] : kNaN;
-    unsigned sel = __ballot_sync(0xffffffffu, x <= tau);
-    while (sel) {
-      int blk[8];
-      float vv[8];
+    const unsigned m = __ballot_sync(0xffffffffu, x <= tau);
+    const int p = nsel + __popc(m & lt);
+    if (x <= tau && p < kCandCap) bl[p] = (int)(g0 + lane);
+    nsel += __popc(m);
+  }
+  if (nsel > kCandCap) {  // >= kCandCap + 1 candidates: force the register-scan path
+    if (lane == 0) atomicAdd(&ncand, kCandCap + 1);
+    nsel = 0;
+  }
+  __syncwarp();
+  for (int i0 = 0; i0 < nsel; i0 += 8) {
+    int blk[8];
+    float vv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {  // up to eight blocks' loads in flight
-        blk[u] = -1;
-        vv[u] = kNaN;
-        if (sel) {
-          const int o = __ffs(sel) - 1;
-          sel &= sel - 1;
-          blk[u] = (int)(g0 + o);
-          const int64_t i = (int64_t)blk[u] * 32 + lane;
-          vv[u] = i < n ? row[i] : kNaN;
-        }
-      }
+    for (int u = 0; u < 8; ++u) {  // up to eight blocks' loads in flight
+      blk[u] = i0 + u < nsel ? bl[i0 + u] : -1;
+      const int e = blk[u] * 32 + lane;
+      vv[u] = blk[u] >= 0 && e < n ? row[e] : kNaN;
+    }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (blk[u] < 0) continue;
-        const bool pass = vv[u] <= tau;
-        const unsigned m = __ballot_sync(0xffffffffu, pass);
-        if (!m) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&ncand, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const int slot = base + __popc(m & lt);
-        if (pass && slot < kCandCap)
-          cand[slot] = ((unsigned long long)fkey(vv[u]) << 32) | (uint32_t)((int64_t)blk[u] * 32 + lane);
-      }
+    for (int u = 0; u < 8; ++u) {
+      if (blk[u] < 0) break;
+      const bool pass = vv[u] <= tau;
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (!m) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&ncand, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int slot = base + __popc(m & lt);
+      if (pass && slot < kCandCap)
+        cand[slot] = ((unsigned long long)fkey(vv[u]) << 32) | (uint32_t)(blk[u] * 32 + lane);
     }
   }
   __syncthreads();
