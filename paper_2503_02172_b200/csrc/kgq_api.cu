@@ -793,6 +793,10 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
                            ctx->np * sizeof(float), ctx->ns * sizeof(float), nb, cudaMemcpyDeviceToDevice, st),
          "shard_dist copy");
   }
+  {  // perf probe only: KGQ_DBG_EMPTY_NODES=n appends n empty dependent kernels (per-node cost)
+    static const int n_empty = [] { const char* e = getenv("KGQ_DBG_EMPTY_NODES"); return e ? atoi(e) : 0; }();
+    for (int i = 0; i < n_empty; ++i) L += launch_empty(st);
+  }
   ctx->launches = L;
   CK(cudaGetLastError(), "submit launch");
   return KGQ_OK;

@@ -324,6 +324,7 @@ int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double
 int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                      int k, int64_t id_base, const int32_t* invalid, float* out_d, int32_t* out_i,
                      cudaStream_t st, const PeerPush& pp);
+int launch_empty(cudaStream_t st);  // perf probe (KGQ_DBG_EMPTY_NODES)
 // N2 (peer.cuh): push of finished output rows [0, B) of (out_d, out_i) (top-k paths without
 // the fused push); the waiting merge (advances the epoch; epoch[1] is its CTA counter).
 int launch_peer_push(const PeerPush& pp, int B, int k, const float* out_d, const int32_t* out_i, cudaStream_t st);
