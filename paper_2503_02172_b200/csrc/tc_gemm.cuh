@@ -704,16 +704,20 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   return 1;
 }
 
-// Launch plan: tile width and tail split, from a cost model in SM clocks calibrated on B200
-// (scripts/tc_probe.cu traces, profiles/r01/tc_splitk_probe.txt):
-//   * a K-block costs max(operand stream, MMA) = max((128 + BN/2) x 5.1, 6.7 BN) clk per SM
-//     ((128 + BN/2) x 192 B at ~38 B/clk vs 12 bf16 MMAs of N = BN);
-//   * complete rounds of whole tiles run back to back (their epilogues overlap the next tile);
-//   * a split tail tile costs kper K-blocks + publishing its partials (~3 us) + ~2.5 us per
-//     other split's partials added by the last arriver, + the final epilogue (~3 us).
+// Launch plan: tile width and tail split, from the measured cost model below.  Complete rounds
+// of whole tiles run back to back (their epilogues overlap the next tile); a split tail tile
+// costs its kper K-blocks + publishing its partials + adding the other splits' partials.
 struct Plan {
   int bn, full, s_tail, kper;
 };
+// Cost model in us, least-squares fit (scripts/fit_plan.py) to every (BN, tail split) plan of 17
+// dense / score shapes of the C2-C4 workloads measured on B200 (`PROBE_SPLITS=1
+// scripts/tc_probe_base`, profiles/r01/tc_plan_fit.txt):
+//   t = c0 + whole rounds x nk x kb[BN] + tail kper x kb[BN] + [split] (pub + (s-1) part) x BN
+// (picks a plan within 3.4 us of the best over all 17 shapes; the previous clock-count model
+// lost ~14 us, mostly on the N = 400 / 1600, K = 800 layers at M = 1-3K).
+constexpr double kKbUs[5] = {0.623, 0.675, 0.687, 0.760, 1.004};  // BN 64 128 160 192 256
+constexpr double kC0Us = 3.40, kPubUs = 0.0230, kPartUs = 0.0113;
 // 160 (split-output dense layers only: 16-column chunks) tiles N = 800 / 1600 exactly
 constexpr int kTileBN[5] = {64, 128, 160, 192, 256};
 struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN, KGQ_GEMM_KB128
@@ -733,7 +737,6 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allo
   static const PlanKnobs knobs;
   const int64_t pairs_m = (M + 2 * BM - 1) / (2 * BM);
   const int nk = (int)((K + BK - 1) / BK);
-  const double kEpi = 5900.0, kPublish = 5900.0, kPartial = 4900.0;  // clk
   Plan best{kTileBN[0], 0, 1, nk};
   double best_cost = 1e300;
   for (int bn : kTileBN) {
@@ -741,15 +744,14 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allo
     if (bn == 160 && (!allow160 || knobs.no160)) continue;
     const int64_t tiles = pairs_m * ((N + bn - 1) / bn);
     const int64_t full = tiles / kClustersMax * kClustersMax, tail = tiles - full;
-    double kb = fmax((128.0 + bn / 2) * 5.1, 6.7 * bn);
+    double kb = kKbUs[bn == 64 ? 0 : bn == 128 ? 1 : bn == 160 ? 2 : bn == 192 ? 3 : 4];
     if (bn == 128 && knobs.kb128 > 0) kb = knobs.kb128;
-    if (bn == 160) kb *= 1.03;  // measured: only worth it when it saves whole tiles (N = 800)
-    const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, nk / 4)) : 1;
+    const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, std::min(6, nk / 4))) : 1;
     for (int s = 1; s <= smax; ++s) {
       const int kper = (nk + s - 1) / s;
       const int se = (nk + kper - 1) / kper;  // no empty split
-      const double cost = (double)(full / kClustersMax) * nk * kb + kEpi +
-                          (tail ? kper * kb + (se > 1 ? kPublish + kPartial * (se - 1) : 0.0) : 0.0);
+      const double cost = kC0Us + (double)(full / kClustersMax) * nk * kb +
+                          (tail ? kper * kb + (se > 1 ? (kPubUs + kPartUs * (se - 1)) * bn : 0.0) : 0.0);
       if (cost < best_cost) {
         best_cost = cost;
         best = Plan{bn, (int)full, se, kper};

@@ -33,7 +33,10 @@ int main() {
   const Shape shapes[] = {{1024, 1600, 1200, false}, {3072, 1600, 1600, false}, {2048, 800, 1600, false},
                           {2048, 800, 800, false},   {1024, 14592, 800, true},  {2048, 14592, 800, true},
                           {1024, 14592, 32, true},   {1024, 1600, 32, false}, {2048, 400, 800, false},
-                          {3072, 400, 800, false},   {1024, 800, 1600, false}, {1024, 1600, 1600, false}};
+                          {3072, 400, 800, false},   {1024, 800, 1600, false}, {1024, 1600, 1600, false},
+                          {1024, 1600, 800, false},  {2048, 1600, 800, false},  {3072, 1600, 800, false},
+                          {2048, 1600, 1600, false}, {3072, 800, 1600, false},  {3072, 800, 800, false},
+                          {1024, 400, 800, false}};
 #ifdef KGQ_TC_TRACE
   unsigned long long* tr;
   cudaMalloc(&tr, 8192 * 64);
@@ -101,6 +104,28 @@ int main() {
     const double us = time_us([&] { run(pick); });
     printf(" | plan %d full %d split %d: %.1f us %.1f TFLOP/s useful\n", pick, plan.full, plan.s_tail, us,
            2.0 * M * N * K / us * 1e-6);
+    if (getenv("PROBE_SPLITS")) {  // every (BN, tail split) combination: the planner's search space
+      printf("    splits:");
+      double best = 1e30;
+      int bb = 0, bs = 0;
+      for (int bn : {64, 128, 160, 192, 256}) {
+        if (bn % 64 && sh.score) continue;
+        const int nkb = (K + 31) / 32;
+        const int tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
+        const int full = tiles / 74 * 74, tail = tiles - full;
+        for (int sp = 1; sp <= 4; ++sp) {
+          if (tail == 0 && sp > 1) break;
+          if (sp > 1 && tail * sp > 74) break;
+          const int kper = (nkb + sp - 1) / sp;
+          sc = sp == 1 ? whole : tc::Sched{full, sp, kper, gws.ws, gws.cnt};
+          const double t = time_us([&] { run(bn); });
+          printf(" %d/%d:%.1f", bn, sp, t);
+          if (t < best) { best = t; bb = bn; bs = sp; }
+        }
+      }
+      printf("  | best %d/%d %.1f us (plan %.1f)\n", bb, bs, best, us);
+      sc = tc::Sched{plan.full, plan.s_tail, plan.kper, gws.ws, gws.cnt};
+    }
 #ifdef KGQ_TC_TRACE
     {
       const int tiles0 = ((M + 255) / 256) * ((N + pick - 1) / pick);
