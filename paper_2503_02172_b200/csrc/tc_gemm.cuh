@@ -720,7 +720,7 @@ constexpr double kKbUs[5] = {0.623, 0.675, 0.687, 0.760, 1.004};  // BN 64 128 1
 constexpr double kC0Us = 3.40, kPubUs = 0.0230, kPartUs = 0.0113;
 // 160 (split-output dense layers only: 16-column chunks) tiles N = 800 / 1600 exactly
 constexpr int kTileBN[5] = {64, 128, 160, 192, 256};
-struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN, KGQ_GEMM_KB128
+struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN, KGQ_GEMM_KB128 (us per K-block)
   int force_bn = 0;
   double kb128 = 0.0;
   bool no160 = false;
