@@ -468,6 +468,33 @@ def main():
             torch.cuda.synchronize()
             e2e_as += time.perf_counter() - t0
         e2e_async_v = queries / e2e_as
+    else:
+        # N > 1: the sharded public API (ShardedEngine.submit: local top-k + all-gather + merge)
+        # with the step's inputs copied from pinned host memory and the merged top-k copied
+        # back into pinned host buffers, one synchronisation per step; max over ranks
+        dev_in = {s: (torch.empty_like(qs[s][2]), torch.empty_like(qs[s][3])) for s in STRUCTS}
+        pin_i = {s: (qs[s][2].cpu().pin_memory(), qs[s][3].cpu().pin_memory()) for s in STRUCTS}
+
+        def e2e_step():
+            for s in STRUCTS:
+                dev_in[s][0].copy_(pin_i[s][0], non_blocking=True)
+                dev_in[s][1].copy_(pin_i[s][1], non_blocking=True)
+                td, ti = seng.submit(s, dev_in[s][0], dev_in[s][1], K)
+                hout_t[s][0].copy_(td, non_blocking=True)
+                hout_t[s][1].copy_(ti, non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_step()
+        e2e_as = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            e2e_as += time.perf_counter() - t0
+        tt = torch.tensor([e2e_as], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_async_v = queries / float(tt.item())
+        h2d = sum(pin_i[s][0].numel() * 4 + pin_i[s][1].numel() * 4 for s in STRUCTS)
 
     # ---- roofline of the dominant kernel: the tcgen05 bf16x3 GEMM (k_gemm), which runs every
     # dense layer of the chain (stage "dense") and the BetaE scorer contraction (stage "score").
@@ -515,9 +542,12 @@ def main():
             "mixed_submit": mixed,
             "e2e": {"value": e2e_async_v, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "how": "per step: kgq_submit_host_async per type (pinned H2D, path, D2H into pinned "
-                           "host outputs) and one stream synchronisation; wall clock per step, L2 flushed "
-                           "before each step (untimed)",
+                    "how": ("per step: kgq_submit_host_async per type (pinned H2D, path, D2H into pinned "
+                            "host outputs) and one stream synchronisation; wall clock per step, L2 flushed "
+                            "before each step (untimed)") if world == 1 else
+                           ("per step: pinned H2D, ShardedEngine.submit per type (local top-k, all-gather, "
+                            "merge), D2H of the merged top-k into pinned host buffers, one synchronisation; "
+                            "wall clock per step, max over ranks"),
                     "sync_per_call": {"value": e2e_v,
                                       "how": "kgq_submit_host (synchronises after every type)"}},
             "clocks": clk.summary(),
