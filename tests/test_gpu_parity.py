@@ -61,6 +61,14 @@ def run_case(model, s, dist="kgr-init", B=SMALL["B"], k=10, **kw):
     return e
 
 
+@pytest.mark.parametrize("s", ["1p", "3in", "up"])
+def test_betae_medium_dims_split_k_plans(s):
+    """K = 256-512 and 300 queries: the planner's split-K tails (publish / last-arriver reduce),
+    BN = 160 / 192 tiles and multi-M-pair grids run here (the SMALL config has K <= 120, one
+    K-split); distances, top-k and chain vs the oracle."""
+    run_case("betae", s, B=300, k=10, N=3000, R=40, d=128, H=512, max_batch=320)
+
+
 @pytest.mark.parametrize("s", ["1p", "2p", "2i"])
 def test_toy_gqe_config(s):
     # BASELINE.json configs[0]: GQE 1p/2p/2i on a toy KG, 200 entities, 10 rels, dim 32, B 16
