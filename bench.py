@@ -396,8 +396,10 @@ def main():
         meng = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH * len(STRUCTS), max_k=K, device=local)
         meng.load_tables(t)
         groups = [(s, qs[s][2].int(), qs[s][3].int()) for s in STRUCTS]
+        mout = (torch.empty((BATCH * len(STRUCTS), K), device="cuda"),
+                torch.empty((BATCH * len(STRUCTS), K), dtype=torch.int32, device="cuda"))
         for _ in range(args.warmup):
-            meng.submit_mixed(groups, K)
+            meng.submit_mixed(groups, K, out=mout)
         torch.cuda.synchronize()
         meng.check_errors()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -407,7 +409,7 @@ def main():
             for _ in range(args.steps):
                 flush.zero_()
                 e0.record()
-                meng.submit_mixed(groups, K)
+                meng.submit_mixed(groups, K, out=mout)
                 e1.record()
                 torch.cuda.synchronize()
                 ms += e0.elapsed_time(e1)

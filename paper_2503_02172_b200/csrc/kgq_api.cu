@@ -172,6 +172,15 @@ void destroy_graph_entry(kgq_ctx::GraphEntry& g) {
   g.evs.clear();
 }
 
+void clear_mix_graphs(kgq_ctx* ctx) {
+  for (auto& m : ctx->mgraphs) {
+    if (m.exec) cudaGraphExecDestroy(m.exec);
+    if (m.map_host) cudaFreeHost(m.map_host);
+  }
+  ctx->mgraphs.clear();
+}
+
+
 ChainArgs chain_args(kgq_ctx* ctx, const Plan* P, int B, const int32_t* anchors,
                      const int32_t* rels) {
   ChainArgs a{};
@@ -556,6 +565,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage); F(ctx->d_epoch);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
+  clear_mix_graphs(ctx);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (auto& r : ctx->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   delete ctx;
@@ -940,7 +950,7 @@ static int mix_mlp(kgq_ctx* ctx, const MixSegs& sg, int M, int neg0, cudaStream_
 }
 
 static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int32_t k, float* topk_dist,
-                              int32_t* topk_id, cudaStream_t st) {
+                              int32_t* topk_id, cudaStream_t st, int64_t* own_map = nullptr) {
   const int d = ctx->cfg.dim;
   int L = 0;
   CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)Q * sizeof(int32_t), st), "reset flags");
@@ -1059,9 +1069,12 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
   int R1 = 0, R2 = 0;
   for (auto& g : G) (g.P->n_out == 1 ? R1 : R2) += g.B * g.P->n_out;
   const int Q1 = R1, Q2 = R2 / 2;
-  if (ctx->mix_map_ev) CK(cudaEventSynchronize(ctx->mix_map_ev), "mixed staging");
-  int64_t* srcrow = ctx->mix_map_host;
-  int64_t* outrow = ctx->mix_map_host + (R1 + R2);  // stored as int64 pairs of int32 below
+  // the shared pinned staging buffer is rewritten only after its previous upload finished; a
+  // graph capture writes its own pinned copy instead (the graph's memcpy node reads it at replay)
+  if (!own_map && ctx->mix_map_ev) CK(cudaEventSynchronize(ctx->mix_map_ev), "mixed staging");
+  int64_t* const map_host = own_map ? own_map : ctx->mix_map_host;
+  int64_t* srcrow = map_host;
+  int64_t* outrow = map_host + (R1 + R2);  // stored as int64 pairs of int32 below
   int32_t* outrow32 = reinterpret_cast<int32_t*>(outrow);
   {
     int r = 0, o = 0;
@@ -1080,8 +1093,8 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
         }
   }
   const size_t map_bytes = (size_t)(R1 + R2) * sizeof(int64_t) + (size_t)(Q1 + Q2) * sizeof(int32_t);
-  CK(cudaMemcpyAsync(ctx->mix_map, ctx->mix_map_host, map_bytes, cudaMemcpyHostToDevice, st), "mixed map upload");
-  CK(cudaEventRecord(ctx->mix_map_ev, st), "mixed staging");
+  CK(cudaMemcpyAsync(ctx->mix_map, map_host, map_bytes, cudaMemcpyHostToDevice, st), "mixed map upload");
+  if (!own_map) CK(cudaEventRecord(ctx->mix_map_ev, st), "mixed staging");
   const int64_t* d_srcrow = ctx->mix_map;
   const int32_t* d_outrow = reinterpret_cast<const int32_t*>(ctx->mix_map + (R1 + R2));
   {
@@ -1176,7 +1189,47 @@ kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* struc
     CK(cudaMallocHost((void**)&ctx->mix_map_host, (size_t)(3 * ctx->cfg.max_batch) * sizeof(int64_t)), "mixed staging");
     CK(cudaEventCreateWithFlags(&ctx->mix_map_ev, cudaEventDisableTiming), "mixed staging");
   }
-  return mixed_betae(ctx, G, (int)Q, k, topk_dist, topk_id, cs);
+  if (!ctx->use_graphs || ctx->profile) return mixed_betae(ctx, G, (int)Q, k, topk_dist, topk_id, cs);
+  // ---- graph replay of identical batched mixed submits (first call eager, second captures) ----
+  std::vector<int32_t> key;
+  for (int i = 0; i < n_groups; ++i) {
+    key.push_back(structures[i]);
+    key.push_back(batches[i]);
+  }
+  const void* ptrs[4] = {anchors, rels, topk_dist, topk_id};
+  kgq_ctx::MixGraphEntry* e = nullptr;
+  for (auto& m : ctx->mgraphs)
+    if (m.k == k && m.key == key && std::equal(ptrs, ptrs + 4, m.ptr)) e = &m;
+  if (e && e->exec) {
+    CK(cudaGraphLaunch(e->exec, cs), "mixed graph launch");
+    ctx->launches = e->launches;
+    return KGQ_OK;
+  }
+  if (!e) {
+    if (ctx->mgraphs.size() >= 16) clear_mix_graphs(ctx);
+    ctx->mgraphs.push_back(kgq_ctx::MixGraphEntry{key, {ptrs[0], ptrs[1], ptrs[2], ptrs[3]}, k, nullptr, 0, 1, nullptr});
+    return mixed_betae(ctx, G, (int)Q, k, topk_dist, topk_id, cs);
+  }
+  if (e->seen != 1) return mixed_betae(ctx, G, (int)Q, k, topk_dist, topk_id, cs);  // capture failed before
+  e->seen = 2;
+  CK(cudaMallocHost((void**)&e->map_host, (size_t)(3 * ctx->cfg.max_batch) * sizeof(int64_t)), "mixed graph map");
+  if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking), "capture stream");
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+  kgq_status r = mixed_betae(ctx, G, (int)Q, k, topk_dist, topk_id, ctx->cap_stream, e->map_host);
+  cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (r == KGQ_OK && ce == cudaSuccess && graph) ce = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (r != KGQ_OK || ce != cudaSuccess || !exec) {
+    cudaGetLastError();
+    e->seen = 3;  // never retry this key; run eagerly
+    return mixed_betae(ctx, G, (int)Q, k, topk_dist, topk_id, cs);
+  }
+  e->exec = exec;
+  e->launches = ctx->launches;
+  CK(cudaGraphLaunch(exec, cs), "mixed graph launch");
+  return KGQ_OK;
 }
 
 kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
@@ -1291,6 +1344,7 @@ kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const*
     destroy_graph_entry(gr);
   }
   ctx->graphs.clear();
+  clear_mix_graphs(ctx);
   if (world == 0) {
     ctx->peers = PeerPush{};
     return KGQ_OK;

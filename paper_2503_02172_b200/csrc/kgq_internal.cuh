@@ -144,6 +144,18 @@ struct kgq_ctx {
   double prof_acc_ms[kgq::kStNum] = {}, prof_acc_work[kgq::kStNum] = {};
   int64_t prof_acc_n[kgq::kStNum] = {};
   std::vector<GraphEntry> graphs;
+  // CUDA graphs of batched mixed submits, keyed by the (structure, batch) list, k and pointers;
+  // each owns the pinned copy of its row map that its memcpy node uploads
+  struct MixGraphEntry {
+    std::vector<int32_t> key;
+    const void* ptr[4];
+    int k;
+    cudaGraphExec_t exec;
+    int launches;
+    int seen;
+    int64_t* map_host;
+  };
+  std::vector<MixGraphEntry> mgraphs;
   bool use_graphs = true;
   uint64_t graph_clock = 0;
   cudaStream_t cap_stream = nullptr;

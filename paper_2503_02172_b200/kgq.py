@@ -239,8 +239,19 @@ class Engine:
         ss = (ctypes.c_int32 * len(groups))(*[structure_id(g[0]) for g in groups])
         bs = (ctypes.c_int32 * len(groups))(*[int(g[1].shape[0]) for g in groups])
         dev = groups[0][1].device if groups else torch.device("cuda")
-        a = torch.cat([g[1].reshape(-1) for g in groups]) if groups else torch.empty(0, dtype=torch.int32, device=dev)
-        r = torch.cat([g[2].reshape(-1) for g in groups]) if groups else torch.empty(0, dtype=torch.int32, device=dev)
+        # inputs packed into per-engine staging buffers (stable addresses: an identical later call
+        # replays the library's captured graph of the whole mixed submit)
+        na = sum(int(g[1].numel()) for g in groups)
+        nr = sum(int(g[2].numel()) for g in groups)
+        st = getattr(self, "_mix_in", None)
+        if st is None or st[0].numel() < na or st[1].numel() < nr or st[0].device != dev:
+            st = (torch.empty(max(na, 1), dtype=torch.int32, device=dev),
+                  torch.empty(max(nr, 1), dtype=torch.int32, device=dev))
+            self._mix_in = st
+        a, r = st[0][:na], st[1][:nr]
+        if groups:
+            torch.cat([g[1].reshape(-1).to(torch.int32) for g in groups], out=a)
+            torch.cat([g[2].reshape(-1).to(torch.int32) for g in groups], out=r)
         Q = sum(int(g[1].shape[0]) for g in groups)
         if out is None:
             td = torch.empty((Q, k), dtype=torch.float32, device=dev)
