@@ -190,6 +190,48 @@ __device__ __forceinline__ double lnbeta_f64(double a, double b) {
          0.91893853320467274178 + ser(ra) + ser(rb) - ser(rc) + log_pos(ratio);
 }
 
+// Table-driven fp64 log for normal x > 0 (the P_q prep's FP64 pipe is its bound): x = 2^e m,
+// m in [1, 2), c_i = 1 + i/128 from the top 7 mantissa bits, r = (m - c_i) / c_i in [0, 1/128)
+// (m - c_i exact), ln x = e ln 2 + ln c_i + ln(1 + r) with the series through r^7 (truncation
+// < 2e-18).  lnc / invc: ln c_i and 1 / c_i (host-computed, kLogTab entries each, in shared
+// memory).  ~11 fp64 operations instead of ~20 for log_pos.
+constexpr int kLogTab = 128;
+__device__ __forceinline__ double log_tab(double x, const double* lnc, const double* invc) {
+  int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  const int e = (hi >> 20) - 1023;
+  const int i = (hi >> 13) & (kLogTab - 1);
+  hi = (hi & 0x000FFFFF) | 0x3FF00000;
+  const double m = __hiloint2double(hi, lo);
+  const double r = (m - (1.0 + i * (1.0 / kLogTab))) * invc[i];
+  const double p = r * (1.0 + r * (-1.0 / 2 + r * (1.0 / 3 + r * (-1.0 / 4 + r * (1.0 / 5 + r * (-1.0 / 6 + r * (1.0 / 7)))))));
+  return (double)e * 0.69314718055994530942 + (lnc[i] + p);
+}
+// lnbeta_f64 with the table log (same formula and error budget)
+__device__ __forceinline__ double lnbeta_f64_tab(double a, double b, const double* lnc, const double* invc) {
+  const double c = a + b;
+  double pa = a, pb = b, pc = c;
+#pragma unroll
+  for (int i = 1; i < 8; ++i) {
+    pa *= a + i;
+    pb *= b + i;
+    pc *= c + i;
+  }
+  const double ya = a + 8.0, yb = b + 8.0, yc = c + 8.0;
+  const double yab = ya * yb;
+  const double rall = rcp_nr(yab * yc);
+  const double ra = rall * yb * yc, rb = rall * ya * yc, rc = rall * yab;
+  auto ser = [](double r) {
+    const double z = r * r;
+    return r * (1.0 / 12 + z * (-1.0 / 360 + z * (1.0 / 1260 + z * (-1.0 / 1680 + z * (1.0 / 1188)))));
+  };
+  const double pab = pa * pb;
+  const double ratio = pab < 1e30 ? pc * rcp_nr(pab) : pc / pab;
+  return (ya - 0.5) * log_tab(ya, lnc, invc) + (yb - 0.5) * log_tab(yb, lnc, invc) -
+         (yc - 0.5) * log_tab(yc, lnc, invc) - ya - yb + yc + 0.91893853320467274178 + ser(ra) + ser(rb) - ser(rc) +
+         log_tab(ratio, lnc, invc);
+}
+
 // fp64 digamma: recurrence psi(x) = psi(x+1) - 1/x up to x >= 10, then the asymptotic
 // series ln x - 1/(2x) - sum_n B_2n / (2n x^2n) through x^-14 (truncation < 1e-16 there).
 __device__ __forceinline__ double digamma_f64(double x) {

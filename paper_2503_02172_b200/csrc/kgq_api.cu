@@ -687,7 +687,16 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st && c.model == KGQ_BETAE) {
     st = alloc_split(ctx, &ctx->uv, ctx->np, 2 * d, "uv table");
     if (!st) st = dalloc(ctx, &ctx->Esum, (size_t)ctx->np, "entity sums");
-    if (!st) st = dalloc(ctx, &ctx->uvsums, (size_t)(2 * d), "uv sums");
+    if (!st) st = dalloc(ctx, &ctx->uvsums, (size_t)(2 * d + 2 * kLogTab), "uv sums + log table");
+    if (!st) {  // ln c_i and 1 / c_i, c_i = 1 + i / kLogTab, after the sums (common.cuh log_tab)
+      double tab[2 * kLogTab];
+      for (int i = 0; i < kLogTab; ++i) {
+        const double ci = 1.0 + (double)i / kLogTab;
+        tab[i] = std::log(ci);
+        tab[kLogTab + i] = 1.0 / ci;
+      }
+      CK(cudaMemcpy(ctx->uvsums + 2 * d, tab, sizeof tab, cudaMemcpyHostToDevice), "log table");
+    }
     if (!st) st = alloc_split(ctx, &ctx->Atc, 2 * ctx->bchunk, 2 * d, "tc query rows");
     if (!st) st = dalloc(ctx, &ctx->Ptc, (size_t)(2 * ctx->bchunk), "tc query sums");
   }

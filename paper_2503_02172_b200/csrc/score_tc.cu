@@ -88,6 +88,9 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
   pdl_grid_sync();
   const int r = blockIdx.x;
   __shared__ double red[32];
+  __shared__ double tab[2 * kLogTab];  // ln c_i, 1 / c_i (stored after the [2][d] sums)
+  for (int i = threadIdx.x; i < 2 * kLogTab; i += blockDim.x) tab[i] = sums[2 * d + i];
+  __syncthreads();
   double p = 0.0;
   const double inv = 1.0 / (double)ns;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
@@ -95,7 +98,7 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
     store_split(A, (int64_t)r * A.ld + j, a);
     store_split(A, (int64_t)r * A.ld + d + j, b);
     const double da = a, db = b;
-    p += lnbeta_f64(da, db) + da * sums[j] * inv + db * sums[d + j] * inv;
+    p += lnbeta_f64_tab(da, db, tab, tab + kLogTab) + da * sums[j] * inv + db * sums[d + j] * inv;
   }
   p = warp_sum(p);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
@@ -120,6 +123,9 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
   pdl_grid_sync();
   const int r = blockIdx.x;
   __shared__ double red[32];
+  __shared__ double tab[2 * kLogTab];  // ln c_i, 1 / c_i (stored after the [2][d] sums)
+  for (int i = threadIdx.x; i < 2 * kLogTab; i += blockDim.x) tab[i] = sums[2 * d + i];
+  __syncthreads();
   double p = 0.0;
   const double inv = 1.0 / (double)ns;
   const int64_t srow = srcrow ? srcrow[r] : (int64_t)(r % nout) * B + b0 + r / nout;
@@ -129,7 +135,7 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
     store_split(A, a0 + j, a);
     store_split(A, a0 + d + j, b);
     const double da = a, db = b;
-    p += lnbeta_f64(da, db) + da * sums[j] * inv + db * sums[d + j] * inv;
+    p += lnbeta_f64_tab(da, db, tab, tab + kLogTab) + da * sums[j] * inv + db * sums[d + j] * inv;
   }
   p = warp_sum(p);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
