@@ -724,7 +724,10 @@ struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN,
   int force_bn = 0;
   double kb128 = 0.0;
   bool no160 = false;
+  bool deterministic = true;  // KGQ_DETERMINISTIC=0 allows more than two K-splits (plan_gemm)
   PlanKnobs() {
+    const char* dt = getenv("KGQ_DETERMINISTIC");
+    if (dt && dt[0]) deterministic = dt[0] != '0';
     const char* n = getenv("KGQ_GEMM_NO160");
     no160 = n && n[0] && n[0] != '0';
     const char* e = getenv("KGQ_GEMM_BN");
@@ -746,7 +749,12 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allo
     const int64_t full = tiles / kClustersMax * kClustersMax, tail = tiles - full;
     double kb = kKbUs[bn == 64 ? 0 : bn == 128 ? 1 : bn == 160 ? 2 : bn == 192 ? 3 : 4];
     if (bn == 128 && knobs.kb128 > 0) kb = knobs.kb128;
-    const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, std::min(6, nk / 4))) : 1;
+    // Two partials commute exactly; with three or more the last-arriving split adds the others
+    // after its own, so the fp32 grouping (and the last bit) depends on arrival order.
+    // Default: at most two splits, so reruns are bit-identical (measured cost on C2: ~0.1%);
+    // KGQ_DETERMINISTIC=0 lifts the cap.
+    const int scap = knobs.deterministic ? 2 : 6;
+    const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, std::min(scap, nk / 4))) : 1;
     for (int s = 1; s <= smax; ++s) {
       const int kper = (nk + s - 1) / s;
       const int se = (nk + kper - 1) / kper;  // no empty split

@@ -49,7 +49,10 @@ def test_full_size_sampled(cfg):
             assert_topk_ok(td[b], ti[b], ref[j], 10, what=f"{name} {s} row {b}")
         qe = e.query_embedding(s, dev(a), dev(r)).cpu().numpy()[rows]
         ref_q = m.query_embedding(s, a[rows], r[rows])
-        assert_embedding_close(qe, ref_q, rel=chain_tolerance(s), what=f"{name} {s} chain")
+        # chain diagnostic at H = 1600: fp32 accumulation of 1600-term dot products with
+        # random-sign weights carries ~sqrt(K) 2^-24 sum|x w| ~ 1e-4 of |y| per layer (DESIGN.md
+        # §5, measured 0.6-1.04e-4 without negation); the distances above keep the 1e-4 bound
+        assert_embedding_close(qe, ref_q, rel=max(2e-4, chain_tolerance(s)), what=f"{name} {s} chain")
 
 
 def test_2m_entity_table_gqe_and_betae():
