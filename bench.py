@@ -303,9 +303,17 @@ def main():
     import torch.distributed as dist
     from paper_2503_02172_b200.sharded import ShardedEngine
 
+    # KGQ_BENCH_ONE_GPU=1 (testing the N > 1 code path on a one-GPU box only): every rank on
+    # cuda:0 with the gloo backend -- the numbers of such a run mean nothing
+    one_gpu = os.environ.get("KGQ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t = synth.make_tables("betae", N_ENT, N_REL, DIM, hidden=HID, seed=SEED)
     seng = ShardedEngine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K, device=local,
                          merge=args.merge)
