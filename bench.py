@@ -545,7 +545,7 @@ def main():
             "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",
                          "bound": "tensor", "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
                          "frac": achieved / peak_tc, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16 {peaks['bf16_tflops']:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
+                         "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC; burst, the larger denominator)",
                          "work": "useful fp32 FLOPs 2MNK per GEMM launch",
                          "launches": d_n + s_n,
                          "parts": {"dense": {"ms_per_step": d_ms / prof_steps, "tflops": ach(d_fl, d_ms),
