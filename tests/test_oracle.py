@@ -102,6 +102,60 @@ def test_q2b_box_distance_worked_example():
     np.testing.assert_allclose(d, g["dist"], rtol=1e-14)
 
 
+def betae_identity_mlp_tables():
+    """GOLD betae_anchor_identity_mlp: d = 1, one hidden layer of width 2 that copies
+    [alpha; beta] (W1 = [[1,0,0],[0,1,0]]), W0 = I2, zero biases, zero attention weights."""
+    g = GOLD["betae_anchor_identity_mlp"]
+    t = synth.make_tables("betae", 3, 1, 1, hidden=2, n_layers=1, seed=1)
+    t["entity"] = np.array(g["entity_raw"], np.float32)
+    t["relation"][:] = 0.7            # must not leak into the output: W1's relation column is 0
+    t["W:proj.layer1"] = np.array([[1, 0, 0], [0, 1, 0]], np.float32)
+    t["W:proj.layer0"] = np.eye(2, dtype=np.float32)
+    for k in list(t):
+        if k.startswith("b:") or k.startswith("W:inter"):
+            t[k] = np.zeros_like(t[k])
+    return g, O.Model("betae", t, dim=1, n_layers=1)
+
+
+def test_betae_anchor_regulariser_worked_example():
+    """Q12 pin (Eq. 3: Beta parameters > 0): anchors are the regularised entity rows
+    clamp(x + 1, 0.05, 1e9) -- raw 1.0 -> 2.0, raw -3.0 -> 0.05 (floor), raw 0.5 -> 1.5 -- and
+    an identity-copy MLP shows them through the projection terminal (clamp(y + 1)): a missing
+    or doubled anchor regulariser changes every value below."""
+    g, m = betae_identity_mlp_tables()
+    np.testing.assert_array_equal(m.anchor(np.arange(3)), np.array(g["anchor_view"]))
+    assert m.anchor(np.array([1]))[0, 0] == 0.05 and m.anchor(np.array([0]))[0, 0] == 2.0
+    q = m.query_embedding("1p", np.arange(3)[:, None], np.zeros((3, 1), np.int64))[:, 0]
+    np.testing.assert_allclose(q, np.array(g["query_1p"]), rtol=1e-15)
+    d = m.scores("1p", np.array([[0]]), np.array([[0]]))[0, 0]   # KL(Beta(2,2) || Beta(3,3))
+    assert d == pytest.approx(g["dist_1p_anchor0_to_entity0"], rel=1e-13)
+    two = g["query_2i_zero_attention"]
+    q2 = m.query_embedding("2i", np.array([two["anchors"]]), np.zeros((1, 2), np.int64))[0, 0]
+    np.testing.assert_allclose(q2, two["value"], rtol=1e-15)
+    # identical Beta(2,2) anchors through 2i -> the 1p embedding Beta(3,3)
+    q3 = m.query_embedding("2i", np.array([[0, 0]]), np.zeros((1, 2), np.int64))[0, 0]
+    np.testing.assert_allclose(q3, [3.0, 3.0], rtol=1e-15)
+
+
+def test_q2b_offset_projection_worked_example():
+    """Q11 pin: the Q2B projection translates the box, (c, o) -> (c + R_c[r], o + R_o[r]) with
+    the identity offset activation and a zero anchor offset (Q10); hand-worked 1p / 2p boxes
+    and box distances (GOLD q2b_offset_projection)."""
+    g = GOLD["q2b_offset_projection"]
+    t = synth.make_tables("q2b", 5, 2, 2, seed=1)
+    t["entity"] = np.array(g["entity"], np.float32)
+    t["relation"] = np.array(g["relation"], np.float32)
+    t["offset"] = np.array(g["offset"], np.float32)
+    m = O.Model("q2b", t, dim=2)
+    q1 = m.query_embedding("1p", np.array([[0]]), np.array([[0]]))[0, 0]
+    np.testing.assert_allclose(q1, g["box_1p"], rtol=1e-7)
+    np.testing.assert_allclose(m.scores("1p", np.array([[0]]), np.array([[0]]))[0], g["dist_1p"], rtol=1e-6)
+    q2 = m.query_embedding("2p", np.array([[0]]), np.array([[0, 1]]))[0, 0]
+    np.testing.assert_allclose(q2, g["box_2p"], rtol=1e-7)
+    d2 = m.scores("2p", np.array([[0]]), np.array([[0, 1]]))[0]
+    np.testing.assert_allclose(d2[g["dist_2p_entities"]], g["dist_2p"], rtol=1e-6, atol=1e-7)
+
+
 def test_q2b_zero_offsets_equals_gqe_l1():
     t = tiny_tables("q2b")
     t["offset"][:] = 0
