@@ -1,4 +1,4 @@
-// tcgen05 3xTF32 GEMM core shared by the dense layers (linear_tc.cu) and the tensor-core
+// tcgen05 bf16x3 GEMM core shared by the dense layers (linear_tc.cu) and the tensor-core
 // BetaE scorer (score_tc.cu).
 //
 // acc[m, n] = sum_k A[m, k] W[n, k] in bf16x3: every fp32 operand is held as three bf16 planes
@@ -197,6 +197,24 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t da, uint6
       "}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
+// A operand from TMEM ("ts" form): D[tmem] (+)= A[tmem] . B[smem]; tmem_a = the A slice's first
+// column (128 lanes = this CTA's rows, 8 columns = 16 bf16 of K per lane).
+__device__ __forceinline__ void mma_bf16_2sm_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate));
+}
+// smem -> TMEM copy of a 128-row x 32-byte K-major slice (one K16 step of one bf16 plane of A),
+// issued by the leader for both CTAs of the pair (each copies its own smem into its own TMEM);
+// ordered before the MMAs issued after it (tcgen05.cp -> tcgen05.mma pipeline order).
+__device__ __forceinline__ void tmem_cp_2sm_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {  // arrive on bar in both CTAs
   const uint16_t mask = 3;
   asm volatile(
@@ -224,11 +242,14 @@ __device__ unsigned long long* g_tc_trace;
 #endif
 
 // K-blocks per TMEM partial (see header comment).
-// 8 for bf16x3: 2.7e-7 of sum|x w| at K = 1600 (DRAIN 2: 7.3e-8, 4: 1.4e-7, 16: 5.3e-7;
-// scripts/tc_bn_check.cu 1600) and 5-8% faster mainloops than DRAIN 2 -- a longer partial
-// hides the accumulator hand-off (MMA commit -> epilogue drain -> accempty) better.
+// 4 for bf16x3: 1.4e-7 of sum|x w| at K = 1600 (DRAIN 2: 7.3e-8, 8: 2.7e-7, 16: 5.3e-7;
+// scripts/tc_bn_check.cu 1600).  Round 2 measured the chain embeddings of every structure
+// against the oracle at DRAIN 8 / 4 / 2 (profiles/r02/chain_err_drain.txt): DRAIN 8 left the
+// non-negation structures at up to 9.9e-5 of the 1e-4 bound, DRAIN 4 at <= 6.5e-5 for -1% of
+// the C2 step, DRAIN 2 at <= 2.6e-5 for -5% (its shorter partials hide the accumulator hand-off
+// -- MMA commit -> epilogue drain -> accempty -- worse).
 #ifndef KGQ_TC_DRAIN
-#define KGQ_TC_DRAIN 8
+#define KGQ_TC_DRAIN 4
 #endif
 constexpr int DRAIN = KGQ_TC_DRAIN;
 
@@ -236,9 +257,11 @@ constexpr int DRAIN = KGQ_TC_DRAIN;
 // epilogue warp owns NBUF x 4 KB holding a 32-row chunk of its columns in the 128-byte
 // (1 plane, 32 columns) or 64-byte (2 planes, 16 columns each) swizzled layout of the output
 // tensor map's box -- then the barriers.
+#ifndef KGQ_TC_ATMEM
+#define KGQ_TC_ATMEM 0
+#endif
 template <int BN, bool NBUF2 = false>
 struct Layout {
-  static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int A_BYTES = BM * BK * 2;         // one bf16 plane of A: 8 KB
   static constexpr int W_BYTES = (BN / 2) * BK * 2;   // one plane of this CTA's half of the W tile
   static constexpr int STAGE_BYTES = 3 * A_BYTES + 3 * W_BYTES;
@@ -252,6 +275,12 @@ struct Layout {
   static constexpr int FIT2 = (BUDGET - 2 * EPI_WARPS * BUF_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = NBUF2 && FIT2 >= 3 ? (FIT2 > 6 ? 6 : FIT2) : (FIT > 6 ? 6 : FIT);
   static constexpr int NBUF = BUDGET - STAGES * STAGE_BYTES >= 2 * EPI_WARPS * BUF_BYTES ? 2 : 1;
+  // A operand staged in TMEM (tcgen05.cp once per plane and K16 step, then the six MMAs read A
+  // from TMEM and only B from shared memory): one 48-column A slot (3 planes x 2 K16 steps x 8
+  // columns) per operand stage next to the two BN-column accumulators, if it fits in 512.
+  static constexpr int A_SLOT_COLS = 3 * (BK / 16) * 8;
+  static constexpr bool ATM = KGQ_TC_ATMEM && 2 * BN + A_SLOT_COLS * STAGES <= 512;
+  static constexpr int TMEM_COLS = ATM ? 512 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = STG_OFF + NBUF * EPI_WARPS * BUF_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
@@ -421,17 +450,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
           const uint32_t a0 = st, a1 = st + L::A_BYTES, a2 = st + 2 * L::A_BYTES;
           const uint32_t w0 = st + 3 * L::A_BYTES, w1 = w0 + L::W_BYTES, w2 = w1 + L::W_BYTES;
+          if constexpr (L::ATM) {
+            // A slot of this stage (free: the MMAs of the stage's previous K-block completed
+            // before the producer refilled the stage, i.e. before full[s] fired)
+            const uint32_t ta = tmem + 2 * BN + s * L::A_SLOT_COLS;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 32 bytes per MMA along K
-            const uint32_t off = kk * 32;
-            // small terms first; x0 w0 last
-            mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w2 + off), idesc,
-                         (first && kk == 0) ? 0u : 1u);
-            mma_bf16_2sm(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w1 + off), idesc, 1u);
-            mma_bf16_2sm(d, umma_desc_sw64(a2 + off), umma_desc_sw64(w0 + off), idesc, 1u);
-            mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w1 + off), idesc, 1u);
-            mma_bf16_2sm(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w0 + off), idesc, 1u);
-            mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w0 + off), idesc, 1u);
+            for (int p = 0; p < 3; ++p)
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                tmem_cp_2sm_128x256b(ta + (p * (BK / 16) + kk) * 8, umma_desc_sw64(st + p * L::A_BYTES + kk * 32));
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t off = kk * 32;
+              const uint32_t t0 = ta + kk * 8, t1 = t0 + (BK / 16) * 8, t2 = t1 + (BK / 16) * 8;
+              mma_bf16_2sm_ts(d, t0, umma_desc_sw64(w2 + off), idesc, (first && kk == 0) ? 0u : 1u);
+              mma_bf16_2sm_ts(d, t1, umma_desc_sw64(w1 + off), idesc, 1u);
+              mma_bf16_2sm_ts(d, t2, umma_desc_sw64(w0 + off), idesc, 1u);
+              mma_bf16_2sm_ts(d, t0, umma_desc_sw64(w1 + off), idesc, 1u);
+              mma_bf16_2sm_ts(d, t1, umma_desc_sw64(w0 + off), idesc, 1u);
+              mma_bf16_2sm_ts(d, t0, umma_desc_sw64(w0 + off), idesc, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 32 bytes per MMA along K
+              const uint32_t off = kk * 32;
+              // small terms first; x0 w0 last
+              mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w2 + off), idesc,
+                           (first && kk == 0) ? 0u : 1u);
+              mma_bf16_2sm(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w1 + off), idesc, 1u);
+              mma_bf16_2sm(d, umma_desc_sw64(a2 + off), umma_desc_sw64(w0 + off), idesc, 1u);
+              mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w1 + off), idesc, 1u);
+              mma_bf16_2sm(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w0 + off), idesc, 1u);
+              mma_bf16_2sm(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w0 + off), idesc, 1u);
+            }
           }
           mma_commit_2sm(&empty[s]);  // frees the smem stage (both CTAs) once these MMAs have read it
           if ((kr % DRAIN) == DRAIN - 1 || kb == kb1 - 1) mma_commit_2sm(&accfull[a]);
@@ -678,11 +729,8 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
     return -1;
   }
   auto kern = k_gemm<BN, Epi>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<BN, Epi::PLANES == 3>::TOTAL);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  smem_attr_once(kern, Layout<BN, Epi::PLANES == 3>::TOTAL, attr);
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
   if (sc.s_tail <= 1 || !sc.ws || !sc.cnt) {
     sc.full = tiles;

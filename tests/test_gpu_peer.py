@@ -10,7 +10,9 @@ import numpy as np
 import pytest
 import torch
 
+import oracle as O
 import synth
+from parity import assert_topk_ok
 
 pytestmark = pytest.mark.gpu
 
@@ -41,6 +43,7 @@ def test_peer_merge_equals_single_gpu(model, structs, ks):
     t = synth.make_tables(model, N, R, D, hidden=H, seed=5)
     full = Engine(model, N, R, D, hidden=H, max_batch=64, max_k=64)
     full.load_tables(t)
+    m = O.Model(model, t, dim=D)
     for W in (2, 3, 8):
         engs, bufs = peer_ranks(model, t, W)
         for s in structs:
@@ -57,6 +60,11 @@ def test_peer_merge_equals_single_gpu(model, structs, ks):
                     local = [e.submit(s, da, dr, k) for e in engs]   # push to every rank
                     merged = [e.merge_peers(33, k) for e in engs]      # wait + merge on every rank
                     torch.cuda.synchronize()
+                    if rnd == 0 or W == 3:  # the merged lists against the oracle (Q15)
+                        ref = m.scores(s, a, r)
+                        mdn, min_ = merged[-1][0].cpu().numpy(), merged[-1][1].cpu().numpy()
+                        for b in range(33):
+                            assert_topk_ok(mdn[b], min_[b], ref[b], k, what=f"p2p W={W} {s} k={k} row {b}")
                     for rank, (md, mi) in enumerate(merged):
                         assert torch.equal(mi, fi), (model, s, k, W, rnd, rank)
                         assert torch.equal(md, fd), (model, s, k, W, rnd, rank)
@@ -81,6 +89,7 @@ def test_peer_mixed_batch_and_invalid_rows():
     full = Engine("betae", N, R, D, hidden=H, max_batch=128, max_k=32)
     full.load_tables(t)
     fd, fi = full.submit_mixed(groups, 12)
+    m = O.Model("betae", t, dim=D)
     with pytest.raises(KgqError, match="ERANGE"):
         full.check_errors()
     engs, bufs = peer_ranks("betae", t, 3, max_batch=128, max_k=32)
@@ -93,6 +102,15 @@ def test_peer_mixed_batch_and_invalid_rows():
         assert torch.equal(torch.nan_to_num(md, nan=-7.0), torch.nan_to_num(fd, nan=-7.0))
     bad = 9 + 3
     assert torch.all(mi[bad] == -1) and torch.all(torch.isnan(md[bad]))
+    mdn, min_ = md.cpu().numpy(), mi.cpu().numpy()
+    q = 0
+    for s, a, r in groups:   # every valid merged row against the oracle (Q15)
+        an, rn = a.cpu().numpy(), r.cpu().numpy()
+        ok = [b for b in range(an.shape[0]) if q + b != bad]
+        ref = m.scores(s, an[ok], rn[ok])
+        for j, b in enumerate(ok):
+            assert_topk_ok(mdn[q + b], min_[q + b], ref[j], 12, what=f"p2p mixed {s} row {b}")
+        q += an.shape[0]
     for e in engs:
         with pytest.raises(KgqError, match="ERANGE"):
             e.check_errors()
@@ -101,6 +119,9 @@ def test_peer_mixed_batch_and_invalid_rows():
 
 
 def test_peer_missing_rank_times_out_instead_of_hanging():
+    """A rank that never pushes: the merge times out (no GPU hang), its rows are NaN / -1, the
+    session is poisoned on every rank (later merges fail loudly instead of pairing lists of
+    different submits), and kgq_set_peers on every rank restores it."""
     t = synth.make_tables("betae", N, R, D, hidden=H, seed=5)
     os.environ["KGQ_PEER_TIMEOUT_MS"] = "200"
     try:
@@ -108,12 +129,60 @@ def test_peer_missing_rank_times_out_instead_of_hanging():
     finally:
         del os.environ["KGQ_PEER_TIMEOUT_MS"]
     a, r = synth.make_queries("1p", 20, N, R, seed=3)
-    ld, li = engs[0].submit("1p", dev(a), dev(r), 10)  # rank 1 never pushes
+    engs[0].submit("1p", dev(a), dev(r), 10)  # rank 1 never pushes
     md, mi = engs[0].merge_peers(20, 10)
     torch.cuda.synchronize()
     with pytest.raises(KgqError, match="rank 1 did not publish"):
         engs[0].check_errors()
-    assert torch.equal(mi, li) and torch.equal(md, ld)  # rank 1's lists are treated as empty
+    assert torch.all(mi == -1) and torch.all(torch.isnan(md))
+    # both ranks push and merge now, but the session stays closed on both
+    for e in engs:
+        e.submit("1p", dev(a), dev(r), 10)
+    outs = [e.merge_peers(20, 10) for e in engs]
+    torch.cuda.synchronize()
+    for e, (md, mi) in zip(engs, outs):
+        assert torch.all(mi == -1)
+        with pytest.raises(KgqError, match="closed by an earlier timeout"):
+            e.check_errors()
+    # re-registration on every rank reopens it
+    for rk, e in enumerate(engs):
+        e.set_peers(rk, 2, [b.data_ptr() for b in bufs])
+    full = Engine("betae", N, R, D, hidden=H, max_batch=64, max_k=64)
+    full.load_tables(t)
+    fd, fi = full.submit("1p", dev(a), dev(r), 10)
+    for e in engs:
+        e.submit("1p", dev(a), dev(r), 10)
+    outs = [e.merge_peers(20, 10) for e in engs]
+    torch.cuda.synchronize()
+    for e, (md, mi) in zip(engs, outs):
+        e.check_errors()
+        assert torch.equal(mi, fi) and torch.equal(md, fd)
+    for e in engs + [full]:
+        e.close()
+
+
+def test_peer_push_and_merge_are_paired():
+    """A second pushing submit before the merge, or a merge without a push, is rejected
+    (KGQ_ESTATE) instead of racing a peer's read of the same slot."""
+    t = synth.make_tables("gqe", N, R, D, hidden=H, seed=5)
+    engs, bufs = peer_ranks("gqe", t, 2)
+    a, r = synth.make_queries("1p", 8, N, R, seed=1)
+    with pytest.raises(KgqError, match="no pushing submit"):
+        engs[0].merge_peers(8, 5)
+    engs[0].submit("1p", dev(a), dev(r), 5)
+    with pytest.raises(KgqError, match="has not been merged"):
+        engs[0].submit("1p", dev(a), dev(r), 5)
+    with pytest.raises(KgqError, match="has not been merged"):
+        engs[0].submit_host("1p", a, r, 5)
+    with pytest.raises(KgqError, match="has not been merged"):
+        engs[0].submit_mixed([("1p", dev(a), dev(r))], 5)
+    engs[1].submit("1p", dev(a), dev(r), 5)
+    m0 = engs[0].merge_peers(8, 5)
+    m1 = engs[1].merge_peers(8, 5)
+    torch.cuda.synchronize()
+    for e in engs:
+        e.check_errors()
+    assert torch.equal(m0[1], m1[1])
     for e in engs:
         e.close()
 
