@@ -40,7 +40,8 @@ typedef enum {
   KGQ_EUNSUPPORTED = 3, /* e.g. negation structure on GQE / Q2B                        */
   KGQ_ESTATE = 4,       /* missing tables, not finalized, finalized twice                     */
   KGQ_ENOMEM = 5,       /* device allocation failed                                           */
-  KGQ_ECUDA = 6         /* CUDA runtime / launch error                                        */
+  KGQ_ECUDA = 6,        /* CUDA runtime / launch error                                        */
+  KGQ_ENCCL = 7         /* NCCL cannot be loaded, or a collective of the communicator failed  */
 } kgq_status;
 
 typedef enum { KGQ_GQE = 0, KGQ_Q2B = 1, KGQ_BETAE = 2 } kgq_model;
@@ -214,6 +215,40 @@ int64_t kgq_peer_bytes(const kgq_ctx* ctx, int32_t world);
 kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const* peer_bufs);
 kgq_status kgq_merge_peers(kgq_ctx* ctx, int32_t batch, int32_t k, float* out_dist, int32_t* out_id,
                            kgq_stream stream);
+/* ---- multi-GPU data plane: the library's own NCCL communicator ------
+ * One process (one context) per GPU.  NCCL is loaded at run time (the copy the process already
+ * uses, else libnccl.so.2); without it these calls return KGQ_ENCCL and nothing else changes.
+ *
+ * kgq_query_range: the row split of a replicated batch in query-split mode (pure host): rank r
+ *   owns rows [lo, hi) = [min(B, r c), min(B, r c + c)), c = ceil(B / world).
+ * kgq_nccl_unique_id: ncclGetUniqueId into host id[128] (128 bytes).  Call on one rank, send the
+ *   bytes to the others over any channel (e.g. torch.distributed broadcast), then every rank
+ *   calls kgq_comm_init with them.
+ * kgq_comm_init: ncclCommInitRank(world, id, rank) on cfg.device -- collective, every rank of the
+ *   job calls it.  `split` selects the data plane of every later submit (kgq_submit,
+ *   kgq_submit_host[_async], kgq_submit_mixed; all on the caller's stream, no host sync):
+ *   KGQ_SPLIT_ENTITIES (BASELINE north_star: the 2M-entity table sharded): needs
+ *     cfg.world_size == world and cfg.rank == rank.  The batch is replicated; each rank scores
+ *     its entity shard, selects its local top-k, one ncclAllGather exchanges the W [batch, k]
+ *     lists (distance and id, one NCCL group) and the merge kernel (a9) writes the GLOBAL top-k
+ *     to the caller's outputs on every rank.  shard_dist, if given, is this shard's.
+ *     kgq_rank_answers with KGQ_RANK_FILTERED reduces over the shards inside (all-reduce min
+ *     of the answer distances, all-reduce sum of the counts).
+ *   KGQ_SPLIT_QUERIES (small tables, e.g. FB15k-237: the operator chain dominates): needs
+ *     cfg.world_size == 1 (every rank holds all entities).  The batch is replicated; each rank
+ *     runs only its rows kgq_query_range(batch, world, rank) through the whole path and one
+ *     ncclAllGather of the [rows, k] results gives every rank the whole batch's top-k.
+ *     shard_dist must be NULL.  Error reports name the row within the rank's slice.
+ *   Exclusive with kgq_set_peers (N2).  Invalidates captured submit graphs.  Errors: KGQ_ENCCL
+ *   (the NCCL message), KGQ_EINVAL (shape / mode mismatch), KGQ_ESTATE (peers set, or already
+ *   initialised).  kgq_check_errors also reports an asynchronous NCCL error (KGQ_ENCCL).
+ * kgq_comm_destroy: ncclCommDestroy; submits are local again.  kgq_destroy calls it.          */
+typedef enum { KGQ_SPLIT_ENTITIES = 0, KGQ_SPLIT_QUERIES = 1 } kgq_split;
+kgq_status kgq_query_range(int32_t batch, int32_t world, int32_t rank, int32_t* lo, int32_t* hi);
+kgq_status kgq_nccl_unique_id(uint8_t* id);
+kgq_status kgq_comm_init(kgq_ctx* ctx, const uint8_t* id, int32_t world, int32_t rank, int32_t split);
+kgq_status kgq_comm_destroy(kgq_ctx* ctx);
+
 /* N1: filtered ranking of given answers (KGReasoning test protocol behind the
  * paper's MRR consistency check).  Query b's answer set (easy and hard, distinct
  * global ids) is ans_id[ans_off[b] .. ans_off[b+1]) (device int32 CSR, ans_off [batch+1],
@@ -225,15 +260,27 @@ kgq_status kgq_merge_peers(kgq_ctx* ctx, int32_t batch, int32_t k, float* out_di
  *   KGQ_RANK_DIST: writes ans_dist for answers inside this shard, +inf for the others
  *                  (min-reduce it across ranks); count is not touched.
  *   KGQ_RANK_COUNT: reads ans_dist (the reduced one), writes count.
+ *   KGQ_RANK_FILTERED: writes the filtered RANK (1 + the sum over shards of count) into count:
+ *                  one shard, or entity shards with a communicator (kgq_comm_init; the two
+ *                  phases and their all-reduces run inside, on `stream`).
  * Runs the operator chain and the scorer like kgq_submit.  A query with more than 2048
  * answers makes kgq_check_errors() return KGQ_EINVAL. */
-enum { KGQ_RANK_LOCAL = 0, KGQ_RANK_DIST = 1, KGQ_RANK_COUNT = 2 };
+enum { KGQ_RANK_LOCAL = 0, KGQ_RANK_DIST = 1, KGQ_RANK_COUNT = 2, KGQ_RANK_FILTERED = 3 };
 kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
                             const int32_t* rels, const int32_t* ans_off, const int32_t* ans_id,
                             int32_t n_ans, int32_t mode, float* ans_dist, int32_t* count,
                             kgq_stream stream);
+/* MRR / Hits@k of filtered ranks (N1; KGReasoning averaging): ranks int32
+ * [n_ans] (1-based, e.g. from KGQ_RANK_FILTERED) in the CSR layout of ans_off [batch+1];
+ * hard uint8 [n_ans] marks the answers that are scored (the hard answers), NULL = all.  Writes
+ * device fp64 metrics[5] = {MRR, Hits@1, Hits@3, Hits@10, number of queries averaged}: the mean
+ * over queries with at least one scored answer of the per-query mean of 1/rank and [rank <= k].
+ * Device pointers, asynchronous on `stream`, one kernel. */
+kgq_status kgq_rank_metrics(kgq_ctx* ctx, int32_t batch, const int32_t* ans_off, const int32_t* ranks,
+                            const uint8_t* hard, double* metrics, kgq_stream stream);
 /* Synchronise `stream`; KGQ_ERANGE (message names query row and slot) if any submit since
- * the last check saw an out-of-range id, KGQ_ECUDA on an asynchronous CUDA error. */
+ * the last check saw an out-of-range id, KGQ_ECUDA on an asynchronous CUDA error, KGQ_ENCCL on
+ * an asynchronous error of the context's communicator. */
 kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream);
 
 /* ---- introspection (parity / bench) ----------------------------------------------------- */

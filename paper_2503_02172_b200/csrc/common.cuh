@@ -9,6 +9,21 @@
 
 namespace kgq {
 
+// Opt a kernel into more than 48 KB of dynamic shared memory on the CURRENT device.  The
+// attribute is per (function, device): a process-wide "done" flag would leave a second
+// context on another device launching with the 48 KB default (every launch there fails), so
+// the flag is one bit per device, per call site (F = the kernel's function pointer type +
+// the calling template instance).  cudaGetDevice is a host-side lookup (no sync).
+template <class F>
+inline void smem_attr_once(F* kern, int bytes, unsigned long long& done_mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(&done_mask, __ATOMIC_ACQUIRE) & bit) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  __atomic_fetch_or(&done_mask, bit, __ATOMIC_ACQ_REL);
+}
+
 // fp32 tensor held as three bf16 planes, the operand format of the tensor-core GEMMs
 // (tc_gemm.cuh, bf16x3): b0 = RN_bf16(x), b1 = RN_bf16(x - b0), b2 = RN_bf16(x - b0 - b1).
 // Each remainder is exact in fp32 and the last one has <= 8 significant bits, so

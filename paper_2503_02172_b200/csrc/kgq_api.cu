@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "kgq_internal.cuh"
+#include "nccl_dl.h"
 
 using namespace kgq;
 
@@ -466,6 +467,7 @@ const char* kgq_status_string(kgq_status s) {
     case KGQ_ESTATE: return "KGQ_ESTATE";
     case KGQ_ENOMEM: return "KGQ_ENOMEM";
     case KGQ_ECUDA: return "KGQ_ECUDA";
+    case KGQ_ENCCL: return "KGQ_ENCCL";
   }
   return "KGQ_UNKNOWN";
 }
@@ -564,6 +566,8 @@ void kgq_destroy(kgq_ctx* ctx) {
   if (ctx->mix_map_ev) cudaEventDestroy(ctx->mix_map_ev);
   F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage); F(ctx->d_epoch);
+  if (ctx->comm) nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
+  F(ctx->cm_d); F(ctx->cm_i); F(ctx->cg_d); F(ctx->cg_i);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
   clear_mix_graphs(ctx);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -887,17 +891,99 @@ static kgq_status submit_graphed(kgq_ctx* ctx, int32_t s, int32_t B, const int32
   return KGQ_OK;
 }
 
+// ---- N2 host-side pairing of pushes and merges (peer.cuh) ----
+constexpr int64_t kPeerHdrBytes = 256;
+static int64_t peer_flag_bytes(const kgq_ctx* ctx, int world) {  // header + flags, 256-byte aligned
+  return kPeerHdrBytes + ((int64_t)2 * world * ctx->cfg.max_batch * (int64_t)sizeof(uint32_t) + 255) / 256 * 256;
+}
+// A pushing submit and its merge come in pairs (peer.cuh): reject a second push before the merge.
+static kgq_status peer_push_check(kgq_ctx* ctx) {
+  if (ctx->peers.on() && ctx->push_outstanding)
+    return fail(ctx, KGQ_ESTATE, "peered context: the previous submit's top-k push has not been merged "
+                                 "(call kgq_merge_peers after every submit)");
+  return KGQ_OK;
+}
+static kgq_status peer_push_done(kgq_ctx* ctx, kgq_status st) {
+  if (st == KGQ_OK && ctx->peers.on()) ctx->push_outstanding = true;
+  return st;
+}
+
+// ---- multi-GPU data plane (kgq_comm_init): the context's NCCL communicator ------------------
+static void query_range(int32_t B, int32_t W, int32_t r, int32_t* lo, int32_t* hi) {
+  const int32_t c = (B + W - 1) / W;
+  *lo = std::min<int64_t>(B, (int64_t)r * c);
+  *hi = std::min<int64_t>(B, (int64_t)*lo + c);
+}
+static kgq_status nccl_fail(kgq_ctx* ctx, ncclResult_t r, const char* what) {
+  return fail(ctx, KGQ_ENCCL, "%s: %s", what, nccl_api().GetErrorString(r));
+}
+// All-gather n floats + n ints per rank (this rank's cm_d / cm_i) into cg_d / cg_i [W * n], one
+// NCCL group (one kernel) on the caller's stream.
+static kgq_status comm_gather(kgq_ctx* ctx, size_t n, cudaStream_t cs) {
+  const NcclApi& api = nccl_api();
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->comm);
+  ncclResult_t r = api.GroupStart();
+  if (r == ncclSuccess) r = api.AllGather(ctx->cm_d, ctx->cg_d, n, ncclFloat32, comm, cs);
+  if (r == ncclSuccess) r = api.AllGather(ctx->cm_i, ctx->cg_i, n, ncclInt32, comm, cs);
+  const ncclResult_t r2 = api.GroupEnd();
+  if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllGather");
+  if (r2 != ncclSuccess) return nccl_fail(ctx, r2, "ncclGroupEnd");
+  return KGQ_OK;
+}
+// The local (one-shard, one-device) path: a captured graph when possible, else eager launches.
+static kgq_status submit_local(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t* anchors, const int32_t* rels,
+                               int32_t k, float* td, int32_t* ti, float* sd, cudaStream_t cs) {
+  if (ctx->use_graphs && !sd && B <= ctx->bchunk) return submit_graphed(ctx, s, B, anchors, rels, k, td, ti, cs);
+  return submit_impl(ctx, s, B, anchors, rels, k, td, ti, sd, cs);
+}
+// A submit of the replicated batch through the communicator's data plane (kgq.h kgq_comm_init).
+static kgq_status submit_comm(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t* anchors, const int32_t* rels,
+                              int32_t k, float* td, int32_t* ti, float* sd, cudaStream_t cs) {
+  const int W = ctx->comm_world;
+  if (ctx->comm_split == KGQ_SPLIT_ENTITIES) {  // local top-k -> all-gather -> merge (a9)
+    kgq_status st = submit_local(ctx, s, B, anchors, rels, k, ctx->cm_d, ctx->cm_i, sd, cs);
+    if (st) return st;
+    int L = ctx->launches;
+    if ((st = comm_gather(ctx, (size_t)B * k, cs))) return st;
+    L += launch_merge(W, B, k, ctx->cg_d, ctx->cg_i, td, ti, cs);
+    ctx->launches = L;
+    CK(cudaGetLastError(), "merge launch");
+    return KGQ_OK;
+  }
+  if (sd) return fail(ctx, KGQ_EINVAL, "shard_dist is not available in query-split mode");
+  const Plan* P = plan_of(s);
+  int32_t lo, hi;
+  query_range(B, W, ctx->comm_rank, &lo, &hi);
+  const int32_t c = (B + W - 1) / W;
+  ctx->launches = 0;
+  if (hi > lo) {
+    kgq_status st = submit_local(ctx, s, hi - lo, anchors + (int64_t)lo * P->n_anchor,
+                                 rels + (int64_t)lo * P->n_rel, k, ctx->cm_d, ctx->cm_i, nullptr, cs);
+    if (st) return st;
+  }
+  kgq_status st = comm_gather(ctx, (size_t)c * k, cs);  // rank r's rows land at [r c, r c + c)
+  if (st) return st;
+  CK(cudaMemcpyAsync(td, ctx->cg_d, (size_t)B * k * sizeof(float), cudaMemcpyDeviceToDevice, cs), "gather copy");
+  CK(cudaMemcpyAsync(ti, ctx->cg_i, (size_t)B * k * sizeof(int32_t), cudaMemcpyDeviceToDevice, cs), "gather copy");
+  return KGQ_OK;
+}
+static kgq_status submit_dev(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t* anchors, const int32_t* rels,
+                             int32_t k, float* td, int32_t* ti, float* sd, cudaStream_t cs) {
+  return ctx->comm ? submit_comm(ctx, s, B, anchors, rels, k, td, ti, sd, cs)
+                   : submit_local(ctx, s, B, anchors, rels, k, td, ti, sd, cs);
+}
+
 kgq_status kgq_submit(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors, const int32_t* rels,
                       int32_t k, float* topk_dist, int32_t* topk_id, float* shard_dist, kgq_stream stream) {
   kgq_status st = check_submit(ctx, s, batch, k, true);
   if (st) return st;
   if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
   if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  if ((st = peer_push_check(ctx))) return st;
   DeviceGuard g(ctx->cfg.device);
   ctx->push_row0 = ctx->peers.on() ? 0 : -1;
-  if (ctx->use_graphs && !shard_dist && batch <= ctx->bchunk)
-    return submit_graphed(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, (cudaStream_t)stream);
-  return submit_impl(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, shard_dist, (cudaStream_t)stream);
+  return peer_push_done(ctx, submit_dev(ctx, s, batch, anchors, rels, k, topk_dist, topk_id, shard_dist,
+                                        (cudaStream_t)stream));
 }
 
 // ---- mixed-structure batches ---------------------------------------------
@@ -1129,10 +1215,9 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
   return KGQ_OK;
 }
 
-kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures, const int32_t* batches,
-                            const int32_t* anchors, const int32_t* rels, int32_t k, float* topk_dist,
-                            int32_t* topk_id, kgq_stream stream) {
-  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+static kgq_status submit_mixed_impl(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures,
+                                    const int32_t* batches, const int32_t* anchors, const int32_t* rels, int32_t k,
+                                    float* topk_dist, int32_t* topk_id, kgq_stream stream) {
   if (n_groups < 0 || (n_groups > 0 && (!structures || !batches)))
     return fail(ctx, KGQ_EINVAL, "mixed submit: bad group arrays");
   int64_t Q = 0;
@@ -1241,6 +1326,72 @@ kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* struc
   return KGQ_OK;
 }
 
+kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures, const int32_t* batches,
+                            const int32_t* anchors, const int32_t* rels, int32_t k, float* topk_dist,
+                            int32_t* topk_id, kgq_stream stream) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  kgq_status st = peer_push_check(ctx);
+  if (st) return st;
+  int64_t Q = 0;
+  for (int i = 0; structures && batches && i < n_groups; ++i) Q += batches[i] > 0 ? batches[i] : 0;
+  if (!ctx->comm || Q == 0) {
+    st = submit_mixed_impl(ctx, n_groups, structures, batches, anchors, rels, k, topk_dist, topk_id, stream);
+    return Q > 0 ? peer_push_done(ctx, st) : st;
+  }
+  // communicator data plane (kgq_comm_init), as submit_comm for one structure
+  for (int i = 0; i < n_groups; ++i)
+    if ((st = check_submit(ctx, structures[i], batches[i], k, true))) return st;
+  if (Q > ctx->cfg.max_batch)
+    return fail(ctx, KGQ_EINVAL, "mixed submit: %lld queries > max_batch %d", (long long)Q, ctx->cfg.max_batch);
+  if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  DeviceGuard dg(ctx->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int W = ctx->comm_world;
+  if (ctx->comm_split == KGQ_SPLIT_ENTITIES) {
+    st = submit_mixed_impl(ctx, n_groups, structures, batches, anchors, rels, k, ctx->cm_d, ctx->cm_i, stream);
+    if (st) return st;
+    int L = ctx->launches;
+    if ((st = comm_gather(ctx, (size_t)Q * k, cs))) return st;
+    L += launch_merge(W, (int)Q, k, ctx->cg_d, ctx->cg_i, topk_dist, topk_id, cs);
+    ctx->launches = L;
+    CK(cudaGetLastError(), "merge launch");
+    return KGQ_OK;
+  }
+  // query split: this rank's global rows [lo, hi) cut across the groups; the groups' anchor /
+  // relation blocks are concatenated in row order, so the slice's inputs are contiguous
+  int32_t lo, hi;
+  query_range((int32_t)Q, W, ctx->comm_rank, &lo, &hi);
+  const int32_t c = ((int32_t)Q + W - 1) / W;
+  std::vector<int32_t> ss, bs;
+  const int32_t *a_loc = nullptr, *r_loc = nullptr;
+  int64_t q0 = 0, ao = 0, ro = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    const Plan* P = plan_of(structures[i]);
+    const int64_t b0 = std::max<int64_t>(q0, lo), b1 = std::min<int64_t>(q0 + batches[i], hi);
+    if (b1 > b0) {
+      if (!a_loc) {
+        a_loc = anchors + ao + (b0 - q0) * P->n_anchor;
+        r_loc = rels + ro + (b0 - q0) * P->n_rel;
+      }
+      ss.push_back(structures[i]);
+      bs.push_back((int32_t)(b1 - b0));
+    }
+    q0 += batches[i];
+    ao += (int64_t)batches[i] * P->n_anchor;
+    ro += (int64_t)batches[i] * P->n_rel;
+  }
+  ctx->launches = 0;
+  if (!ss.empty()) {
+    st = submit_mixed_impl(ctx, (int32_t)ss.size(), ss.data(), bs.data(), a_loc, r_loc, k, ctx->cm_d, ctx->cm_i,
+                           stream);
+    if (st) return st;
+  }
+  if ((st = comm_gather(ctx, (size_t)c * k, cs))) return st;
+  CK(cudaMemcpyAsync(topk_dist, ctx->cg_d, (size_t)Q * k * sizeof(float), cudaMemcpyDeviceToDevice, cs), "gather copy");
+  CK(cudaMemcpyAsync(topk_id, ctx->cg_i, (size_t)Q * k * sizeof(int32_t), cudaMemcpyDeviceToDevice, cs), "gather copy");
+  return KGQ_OK;
+}
+
 kgq_status kgq_submit_host(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
                            const int32_t* rels, int32_t k, float* topk_dist, int32_t* topk_id,
                            kgq_stream stream) {
@@ -1257,6 +1408,7 @@ kgq_status kgq_submit_host_async(kgq_ctx* ctx, int32_t s, int32_t batch, const i
   if (st) return st;
   if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
   if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL host pointer");
+  if ((st = peer_push_check(ctx))) return st;
   DeviceGuard g(ctx->cfg.device);
   cudaStream_t cs = (cudaStream_t)stream;
   const Plan* P = plan_of(s);
@@ -1265,13 +1417,10 @@ kgq_status kgq_submit_host_async(kgq_ctx* ctx, int32_t s, int32_t batch, const i
   CK(cudaMemcpyAsync(ctx->d_rel_stage, rels, (size_t)batch * P->n_rel * sizeof(int32_t),
                      cudaMemcpyHostToDevice, cs), "relation upload");
   ctx->push_row0 = ctx->peers.on() ? 0 : -1;
-  if (ctx->use_graphs && batch <= ctx->bchunk)
-    st = submit_graphed(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage,
-                        ctx->d_topi_stage, cs);
-  else
-    st = submit_impl(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage,
-                     ctx->d_topi_stage, nullptr, cs);
+  st = submit_dev(ctx, s, batch, ctx->d_anchor_stage, ctx->d_rel_stage, k, ctx->d_topd_stage, ctx->d_topi_stage,
+                  nullptr, cs);
   if (st) return st;
+  peer_push_done(ctx, st);
   CK(cudaMemcpyAsync(topk_dist, ctx->d_topd_stage, (size_t)batch * k * sizeof(float), cudaMemcpyDeviceToHost, cs),
      "top-k download");
   CK(cudaMemcpyAsync(topk_id, ctx->d_topi_stage, (size_t)batch * k * sizeof(int32_t), cudaMemcpyDeviceToHost, cs),
@@ -1315,6 +1464,12 @@ kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
   if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
   DeviceGuard g(ctx->cfg.device);
   CK(cudaStreamSynchronize((cudaStream_t)stream), "stream synchronize");
+  if (ctx->comm) {
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = nccl_api().CommGetAsyncError(static_cast<ncclComm_t>(ctx->comm), &ar);
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommGetAsyncError");
+    if (ar != ncclSuccess) return nccl_fail(ctx, ar, "communicator (asynchronous)");
+  }
   int32_t e[4];
   CK(cudaMemcpy(e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost), "error word");
   if (e[0] == 2) {
@@ -1323,8 +1478,14 @@ kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
   }
   if (e[0] == 3) {
     CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
-    return fail(ctx, KGQ_ESTATE, "kgq_merge_peers: rank %d did not publish row %d within %lld ms", e[2], e[1],
+    return fail(ctx, KGQ_ESTATE, "kgq_merge_peers: rank %d did not publish row %d within %lld ms; the peer "
+                "session is closed (every rank must call kgq_set_peers again)", e[2], e[1],
                 ctx->peer_timeout_ns / 1000000);
+  }
+  if (e[0] == 4) {
+    CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
+    return fail(ctx, KGQ_ESTATE, "kgq_merge_peers: the peer session was closed by an earlier timeout; every "
+                "rank must call kgq_set_peers again");
   }
   if (e[0]) {
     CK(cudaMemset(ctx->d_err, 0, sizeof e), "error reset");
@@ -1335,10 +1496,6 @@ kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
 }
 
 // ---- N2: fused top-k all-gather over peer memory (peer.cuh) --------------------------------
-static int64_t peer_flag_bytes(const kgq_ctx* ctx, int world) {
-  return ((int64_t)2 * world * ctx->cfg.max_batch * (int64_t)sizeof(uint32_t) + 255) / 256 * 256;
-}
-
 int64_t kgq_peer_bytes(const kgq_ctx* ctx, int32_t world) {
   if (!ctx || world < 1 || world > kMaxPeers) return -1;
   return peer_flag_bytes(ctx, world) +
@@ -1347,6 +1504,8 @@ int64_t kgq_peer_bytes(const kgq_ctx* ctx, int32_t world) {
 
 kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const* peer_bufs) {
   if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (ctx->comm && world != 0)
+    return fail(ctx, KGQ_ESTATE, "kgq_set_peers: the context has a communicator (kgq_comm_destroy first)");
   DeviceGuard g(ctx->cfg.device);
   for (auto& gr : ctx->graphs) {  // captured submits bake in the old push arguments
     if (gr.pending) harvest(ctx, gr.evs, false);
@@ -1356,6 +1515,7 @@ kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const*
   clear_mix_graphs(ctx);
   if (world == 0) {
     ctx->peers = PeerPush{};
+    ctx->push_outstanding = false;
     return KGQ_OK;
   }
   if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
@@ -1378,7 +1538,8 @@ kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const*
   pp.epoch = ctx->d_epoch;
   const int64_t fb = peer_flag_bytes(ctx, world);
   for (int p = 0; p < world; ++p) {
-    pp.flag[p] = static_cast<uint32_t*>(peer_bufs[p]);
+    pp.hdr[p] = static_cast<uint32_t*>(peer_bufs[p]);
+    pp.flag[p] = reinterpret_cast<uint32_t*>(static_cast<char*>(peer_bufs[p]) + kPeerHdrBytes);
     pp.key[p] = reinterpret_cast<unsigned long long*>(static_cast<char*>(peer_bufs[p]) + fb);
   }
   CK(cudaMemset(peer_bufs[rank], 0, (size_t)kgq_peer_bytes(ctx, world)), "peer buffer reset");
@@ -1386,6 +1547,7 @@ kgq_status kgq_set_peers(kgq_ctx* ctx, int32_t rank, int32_t world, void* const*
   CK(cudaMemcpy(ctx->d_epoch, ep0, sizeof ep0, cudaMemcpyHostToDevice), "peer epoch reset");
   CK(cudaDeviceSynchronize(), "kgq_set_peers");
   ctx->peers = pp;
+  ctx->push_outstanding = false;
   return KGQ_OK;
 }
 
@@ -1397,12 +1559,117 @@ kgq_status kgq_merge_peers(kgq_ctx* ctx, int32_t batch, int32_t k, float* out_di
   if (k < 1 || k > ctx->cfg.max_k) return fail(ctx, KGQ_EINVAL, "k %d outside [1, max_k=%d]", k, ctx->cfg.max_k);
   if (batch == 0) { ctx->launches = 0; return KGQ_OK; }
   if (!out_dist || !out_id) return fail(ctx, KGQ_EINVAL, "NULL device pointer");
+  if (!ctx->push_outstanding)
+    return fail(ctx, KGQ_ESTATE, "kgq_merge_peers: no pushing submit since the last merge on this rank");
+  ctx->push_outstanding = false;
   DeviceGuard g(ctx->cfg.device);
   PeerPush pp = ctx->peers;
   pp.row0 = 0;
   ctx->launches = launch_peer_merge(pp, batch, k, out_dist, out_id, ctx->d_err, ctx->peer_timeout_ns,
                                     (cudaStream_t)stream);
   CK(cudaGetLastError(), "kgq_merge_peers launch");
+  return KGQ_OK;
+}
+
+kgq_status kgq_query_range(int32_t batch, int32_t world, int32_t rank, int32_t* lo, int32_t* hi) {
+  if (batch < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi)
+    return fail(nullptr, KGQ_EINVAL, "kgq_query_range: batch %d, world %d, rank %d", batch, world, rank);
+  query_range(batch, world, rank, lo, hi);
+  return KGQ_OK;
+}
+
+kgq_status kgq_nccl_unique_id(uint8_t* id) {
+  if (!id) return fail(nullptr, KGQ_EINVAL, "kgq_nccl_unique_id: id is NULL");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(nullptr, KGQ_ENCCL, "%s", api.why.c_str());
+  ncclUniqueId u;
+  static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+  ncclResult_t r = api.GetUniqueId(&u);
+  if (r != ncclSuccess) return fail(nullptr, KGQ_ENCCL, "ncclGetUniqueId: %s", api.GetErrorString(r));
+  memcpy(id, &u, sizeof u);
+  return KGQ_OK;
+}
+
+kgq_status kgq_comm_init(kgq_ctx* ctx, const uint8_t* id, int32_t world, int32_t rank, int32_t split) {
+  if (!ctx || !id) return fail(ctx, KGQ_EINVAL, "kgq_comm_init: NULL argument");
+  if (ctx->comm) return fail(ctx, KGQ_ESTATE, "kgq_comm_init: the context already has a communicator");
+  if (ctx->peers.on()) return fail(ctx, KGQ_ESTATE, "kgq_comm_init: peers are set (kgq_set_peers(ctx, 0, 0, NULL) first)");
+  if (world < 1 || world > 4096 || rank < 0 || rank >= world)
+    return fail(ctx, KGQ_EINVAL, "kgq_comm_init: rank %d / world %d", rank, world);
+  if (split == KGQ_SPLIT_ENTITIES) {
+    if (ctx->cfg.world_size != world || ctx->cfg.rank != rank)
+      return fail(ctx, KGQ_EINVAL, "kgq_comm_init: entity split needs cfg.world_size == %d and cfg.rank == %d "
+                  "(context: %d / %d)", world, rank, ctx->cfg.world_size, ctx->cfg.rank);
+  } else if (split == KGQ_SPLIT_QUERIES) {
+    if (ctx->cfg.world_size != 1)
+      return fail(ctx, KGQ_EINVAL, "kgq_comm_init: query split needs a context with the whole entity table "
+                  "(cfg.world_size == 1)");
+  } else {
+    return fail(ctx, KGQ_EINVAL, "kgq_comm_init: bad split %d", split);
+  }
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(ctx, KGQ_ENCCL, "%s", api.why.c_str());
+  DeviceGuard g(ctx->cfg.device);
+  const size_t n = (size_t)ctx->cfg.max_batch * ctx->cfg.max_k;
+  kgq_status st = KGQ_OK;
+  if (!ctx->cm_d) {
+    st = dalloc(ctx, &ctx->cm_d, n, "comm top-k");
+    if (!st) st = dalloc(ctx, &ctx->cm_i, n, "comm top-k");
+  }
+  if (!st) {
+    if (ctx->cg_d) cudaFree(ctx->cg_d);
+    if (ctx->cg_i) cudaFree(ctx->cg_i);
+    ctx->cg_d = nullptr;
+    ctx->cg_i = nullptr;
+    // query split pads each rank's slice to ceil(B / W) rows: W * ceil(B / W) <= B + W - 1
+    const size_t ng = (size_t)world * n + (size_t)world * ctx->cfg.max_k;
+    st = dalloc(ctx, &ctx->cg_d, ng, "comm gather");
+    if (!st) st = dalloc(ctx, &ctx->cg_i, ng, "comm gather");
+  }
+  if (st) return st;
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof u);
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = api.CommInitRank(&comm, world, u, rank);
+  if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommInitRank");
+  for (auto& gr : ctx->graphs) {  // the data plane changed under the captured submits
+    if (gr.pending) harvest(ctx, gr.evs, false);
+    destroy_graph_entry(gr);
+  }
+  ctx->graphs.clear();
+  clear_mix_graphs(ctx);
+  ctx->comm = comm;
+  ctx->comm_world = world;
+  ctx->comm_rank = rank;
+  ctx->comm_split = split;
+  return KGQ_OK;
+}
+
+kgq_status kgq_comm_destroy(kgq_ctx* ctx) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (!ctx->comm) return KGQ_OK;
+  DeviceGuard g(ctx->cfg.device);
+  CK(cudaDeviceSynchronize(), "kgq_comm_destroy");
+  ncclResult_t r = nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
+  ctx->comm = nullptr;
+  ctx->comm_world = 0;
+  for (auto& gr : ctx->graphs) {
+    if (gr.pending) harvest(ctx, gr.evs, false);
+    destroy_graph_entry(gr);
+  }
+  ctx->graphs.clear();
+  clear_mix_graphs(ctx);
+  if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommDestroy");
+  return KGQ_OK;
+}
+
+kgq_status kgq_rank_metrics(kgq_ctx* ctx, int32_t batch, const int32_t* ans_off, const int32_t* ranks,
+                            const uint8_t* hard, double* metrics, kgq_stream stream) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (batch < 0 || !ans_off || !ranks || !metrics) return fail(ctx, KGQ_EINVAL, "kgq_rank_metrics: bad argument");
+  DeviceGuard g(ctx->cfg.device);
+  ctx->launches = launch_rank_metrics(batch, ans_off, ranks, hard, metrics, (cudaStream_t)stream);
+  CK(cudaGetLastError(), "rank metrics launch");
   return KGQ_OK;
 }
 
@@ -1429,9 +1696,13 @@ kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_
                             kgq_stream stream) {
   kgq_status st = check_submit(ctx, s, batch, 0, false);
   if (st) return st;
-  if (mode < KGQ_RANK_LOCAL || mode > KGQ_RANK_COUNT) return fail(ctx, KGQ_EINVAL, "bad rank mode %d", mode);
-  if (mode == KGQ_RANK_LOCAL && ctx->cfg.world_size > 1)
-    return fail(ctx, KGQ_EINVAL, "KGQ_RANK_LOCAL needs a single shard; use KGQ_RANK_DIST + min-reduce + KGQ_RANK_COUNT");
+  if (mode < KGQ_RANK_LOCAL || mode > KGQ_RANK_FILTERED) return fail(ctx, KGQ_EINVAL, "bad rank mode %d", mode);
+  const bool sharded = ctx->cfg.world_size > 1;
+  if (mode == KGQ_RANK_LOCAL && sharded)
+    return fail(ctx, KGQ_EINVAL, "KGQ_RANK_LOCAL needs a single shard; use KGQ_RANK_DIST + min-reduce + KGQ_RANK_COUNT"
+                " or KGQ_RANK_FILTERED with a communicator");
+  if (mode == KGQ_RANK_FILTERED && sharded && !(ctx->comm && ctx->comm_split == KGQ_SPLIT_ENTITIES))
+    return fail(ctx, KGQ_EINVAL, "KGQ_RANK_FILTERED over entity shards needs the communicator (kgq_comm_init)");
   if (batch == 0 || n_ans == 0) { ctx->launches = 0; return KGQ_OK; }
   if (!anchors || !rels || !ans_off || !ans_id || !ans_dist || (mode != KGQ_RANK_DIST && !count))
     return fail(ctx, KGQ_EINVAL, "NULL device pointer");
@@ -1439,18 +1710,45 @@ kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_
   cudaStream_t cs = (cudaStream_t)stream;
   const Plan* P = plan_of(s);
   int L = 0;
-  CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)batch * sizeof(int32_t), cs), "reset flags");
-  const bool from_state = q_in_state(ctx, P, batch);
-  L += run_chain(ctx, s, batch, anchors, rels, cs, !from_state);
-  for (int64_t b0 = 0; b0 < batch; b0 += ctx->bchunk) {
-    const int nb = (int)std::min<int64_t>(ctx->bchunk, batch - b0);
-    L += score_rows(ctx, P, b0, nb, cs, batch, from_state);
-    if (mode != KGQ_RANK_COUNT)
-      L += launch_answer_dist(ctx->dist, ctx->np, ctx->e0, ctx->ns, (int)b0, nb, ans_off, ans_id, ans_dist, cs);
-    if (mode != KGQ_RANK_DIST)
-      L += launch_filtered_counts(ctx->dist, ctx->np, ctx->e0, ctx->ns, (int)b0, nb, ans_off, ans_id, ans_dist,
-                                  count, ctx->d_err, cs);
+  // one pass: chain, then per chunk of rows the scorer and the answer-distance / count kernels
+  auto pass = [&](int m, bool count_only) {
+    if (!count_only) {
+      CK(cudaMemsetAsync(ctx->d_invalid, 0, (size_t)batch * sizeof(int32_t), cs), "reset flags");
+    }
+    const bool from_state = q_in_state(ctx, P, batch);
+    if (!count_only) L += run_chain(ctx, s, batch, anchors, rels, cs, !from_state);
+    for (int64_t b0 = 0; b0 < batch; b0 += ctx->bchunk) {
+      const int nb = (int)std::min<int64_t>(ctx->bchunk, batch - b0);
+      if (!count_only) L += score_rows(ctx, P, b0, nb, cs, batch, from_state);
+      if (m != KGQ_RANK_COUNT)
+        L += launch_answer_dist(ctx->dist, ctx->np, ctx->e0, ctx->ns, (int)b0, nb, ans_off, ans_id, ans_dist, cs);
+      if (m != KGQ_RANK_DIST)
+        L += launch_filtered_counts(ctx->dist, ctx->np, ctx->e0, ctx->ns, (int)b0, nb, ans_off, ans_id, ans_dist,
+                                    count, ctx->d_err, cs);
+    }
+    return KGQ_OK;
+  };
+  st = KGQ_OK;
+  if (mode != KGQ_RANK_FILTERED) {
+    st = pass(mode, false);
+  } else if (!sharded) {
+    st = pass(KGQ_RANK_LOCAL, false);
+    if (!st) L += launch_add_one(count, n_ans, cs);
+  } else {  // entity shards: answer distances from their owning shard, then every shard's counts
+    const NcclApi& api = nccl_api();
+    ncclComm_t comm = static_cast<ncclComm_t>(ctx->comm);
+    st = pass(KGQ_RANK_DIST, false);
+    if (st) return st;
+    ncclResult_t r = api.AllReduce(ans_dist, ans_dist, (size_t)n_ans, ncclFloat32, ncclMin, comm, cs);
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllReduce(min)");
+    // one chunk: the distance block of the pass above is still there; else score again
+    st = pass(KGQ_RANK_COUNT, batch <= ctx->bchunk);
+    if (st) return st;
+    r = api.AllReduce(count, count, (size_t)n_ans, ncclInt32, ncclSum, comm, cs);
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllReduce(sum)");
+    L += launch_add_one(count, n_ans, cs);
   }
+  if (st) return st;
   ctx->launches = L;
   CK(cudaGetLastError(), "rank launch");
   return KGQ_OK;

@@ -162,8 +162,16 @@ struct kgq_ctx {
   // N2: fused top-k all-gather over peer memory (kgq_set_peers); peers.world == 0: off
   kgq::PeerPush peers{};
   uint32_t* d_epoch = nullptr;             // [2]: epoch, merge CTA counter
+  bool push_outstanding = false;  // N2: a submit pushed its top-k and kgq_merge_peers has not run yet
   int push_row0 = -1;      // set by the entry points: output-row offset of submit_impl's pushes (-1: none)
   long long peer_timeout_ns = 10000000000LL;  // KGQ_PEER_TIMEOUT_MS
+  // multi-GPU data plane (kgq_comm_init): the context's NCCL communicator (ncclComm_t)
+  void* comm = nullptr;
+  int comm_world = 0, comm_rank = 0, comm_split = 0;
+  float* cm_d = nullptr;                   // [max_batch, max_k] this rank's top-k (or row slice)
+  int32_t* cm_i = nullptr;
+  float* cg_d = nullptr;                   // [world * max_batch, max_k] all-gathered lists
+  int32_t* cg_i = nullptr;
 
 };
 
@@ -316,6 +324,9 @@ int launch_topk(const float* dist, int64_t ldd, int B, int64_t n, int k, int64_t
                 cudaStream_t st);
 bool score_uses_stream(int model, int nbq, int B);
 // N1 filtered ranking (rank.cu)
+int launch_add_one(int32_t* v, int n, cudaStream_t st);
+int launch_rank_metrics(int B, const int32_t* ans_off, const int32_t* ranks, const uint8_t* hard, double* out,
+                        cudaStream_t st);
 int launch_answer_dist(const float* dist, int64_t ldd, int64_t e0, int64_t ns, int b0, int nb,
                        const int32_t* ans_off, const int32_t* ans_id, float* ans_dist, cudaStream_t st);
 int launch_filtered_counts(const float* dist, int64_t ldd, int64_t e0, int64_t ns, int b0, int nb,
@@ -323,7 +334,7 @@ int launch_filtered_counts(const float* dist, int64_t ldd, int64_t e0, int64_t n
                            int32_t* count, int32_t* err, cudaStream_t st);
 // Tensor-core BetaE scorer (score_tc.cu): finalize builds the centred split table
 // uv [np][2d], E_e = sum_d C_ed (fp64) and the per-dim U/V sums; per batch it splits the
-// query rows, computes P_q (fp64) and runs the 3xTF32 GEMM with the score epilogue.
+// query rows, computes P_q (fp64) and runs the bf16x3 tcgen05 GEMM with the score epilogue.
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
                           double* sums, Split uv, float2* Esum, cudaStream_t st);
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,

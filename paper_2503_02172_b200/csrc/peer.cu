@@ -49,8 +49,9 @@ __global__ void k_peer_push(const PeerPush pp, int B, int k, const float* __rest
 
 // One warp per row: wait until every rank published this row for the current epoch (system-
 // scope acquire on this rank's own flags), then a world-way merge of the sorted key lists.  A
-// rank that does not deliver within timeout_ns is reported through err (kind 3: row, rank) and
-// its list is treated as empty, so a missing peer cannot hang the GPU.  The CTA that finishes
+// rank that does not deliver within timeout_ns is reported through err (kind 3: row, rank), the
+// row is output as NaN / -1 and the session is poisoned on every rank (peer.cuh; later merges
+// report kind 4), so a missing peer can neither hang the GPU nor pair lists of different submits.  The CTA that finishes
 // last advances the epoch for the next submit (done: a zeroed counter, reset by that CTA).
 constexpr int kMergeWarps = 4;
 __global__ void __launch_bounds__(32 * kMergeWarps)
@@ -73,7 +74,14 @@ __global__ void __launch_bounds__(32 * kMergeWarps)
   const int W = pp.world;
   unsigned long long* s = sk + (size_t)wid * W * k;
   bool ok = true;
-  if (lane < W) {
+  if (ld_acquire_sys(pp.hdr[pp.rank]) != 0u) {  // poisoned session: no list can be trusted
+    ok = false;
+    if (lane == 0 && atomicCAS(err, 0, 4) == 0) {
+      err[1] = row;
+      err[2] = 0;
+      err[3] = 0;
+    }
+  } else if (lane < W) {
     const uint32_t* f = pp.flag[pp.rank] + pp.slot(ep, lane, row);
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -90,11 +98,13 @@ __global__ void __launch_bounds__(32 * kMergeWarps)
           err[2] = lane;
           err[3] = 0;
         }
+        for (int p = 0; p < W; ++p) st_release_sys(pp.hdr[p], 1u);  // poison every rank's session
         break;
       }
     }
   }
-  const unsigned okm = __ballot_sync(0xffffffffu, ok);
+  unsigned okm = __ballot_sync(0xffffffffu, ok);
+  if (okm != 0xffffffffu) okm = 0u;  // a missing rank or a poisoned session: the row is NaN / -1
   const unsigned long long* keys = pp.key[pp.rank];
   for (int i = lane; i < W * k; i += 32) {
     const int src = i / k, j = i - src * k;
@@ -128,11 +138,8 @@ int launch_peer_merge(const PeerPush& pp, int B, int k, float* out_d, int32_t* o
                       long long timeout_ns, cudaStream_t st) {
   if (B <= 0) return 0;
   const size_t smem = (size_t)kMergeWarps * pp.world * k * sizeof(unsigned long long);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_peer_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  smem_attr_once(k_peer_merge, 200 * 1024, attr);
   launch_pdl(k_peer_merge, dim3((B + kMergeWarps - 1) / kMergeWarps), dim3(32 * kMergeWarps), smem, st, pp, B, k,
              out_d, out_i, err, timeout_ns, const_cast<uint32_t*>(pp.epoch), const_cast<uint32_t*>(pp.epoch) + 1);
   return 1;

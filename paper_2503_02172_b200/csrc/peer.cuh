@@ -4,6 +4,7 @@
 //
 // Every rank owns one "peer buffer" of identical layout (symmetric allocation; the pointers of
 // all ranks' buffers are registered with kgq_set_peers):
+//   hdr  [64]                          uint32   hdr[0] = session broken (a rank timed out)
 //   flag [2][world][max_rows]          uint32   epoch of the last push of (parity, source, row)
 //   key  [2][world][max_rows][max_k]   uint64   (order key of dist << 32) | global id, ascending
 // The context's device epoch starts at 1 (kgq_set_peers) and kgq_merge_peers advances it once
@@ -13,7 +14,14 @@
 // world flags of each row and merges the world sorted lists.  Parity double-buffering makes
 // back-to-back submits safe: rank p can only push epoch e + 2 after its merge of e + 1, which
 // waited for this rank's push of e + 1, which this rank issued after its merge of e finished
-// reading the parity-(e & 1) slots.
+// reading the parity-(e & 1) slots.  The host side keeps pushes and merges paired: a submit on a
+// peered context is rejected while its previous push has not been merged, and a merge without
+// a push is rejected (kgq_api.cu push_outstanding), so a push can never overwrite a slot that
+// a peer's merge of the same epoch is reading.  A merge that times out on a missing rank
+// poisons the session: it sets hdr[0] in EVERY rank's buffer, and from then on every merge on
+// every rank returns NaN / -1 rows and reports KGQ_ESTATE until all ranks call kgq_set_peers
+// again -- the epochs of the ranks may have diverged, and pairing lists of different submits
+// silently is what the poison prevents.
 #pragma once
 #include <stdint.h>
 
@@ -24,6 +32,7 @@ constexpr int kMaxPeers = 8;
 struct PeerPush {
   unsigned long long* key[kMaxPeers] = {};  // rank p's key array
   uint32_t* flag[kMaxPeers] = {};           // rank p's flag array
+  uint32_t* hdr[kMaxPeers] = {};            // rank p's header (hdr[0]: session broken)
   const uint32_t* epoch = nullptr;          // this context's device epoch (bumped per submit)
   int world = 0, rank = 0, max_rows = 0, max_k = 0;
   int row0 = 0;                             // output row offset of this launch's rows

@@ -118,7 +118,63 @@ __global__ void __launch_bounds__(kThreads)
     count[a0 + i] = (int32_t)diff[j];
   }
 }
+
+__global__ void k_add_one(int32_t* v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] += 1;
+}
+
+// MRR / Hits@{1,3,10} (KGReasoning averaging): per query the mean over its scored answers, then
+// the mean over the queries that have one.  One CTA; fp64 sums in registers then shared memory
+// (batch <= max_batch, a few thousand queries: one pass).
+__global__ void __launch_bounds__(256) k_rank_metrics(int B, const int32_t* __restrict__ ans_off,
+                                                      const int32_t* __restrict__ ranks,
+                                                      const uint8_t* __restrict__ hard, double* out) {
+  double acc[5] = {0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    double s[4] = {0, 0, 0, 0};
+    int n = 0;
+    for (int j = ans_off[b]; j < ans_off[b + 1]; ++j) {
+      if (hard && !hard[j]) continue;
+      const int r = ranks[j];
+      s[0] += 1.0 / r;
+      s[1] += r <= 1;
+      s[2] += r <= 3;
+      s[3] += r <= 10;
+      ++n;
+    }
+    if (n) {
+      for (int i = 0; i < 4; ++i) acc[i] += s[i] / n;
+      acc[4] += 1.0;
+    }
+  }
+  __shared__ double red[5][256];
+  for (int i = 0; i < 5; ++i) red[i][threadIdx.x] = acc[i];
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if ((int)threadIdx.x < w)
+      for (int i = 0; i < 5; ++i) red[i][threadIdx.x] += red[i][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double q = red[4][0];
+    for (int i = 0; i < 4; ++i) out[i] = q > 0 ? red[i][0] / q : 0.0;
+    out[4] = q;
+  }
+}
 }  // namespace
+
+int launch_add_one(int32_t* v, int n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_add_one<<<(n + 255) / 256, 256, 0, st>>>(v, n);
+  return 1;
+}
+
+int launch_rank_metrics(int B, const int32_t* ans_off, const int32_t* ranks, const uint8_t* hard, double* out,
+                        cudaStream_t st) {
+  k_rank_metrics<<<1, 256, 0, st>>>(B, ans_off, ranks, hard, out);
+  return 1;
+}
 
 int launch_answer_dist(const float* dist, int64_t ldd, int64_t e0, int64_t ns, int b0, int nb,
                        const int32_t* ans_off, const int32_t* ans_id, float* ans_dist, cudaStream_t st) {

@@ -255,11 +255,8 @@ void launch_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d
               float* dist, int64_t ldd, int B, cudaStream_t st) {
   constexpr int NQ = Planes<MODEL>::NQ, NE = Planes<MODEL>::NE;
   const size_t smem = (size_t)2 * (NQ * DK * TQ + NE * DK * TE) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_score<MODEL, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  smem_attr_once(k_score<MODEL, NB>, (int)smem, attr);
   const int rows = B * NB;
   dim3 grid((unsigned)(np / TE), (unsigned)((rows + TQ - 1) / TQ));
   k_score<MODEL, NB><<<grid, 256, smem, st>>>(Qt, rpad, tab, np, d, cen, dist, ldd, B);

@@ -527,11 +527,8 @@ void launch_topk_kernel(dim3 grid, const float* dist, int64_t ldd, int64_t n, in
   int Q = 1;
   while (Q < (kTopkThreads / 32) * k) Q <<= 1;
   const int smem = (int)(((kTopkThreads / 32) * P + Q) * sizeof(unsigned long long));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  smem_attr_once(k_topk, 64 * 1024, attr);
   k_topk<<<grid, kTopkThreads, smem, st>>>(dist, ldd, n, chunk, k, id_base, invalid, od, oi, B, P);
 }
 

@@ -23,7 +23,7 @@ MODELS = {"gqe": 0, "q2b": 1, "betae": 2}
 STRUCTURES = ("1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up",
               "2in", "3in", "inp", "pin", "pni", "2u-DM", "up-DM")
 STATUS = {0: "KGQ_OK", 1: "KGQ_EINVAL", 2: "KGQ_ERANGE", 3: "KGQ_EUNSUPPORTED",
-          4: "KGQ_ESTATE", 5: "KGQ_ENOMEM", 6: "KGQ_ECUDA"}
+          4: "KGQ_ESTATE", 5: "KGQ_ENOMEM", 6: "KGQ_ECUDA", 7: "KGQ_ENCCL"}
 LAYER_PROJ_OUT, LAYER_PROJ_HIDDEN = 0, 1
 LAYER_INTER_1, LAYER_INTER_2, LAYER_OFFSET_1, LAYER_OFFSET_2 = 16, 17, 18, 19
 REL_MAIN, REL_OFFSET = 0, 1
@@ -38,8 +38,10 @@ EXPORTS = (
     "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_submit_host_async", "kgq_submit_mixed", "kgq_query_embedding", "kgq_merge_topk",
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
     "kgq_profile_read", "kgq_rank_answers", "kgq_peer_bytes", "kgq_set_peers", "kgq_merge_peers",
+    "kgq_query_range", "kgq_nccl_unique_id", "kgq_comm_init", "kgq_comm_destroy", "kgq_rank_metrics",
 )
-RANK_LOCAL, RANK_DIST, RANK_COUNT = 0, 1, 2
+RANK_LOCAL, RANK_DIST, RANK_COUNT, RANK_FILTERED = 0, 1, 2, 3
+SPLIT_ENTITIES, SPLIT_QUERIES = 0, 1
 
 
 class KgqConfig(ctypes.Structure):
@@ -89,6 +91,11 @@ _sig = {
     "kgq_merge_peers": (_I32, [_P, _I32, _I32, _P, _P, _P]),
     "kgq_profile_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                               ctypes.POINTER(ctypes.c_double)]),
+    "kgq_query_range": (_I32, [_I32, _I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "kgq_nccl_unique_id": (_I32, [ctypes.c_char_p]),
+    "kgq_comm_init": (_I32, [_P, ctypes.c_char_p, _I32, _I32, _I32]),
+    "kgq_comm_destroy": (_I32, [_P]),
+    "kgq_rank_metrics": (_I32, [_P, _I32, _P, _P, _P, _P, _P]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -126,6 +133,25 @@ def shard_range(n_entity, world_size, rank):
     return b.value, e.value
 
 
+def query_range(batch, world_size, rank):
+    """Rows [lo, hi) of a replicated batch that `rank` runs in query-split mode (kgq_query_range)."""
+    lo, hi = _I32(), _I32()
+    st = _lib.kgq_query_range(batch, world_size, rank, ctypes.byref(lo), ctypes.byref(hi))
+    if st:
+        raise KgqError(st, _lib.kgq_last_error(None).decode())
+    return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (kgq_nccl_unique_id); raises KgqError(KGQ_ENCCL) without NCCL."""
+    import torch  # noqa: F401  -- load the process's NCCL (torch's) before libkgq looks for one
+    buf = ctypes.create_string_buffer(128)
+    st = _lib.kgq_nccl_unique_id(buf)
+    if st:
+        raise KgqError(st, _lib.kgq_last_error(None).decode())
+    return buf.raw
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
@@ -134,6 +160,21 @@ def _stream(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _on_stream(stream):
+    """Context that makes `stream` current for the binding's own allocations and staging
+    copies (so the caching allocator and the copies are ordered with the library's launches on
+    that stream), after making it wait for the caller's current stream (which produced the
+    inputs).  No-op for stream=None (the library then runs on the current stream)."""
+    import contextlib
+    import torch
+    if stream is None:
+        return contextlib.nullcontext()
+    cur = torch.cuda.current_stream()
+    if stream != cur:
+        stream.wait_stream(cur)
+    return torch.cuda.stream(stream)
 
 
 def layer_id(name: str) -> int:
@@ -220,13 +261,14 @@ class Engine:
         s = structure_id(structure)
         B = anchors.shape[0]
         dev = anchors.device
-        if out is None:
-            td = torch.empty((B, k), dtype=torch.float32, device=dev)
-            ti = torch.empty((B, k), dtype=torch.int32, device=dev)
-        else:
-            td, ti = out
-        sd = (torch.empty((B, self.shard[1] - self.shard[0]), dtype=torch.float32, device=dev)
-              if shard_dist else None)
+        with _on_stream(stream):
+            if out is None:
+                td = torch.empty((B, k), dtype=torch.float32, device=dev)
+                ti = torch.empty((B, k), dtype=torch.int32, device=dev)
+            else:
+                td, ti = out
+            sd = (torch.empty((B, self.shard[1] - self.shard[0]), dtype=torch.float32, device=dev)
+                  if shard_dist else None)
         self._check(_lib.kgq_submit(self._h, s, B, _ptr(anchors), _ptr(rels), k, _ptr(td),
                                     _ptr(ti), _ptr(sd), _stream(stream)))
         return (td, ti, sd) if shard_dist else (td, ti)
@@ -243,24 +285,33 @@ class Engine:
         # replays the library's captured graph of the whole mixed submit)
         na = sum(int(g[1].numel()) for g in groups)
         nr = sum(int(g[2].numel()) for g in groups)
-        st = getattr(self, "_mix_in", None)
-        if st is None or st[0].numel() < na or st[1].numel() < nr or st[0].device != dev:
-            st = (torch.empty(max(na, 1), dtype=torch.int32, device=dev),
-                  torch.empty(max(nr, 1), dtype=torch.int32, device=dev))
-            self._mix_in = st
-        a, r = st[0][:na], st[1][:nr]
-        if groups:
-            torch.cat([g[1].reshape(-1).to(torch.int32) for g in groups], out=a)
-            torch.cat([g[2].reshape(-1).to(torch.int32) for g in groups], out=r)
         Q = sum(int(g[1].shape[0]) for g in groups)
-        if out is None:
-            td = torch.empty((Q, k), dtype=torch.float32, device=dev)
-            ti = torch.empty((Q, k), dtype=torch.int32, device=dev)
-        else:
-            td, ti = out
-        self._keep = (a, r)  # the launch is asynchronous: keep the concatenated inputs alive
-        self._check(_lib.kgq_submit_mixed(self._h, len(groups), ss, bs, _ptr(a), _ptr(r), k, _ptr(td),
-                                          _ptr(ti), _stream(stream)))
+        with _on_stream(stream):
+            st = getattr(self, "_mix_in", None)
+            if st is None or st[0].numel() < na or st[1].numel() < nr or st[0].device != dev:
+                st = (torch.empty(max(na, 1), dtype=torch.int32, device=dev),
+                      torch.empty(max(nr, 1), dtype=torch.int32, device=dev))
+                self._mix_in = st
+                self._mix_ev = None
+            a, r = st[0][:na], st[1][:nr]
+            # the staging buffers are reused: the previous mixed submit (possibly on another
+            # stream) must have read them before they are overwritten
+            if getattr(self, "_mix_ev", None) is not None:
+                torch.cuda.current_stream().wait_event(self._mix_ev)
+            if groups:
+                torch.cat([g[1].reshape(-1).to(torch.int32) for g in groups], out=a)
+                torch.cat([g[2].reshape(-1).to(torch.int32) for g in groups], out=r)
+            if out is None:
+                td = torch.empty((Q, k), dtype=torch.float32, device=dev)
+                ti = torch.empty((Q, k), dtype=torch.int32, device=dev)
+            else:
+                td, ti = out
+            self._keep = (a, r)  # the launch is asynchronous: keep the concatenated inputs alive
+            self._check(_lib.kgq_submit_mixed(self._h, len(groups), ss, bs, _ptr(a), _ptr(r), k, _ptr(td),
+                                              _ptr(ti), _stream(stream)))
+            if groups:
+                self._mix_ev = torch.cuda.Event()
+                self._mix_ev.record()
         return td, ti
 
     def submit_host(self, structure, anchors: np.ndarray, rels: np.ndarray, k: int,
@@ -286,8 +337,9 @@ class Engine:
         import torch
         s = structure_id(structure)
         B = anchors.shape[0]
-        out = torch.empty((B, num_branches(s), self.width), dtype=torch.float32,
-                          device=anchors.device)
+        with _on_stream(stream):
+            out = torch.empty((B, num_branches(s), self.width), dtype=torch.float32,
+                              device=anchors.device)
         self._check(_lib.kgq_query_embedding(self._h, s, B, _ptr(anchors), _ptr(rels), _ptr(out),
                                              _stream(stream)))
         return out
@@ -296,11 +348,12 @@ class Engine:
         """parts_*: CUDA tensors [W, B, k] -> (dist [B,k], ids [B,k])."""
         import torch
         W, B, kk = parts_dist.shape
-        od = torch.empty((B, k), dtype=torch.float32, device=parts_dist.device)
-        oi = torch.empty((B, k), dtype=torch.int32, device=parts_dist.device)
-        self._check(_lib.kgq_merge_topk(self._h, W, B, kk, _ptr(parts_dist.contiguous()),
-                                        _ptr(parts_id.contiguous()), _ptr(od), _ptr(oi),
-                                        _stream(stream)))
+        with _on_stream(stream):
+            od = torch.empty((B, k), dtype=torch.float32, device=parts_dist.device)
+            oi = torch.empty((B, k), dtype=torch.int32, device=parts_dist.device)
+            pd, pi = parts_dist.contiguous(), parts_id.contiguous()
+            self._check(_lib.kgq_merge_topk(self._h, W, B, kk, _ptr(pd), _ptr(pi), _ptr(od), _ptr(oi),
+                                            _stream(stream)))
         return od, oi
 
     # ---- N2: fused top-k all-gather over peer memory (kgq_set_peers / kgq_merge_peers) ----
@@ -320,26 +373,51 @@ class Engine:
     def merge_peers(self, batch, k, out=None, stream=None):
         """Waits for every rank's push of the current submit and merges: (dist, ids) [batch, k]."""
         import torch
-        if out is None:
-            td = torch.empty((batch, k), dtype=torch.float32, device=f"cuda:{self.device}")
-            ti = torch.empty((batch, k), dtype=torch.int32, device=f"cuda:{self.device}")
-        else:
-            td, ti = out
+        with _on_stream(stream):
+            if out is None:
+                td = torch.empty((batch, k), dtype=torch.float32, device=f"cuda:{self.device}")
+                ti = torch.empty((batch, k), dtype=torch.int32, device=f"cuda:{self.device}")
+            else:
+                td, ti = out
         self._check(_lib.kgq_merge_peers(self._h, batch, k, _ptr(td), _ptr(ti), _stream(stream)))
         return td, ti
+
+    # ---- multi-GPU data plane: the library's NCCL communicator (kgq_comm_init) ----------------
+    def comm_init(self, unique_id: bytes, world, rank, split=SPLIT_ENTITIES):
+        """Collective over the job's `world` ranks (one context each, same unique_id)."""
+        import torch  # noqa: F401  -- the process's NCCL (torch's) is the one libkgq binds to
+        if len(unique_id) != 128:
+            raise ValueError("the NCCL unique id is 128 bytes")
+        self._check(_lib.kgq_comm_init(self._h, unique_id, world, rank, split))
+
+    def comm_destroy(self):
+        self._check(_lib.kgq_comm_destroy(self._h))
+
+    def rank_metrics(self, ans_off, ranks, hard=None, stream=None):
+        """MRR, Hits@1/3/10 and the number of queries averaged (kgq_rank_metrics): fp64 CUDA
+        tensor [5].  ranks: int32 1-based filtered ranks in the CSR layout of ans_off."""
+        import torch
+        B = int(ans_off.shape[0]) - 1
+        with _on_stream(stream):
+            out = torch.empty(5, dtype=torch.float64, device=ranks.device)
+        self._check(_lib.kgq_rank_metrics(self._h, B, _ptr(ans_off), _ptr(ranks), _ptr(hard), _ptr(out),
+                                          _stream(stream)))
+        return out
 
     def rank_answers(self, structure, anchors, rels, ans_off, ans_id, mode=RANK_LOCAL,
                      ans_dist=None, stream=None):
         """N1 filtered ranking (kgq_rank_answers).  ans_off int32 [B+1], ans_id int32 [n] CUDA
         tensors (CSR of each query's easy + hard answers).  Returns (ans_dist, count): the
-        filtered rank of answer j is 1 + count[j] (summed over shards)."""
+        filtered rank of answer j is 1 + count[j] (summed over shards); with RANK_FILTERED
+        `count` already holds that rank (over all shards through the communicator)."""
         import torch
         s = structure_id(structure)
         B = anchors.shape[0]
         n = int(ans_id.shape[0])
-        if ans_dist is None:
-            ans_dist = torch.empty(n, dtype=torch.float32, device=anchors.device)
-        count = torch.zeros(n, dtype=torch.int32, device=anchors.device)
+        with _on_stream(stream):
+            if ans_dist is None:
+                ans_dist = torch.empty(n, dtype=torch.float32, device=anchors.device)
+            count = torch.zeros(n, dtype=torch.int32, device=anchors.device)
         self._check(_lib.kgq_rank_answers(self._h, s, B, _ptr(anchors), _ptr(rels), _ptr(ans_off),
                                           _ptr(ans_id), n, mode, _ptr(ans_dist),
                                           _ptr(count) if mode != RANK_DIST else None,

@@ -81,3 +81,31 @@ def test_peer_entry_points_validate_without_a_gpu():
     from paper_2503_02172_b200.sharded import ShardedEngine
     with pytest.raises(ValueError, match="merge"):
         ShardedEngine("betae", 100, 5, 8, merge="allreduce")
+    with pytest.raises(ValueError, match="split"):
+        ShardedEngine("betae", 100, 5, 8, split="rows")
+
+
+@pytest.mark.parametrize("B,W", [(0, 1), (1, 8), (10, 3), (1024, 8), (1023, 8), (4096, 3), (7, 7)])
+def test_query_range_partitions_the_batch(B, W):
+    """Query-split mode (kgq_query_range): contiguous rows, ceil(B / W) per rank, the ranges
+    tile [0, B) exactly in rank order."""
+    c = -(-B // W) if B else 0
+    got = [kgq.query_range(B, W, r) for r in range(W)]
+    assert got[0][0] == 0 and got[-1][1] == B
+    for r, (lo, hi) in enumerate(got):
+        assert lo == min(B, r * c) and hi == min(B, lo + c)
+        if r:
+            assert lo == got[r - 1][1]
+    with pytest.raises(kgq.KgqError):
+        kgq.query_range(B, W, W)
+
+
+def test_comm_entry_points_validate_without_a_gpu():
+    """The communicator entry points' host-side checks (no device work)."""
+    assert kgq._lib.kgq_comm_init(None, b"\0" * 128, 1, 0, 0) == 1       # NULL context
+    assert kgq._lib.kgq_comm_destroy(None) == 1
+    assert kgq._lib.kgq_rank_metrics(None, 1, None, None, None, None, None) == 1
+    assert kgq._lib.kgq_nccl_unique_id(None) == 1
+    assert kgq.STATUS[7] == "KGQ_ENCCL"
+    uid = kgq.nccl_unique_id()   # NCCL's bootstrap id needs no GPU
+    assert len(uid) == 128 and uid != kgq.nccl_unique_id()

@@ -139,3 +139,66 @@ def test_two_phase_filtered_rank_protocol_over_gloo():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+def _query_split_worker(rank, world, port, q):
+    """Query-split data plane (kgq_comm_init KGQ_SPLIT_QUERIES) on CPU: the replicated batch's
+    rows kgq_query_range(B, W, r) run on rank r (the oracle stands in for the GPU path), each rank
+    contributes ceil(B / W) rows (padded: NaN / -1) to one all-gather, and the first B gathered
+    rows are the whole batch's top-k -- the same steps and buffer layout as submit_comm."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N, R, d, k = 211, 6, 8, 7
+        t = synth.make_tables("betae", N, R, d, hidden=16, seed=9)
+        m = O.Model("betae", t, dim=d)
+        out = {}
+        for s, B in (("2p", 11), ("up", 3), ("inp", 1)):
+            a, r = synth.make_queries(s, B, N, R, seed=13)   # replicated on every rank
+            lo, hi = kgq.query_range(B, world, rank)
+            c = -(-B // world)
+            send_d = torch.full((c, k), float("nan"), dtype=torch.float64)
+            send_i = torch.full((c, k), -1, dtype=torch.int64)
+            if hi > lo:
+                ld, li = O.topk(m.scores(s, a[lo:hi], r[lo:hi]), k)
+                send_d[: hi - lo] = torch.from_numpy(ld)
+                send_i[: hi - lo] = torch.from_numpy(li)
+            gd = torch.empty((world * c, k), dtype=torch.float64)
+            gi = torch.empty((world * c, k), dtype=torch.int64)
+            dist.all_gather_into_tensor(gd, send_d)
+            dist.all_gather_into_tensor(gi, send_i)
+            out[s] = (gd[:B].numpy(), gi[:B].numpy())
+        q.put((rank, out))
+    except Exception as e:
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_query_split_protocol_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_query_split_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for v in res.values():
+        assert not isinstance(v, str), v
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N, R, d, k = 211, 6, 8, 7
+    t = synth.make_tables("betae", N, R, d, hidden=16, seed=9)
+    m = O.Model("betae", t, dim=d)
+    for s, B in (("2p", 11), ("up", 3), ("inp", 1)):
+        a, r = synth.make_queries(s, B, N, R, seed=13)
+        gd, gi = O.topk(m.scores(s, a, r), k)
+        for rank in range(world):
+            md, mi = res[rank][s]
+            np.testing.assert_array_equal(mi, gi)
+            # fp64 BLAS groups the MLP sums differently for a row slice than for the batch
+            np.testing.assert_allclose(md, gd, rtol=1e-12)
