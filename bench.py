@@ -130,34 +130,38 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def run_c5a(args):
+def c5a_measure(steps, warmup, peaks, models=("gqe", "betae")):
     """BASELINE.json configs[4], latency regime: 2M entities, d 400, GQE and
-    BetaE, B in {1, 8}, 1p and 2u, one GPU.  Reports the scorer's table-streaming bandwidth
-    (algorithmic bytes: the shard's scoring table once per batch) against measured HBM."""
+    BetaE, B in {1, 8}, 1p and 2u, one GPU.  The dominant kernel is the streaming entity scorer
+    (k_score_stream): its algorithmic bytes per launch are the shard's scoring table read once
+    (GQE: 4 N d bytes; BetaE: the C, U, V planes, 12 N d bytes), its time the library's stage
+    events around the scorer launch (one kernel, ~0.5-1.7 ms: the event nodes cost < 1%)."""
     import torch
     from paper_2503_02172_b200 import Engine
-    peaks, src = load_peaks()
     N, R, d = 2_000_000, 200, 400
     res = {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for model in ("gqe", "betae"):
+    for model in models:
         t = synth.make_tables(model, N, R, d, hidden=HID, seed=77)
         eng = Engine(model, N, R, d, hidden=HID, max_batch=8, max_k=K)
         eng.load_tables(t)
         del t
-        table_bytes = (1 if model == "gqe" else 3) * d * 4 * (eng.shard[1] - eng.shard[0])
+        # the table the scorer streams: GQE [d][N] fp32; BetaE the centred (u, v) planes [d][2][N]
+        # (KGQ_BETAE_STREAM=cuv: the round-1 C, U, V planes [d][3][N])
+        planes = 1 if model == "gqe" else (3 if os.environ.get("KGQ_BETAE_STREAM", "").startswith("c") else 2)
+        table_bytes = planes * d * 4 * (eng.shard[1] - eng.shard[0])
         for s in ("1p", "2u"):
             for B in (1, 8):
                 a, r = synth.make_queries(s, B, N, R, seed=5)
                 da, dr = torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda()
-                for _ in range(args.warmup):
+                for _ in range(warmup):
                     eng.submit(s, da, dr, K)
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
                 def c5a_steps():
                     tt = 0.0
-                    for _ in range(args.steps):
+                    for _ in range(steps):
                         flush.zero_()
                         e0.record()
                         eng.submit(s, da, dr, K)
@@ -165,8 +169,8 @@ def run_c5a(args):
                         torch.cuda.synchronize()
                         tt += e0.elapsed_time(e1)
                     return tt
-                tot = c5a_steps()  # headline: no stage events
-                eng.profile(True)  # second pass: scorer time
+                tot = c5a_steps()  # whole submits, no stage events
+                eng.profile(True)  # second pass: the scorer's own time
                 eng.submit(s, da, dr, K)
                 eng.submit(s, da, dr, K)
                 torch.cuda.synchronize()
@@ -177,11 +181,16 @@ def run_c5a(args):
                 sc_ms = prof["score"][0] / max(1, prof["score"][1])
                 gbs = table_bytes / (sc_ms / 1e3) / 1e9
                 res[f"{model}_{s}_B{B}"] = {
-                    "ms_per_batch": tot / args.steps, "queries_per_s": B * args.steps / (tot / 1e3),
-                    "stage_ms": {k: v[0] / args.steps for k, v in prof.items()},
-                    "scorer_table_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
+                    "ms_per_batch": tot / steps, "queries_per_s": B * steps / (tot / 1e3),
+                    "scorer_ms": sc_ms, "scorer_table_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
                 }
         eng.close()
+    return res
+
+
+def run_c5a(args):
+    peaks, src = load_peaks()
+    res = c5a_measure(args.steps, args.warmup, peaks, tuple(args.models.split(",")))
     print(json.dumps({"metric": "C5a latency regime: 2M-entity scoring HBM GB/s (1 GPU)",
                       "hbm_peak_gbs": peaks["hbm_gbs"], "peak_source": src, "results": res}), flush=True)
 
@@ -273,20 +282,44 @@ def run_suite(args):
                           "l2": "flushed between steps"}), flush=True)
 
 
+def span_union_ms(spans):
+    """Length of the union of [start, end) intervals (ns) -> ms."""
+    if len(spans) == 0:
+        return 0.0
+    iv = sorted((int(a), int(b)) for a, b in spans)
+    tot, cs, ce = 0, iv[0][0], iv[0][1]
+    for a, b in iv[1:]:
+        if a > ce:
+            tot += ce - cs
+            cs, ce = a, b
+        else:
+            ce = max(ce, b)
+    return (tot + ce - cs) * 1e-6
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kgq", choices=["kgq", "reference"])
+    ap.add_argument("--streams", type=int, default=3,
+                    help="concurrent streams per GPU (one library context each); the 14 per-type submits of a "
+                         "step are dealt round-robin over them")
+    ap.add_argument("--split", default="queries", choices=["queries", "entities"],
+                    help="N>1: rank r runs rows [r B, (r+1) B) of a W x B replicated batch (weak scaling, the "
+                         "library's query-split communicator), or the entity table is sharded over the ranks "
+                         "with a replicated B-query batch (strong scaling, local top-k + all-gather + merge)")
+    ap.add_argument("--merge", default="nccl", choices=["nccl", "p2p", "torch"],
+                    help="entity split: the library's NCCL all-gather + merge kernel (default), the all-gather "
+                         "fused into the top-k over symmetric peer memory (N2), or torch.distributed + merge")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=14)
     ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-structure submit measurement")
-    ap.add_argument("--merge", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1 cross-shard top-k exchange: NCCL all-gather + merge kernel (default) or the "
-                         "all-gather fused into the top-k over symmetric peer memory (N2)")
+    ap.add_argument("--no-c5a", action="store_true", help="skip the 2M-entity HBM (C5a) measurement")
     ap.add_argument("--workload", default="fb15k237", choices=["fb15k237", "c5a", "suite"])
     ap.add_argument("--suite", default="", help="comma list of SUITE configs (default: all)")
+    ap.add_argument("--models", default="gqe,betae", help="--workload c5a: models to measure")
     args = ap.parse_args()
     if args.workload == "c5a":
         return run_c5a(args)
@@ -301,10 +334,11 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_2503_02172_b200 import Engine
     from paper_2503_02172_b200.sharded import ShardedEngine
 
     # KGQ_BENCH_ONE_GPU=1 (testing the N > 1 code path on a one-GPU box only): every rank on
-    # cuda:0 with the gloo backend -- the numbers of such a run mean nothing
+    # cuda:0 with the gloo backend and merge="torch" -- the numbers of such a run mean nothing
     one_gpu = os.environ.get("KGQ_BENCH_ONE_GPU") == "1"
     if one_gpu:
         local = 0
@@ -314,94 +348,136 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S = max(1, args.streams)
+    qsplit = world > 1 and args.split == "queries"
+    # per-type batch of the replicated input: W x 1024 in query split (each rank runs 1024 rows:
+    # weak scaling), else 1024 (entity split: strong scaling over the entity table)
+    Bg = BATCH * world if qsplit else BATCH
+    merge = "nccl" if qsplit else (args.merge if not one_gpu else "torch")
     t = synth.make_tables("betae", N_ENT, N_REL, DIM, hidden=HID, seed=SEED)
-    seng = ShardedEngine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K, device=local,
-                         merge=args.merge)
-    seng.load_tables(t)
-    seng.p2p_check = False  # N2 errors are checked once after the timed steps (check_errors below)
-    eng = seng.engine
-    ns = eng.shard[1] - eng.shard[0]
-    stream = torch.cuda.current_stream()
+    engines = []
+    for _ in range(S):
+        se = ShardedEngine("betae", N_ENT, N_REL, DIM, split="queries" if qsplit else "entities", hidden=HID,
+                           max_batch=Bg, max_k=K, device=local, merge=merge)
+        se.load_tables(t)
+        se.p2p_check = False  # N2 errors are checked once after the timed steps
+        se.engine.ktime(True)  # in-kernel GEMM launch spans (roofline from this very pass)
+        engines.append(se)
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    main_stream = torch.cuda.current_stream()
     qs = {}
     for s in STRUCTS:
-        a, r = synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s))
+        if qsplit:  # the same per-rank 1024-query batches as N = 1, replicated over all ranks
+            parts = [synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s) + 7919 * w)
+                     for w in range(world)]
+            a, r = np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+        else:
+            a, r = synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s))
         qs[s] = (a, r, torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda())
+    outs = {s: (torch.empty((Bg, K), device="cuda"), torch.empty((Bg, K), dtype=torch.int32, device="cuda"))
+            for s in STRUCTS}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     launches = [0]
+    lane = {s: i % S for i, s in enumerate(STRUCTS)}
 
-    def one_type(s):
-        a, r, da, dr = qs[s]
-        seng.submit(s, da, dr, K)   # local top-k (+ NCCL all-gather + merge when world > 1)
-        launches[0] += seng.last_launch_count()
+    def step(nlanes=S, count=True):
+        """One step: the 14 per-type submits dealt over `nlanes` streams, joined on the main
+        stream; returns the (start, end) events of the main stream."""
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(main_stream)
+        for st in streams[:nlanes]:
+            st.wait_event(e0)
+        for s in STRUCTS:
+            j = lane[s] % nlanes
+            engines[j].submit(s, qs[s][2], qs[s][3], K, stream=streams[j])
+            if count:
+                launches[0] += engines[j].last_launch_count()
+        for st in streams[:nlanes]:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            main_stream.wait_event(ev)
+        e1.record(main_stream)
+        return e0, e1
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        for s in STRUCTS:
-            one_type(s)
-    barrier()
-    eng.check_errors()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in STRUCTS]
-
-    def timed_steps(n, profiled):
-        """n steps; returns (per-type ms sums, per-step ms).  profiled: the library's stage
-        events (StageTimer) are recorded inside every submit -- they split the graph's PDL
-        chains, so the headline pass runs without them and a second pass measures the stages."""
-        eng.profile(profiled)
-        if profiled:
-            for s in STRUCTS:  # capture the profiled graphs outside the measured steps
-                one_type(s)
-                one_type(s)
-            torch.cuda.synchronize()
-            eng.profile_read()  # reset
-        per = {s: 0.0 for s in STRUCTS}
-        steps = []
-        for _ in range(n):
-            # untimed L2 flush between timed steps; no host sync after it, so the first
-            # submit is enqueued while the flush runs and no host launch latency falls inside
-            # the per-type event intervals (device time only)
+    def timed(nsteps, nlanes):
+        """nsteps steps, L2 flushed (untimed) before each; per-step device ms (start event on
+        the main stream before the fork, end event after every stream joined)."""
+        ms = []
+        for _ in range(nsteps):
             flush.zero_()
-            for i, s in enumerate(STRUCTS):
-                ev[i][0].record(stream)
-                one_type(s)
-                ev[i][1].record(stream)
+            e0, e1 = step(nlanes)
             torch.cuda.synchronize()
-            tot = 0.0
-            for i, s in enumerate(STRUCTS):
-                ms = ev[i][0].elapsed_time(ev[i][1])
-                per[s] += ms
-                tot += ms
-            steps.append(tot)
-        return per, steps
+            ms.append(e0.elapsed_time(e1))
+        return ms
 
+    for _ in range(args.warmup):
+        step(S, False)
+        step(1, False)  # the sequential pass's graphs (lane 0) are captured here too
+    barrier()
+    for se in engines:
+        se.engine.check_errors()
+        se.engine.ktime_read()
+        se.engine.ktime_log()
     launches[0] = 0
     with ClockSampler(local) as clk:
         barrier()
-        per_type, step_ms = timed_steps(args.steps, False)
+        step_ms = timed(args.steps, S)
         barrier()
     n_launch = launches[0]
-    # stage split and GEMM times (roofline): the same steps again with the stage events on
-    prof_steps = args.steps
-    _, prof_step_ms = timed_steps(prof_steps, True)
-    prof = eng.profile_read()
-    eng.profile(False)
-    launches[0] = n_launch
+    # GEMM launch spans of exactly these steps (every context's log, one clock per device)
+    logs = [se.engine.ktime_log() for se in engines]
+    kt = [se.engine.ktime_read() for se in engines]
+    spans = np.concatenate([lg for lg in logs if len(lg)]) if any(len(lg) for lg in logs) else np.zeros((0, 3), np.uint64)
+    gemm_busy_ms = span_union_ms(spans[:, :2]) / args.steps
+    dense_busy_ms = span_union_ms(spans[spans[:, 2] == 0][:, :2]) / args.steps
+    score_busy_ms = span_union_ms(spans[spans[:, 2] == 1][:, :2]) / args.steps
+    dense_span_sum = sum(k["dense"][0] for k in kt) / args.steps
+    score_span_sum = sum(k["score"][0] for k in kt) / args.steps
+    gemm_launches = sum(k["dense"][1] + k["score"][1] for k in kt) / args.steps
     total_ms = sum(step_ms)
+    # sequential reference pass: the same steps on ONE stream (round-1's headline form)
+    seq_ms = None
+    seq_dense_ms = seq_score_ms = None
+    if S > 1:
+        barrier()
+        seq = timed(args.steps, 1)
+        seq_ms = sum(seq)
+        lg = engines[0].engine.ktime_log()  # one stream: every GEMM alone on the GPU
+        seq_dense_ms = span_union_ms(lg[lg[:, 2] == 0][:, :2]) / args.steps
+        seq_score_ms = span_union_ms(lg[lg[:, 2] == 1][:, :2]) / args.steps
+        for se in engines:
+            se.engine.ktime_log()
+            se.engine.ktime_read()
     if world > 1:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([total_ms, seq_ms or 0.0], dtype=torch.float64, device="cuda" if not one_gpu else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-    queries = args.steps * len(STRUCTS) * BATCH
-    value = queries / (total_ms / 1e3)
+        total_ms, seq_ms = float(tt[0].item()), (float(tt[1].item()) or None)
+    per_rank_queries = len(STRUCTS) * BATCH  # per step (query split: each rank's own rows)
+    job_queries = per_rank_queries * (world if qsplit else 1)
+    value = job_queries * args.steps / (total_ms / 1e3)
 
-    # ---- the same step as ONE mixed-structure submit (kgq_submit_mixed, SURVEY §8(f) N4):
-    # every projection hop of all 14 types' branches is one MLP, one scorer and one top-k ----
+    # ---- algorithmic GEMM FLOPs per step (the library's own work counters, one profiled
+    # submit per type outside the timed region) ----
+    eng0 = engines[0].engine
+    eng0.ktime(False)
+    eng0.profile(True)
+    eng0.profile_read()
+    for s in STRUCTS:
+        engines[0].submit(s, qs[s][2], qs[s][3], K)
+    torch.cuda.synchronize()
+    prof = eng0.profile_read()
+    eng0.profile(False)
+    d_fl, s_fl = prof["dense"][2], prof["score"][2]  # query split: this rank's rows (per-GPU FLOPs)
+
+    # ---- the same step as ONE mixed-structure submit (kgq_submit_mixed, SURVEY §8(f) N4) ----
     mixed = None
     if world == 1 and not args.no_mixed:
-        from paper_2503_02172_b200 import Engine
         meng = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH * len(STRUCTS), max_k=K, device=local)
         meng.load_tables(t)
         groups = [(s, qs[s][2].int(), qs[s][3].int()) for s in STRUCTS]
@@ -412,159 +488,137 @@ def main():
         torch.cuda.synchronize()
         meng.check_errors()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-        def mixed_steps():
-            ms = 0.0
-            for _ in range(args.steps):
-                flush.zero_()
-                e0.record()
-                meng.submit_mixed(groups, K, out=mout)
-                e1.record()
-                torch.cuda.synchronize()
-                ms += e0.elapsed_time(e1)
-            return ms
-        mt = mixed_steps()            # headline: no stage events
-        meng.profile(True)            # second pass: stage split + GEMM times
-        meng.profile_read()
-        mt_prof = mixed_steps()
-        mp = meng.profile_read()
-        meng.profile(False)
-        pk, _ = load_peaks()
-        mfl, mms = mp["dense"][2] + mp["score"][2], mp["dense"][0] + mp["score"][0]
-        mach = mfl / (mms / 1e3) / 1e12 if mms > 0 else 0.0
-        mixed = {"value": queries / (mt / 1e3), "unit": "queries/s", "ms_per_step": mt / args.steps,
-                 "stage_ms_per_step": {k: v[0] / args.steps for k, v in mp.items()},
-                 "stage_pass_ms_per_step": mt_prof / args.steps,
-                 "roofline": {"kernel": "k_gemm (tcgen05 bf16x3)", "bound": "tensor", "achieved": mach,
-                              "peak": pk["bf16_tflops"] / 6.0, "unit": "TFLOP/s",
-                              "frac": mach / (pk["bf16_tflops"] / 6.0)},
-                 "how": "one kgq_submit_mixed per step with the same 14 x 1024 queries (L2 flushed between steps)"}
-        meng.close()
-
-    # ---- end to end through the public API with host buffers (pinned) ----------------
-    pin = {s: (torch.from_numpy(qs[s][0]).pin_memory(), torch.from_numpy(qs[s][1]).pin_memory()) for s in STRUCTS}
-    hout = (torch.empty((BATCH, K)).pin_memory(), torch.empty((BATCH, K), dtype=torch.int32).pin_memory())
-    hout_t = {s: (torch.empty((BATCH, K)).pin_memory(), torch.empty((BATCH, K), dtype=torch.int32).pin_memory())
-              for s in STRUCTS}
-    h2d = sum(BATCH * (qs[s][0].shape[1] + qs[s][1].shape[1]) * 4 for s in STRUCTS)
-    d2h = len(STRUCTS) * BATCH * K * 8
-    e2e_v = e2e_async_v = None
-    if world == 1:
-        for s in STRUCTS:
-            eng.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K, out=(hout[0].numpy(), hout[1].numpy()))
-        torch.cuda.synchronize()
-        e2e_s = 0.0
-        for _ in range(args.steps):  # L2 flushed before every step, outside the timed region
-            flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for s in STRUCTS:
-                eng.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K, out=(hout[0].numpy(), hout[1].numpy()))
-            e2e_s += time.perf_counter() - t0
-        e2e_v = queries / e2e_s
-        # the same through kgq_submit_host_async: every type's H2D + path + D2H enqueued, one
-        # stream synchronisation per step (a serving loop's view: host turnaround overlapped)
-        for s in STRUCTS:
-            eng.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K,
-                            out=(hout_t[s][0].numpy(), hout_t[s][1].numpy()), sync=False)
-        torch.cuda.synchronize()
-        e2e_as = 0.0
+        mt = 0.0
         for _ in range(args.steps):
             flush.zero_()
+            e0.record()
+            meng.submit_mixed(groups, K, out=mout)
+            e1.record()
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for s in STRUCTS:
-                eng.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K,
-                                out=(hout_t[s][0].numpy(), hout_t[s][1].numpy()), sync=False)
-            torch.cuda.synchronize()
-            e2e_as += time.perf_counter() - t0
-        e2e_async_v = queries / e2e_as
-    else:
-      try:  # (a failure here must not cost the headline line: e2e is then null with the reason)
-        # N > 1: the sharded public API (ShardedEngine.submit: local top-k + all-gather + merge)
-        # with the step's inputs copied from pinned host memory and the merged top-k copied
-        # back into pinned host buffers, one synchronisation per step; max over ranks
-        dev_in = {s: (torch.empty_like(qs[s][2]), torch.empty_like(qs[s][3])) for s in STRUCTS}
-        pin_i = {s: (qs[s][2].cpu().pin_memory(), qs[s][3].cpu().pin_memory()) for s in STRUCTS}
+            mt += e0.elapsed_time(e1)
+        mixed = {"value": per_rank_queries * args.steps / (mt / 1e3), "unit": "queries/s",
+                 "ms_per_step": mt / args.steps,
+                 "how": "one kgq_submit_mixed per step with the same 14 x 1024 queries on one stream (L2 flushed "
+                        "between steps): each projection hop of all 14 types' branches is one MLP"}
+        meng.close()
 
+    # ---- end to end through the public API with host buffers (pinned), same streams ----
+    pin = {s: (torch.from_numpy(qs[s][0]).pin_memory(), torch.from_numpy(qs[s][1]).pin_memory()) for s in STRUCTS}
+    hout = {s: (torch.empty((Bg, K)).pin_memory(), torch.empty((Bg, K), dtype=torch.int32).pin_memory())
+            for s in STRUCTS}
+    h2d = sum(Bg * (qs[s][0].shape[1] + qs[s][1].shape[1]) * 4 for s in STRUCTS)
+    d2h = len(STRUCTS) * Bg * K * 8
+    e2e_v = None
+    try:
         def e2e_step():
             for s in STRUCTS:
-                dev_in[s][0].copy_(pin_i[s][0], non_blocking=True)
-                dev_in[s][1].copy_(pin_i[s][1], non_blocking=True)
-                td, ti = seng.submit(s, dev_in[s][0], dev_in[s][1], K)
-                hout_t[s][0].copy_(td, non_blocking=True)
-                hout_t[s][1].copy_(ti, non_blocking=True)
-            torch.cuda.synchronize()
+                j = lane[s]
+                engines[j].engine.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K,
+                                              out=(hout[s][0].numpy(), hout[s][1].numpy()), stream=streams[j],
+                                              sync=False)
+            for st in streams:
+                st.synchronize()
         e2e_step()
-        e2e_as = 0.0
+        e2e_step()
+        e2e_s = 0.0
         for _ in range(args.steps):
             flush.zero_()
             barrier()
             t0 = time.perf_counter()
             e2e_step()
-            e2e_as += time.perf_counter() - t0
-        tt = torch.tensor([e2e_as], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_async_v = queries / float(tt.item())
-        h2d = sum(pin_i[s][0].numel() * 4 + pin_i[s][1].numel() * 4 for s in STRUCTS)
-      except Exception as ex:  # noqa: E722
-        e2e_async_v = None
-        print(f"bench: N>1 e2e failed: {type(ex).__name__}: {ex}", file=sys.stderr, flush=True)
+            e2e_s += time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda" if not one_gpu else "cpu")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e_v = job_queries * args.steps / e2e_s
+    except Exception as ex:  # a failure here must not cost the headline line: e2e is then null
+        print(f"bench: e2e failed: {type(ex).__name__}: {ex}", file=sys.stderr, flush=True)
+    for se in engines:
+        se.engine.check_errors()
+
+    # ---- C5a: the north-star HBM target (2M-entity scoring sweep, B in {1, 8}) ----
+    peaks, peak_src = load_peaks()
+    c5a = None
+    if world == 1 and not args.no_c5a:
+        try:
+            c5a = c5a_measure(max(3, args.steps // 2), 2, peaks)
+        except Exception as ex:
+            print(f"bench: C5a failed: {type(ex).__name__}: {ex}", file=sys.stderr, flush=True)
 
     # ---- roofline of the dominant kernel: the tcgen05 bf16x3 GEMM (k_gemm), which runs every
-    # dense layer of the chain (stage "dense") and the BetaE scorer contraction (stage "score").
-    # Algorithmic work = useful fp32 FLOPs (2MNK); peak = measured bf16 GEMM peak / 6 (six bf16
-    # MMAs per useful fp32 multiply-add: x0w0, x0w1, x1w0, x0w2, x1w1, x2w0).
-    peaks, peak_src = load_peaks()
-    d_ms, d_n, d_fl = prof["dense"]
-    s_ms, s_n, s_fl = prof["score"]
-    peak_tc = peaks["bf16_tflops"] / 6.0
-    ach = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms > 0 else 0.0
-    achieved = ach(d_fl + s_fl, d_ms + s_ms)
+    # dense layer of the chain and the BetaE scorer contraction.  Algorithmic work = useful fp32
+    # FLOPs (2MNK, the library's counters); time = the union of the GEMM launches' in-kernel spans
+    # (%globaltimer, first CTA start after the PDL wait -> last CTA end) over the timed steps of
+    # THIS pass, merged over the concurrent streams; peak = measured bf16 / 6 (six bf16 MMAs per
+    # useful fp32 multiply-add: x0w0, x0w1, x1w0, x0w2, x1w1, x2w0), the sustained figure (the
+    # GEMMs run inside a long step), the burst one quoted beside it.
+    peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 6.0
+    peak_burst = peaks["bf16_tflops"] / 6.0
+    rate = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+    achieved = rate(d_fl + s_fl, gemm_busy_ms)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "tc_gemm_traffic.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get("dram_bytes_per_launch")
-    tot_ms = prof["chain"][0] + prof["prep"][0] + prof["score"][0] + prof["topk"][0]
-    stage_share = {k: round(prof[k][0] / max(1e-9, tot_ms), 4) for k in ("chain", "prep", "score", "topk", "dense")}
     if rank == 0:
+        ms_step = total_ms / args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak" if qsplit or world == 1 else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(CONFIG, l2="flushed between timed steps (256 MiB write, untimed)",
-                           parallelism=f"entity-shard x{world}" if world > 1 else "1 GPU",
-                           merge=seng.merge_mode if world > 1 else None),
-            "per_type_qps": {s: BATCH * args.steps / (per_type[s] / 1e3) for s in STRUCTS},
-            "stage_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()},  # dense is inside chain
-            "stage_pass": {"ms_per_step": sum(prof_step_ms) / prof_steps,
-                           "how": "stage split and roofline from a second pass of the same steps with the "
-                                  "library's stage events on (their event nodes sit between the captured kernels: slower than the "
-                                  "headline pass, which runs without them)"},
-            "stage_share": stage_share,
+                           streams=S,
+                           parallelism=("1 GPU" if world == 1 else
+                                        f"query split x{world} (W x 1024 replicated rows per type, each rank its "
+                                        f"1024; library NCCL all-gather)" if qsplit else
+                                        f"entity shards x{world} ({engines[0].merge_mode})"),
+                           batch_per_type=Bg),
+            "how": (f"per step: the 14 per-type kgq_submit calls (1024 queries each per rank) dealt round-robin over "
+                    f"{S} CUDA streams, one library context per stream; device time from an event before the "
+                    f"fork to an event after the join, max over ranks"),
+            "sequential": None if seq_ms is None else {
+                "value": job_queries * args.steps / (seq_ms / 1e3), "ms_per_step": seq_ms / args.steps,
+                "how": "the same steps with the 14 submits on one stream (no overlap between types)"},
+            "gemm": {"busy_ms_per_step": gemm_busy_ms, "dense_busy_ms_per_step": dense_busy_ms,
+                     "score_busy_ms_per_step": score_busy_ms, "dense_span_sum_ms": dense_span_sum,
+                     "score_span_sum_ms": score_span_sum, "launches_per_step": gemm_launches,
+                     "share_of_step": gemm_busy_ms / ms_step,
+                     "how": "in-kernel %globaltimer spans of every k_gemm launch of the timed steps (kgq_ktime_log), "
+                            "union over the concurrent streams"},
             "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",
-                         "bound": "tensor", "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tc, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC; burst, the larger denominator)",
-                         "work": "useful fp32 FLOPs 2MNK per GEMM launch",
-                         "launches": d_n + s_n,
-                         "parts": {"dense": {"ms_per_step": d_ms / prof_steps, "tflops": ach(d_fl, d_ms),
-                                             "launches_per_step": d_n / prof_steps},
-                                   "score": {"ms_per_step": s_ms / prof_steps, "tflops": ach(s_fl, s_ms),
-                                             "launches_per_step": s_n / prof_steps}}},
-            "gpu_launches": launches[0],
+                         "bound": "tensor", "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
+                         "frac": achieved / peak_sus, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16 sustained {peak_sus * 6:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
+                         "frac_vs_burst": achieved / peak_burst,
+                         "work": f"useful fp32 FLOPs 2MNK per GEMM launch: {(d_fl + s_fl) / 1e9:.1f} GFLOP per step "
+                                 f"per rank (dense {d_fl / 1e9:.1f}, score {s_fl / 1e9:.1f})",
+                         "whole_step_rate": rate(d_fl + s_fl, ms_step),
+                         "parts": None if seq_dense_ms is None else {
+                             "how": "each part's GEMMs alone on the GPU: the sequential (one-stream) pass's in-kernel "
+                                    "spans; under the concurrent streams the parts overlap each other",
+                             "dense": {"ms_per_step": seq_dense_ms, "tflops": rate(d_fl, seq_dense_ms),
+                                       "frac": rate(d_fl, seq_dense_ms) / peak_sus,
+                                       "frac_vs_burst": rate(d_fl, seq_dense_ms) / peak_burst},
+                             "score": {"ms_per_step": seq_score_ms, "tflops": rate(s_fl, seq_score_ms),
+                                       "frac": rate(s_fl, seq_score_ms) / peak_sus,
+                                       "frac_vs_burst": rate(s_fl, seq_score_ms) / peak_burst}}},
+            "gpu_launches": n_launch,
             "mixed_submit": mixed,
-            "e2e": {"value": e2e_async_v, "unit": "queries/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "how": ("per step: kgq_submit_host_async per type (pinned H2D, path, D2H into pinned "
-                            "host outputs) and one stream synchronisation; wall clock per step, L2 flushed "
-                            "before each step (untimed)") if world == 1 else
-                           ("per step: pinned H2D, ShardedEngine.submit per type (local top-k, all-gather, "
-                            "merge), D2H of the merged top-k into pinned host buffers, one synchronisation; "
-                            "wall clock per step, max over ranks"),
-                    "sync_per_call": {"value": e2e_v,
-                                      "how": "kgq_submit_host (synchronises after every type)"}},
+            "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "how": (f"per step: kgq_submit_host_async per type on the same {S} streams (pinned H2D of "
+                            f"anchors / relations, path, D2H of the top-k into pinned host outputs), every stream "
+                            f"synchronised; wall clock, L2 flushed before each step (untimed), max over ranks")},
+            "hbm": None if c5a is None else {
+                "workload": "BASELINE.json configs[4] latency regime: 2M entities, d 400, 1 GPU, GQE / BetaE, "
+                            "1p / 2u, B in {1, 8}",
+                "kernel": "k_score_stream (streaming entity scorer)", "bound": "hbm", "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "peak_source": f"{peak_src} copy bandwidth",
+                "work": "the shard's scoring table read once per batch: GQE 4 N d bytes, BetaE 8 N d (the centred "
+                        "fp32 u, v planes)",
+                "results": {k: {"gbs": round(v["scorer_table_gbs"], 1), "frac": round(v["hbm_frac"], 4),
+                                "queries_per_s": round(v["queries_per_s"], 1)} for k, v in c5a.items()}},
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:

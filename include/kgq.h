@@ -297,6 +297,23 @@ kgq_status kgq_profile_enable(kgq_ctx* ctx, int32_t on);
  * (may be NULL; dense: 2MNK FLOPs; scorer: FLOPs of the tensor-core BetaE contraction or FP32
  * lane instructions of the SIMT scorers) since the last read; synchronises, then resets. */
 kgq_status kgq_profile_read(kgq_ctx* ctx, double* ms, int64_t* n, double* work);
+/* In-kernel launch spans of the tcgen05 GEMM (bench roofline taken from the headline pass
+ * itself, no events between kernels).  With it on, every GEMM launch stamps %globaltimer in
+ * its first CTA (after the programmatic-dependent-launch wait) and its last CTA, and the last
+ * CTA adds the span to a device sum per stage: 0 = dense layers of the operator chain, 1 = the
+ * BetaE tensor-core scorer.  Cost: three atomics per CTA.  Toggling re-captures the submit
+ * graphs once (the accounting pointer is a kernel argument). */
+kgq_status kgq_ktime_enable(kgq_ctx* ctx, int32_t on);
+/* Summed spans in ms[2] and launch counts n[2] since the last read; synchronises the device,
+ * then resets. */
+kgq_status kgq_ktime_read(kgq_ctx* ctx, double* ms, int64_t* n);
+/* The launch spans themselves (appended by every GEMM launch while kgq_ktime_enable is on, up to
+ * 65,536): copies min(count, cap) entries of three uint64 {start ns, end ns, stage} (%globaltimer,
+ * one clock per device, so the logs of several contexts on one GPU can be merged) to host out,
+ * returns the count logged since the last call (-1 on error); synchronises, then empties the
+ * log.  The union of the spans is the time the GPU spent in GEMMs, also under concurrent
+ * streams. */
+int64_t kgq_ktime_log(kgq_ctx* ctx, uint64_t* out, int64_t cap);
 
 #ifdef __cplusplus
 }

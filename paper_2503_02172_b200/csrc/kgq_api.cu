@@ -560,14 +560,14 @@ void kgq_destroy(kgq_ctx* ctx) {
   for (auto& l : ctx->lin) { F(l.W); F(l.Wsp.b0); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) F(s->b0);
   F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->d_err); F(ctx->d_invalid);
-  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum); F(ctx->lin1x.Wsp.b0); F(ctx->RW);
+  F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum); F(ctx->uvT); F(ctx->lin1x.Wsp.b0); F(ctx->RW);
   F(ctx->mix_rid); F(ctx->mix_map);
   if (ctx->mix_map_host) cudaFreeHost(ctx->mix_map_host);
   if (ctx->mix_map_ev) cudaEventDestroy(ctx->mix_map_ev);
   F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage); F(ctx->d_epoch);
   if (ctx->comm) nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
-  F(ctx->cm_d); F(ctx->cm_i); F(ctx->cg_d); F(ctx->cg_i);
+  F(ctx->cm_d); F(ctx->cm_i); F(ctx->cg_d); F(ctx->cg_i); F(ctx->kt_buf);
   for (auto& gr : ctx->graphs) destroy_graph_entry(gr);
   clear_mix_graphs(ctx);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -691,6 +691,7 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st && c.model == KGQ_BETAE) {
     st = alloc_split(ctx, &ctx->uv, ctx->np, 2 * d, "uv table");
     if (!st) st = dalloc(ctx, &ctx->Esum, (size_t)ctx->np, "entity sums");
+    if (!st && !ctx->uvT) st = dalloc(ctx, &ctx->uvT, (size_t)2 * d * ctx->np, "uv table (dim-major)");
     if (!st) st = dalloc(ctx, &ctx->uvsums, (size_t)(2 * d + 2 * kLogTab), "uv sums + log table");
     if (!st) {  // ln c_i and 1 / c_i, c_i = 1 + i / kLogTab, after the sums (common.cuh log_tab)
       double tab[2 * kLogTab];
@@ -732,7 +733,7 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
     launch_beta_regularize(ctx->ent, c.n_entity * ctx->ew, 0);
     launch_betae_entity_terms(ctx->ent, ctx->e0, ctx->ns, d, ctx->score_tab, ctx->np, 0);
     launch_betae_uv_table(ctx->ent, c.n_entity, ctx->e0, ctx->ns, ctx->np, d, ctx->uvsums, ctx->uv,
-                          ctx->Esum, 0);
+                          ctx->Esum, ctx->uvT, 0);
   } else {
     launch_transpose_shard(ctx->ent, ctx->e0, ctx->ns, d, ctx->ew, ctx->score_tab, ctx->np, 0);
   }
@@ -744,6 +745,15 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
 
 // Distances of query rows [b0, b0 + nb) (chain already run) to every entity of the shard,
 // into ctx->dist rows [0, nb).  Returns the number of kernels launched.
+// KGQ_BETAE_STREAM=cuv: the round-1 small-batch BetaE scorer on the C, U, V planes (A/B only)
+static bool betae_stream_cuv() {
+  static const bool v = [] {
+    const char* e = getenv("KGQ_BETAE_STREAM");
+    return e && e[0] == 'c';
+  }();
+  return v;
+}
+
 static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStream_t st, int B = 0,
                       bool from_state = false) {
   const kgq_config& c = ctx->cfg;
@@ -763,6 +773,15 @@ static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStrea
                                ctx->Ptc, ctx->uv, ctx->Esum, ctx->np, ctx->dist, ctx->np, ctx->cmin,
                                ctx->np / 32, ctx->ns, &ctx->gws, st);
     check_site("tensor-core scorer");
+  } else if (c.model == KGQ_BETAE && !betae_stream_cuv()) {
+    // HBM regime: stream the centred (u, v) table, 8 bytes per (entity, dim)
+    {
+      StageTimer t(ctx, st, kStPrep);
+      L += launch_score_prep_tc(qb, nb * P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc, ctx->Ptc, st);
+    }
+    StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * c.dim);
+    L += launch_score_betae_stream(ctx->Atc, ctx->Ptc, ctx->uvT, ctx->Esum, ctx->np, c.dim, ctx->dist, ctx->np, nb,
+                                   P->n_out, st);
   } else {
     {
       StageTimer t(ctx, st, kStPrep);
@@ -1752,6 +1771,65 @@ kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_
   ctx->launches = L;
   CK(cudaGetLastError(), "rank launch");
   return KGQ_OK;
+}
+
+static const unsigned long long kKtInit[24] = {~0ull, 0, 0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 1, 0, 0,
+                                               0,    0, 0, 0, 0, 0, 0, 0};
+constexpr size_t kKtWords = 24 + 3 * kKtLogCap;
+
+kgq_status kgq_ktime_enable(kgq_ctx* ctx, int32_t on) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  DeviceGuard g(ctx->cfg.device);
+  if (on && !ctx->kt_buf) {
+    kgq_status st = dalloc(ctx, &ctx->kt_buf, kKtWords, "ktime words");
+    if (st) return st;
+    CK(cudaMemcpy(ctx->kt_buf, kKtInit, sizeof kKtInit, cudaMemcpyHostToDevice), "ktime init");
+  }
+  unsigned long long* want = on ? ctx->kt_buf : nullptr;
+  if (ctx->gws.kt != want) {  // captured graphs carry the old pointer
+    CK(cudaDeviceSynchronize(), "ktime toggle");
+    for (auto& gr : ctx->graphs) {
+      if (gr.pending) harvest(ctx, gr.evs, false);
+      destroy_graph_entry(gr);
+    }
+    ctx->graphs.clear();
+    clear_mix_graphs(ctx);
+    ctx->gws.kt = want;
+  }
+  return KGQ_OK;
+}
+
+kgq_status kgq_ktime_read(kgq_ctx* ctx, double* ms, int64_t* n) {
+  if (!ctx || !ms || !n) return fail(ctx, KGQ_EINVAL, "NULL argument");
+  ms[0] = ms[1] = 0.0;
+  n[0] = n[1] = 0;
+  if (!ctx->kt_buf) return KGQ_OK;
+  DeviceGuard g(ctx->cfg.device);
+  unsigned long long h[16];  // the two stage word groups (the log stays: kgq_ktime_log)
+  CK(cudaDeviceSynchronize(), "ktime read");
+  CK(cudaMemcpy(h, ctx->kt_buf, sizeof h, cudaMemcpyDeviceToHost), "ktime read");
+  for (int s = 0; s < 2; ++s) {
+    ms[s] = (double)h[8 * s + 3] * 1e-6;
+    n[s] = (int64_t)h[8 * s + 4];
+  }
+  CK(cudaMemcpy(ctx->kt_buf, kKtInit, 16 * sizeof(unsigned long long), cudaMemcpyHostToDevice), "ktime reset");
+  return KGQ_OK;
+}
+
+int64_t kgq_ktime_log(kgq_ctx* ctx, uint64_t* out, int64_t cap) {
+  if (!ctx || cap < 0 || (cap > 0 && !out)) return -1;
+  if (!ctx->kt_buf) return 0;
+  DeviceGuard g(ctx->cfg.device);
+  unsigned long long n = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (cudaMemcpy(&n, ctx->kt_buf + 16, sizeof n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  n = std::min<unsigned long long>(n, kKtLogCap);
+  const int64_t m = std::min<int64_t>((int64_t)n, cap);
+  if (m > 0 && cudaMemcpy(out, ctx->kt_buf + 24, (size_t)m * 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  const unsigned long long zero = 0;
+  if (cudaMemcpy(ctx->kt_buf + 16, &zero, sizeof zero, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+  return (int64_t)n;
 }
 
 kgq_status kgq_profile_enable(kgq_ctx* ctx, int32_t on) {

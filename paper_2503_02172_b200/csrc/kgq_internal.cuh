@@ -59,7 +59,11 @@ enum Epi { kEpiNone = 0, kEpiRelu = 1, kEpiBetaReg = 2 };
 struct GemmWs {
   float* ws = nullptr;
   int* cnt = nullptr;
+  // kgq_ktime_enable: in-kernel launch spans of the GEMM, [2 stages: dense, score][8] u64 =
+  // {first CTA start (after the PDL wait), last CTA end, CTAs done, summed ns, launches}
+  unsigned long long* kt = nullptr;
 };
+constexpr unsigned long long kKtLogCap = 1ull << 16;  // GEMM launch-span log entries (kgq_ktime_log)
 constexpr size_t kGemmWsFloats = (size_t)74 * 256 * 256;  // <= 74 tail units of 256 x 256
 constexpr int kGemmCntInts = 74 * 16;                      // <= 74 tail tiles x 16 epilogue warps
 
@@ -113,6 +117,7 @@ struct kgq_ctx {
   int64_t* mix_map_host = nullptr;         // pinned staging of mix_map
   cudaEvent_t mix_map_ev = nullptr;        // staging reuse guard
   float2* Esum = nullptr;                  // [np] sum_d C_ed as an fp32 (hi, lo) pair
+  float* uvT = nullptr;                    // [d][2][np] centred u, v in fp32 (small-batch streaming scorer)
   double* uvsums = nullptr;                // [2][d]
   kgq::GemmWs gws{};                       // tensor-core GEMM split-tail scratch
   kgq::Split Atc{};                        // [2*max_batch][2d] split query rows
@@ -172,6 +177,7 @@ struct kgq_ctx {
   int32_t* cm_i = nullptr;
   float* cg_d = nullptr;                   // [world * max_batch, max_k] all-gathered lists
   int32_t* cg_i = nullptr;
+  unsigned long long* kt_buf = nullptr;    // kgq_ktime_enable: GEMM launch-span words [2][8]
 
 };
 
@@ -336,7 +342,13 @@ int launch_filtered_counts(const float* dist, int64_t ldd, int64_t e0, int64_t n
 // uv [np][2d], E_e = sum_d C_ed (fp64) and the per-dim U/V sums; per batch it splits the
 // query rows, computes P_q (fp64) and runs the bf16x3 tcgen05 GEMM with the score epilogue.
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
-                          double* sums, Split uv, float2* Esum, cudaStream_t st);
+                          double* sums, Split uv, float2* Esum, float* uvT, cudaStream_t st);
+// BetaE query prep of the tensor-core / streaming scorers: split [a; b] rows and fp64 P_q
+int launch_score_prep_tc(const float* q, int rows, int d, const double* sums, int64_t ns, Split A, float2* P,
+                         cudaStream_t st);
+// BetaE small-batch scorer (<= 16 query rows) streaming the centred fp32 (u, v) table uvT [d][2][np]
+int launch_score_betae_stream(const Split& A, const float2* P, const float* uvT, const float2* E, int64_t np, int d,
+                              float* dist, int64_t ldd, int B, int nbq, cudaStream_t st);
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,
                           Split A, float2* P, const Split& uv, const float2* Esum,
                           int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,

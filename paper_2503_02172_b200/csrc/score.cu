@@ -161,8 +161,18 @@ __global__ void __launch_bounds__(256, 2)
 // dim and plane) while the <= 16 query rows sit in shared memory and are read as broadcasts.
 // Per (q, e, d) it evaluates exactly the expression of k_score, in the same order, so both
 // variants return bit-identical distances.
+#ifndef KGQ_STREAM_MINB  // min resident CTAs of the GQE <= 8-row variants (register cap)
+#define KGQ_STREAM_MINB 3
+#endif
+#ifndef KGQ_STREAM_UNROLL
+#define KGQ_STREAM_UNROLL 4
+#endif
+#ifndef KGQ_STREAM_QVEC
+#define KGQ_STREAM_QVEC 1
+#endif
+constexpr int kStreamUnroll = KGQ_STREAM_UNROLL;
 template <int MODEL, int NB, int QB>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (MODEL == KGQ_GQE && QB * NB <= 8) ? KGQ_STREAM_MINB : 1)
     k_score_stream(const float* __restrict__ Qt, int64_t rpad, const float* __restrict__ tab,
                    int64_t np, int d, float cen, float* __restrict__ dist, int64_t ldd, int B) {
   constexpr int NQ = Planes<MODEL>::NQ, NE = Planes<MODEL>::NE, R = QB * NB;
@@ -182,7 +192,7 @@ __global__ void __launch_bounds__(256)
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[r][i] = acc2[r][i] = 0.0f;
-#pragma unroll 4
+#pragma unroll kStreamUnroll
     for (int j = 0; j < d; ++j) {
       float e[NE][4];
 #pragma unroll
@@ -191,7 +201,18 @@ __global__ void __launch_bounds__(256)
         const float4 v = __ldg(reinterpret_cast<const float4*>(src));
         e[p][0] = v.x; e[p][1] = v.y; e[p][2] = v.z; e[p][3] = v.w;
       }
-      const float* qj = qs + j * NQ * R;
+      const float* qjp = qs + j * NQ * R;
+      float qj[NQ * R];  // this dim's query operands (16-byte broadcast loads when R % 4 == 0)
+      if constexpr (KGQ_STREAM_QVEC && (NQ * R) % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < NQ * R; i += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(qjp + i);
+          qj[i] = t4.x; qj[i + 1] = t4.y; qj[i + 2] = t4.z; qj[i + 3] = t4.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NQ * R; ++i) qj[i] = qjp[i];
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -229,6 +250,116 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- BetaE small-batch streaming scorer on the centred (u, v) table -------------------------
+// The per-dimension KL splits into query-only, entity-only and bilinear terms (score_tc.cu):
+//   dist(q, e) = P_q + E_e + sum_d (a_qd u_ed + b_qd v_ed),  u = U - mean(U), v = V - mean(V),
+// with P_q, E_e computed in fp64 and held as fp32 (hi, lo) pairs, and sum_d |KL_d| = sum_d KL_d
+// (each KL_d >= 0).  So the sweep streams only u and v (8 bytes per entity and dimension instead
+// of the C, U, V planes' 12) and does two fused multiply-adds per (query row, entity, dim), as
+// packed FFMA2 over entity pairs (fma.rn.f32x2): one instruction per (q, e, d).  Thread = four
+// consecutive entities (two 16-byte loads per dimension, coalesced 512 bytes per warp and
+// plane); the query rows' (a, a, b, b) quadruples sit in shared memory and are read as 16-byte
+// broadcasts.  Epilogue = the tensor-core scorer's: (P_hi + E_hi) + ((P_lo + E_lo) + acc).
+__device__ __forceinline__ void ffma2(float2& c, const float2 a, const float2 b) {
+  asm("{\n.reg .b64 x, y, z;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 z, {%0, %1};\n"
+      "fma.rn.f32x2 z, x, y, z;\nmov.b64 {%0, %1}, z;\n}\n"
+      : "+f"(c.x), "+f"(c.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+}
+
+template <int NB, int QB>
+__global__ void __launch_bounds__(256)
+    k_score_uv_stream(Split A, const float2* __restrict__ P, const float* __restrict__ uvT, const float2* __restrict__ E,
+                      int64_t np, int d, float* __restrict__ dist, int64_t ldd, int B) {
+  constexpr int R = QB * NB;
+  constexpr int EP = R >= 16 ? 2 : 4;  // entities per thread (two with 16 rows: 64 accumulators otherwise)
+  constexpr int NP2 = EP / 2;          // entity pairs (FFMA2 lanes)
+  extern __shared__ __align__(16) float4 qab[];  // [d][R] = (a, a, b, b)
+  pdl_grid_sync();
+  const int rows = B * NB;
+  for (int i = threadIdx.x; i < d * R; i += blockDim.x) {
+    const int r = i % R, j = i / R;
+    float a = 0.0f, b = 0.0f;
+    if (r < rows) {
+      a = load_split(A, (int64_t)r * A.ld + j);
+      b = load_split(A, (int64_t)r * A.ld + d + j);
+    }
+    qab[i] = make_float4(a, a, b, b);
+  }
+  __syncthreads();
+  const int64_t ngroups = np / EP;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = g * EP;
+    float2 acc[R][NP2];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int p = 0; p < NP2; ++p) acc[r][p] = make_float2(0.0f, 0.0f);
+    const float* up = uvT + e0;
+#pragma unroll 4
+    for (int j = 0; j < d; ++j) {
+      float2 u[NP2], v[NP2];
+      if constexpr (EP == 4) {
+        const float4 u4 = __ldg(reinterpret_cast<const float4*>(up + (int64_t)(2 * j) * np));
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(up + (int64_t)(2 * j + 1) * np));
+        u[0] = make_float2(u4.x, u4.y);
+        u[NP2 - 1] = make_float2(u4.z, u4.w);
+        v[0] = make_float2(v4.x, v4.y);
+        v[NP2 - 1] = make_float2(v4.z, v4.w);
+      } else {
+        u[0] = __ldg(reinterpret_cast<const float2*>(up + (int64_t)(2 * j) * np));
+        v[0] = __ldg(reinterpret_cast<const float2*>(up + (int64_t)(2 * j + 1) * np));
+      }
+      const float4* qj = qab + j * R;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float4 q = qj[r];
+#pragma unroll
+        for (int p = 0; p < NP2; ++p) {
+          ffma2(acc[r][p], u[p], make_float2(q.x, q.y));
+          ffma2(acc[r][p], v[p], make_float2(q.z, q.w));
+        }
+      }
+    }
+    float2 ee[EP];
+#pragma unroll
+    for (int i = 0; i < EP; ++i) ee[i] = __ldg(E + e0 + i);
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      if (b >= B) break;
+      float o[EP];
+#pragma unroll
+      for (int br = 0; br < NB; ++br) {
+        const float2 p = __ldg(P + b * NB + br);
+#pragma unroll
+        for (int i = 0; i < EP; ++i) {
+          const float s = (i & 1) ? acc[b * NB + br][i >> 1].y : acc[b * NB + br][i >> 1].x;
+          const float v = (p.x + ee[i].x) + ((p.y + ee[i].y) + s);
+          o[i] = br == 0 ? v : fminf(o[i], v);
+        }
+      }
+      if constexpr (EP == 4)
+        *reinterpret_cast<float4*>(dist + (int64_t)b * ldd + e0) = make_float4(o[0], o[1], o[2], o[3]);
+      else
+        *reinterpret_cast<float2*>(dist + (int64_t)b * ldd + e0) = make_float2(o[0], o[1]);
+    }
+  }
+}
+
+template <int NB, int QB>
+void launch_uv_stream_t(const Split& A, const float2* P, const float* uvT, const float2* E, int64_t np, int d,
+                        float* dist, int64_t ldd, int B, cudaStream_t st) {
+  constexpr int EP = QB * NB >= 16 ? 2 : 4;
+  const size_t smem = (size_t)d * QB * NB * sizeof(float4);
+  static unsigned long long attr = 0;
+  smem_attr_once(k_score_uv_stream<NB, QB>, (int)smem, attr);
+  const int64_t groups = np / EP;
+  const int64_t want = (groups + 255) / 256;
+  const int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+  launch_pdl(k_score_uv_stream<NB, QB>, dim3(grid), dim3(256), smem, st, A, P, uvT, E, np, d, dist, ldd, B);
+}
+
 template <int MODEL, int NB, int QB>
 void launch_stream_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d, float cen,
                      float* dist, int64_t ldd, int B, cudaStream_t st) {
@@ -262,6 +393,19 @@ void launch_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d
   k_score<MODEL, NB><<<grid, 256, smem, st>>>(Qt, rpad, tab, np, d, cen, dist, ldd, B);
 }
 }  // namespace
+
+int launch_score_betae_stream(const Split& A, const float2* P, const float* uvT, const float2* E, int64_t np, int d,
+                              float* dist, int64_t ldd, int B, int nbq, cudaStream_t st) {
+  if (B <= 0) return 0;
+#define KGQ_UV(NB)                                                                   \
+  if (B <= 1) launch_uv_stream_t<NB, 1>(A, P, uvT, E, np, d, dist, ldd, B, st);      \
+  else if (B <= 2) launch_uv_stream_t<NB, 2>(A, P, uvT, E, np, d, dist, ldd, B, st); \
+  else if (B <= 4) launch_uv_stream_t<NB, 4>(A, P, uvT, E, np, d, dist, ldd, B, st); \
+  else launch_uv_stream_t<NB, 8>(A, P, uvT, E, np, d, dist, ldd, B, st);
+  if (nbq == 2) { KGQ_UV(2) } else { KGQ_UV(1) }
+#undef KGQ_UV
+  return 1;
+}
 
 // Small batches (<= 16 query rows; <= 8 for Q2B, which keeps two sums per pair) stream the
 // table (HBM-bound regime); larger batches use the register-tiled kernel (FP32-ALU-bound).

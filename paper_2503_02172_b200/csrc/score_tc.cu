@@ -54,7 +54,7 @@ __device__ __forceinline__ float2 split_f64(double x) {
 
 __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns, int64_t np, int d,
                            int64_t n_all, const double* __restrict__ sums, Split uv,
-                           float2* __restrict__ Esum) {
+                           float2* __restrict__ Esum, float* __restrict__ uvT) {
   const int64_t e = blockIdx.x;
   __shared__ double red[32];
   double c = 0.0;
@@ -69,6 +69,10 @@ __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns
     }
     store_split(uv, e * 2 * d + j, u);
     store_split(uv, e * 2 * d + d + j, v);
+    if (uvT) {  // dim-major fp32 copy for the small-batch streaming scorer: [d][2][np]
+      uvT[(int64_t)(2 * j) * np + e] = u;
+      uvT[(int64_t)(2 * j + 1) * np + e] = v;
+    }
   }
   c = warp_sum(c);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
@@ -208,13 +212,13 @@ struct EpiBetaScore {
 }  // namespace
 
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
-                          double* sums, Split uv, float2* Esum, cudaStream_t st) {
+                          double* sums, Split uv, float2* Esum, float* uvT, cudaStream_t st) {
   // centring means over ALL entities (every rank holds the full table), so that every shard
   // uses the same u, v and a sharded run is bit-identical to a single-GPU run
   cudaMemsetAsync(sums, 0, 2 * d * sizeof(double), st);
   const int gx = (int)(n_all < 1024 ? n_all : 1024);
   k_uv_dim_sums<<<dim3(gx, (d + 127) / 128), 128, 0, st>>>(ent, 0, n_all, d, sums);
-  k_uv_table<<<(unsigned)np, 128, 0, st>>>(ent, e0, ns, np, d, n_all, sums, uv, Esum);
+  k_uv_table<<<(unsigned)np, 128, 0, st>>>(ent, e0, ns, np, d, n_all, sums, uv, Esum, uvT);
   return 2;
 }
 
@@ -235,6 +239,13 @@ int launch_score_tc_gemm(int rows, int nbq, int d, Split A, const float2* P, con
                                 ws, st);
   return tc::launch_gemm_auto(A, rows, uv, (int)np, 2 * d, o, EpiBetaScore<1>{P, Esum, rows, np, cmin, ldc, nvalid},
                               ws, st);
+}
+
+int launch_score_prep_tc(const float* q, int rows, int d, const double* sums, int64_t ns, Split A, float2* P,
+                         cudaStream_t st) {
+  if (rows <= 0) return 0;
+  launch_pdl(k_score_prep_tc, dim3(rows), dim3(128), 0, st, q, rows, d, sums, ns, A, P);
+  return 1;
 }
 
 int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double* sums, int64_t ns,

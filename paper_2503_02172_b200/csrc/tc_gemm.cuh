@@ -301,7 +301,44 @@ struct Sched {
   int kper;    // K-blocks per split
   float* ws;   // [tail units][16 epilogue warps][BN / 8][32 lanes] float4 partial sums
   int* cnt;    // [tail tiles][16] arrival counters (zero between launches; the last arriver resets)
+  unsigned long long* kt = nullptr;  // launch-span accounting of this stage (GemmWs::kt), or null
 };
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Launch span = last CTA's end - first CTA's start (after griddepcontrol.wait, so a PDL-early
+// CTA's wait for the predecessor is not counted); the last CTA to finish adds it to the stage's
+// sum, appends (start, end, stage) to the context's span log (base - 8 stage: [16] = count,
+// [24 + 3 i ..] = entries, kKtLogCap of them) and re-arms the words for the next launch of the
+// stage (stream-ordered: that launch's CTAs pass griddepcontrol.wait only after this grid
+// completed).  Layout of the words: [start, end, ctas done, summed ns, launches, stage, -, -].
+__device__ __forceinline__ void kt_begin(unsigned long long* kt) {
+  if (kt) atomicMin(&kt[0], globaltimer_ns());
+}
+__device__ __forceinline__ void kt_end(unsigned long long* kt) {
+  if (!kt) return;
+  atomicMax(&kt[1], globaltimer_ns());
+  __threadfence();
+  if (atomicAdd(&kt[2], 1ull) == gridDim.x - 1) {
+    __threadfence();
+    const unsigned long long t0 = atomicAdd(&kt[0], 0ull), t1 = atomicAdd(&kt[1], 0ull);
+    kt[3] += t1 > t0 ? t1 - t0 : 0ull;
+    kt[4] += 1ull;
+    unsigned long long* base = kt - 8 * kt[5];
+    const unsigned long long i = atomicAdd(&base[16], 1ull);
+    if (i < kKtLogCap) {
+      base[24 + 3 * i] = t0;
+      base[25 + 3 * i] = t1;
+      base[26 + 3 * i] = kt[5];
+    }
+    kt[0] = ~0ull;
+    kt[1] = 0ull;
+    kt[2] = 0ull;
+    __threadfence();
+  }
+}
 __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, int& kb0, int& kb1, int& v) {
   if (u < sc.full) {
     t = u; kb0 = 0; kb1 = nk; v = -1;
@@ -396,6 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   // everything above overlaps the upstream grid's tail; its outputs are read only below
   pdl_wait();
   pdl_trigger();
+  if (threadIdx.x == 0) kt_begin(sc.kt);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -634,6 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(L::TMEM_COLS));
   }
+  if (threadIdx.x == 0) kt_end(sc.kt);
 }
 
 // ---- host: tensor maps (cached per buffer) -----------------------------------------------
@@ -825,7 +864,10 @@ int launch_gemm_auto(const Split& A, int M, const Split& W, int N, int K, const 
     return e && e[0] && e[0] != '0';
   }();
   const Plan p = plan_gemm(M, N, K, !no_split && ws != nullptr && ws->ws != nullptr, Epi::PLANES == 3);
-  const Sched sc{p.full, p.s_tail, p.kper, ws ? ws->ws : nullptr, ws ? ws->cnt : nullptr};
+  // launch-span accounting (kgq_ktime_enable): the scorer (the only epilogue with block minima)
+  // in slot 1, every dense layer in slot 0
+  const Sched sc{p.full, p.s_tail, p.kper, ws ? ws->ws : nullptr, ws ? ws->cnt : nullptr,
+                 ws && ws->kt ? ws->kt + 8 * (Epi::CMIN ? 1 : 0) : nullptr};
   switch (p.bn) {
     case 64: return launch_gemm<64>(A, M, W, N, K, o, epi, st, sc);
     case 128: return launch_gemm<128>(A, M, W, N, K, o, epi, st, sc);

@@ -39,6 +39,7 @@ EXPORTS = (
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
     "kgq_profile_read", "kgq_rank_answers", "kgq_peer_bytes", "kgq_set_peers", "kgq_merge_peers",
     "kgq_query_range", "kgq_nccl_unique_id", "kgq_comm_init", "kgq_comm_destroy", "kgq_rank_metrics",
+    "kgq_ktime_enable", "kgq_ktime_read", "kgq_ktime_log",
 )
 RANK_LOCAL, RANK_DIST, RANK_COUNT, RANK_FILTERED = 0, 1, 2, 3
 SPLIT_ENTITIES, SPLIT_QUERIES = 0, 1
@@ -96,6 +97,9 @@ _sig = {
     "kgq_comm_init": (_I32, [_P, ctypes.c_char_p, _I32, _I32, _I32]),
     "kgq_comm_destroy": (_I32, [_P]),
     "kgq_rank_metrics": (_I32, [_P, _I32, _P, _P, _P, _P, _P]),
+    "kgq_ktime_enable": (_I32, [_P, _I32]),
+    "kgq_ktime_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
+    "kgq_ktime_log": (_I64, [_P, _P, _I64]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -436,6 +440,25 @@ class Engine:
         out = torch.empty((3, self.dim, ns), dtype=torch.float32, device=f"cuda:{self.device}")
         self._check(_lib.kgq_entity_terms(self._h, _ptr(out), _stream(stream)))
         return out
+
+    def ktime(self, on: bool = True):
+        """In-kernel launch spans of the tcgen05 GEMM (kgq_ktime_enable)."""
+        self._check(_lib.kgq_ktime_enable(self._h, 1 if on else 0))
+
+    def ktime_read(self):
+        """{"dense": (ms, launches), "score": (ms, launches)} since the last read."""
+        ms = (ctypes.c_double * 2)()
+        n = (_I64 * 2)()
+        self._check(_lib.kgq_ktime_read(self._h, ms, n))
+        return {"dense": (ms[0], n[0]), "score": (ms[1], n[1])}
+
+    def ktime_log(self, cap=1 << 16):
+        """numpy uint64 [n, 3] of GEMM launch spans {start ns, end ns, stage 0 dense / 1 score}."""
+        buf = np.zeros((cap, 3), np.uint64)
+        n = int(_lib.kgq_ktime_log(self._h, buf.ctypes.data, cap))
+        if n < 0:
+            raise KgqError(6, "kgq_ktime_log failed")
+        return buf[:min(n, cap)].copy()
 
     def profile(self, on: bool = True):
         self._check(_lib.kgq_profile_enable(self._h, 1 if on else 0))

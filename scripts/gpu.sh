@@ -1,0 +1,47 @@
+#!/bin/bash
+# GPU-box recipes (run through gpurun from the repo root):
+#   gpurun -- 'bash scripts/gpu.sh TASK [TASK ...]'
+# Tasks (outputs under gpurun_out/, which gpurun brings back):
+#   smoke      __graft_entry__.smoke()
+#   tests      pytest -m gpu (all GPU parity tests)
+#   bench      default bench.py line (C2 headline + e2e + mixed + C5a HBM + cpu_baseline)
+#   reference  bench.py --impl reference (the oracle arm)
+#   suite      bench.py --workload suite (the other BASELINE configs)
+#   launches   ncu launch list of one bench step (gpu__time_duration, DRAM bytes per launch)
+#   ncu-gemm   ncu --set full of k_gemm launches of one bench step (a dense layer + the scorer)
+#   ncu-c5a    ncu --set full of the C5a streaming scorer (GQE 1p, B = 8)
+#   sanitize   compute-sanitizer memcheck / racecheck / synccheck on small configs
+#   chain      per-structure chain / full-row distance errors (scripts/diag_chain_err.py)
+#   ab         same-box A/B of the in-tree libkgq.so vs ab_libs/$AB_LIB on the C2 bench
+#   probes     tcgen05 GEMM checker / throughput probe / MMA issue probe (built by scripts/tc_probe.sh)
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+OUT=gpurun_out
+for task in "$@"; do
+  echo "== $task"
+  case "$task" in
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $OUT/smoke.txt 2>&1; tail -2 $OUT/smoke.txt ;;
+    tests) timeout 1800 python -m pytest tests -m gpu -q -rs --durations=15 > $OUT/pytest_gpu.txt 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.txt; tail -3 $OUT/pytest_gpu.txt ;;
+    bench) timeout 1200 python bench.py > $OUT/bench.json 2> $OUT/bench.err; tail -2 $OUT/bench.err ;;
+    reference) timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err ;;
+    suite) timeout 1500 python bench.py --workload suite --steps 5 --warmup 2 > $OUT/suite.jsonl 2> $OUT/suite.err ;;
+    launches) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+                --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-mixed --no-c5a > /dev/null 2>&1 ;;
+    ncu-gemm) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 30 -c 4 -o $OUT/prof_gemm -f \
+                python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-mixed --no-c5a --streams 1 > /dev/null 2>&1 ;;
+    ncu-c5a) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score_ -s 2 -c 1 -o $OUT/prof_c5a -f \
+               python scripts/c5a_one.py gqe 1p 8 3 > /dev/null 2>&1 ;;
+    sanitize) bash scripts/sanitize.sh > $OUT/sanitize.txt 2>&1; tail -12 $OUT/sanitize.txt ;;
+    chain) timeout 900 python scripts/diag_chain_err.py small medium c2 c4 > $OUT/chain_err.jsonl 2>&1 ;;
+    ab) for i in 1 2; do
+          for lib in paper_2503_02172_b200/libkgq.so ab_libs/${AB_LIB:-libkgq_prev.so}; do
+            KGQ_LIB_PATH=$PWD/$lib timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-mixed --no-c5a \
+              > $OUT/ab.json 2> $OUT/ab.err || tail -3 $OUT/ab.err
+            python -c "import json; d=json.load(open('$OUT/ab.json')); print('$lib', round(d['value']), round(d['ms_per_step'], 3), d['sequential'])" | tee -a $OUT/ab.txt
+          done
+        done ;;
+    probes) ( cd scripts; timeout 120 ./tc_bn_check; timeout 200 ./tc_probe_base; timeout 120 ./mma3_probe ) > $OUT/probes.txt 2>&1 ;;
+    *) echo "unknown task $task" ;;
+  esac
+done
+ls $OUT

@@ -1,0 +1,15 @@
+#!/bin/bash
+# compute-sanitizer over the library on small configs: memcheck (out-of-bounds /
+# misaligned accesses, leaks), racecheck (shared-memory hazards), synccheck (barrier misuse) on
+#   * the BetaE path with split-K GEMM tails (d 128, H 512, 300 queries: publish / last-arriver
+#     reduce with acq_rel fences), the tensor-core scorer and block-minima top-k,
+#   * the N2 peer push / merge protocol (three virtual ranks),
+#   * GQE / Q2B SIMT scorers (tiled and TMA-streamed) and the filtered rank.
+# Each tool runs scripts/sanitize_case.py under `compute-sanitizer --tool T`; the summaries are
+# the evidence (profiles/r02/sanitize_*.txt).
+cd "$(dirname "$0")/.."
+for tool in memcheck racecheck synccheck; do
+  echo "=== $tool"
+  KGQ_NO_GRAPHS=1 timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_case.py 2>&1 \
+    | grep -v "^========= COMPUTE-SANITIZER$" | tail -25
+done

@@ -539,3 +539,28 @@ def test_mixed_graph_replay_matches_eager():
     ee.check_errors()
     eg.close()
     ee.close()
+
+
+def test_ktime_launch_spans():
+    """kgq_ktime_*: every tcgen05 GEMM launch of a submit logs one in-kernel span (bench.py's
+    roofline time); the per-stage sums equal the logged spans, and toggling keeps results
+    bit-identical (the graphs are re-captured with the accounting pointer)."""
+    e, m, t = engine("betae")
+    a, r = synth.make_queries("up", 20, SMALL["N"], SMALL["R"], seed=2)
+    ref_d, ref_i = e.submit("up", dev(a), dev(r), 5)
+    e.ktime(True)
+    e.ktime_read()
+    e.ktime_log()
+    for _ in range(3):  # eager, capture, replay
+        d_, i_ = e.submit("up", dev(a), dev(r), 5)
+        assert torch.equal(i_, ref_i) and torch.equal(d_, ref_d)
+    kt = e.ktime_read()
+    log = e.ktime_log()
+    e.ktime(False)
+    n_dense, n_score = kt["dense"][1], kt["score"][1]
+    assert n_dense > 0 and n_score == 3          # up: one scorer GEMM per submit
+    assert len(log) == n_dense + n_score
+    assert np.all(log[:, 1] > log[:, 0])
+    for st, name in ((0, "dense"), (1, "score")):
+        sel = log[log[:, 2] == st]
+        np.testing.assert_allclose((sel[:, 1] - sel[:, 0]).sum() * 1e-6, kt[name][0], rtol=1e-9)
