@@ -180,9 +180,18 @@ def c5a_measure(steps, warmup, peaks, models=("gqe", "betae")):
                 eng.profile(False)
                 sc_ms = prof["score"][0] / max(1, prof["score"][1])
                 gbs = table_bytes / (sc_ms / 1e3) / 1e9
+                # FP32 lane operations per (entity, dim) of the scorer's inner loop: GQE |e - q| and
+                # the sum (2 per query row), BetaE a u + b v (2 FMAs per query row); rows = B x branches
+                rows = B * (2 if s == "2u" else 1)
+                ops = 2 * rows * N * d
+                alu_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+                alu = ops / (sc_ms / 1e3)
                 res[f"{model}_{s}_B{B}"] = {
                     "ms_per_batch": tot / steps, "queries_per_s": B * steps / (tot / 1e3),
                     "scorer_ms": sc_ms, "scorer_table_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
+                    "alu_tops": alu / 1e12, "alu_frac": alu / alu_peak,
+                    # the binding roof: the one the kernel would hit first at 100%
+                    "bound": "hbm" if table_bytes / (peaks["hbm_gbs"] * 1e9) >= ops / alu_peak else "alu",
                 }
         eng.close()
     return res
@@ -617,7 +626,10 @@ def main():
                 "unit": "GB/s", "peak_source": f"{peak_src} copy bandwidth",
                 "work": "the shard's scoring table read once per batch: GQE 4 N d bytes, BetaE 8 N d (the centred "
                         "fp32 u, v planes)",
+                "alu_peak": "148 SMs x 128 FP32 lanes x max SM clock (FFMA2 / FADD counted per lane operation)",
                 "results": {k: {"gbs": round(v["scorer_table_gbs"], 1), "frac": round(v["hbm_frac"], 4),
+                                "alu_frac": round(v["alu_frac"], 4), "bound": v["bound"],
+                                "frac_of_bound": round(v["hbm_frac"] if v["bound"] == "hbm" else v["alu_frac"], 4),
                                 "queries_per_s": round(v["queries_per_s"], 1)} for k, v in c5a.items()}},
             "clocks": clk.summary(),
         }

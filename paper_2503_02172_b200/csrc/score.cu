@@ -161,11 +161,14 @@ __global__ void __launch_bounds__(256, 2)
 // dim and plane) while the <= 16 query rows sit in shared memory and are read as broadcasts.
 // Per (q, e, d) it evaluates exactly the expression of k_score, in the same order, so both
 // variants return bit-identical distances.
+// Tuned on the C5a sweep (2M entities, d 400; r02_stream_ab): GQE 1p B = 8 0.48 -> 0.79 of the
+// measured HBM bandwidth with 16-byte query loads, a register cap of two CTAs per SM for the
+// <= 8-row GQE variants and 8 dims of loads in flight (unroll 8); B = 1 stays at ~1.0.
 #ifndef KGQ_STREAM_MINB  // min resident CTAs of the GQE <= 8-row variants (register cap)
-#define KGQ_STREAM_MINB 3
+#define KGQ_STREAM_MINB 2
 #endif
 #ifndef KGQ_STREAM_UNROLL
-#define KGQ_STREAM_UNROLL 4
+#define KGQ_STREAM_UNROLL 8
 #endif
 #ifndef KGQ_STREAM_QVEC
 #define KGQ_STREAM_QVEC 1
@@ -267,13 +270,21 @@ __device__ __forceinline__ void ffma2(float2& c, const float2 a, const float2 b)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
 }
 
+#ifndef KGQ_UV_UNROLL  // dims of (u, v) loads in flight per thread (r02_stream_ab2: 2 / 4 / 8 ->
+#define KGQ_UV_UNROLL 8   // 2u B = 8 at 0.49 / 0.63 / 0.68 of the measured HBM bandwidth)
+#endif
+constexpr int kUvUnroll = KGQ_UV_UNROLL;
+// Thread = 4 consecutive entities x RS query rows.  With 16 rows (2u at B = 8) the two half-warps
+// take rows 0-7 and 8-15 of the same 16 entity groups (their u, v loads hit the same 256 bytes:
+// one request), so a thread keeps 32 accumulators instead of 64.
 template <int NB, int QB>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     k_score_uv_stream(Split A, const float2* __restrict__ P, const float* __restrict__ uvT, const float2* __restrict__ E,
                       int64_t np, int d, float* __restrict__ dist, int64_t ldd, int B) {
   constexpr int R = QB * NB;
-  constexpr int EP = R >= 16 ? 2 : 4;  // entities per thread (two with 16 rows: 64 accumulators otherwise)
-  constexpr int NP2 = EP / 2;          // entity pairs (FFMA2 lanes)
+  constexpr int HALVES = R >= 16 ? 2 : 1;
+  constexpr int RS = R / HALVES;      // rows per thread
+  constexpr int GPW = 32 / HALVES;    // entity groups per warp
   extern __shared__ __align__(16) float4 qab[];  // [d][R] = (a, a, b, b)
   pdl_grid_sync();
   const int rows = B * NB;
@@ -287,62 +298,54 @@ __global__ void __launch_bounds__(256)
     qab[i] = make_float4(a, a, b, b);
   }
   __syncthreads();
-  const int64_t ngroups = np / EP;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = g * EP;
-    float2 acc[R][NP2];
+  const int lane = threadIdx.x & 31, half = HALVES == 2 ? lane >> 4 : 0;
+  const int r0 = half * RS;
+  const int64_t ngroups = np / 4;
+  const int64_t gpb = (int64_t)(blockDim.x >> 5) * GPW;  // entity groups per CTA pass
+  for (int64_t gb = (int64_t)blockIdx.x * gpb; gb < ngroups; gb += (int64_t)gridDim.x * gpb) {
+    const int64_t g = gb + (threadIdx.x >> 5) * GPW + (lane % GPW);
+    if (g >= ngroups) continue;
+    const int64_t e0 = g * 4;
+    float2 acc[RS][2];
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int p = 0; p < NP2; ++p) acc[r][p] = make_float2(0.0f, 0.0f);
+    for (int r = 0; r < RS; ++r) acc[r][0] = acc[r][1] = make_float2(0.0f, 0.0f);
     const float* up = uvT + e0;
-#pragma unroll 4
+#pragma unroll kUvUnroll
     for (int j = 0; j < d; ++j) {
-      float2 u[NP2], v[NP2];
-      if constexpr (EP == 4) {
-        const float4 u4 = __ldg(reinterpret_cast<const float4*>(up + (int64_t)(2 * j) * np));
-        const float4 v4 = __ldg(reinterpret_cast<const float4*>(up + (int64_t)(2 * j + 1) * np));
-        u[0] = make_float2(u4.x, u4.y);
-        u[NP2 - 1] = make_float2(u4.z, u4.w);
-        v[0] = make_float2(v4.x, v4.y);
-        v[NP2 - 1] = make_float2(v4.z, v4.w);
-      } else {
-        u[0] = __ldg(reinterpret_cast<const float2*>(up + (int64_t)(2 * j) * np));
-        v[0] = __ldg(reinterpret_cast<const float2*>(up + (int64_t)(2 * j + 1) * np));
-      }
-      const float4* qj = qab + j * R;
+      const float4 u4 = __ldg(reinterpret_cast<const float4*>(up + (int64_t)(2 * j) * np));
+      const float4 v4 = __ldg(reinterpret_cast<const float4*>(up + (int64_t)(2 * j + 1) * np));
+      const float2 u[2] = {make_float2(u4.x, u4.y), make_float2(u4.z, u4.w)};
+      const float2 v[2] = {make_float2(v4.x, v4.y), make_float2(v4.z, v4.w)};
+      const float4* qj = qab + j * R + r0;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
+      for (int r = 0; r < RS; ++r) {
         const float4 q = qj[r];
 #pragma unroll
-        for (int p = 0; p < NP2; ++p) {
+        for (int p = 0; p < 2; ++p) {
           ffma2(acc[r][p], u[p], make_float2(q.x, q.y));
           ffma2(acc[r][p], v[p], make_float2(q.z, q.w));
         }
       }
     }
-    float2 ee[EP];
+    float2 ee[4];
 #pragma unroll
-    for (int i = 0; i < EP; ++i) ee[i] = __ldg(E + e0 + i);
+    for (int i = 0; i < 4; ++i) ee[i] = __ldg(E + e0 + i);
 #pragma unroll
-    for (int b = 0; b < QB; ++b) {
+    for (int bl = 0; bl < RS / NB; ++bl) {
+      const int b = r0 / NB + bl;
       if (b >= B) break;
-      float o[EP];
+      float o[4];
 #pragma unroll
       for (int br = 0; br < NB; ++br) {
         const float2 p = __ldg(P + b * NB + br);
 #pragma unroll
-        for (int i = 0; i < EP; ++i) {
-          const float s = (i & 1) ? acc[b * NB + br][i >> 1].y : acc[b * NB + br][i >> 1].x;
+        for (int i = 0; i < 4; ++i) {
+          const float s = (i & 1) ? acc[bl * NB + br][i >> 1].y : acc[bl * NB + br][i >> 1].x;
           const float v = (p.x + ee[i].x) + ((p.y + ee[i].y) + s);
           o[i] = br == 0 ? v : fminf(o[i], v);
         }
       }
-      if constexpr (EP == 4)
-        *reinterpret_cast<float4*>(dist + (int64_t)b * ldd + e0) = make_float4(o[0], o[1], o[2], o[3]);
-      else
-        *reinterpret_cast<float2*>(dist + (int64_t)b * ldd + e0) = make_float2(o[0], o[1]);
+      *reinterpret_cast<float4*>(dist + (int64_t)b * ldd + e0) = make_float4(o[0], o[1], o[2], o[3]);
     }
   }
 }
@@ -350,12 +353,12 @@ __global__ void __launch_bounds__(256)
 template <int NB, int QB>
 void launch_uv_stream_t(const Split& A, const float2* P, const float* uvT, const float2* E, int64_t np, int d,
                         float* dist, int64_t ldd, int B, cudaStream_t st) {
-  constexpr int EP = QB * NB >= 16 ? 2 : 4;
+  constexpr int HALVES = QB * NB >= 16 ? 2 : 1;
   const size_t smem = (size_t)d * QB * NB * sizeof(float4);
   static unsigned long long attr = 0;
   smem_attr_once(k_score_uv_stream<NB, QB>, (int)smem, attr);
-  const int64_t groups = np / EP;
-  const int64_t want = (groups + 255) / 256;
+  const int64_t gpb = 8 * 32 / HALVES;
+  const int64_t want = (np / 4 + gpb - 1) / gpb;
   const int grid = (int)(want < 148 * 8 ? want : 148 * 8);
   launch_pdl(k_score_uv_stream<NB, QB>, dim3(grid), dim3(256), smem, st, A, P, uvT, E, np, d, dist, ldd, B);
 }
