@@ -560,8 +560,10 @@ def main():
     # FLOPs (2MNK, the library's counters); time = the union of the GEMM launches' in-kernel spans
     # (%globaltimer, first CTA start after the PDL wait -> last CTA end) over the timed steps of
     # THIS pass, merged over the concurrent streams; peak = measured bf16 / 6 (six bf16 MMAs per
-    # useful fp32 multiply-add: x0w0, x0w1, x1w0, x0w2, x1w1, x2w0), the sustained figure (the
-    # GEMMs run inside a long step), the burst one quoted beside it.
+    # useful fp32 multiply-add: x0w0, x0w1, x1w0, x0w2, x1w1, x2w0), the BURST figure: the
+    # scorer GEMM alone measures above the driver's sustained (4-s cuBLAS loop under the power
+    # cap) figure in this duty cycle, so only the burst one is a ceiling; the sustained fraction
+    # is quoted beside it.
     peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 6.0
     peak_burst = peaks["bf16_tflops"] / 6.0
     rate = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms > 0 else 0.0
@@ -597,10 +599,10 @@ def main():
                      "how": "in-kernel %globaltimer spans of every k_gemm launch of the timed steps (kgq_ktime_log), "
                             "union over the concurrent streams"},
             "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",
-                         "bound": "tensor", "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
-                         "frac": achieved / peak_sus, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16 sustained {peak_sus * 6:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
-                         "frac_vs_burst": achieved / peak_burst,
+                         "bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
+                         "frac": achieved / peak_burst, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16 burst {peak_burst * 6:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
+                         "frac_vs_sustained": achieved / peak_sus,
                          "work": f"useful fp32 FLOPs 2MNK per GEMM launch: {(d_fl + s_fl) / 1e9:.1f} GFLOP per step "
                                  f"per rank (dense {d_fl / 1e9:.1f}, score {s_fl / 1e9:.1f})",
                          "whole_step_rate": rate(d_fl + s_fl, ms_step),
@@ -608,11 +610,9 @@ def main():
                              "how": "each part's GEMMs alone on the GPU: the sequential (one-stream) pass's in-kernel "
                                     "spans; under the concurrent streams the parts overlap each other",
                              "dense": {"ms_per_step": seq_dense_ms, "tflops": rate(d_fl, seq_dense_ms),
-                                       "frac": rate(d_fl, seq_dense_ms) / peak_sus,
-                                       "frac_vs_burst": rate(d_fl, seq_dense_ms) / peak_burst},
+                                       "frac": rate(d_fl, seq_dense_ms) / peak_burst},
                              "score": {"ms_per_step": seq_score_ms, "tflops": rate(s_fl, seq_score_ms),
-                                       "frac": rate(s_fl, seq_score_ms) / peak_sus,
-                                       "frac_vs_burst": rate(s_fl, seq_score_ms) / peak_burst}}},
+                                       "frac": rate(s_fl, seq_score_ms) / peak_burst}}},
             "gpu_launches": n_launch,
             "mixed_submit": mixed,
             "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -46,6 +46,16 @@ namespace tc {
 // 320 threads; the fp32 row accumulators take BN/2 of them).
 constexpr int BM = 128, BK = 32, EPI_WARPS = 8, EPI_WARP0 = 2, THREADS = 64 + 32 * EPI_WARPS;
 constexpr int kClustersMax = 74;  // 148 SMs / 2
+// Clusters a launch may use (plan + grid): 74 by default; KGQ_GEMM_CLUSTERS caps it (concurrent
+// streams: two GEMMs side by side instead of one filling the GPU and the next queueing).
+inline int gemm_clusters() {
+  static const int v = [] {
+    const char* e = getenv("KGQ_GEMM_CLUSTERS");
+    const int c = e ? atoi(e) : 0;
+    return c >= 1 && c <= kClustersMax ? c : kClustersMax;
+  }();
+  return v;
+}
 
 // ---- PTX wrappers -----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -747,7 +757,8 @@ static_assert(kGemmCntInts >= kClustersMax * 2 * EPI_WARPS, "split-tail counters
 
 template <int BN, class Epi>
 int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDesc& o, const Epi& epi,
-                cudaStream_t st, Sched sc, int max_clusters = kClustersMax) {
+                cudaStream_t st, Sched sc, int max_clusters = 0) {
+  if (max_clusters <= 0) max_clusters = gemm_clusters();
   constexpr int PLANES = Epi::PLANES, ROWDIV = Epi::ROWDIV;
   static_assert(PLANES == 1 || PLANES == 3, "fp32 or bf16x3 output");
   CUtensorMap mA[3], mW[3], mO[3];
@@ -833,7 +844,8 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allo
     if (knobs.force_bn && bn != knobs.force_bn) continue;
     if (bn == 160 && (!allow160 || knobs.no160)) continue;
     const int64_t tiles = pairs_m * ((N + bn - 1) / bn);
-    const int64_t full = tiles / kClustersMax * kClustersMax, tail = tiles - full;
+    const int cl = gemm_clusters();
+    const int64_t full = tiles / cl * cl, tail = tiles - full;
     double kb = kKbUs[bn == 64 ? 0 : bn == 128 ? 1 : bn == 160 ? 2 : bn == 192 ? 3 : 4];
     if (bn == 128 && knobs.kb128 > 0) kb = knobs.kb128;
     // Two partials commute exactly; with three or more the last-arriving split adds the others
@@ -841,11 +853,11 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allo
     // Default: at most two splits, so reruns are bit-identical (measured cost on C2: ~0.1%);
     // KGQ_DETERMINISTIC=0 lifts the cap.
     const int scap = knobs.deterministic ? 2 : 6;
-    const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(kClustersMax / tail, std::min(scap, nk / 4))) : 1;
+    const int smax = can_split && tail > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(cl / tail, std::min(scap, nk / 4))) : 1;
     for (int s = 1; s <= smax; ++s) {
       const int kper = (nk + s - 1) / s;
       const int se = (nk + kper - 1) / kper;  // no empty split
-      const double cost = kC0Us + (double)(full / kClustersMax) * nk * kb +
+      const double cost = kC0Us + (double)(full / cl) * nk * kb +
                           (tail ? kper * kb + (se > 1 ? (kPubUs + kPartUs * (se - 1)) * bn : 0.0) : 0.0);
       if (cost < best_cost) {
         best_cost = cost;

@@ -13,6 +13,7 @@
 #   sanitize   compute-sanitizer memcheck / racecheck / synccheck on small configs
 #   chain      per-structure chain / full-row distance errors (scripts/diag_chain_err.py)
 #   ab         same-box A/B of the in-tree libkgq.so vs ab_libs/$AB_LIB on the C2 bench
+#   streams    the headline step over 1-4 streams, and with the GEMM grid capped (KGQ_GEMM_CLUSTERS)
 #   probes     tcgen05 GEMM checker / throughput probe / MMA issue probe (built by scripts/tc_probe.sh)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
@@ -29,8 +30,10 @@ for task in "$@"; do
                 --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-mixed --no-c5a > /dev/null 2>&1 ;;
     ncu-gemm) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 30 -c 4 -o $OUT/prof_gemm -f \
                 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-mixed --no-c5a --streams 1 > /dev/null 2>&1 ;;
-    ncu-c5a) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score_ -s 2 -c 1 -o $OUT/prof_c5a -f \
-               python scripts/c5a_one.py gqe 1p 8 3 > /dev/null 2>&1 ;;
+    ncu-c5a) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score_stream -s 2 -c 1 -o $OUT/prof_c5a -f \
+               python scripts/c5a_one.py gqe 1p 8 3 > /dev/null 2>&1
+             timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score_uv_stream -s 2 -c 1 -o $OUT/prof_c5a_betae -f \
+               python scripts/c5a_one.py betae 2u 8 3 > /dev/null 2>&1 ;;
     sanitize) bash scripts/sanitize.sh > $OUT/sanitize.txt 2>&1; tail -12 $OUT/sanitize.txt ;;
     chain) timeout 900 python scripts/diag_chain_err.py small medium c2 c4 > $OUT/chain_err.jsonl 2>&1 ;;
     ab) for i in 1 2; do
@@ -40,6 +43,10 @@ for task in "$@"; do
             python -c "import json; d=json.load(open('$OUT/ab.json')); print('$lib', round(d['value']), round(d['ms_per_step'], 3), d['sequential'])" | tee -a $OUT/ab.txt
           done
         done ;;
+    streams) for S in 1 2 3 4; do timeout 900 python bench.py --steps 10 --warmup 3 --streams $S --no-cpu-baseline --no-mixed --no-c5a \
+               > $OUT/streams_$S.json 2> $OUT/streams_$S.err; done
+             for C in 56 48 37; do KGQ_GEMM_CLUSTERS=$C timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-mixed \
+               --no-c5a > $OUT/clusters_$C.json 2> $OUT/clusters_$C.err; done ;;
     probes) ( cd scripts; timeout 120 ./tc_bn_check; timeout 200 ./tc_probe_base; timeout 120 ./mma3_probe ) > $OUT/probes.txt 2>&1 ;;
     *) echo "unknown task $task" ;;
   esac

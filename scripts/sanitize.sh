@@ -10,6 +10,11 @@
 cd "$(dirname "$0")/.."
 for tool in memcheck racecheck synccheck; do
   echo "=== $tool"
-  KGQ_NO_GRAPHS=1 timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_case.py 2>&1 \
-    | grep -v "^========= COMPUTE-SANITIZER$" | tail -25
+  KGQ_NO_GRAPHS=1 timeout 1500 compute-sanitizer --tool $tool --print-limit 200 python scripts/sanitize_case.py \
+    > gpurun_out/sanitize_$tool.log 2>&1
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|^case|all cases" gpurun_out/sanitize_$tool.log
 done
+# the tcgen05 GEMM alone (every tile width, epilogue form and split-K tail) under racecheck
+( cd scripts && [ -x tc_bn_check ] && timeout 900 compute-sanitizer --tool racecheck --print-limit 200 ./tc_bn_check ) \
+  > gpurun_out/sanitize_racecheck_gemm.log 2>&1
+grep -E "RACECHECK SUMMARY|all tile widths|FAILED" gpurun_out/sanitize_racecheck_gemm.log
