@@ -358,7 +358,9 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     S = max(1, args.streams)
-    qsplit = world > 1 and args.split == "queries"
+    # the query split runs through the library's NCCL communicator, which needs one GPU per rank:
+    # the one-GPU path check uses the entity split with the torch.distributed merge instead
+    qsplit = world > 1 and args.split == "queries" and not one_gpu
     # per-type batch of the replicated input: W x 1024 in query split (each rank runs 1024 rows:
     # weak scaling), else 1024 (entity split: strong scaling over the entity table)
     Bg = BATCH * world if qsplit else BATCH

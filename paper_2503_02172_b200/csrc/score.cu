@@ -273,19 +273,23 @@ __device__ __forceinline__ void ffma2(float2& c, const float2 a, const float2 b)
 #ifndef KGQ_UV_UNROLL  // dims of (u, v) loads in flight per thread (r02_stream_ab2: 2 / 4 / 8 ->
 #define KGQ_UV_UNROLL 8   // 2u B = 8 at 0.49 / 0.63 / 0.68 of the measured HBM bandwidth)
 #endif
+#ifndef KGQ_UV_MINB
+#define KGQ_UV_MINB 2
+#endif
 constexpr int kUvUnroll = KGQ_UV_UNROLL;
 // Thread = 4 consecutive entities x RS query rows.  With 16 rows (2u at B = 8) the two half-warps
 // take rows 0-7 and 8-15 of the same 16 entity groups (their u, v loads hit the same 256 bytes:
 // one request), so a thread keeps 32 accumulators instead of 64.
 template <int NB, int QB>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, KGQ_UV_MINB)
     k_score_uv_stream(Split A, const float2* __restrict__ P, const float* __restrict__ uvT, const float2* __restrict__ E,
                       int64_t np, int d, float* __restrict__ dist, int64_t ldd, int B) {
   constexpr int R = QB * NB;
   constexpr int HALVES = R >= 16 ? 2 : 1;
   constexpr int RS = R / HALVES;      // rows per thread
   constexpr int GPW = 32 / HALVES;    // entity groups per warp
-  extern __shared__ __align__(16) float4 qab[];  // [d][R] = (a, a, b, b)
+  static_assert(R % 2 == 0 || R == 1, "query rows are read in pairs");
+  extern __shared__ __align__(16) float2 qab[];  // [d][R] = (a, b); ptxas broadcasts a / b into FFMA2
   pdl_grid_sync();
   const int rows = B * NB;
   for (int i = threadIdx.x; i < d * R; i += blockDim.x) {
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(256, 2)
       a = load_split(A, (int64_t)r * A.ld + j);
       b = load_split(A, (int64_t)r * A.ld + d + j);
     }
-    qab[i] = make_float4(a, a, b, b);
+    qab[i] = make_float2(a, b);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, half = HALVES == 2 ? lane >> 4 : 0;
@@ -316,14 +320,28 @@ __global__ void __launch_bounds__(256, 2)
       const float4 v4 = __ldg(reinterpret_cast<const float4*>(up + (int64_t)(2 * j + 1) * np));
       const float2 u[2] = {make_float2(u4.x, u4.y), make_float2(u4.z, u4.w)};
       const float2 v[2] = {make_float2(v4.x, v4.y), make_float2(v4.z, v4.w)};
-      const float4* qj = qab + j * R + r0;
+      const float2* qj = qab + j * R + r0;
+      if constexpr (RS % 2 == 0) {
 #pragma unroll
-      for (int r = 0; r < RS; ++r) {
-        const float4 q = qj[r];
+        for (int r = 0; r < RS; r += 2) {  // two rows' (a, b) per 16-byte broadcast
+          const float4 q = *reinterpret_cast<const float4*>(qj + r);
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-          ffma2(acc[r][p], u[p], make_float2(q.x, q.y));
-          ffma2(acc[r][p], v[p], make_float2(q.z, q.w));
+          for (int p = 0; p < 2; ++p) {
+            ffma2(acc[r][p], u[p], make_float2(q.x, q.x));
+            ffma2(acc[r][p], v[p], make_float2(q.y, q.y));
+            ffma2(acc[r + 1][p], u[p], make_float2(q.z, q.z));
+            ffma2(acc[r + 1][p], v[p], make_float2(q.w, q.w));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+          const float2 q = qj[r];
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            ffma2(acc[r][p], u[p], make_float2(q.x, q.x));
+            ffma2(acc[r][p], v[p], make_float2(q.y, q.y));
+          }
         }
       }
     }
@@ -354,7 +372,7 @@ template <int NB, int QB>
 void launch_uv_stream_t(const Split& A, const float2* P, const float* uvT, const float2* E, int64_t np, int d,
                         float* dist, int64_t ldd, int B, cudaStream_t st) {
   constexpr int HALVES = QB * NB >= 16 ? 2 : 1;
-  const size_t smem = (size_t)d * QB * NB * sizeof(float4);
+  const size_t smem = (size_t)d * QB * NB * sizeof(float2);
   static unsigned long long attr = 0;
   smem_attr_once(k_score_uv_stream<NB, QB>, (int)smem, attr);
   const int64_t gpb = 8 * 32 / HALVES;

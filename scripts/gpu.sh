@@ -14,6 +14,7 @@
 #   chain      per-structure chain / full-row distance errors (scripts/diag_chain_err.py)
 #   ab         same-box A/B of the in-tree libkgq.so vs ab_libs/$AB_LIB on the C2 bench
 #   streams    the headline step over 1-4 streams, and with the GEMM grid capped (KGQ_GEMM_CLUSTERS)
+#   multirank  the N > 1 bench path with both ranks on the one GPU (gloo; a path check, numbers meaningless)
 #   probes     tcgen05 GEMM checker / throughput probe / MMA issue probe (built by scripts/tc_probe.sh)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
@@ -47,6 +48,9 @@ for task in "$@"; do
                > $OUT/streams_$S.json 2> $OUT/streams_$S.err; done
              for C in 56 48 37; do KGQ_GEMM_CLUSTERS=$C timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-mixed \
                --no-c5a > $OUT/clusters_$C.json 2> $OUT/clusters_$C.err; done ;;
+    multirank) KGQ_BENCH_ONE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+                 --master-port 29517 bench.py --gpus 2 --steps 3 --warmup 3 --no-c5a --no-mixed > $OUT/multirank.json 2> $OUT/multirank.err
+               tail -3 $OUT/multirank.err ;;
     probes) ( cd scripts; timeout 120 ./tc_bn_check; timeout 200 ./tc_probe_base; timeout 120 ./mma3_probe ) > $OUT/probes.txt 2>&1 ;;
     *) echo "unknown task $task" ;;
   esac
