@@ -4,11 +4,14 @@
 Workload (N=1): BASELINE.json configs[1] -- BetaE on the synthetic FB15k-237 shape
 (14,505 entities, 237 relations, d 400, MLP 1600x2), batch 1024, all 14 query types.
 One step = one batch of every query type through the whole path (operator chain ->
-entity scoring -> top-k 10), i.e. 14 x 1024 queries.  value = queries/s over all ranks.
+entity scoring -> top-k 10), i.e. 14 x 1024 queries, submitted as ONE kgq_submit_mixed
+(default; --mode per-type: 14 kgq_submit calls over --streams streams).  value = queries/s
+over all ranks; "per_type" gives each type's own queries/s (the metric's per-type view).
 
-N > 1 (torchrun): the entity table is sharded over the ranks; queries are
-replicated; each rank returns its local top-k, an NCCL all-gather exchanges them and
-kgq_merge_topk merges -> strong scaling of the same workload.
+N > 1 (torchrun): --split queries (default): a W x 14 x 1024 replicated batch, each rank runs its
+own 14 x 1024 queries and the library's NCCL all-gather returns the whole batch's top-k (weak
+scaling); --split entities: the entity table is sharded, every rank scores the replicated batch
+on its shard, local top-k + all-gather + merge inside the library (strong scaling).
 
 --impl reference: the float64 CPU oracle (the reference arm of this tier), on rank 0 only.
 """
@@ -306,25 +309,42 @@ def span_union_ms(spans):
     return (tot + ce - cs) * 1e-6
 
 
+def replicated_groups(world, qsplit):
+    """The step's query groups: (structure, rows, anchors, rels) in submit order.  N = 1 or the
+    entity split: one group of BATCH queries per structure.  Query split: W x 14 groups, rank w's
+    14 groups (its own seeds) contiguous, so the library's row range [w Q, (w+1) Q) of the
+    replicated batch is exactly rank w's 14 x 1024 queries (the same mix of types on every rank)."""
+    out = []
+    for w in range(world if qsplit else 1):
+        for s in STRUCTS:
+            a, r = synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s) + 7919 * w)
+            out.append((s, BATCH, a.astype(np.int32), r.astype(np.int32)))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kgq", choices=["kgq", "reference"])
+    ap.add_argument("--mode", default="mixed", choices=["mixed", "per-type"],
+                    help="headline step: ONE kgq_submit_mixed of the 14 x 1024 queries (each projection hop of "
+                         "every type is one MLP), or the 14 per-type kgq_submit calls dealt over --streams streams")
     ap.add_argument("--streams", type=int, default=3,
-                    help="concurrent streams per GPU (one library context each); the 14 per-type submits of a "
-                         "step are dealt round-robin over them")
+                    help="per-type mode: concurrent streams per GPU (one library context each)")
     ap.add_argument("--split", default="queries", choices=["queries", "entities"],
-                    help="N>1: rank r runs rows [r B, (r+1) B) of a W x B replicated batch (weak scaling, the "
-                         "library's query-split communicator), or the entity table is sharded over the ranks "
-                         "with a replicated B-query batch (strong scaling, local top-k + all-gather + merge)")
+                    help="N>1: rank r runs its 14 x 1024 queries of a W x 14 x 1024 replicated batch (weak scaling, "
+                         "the library's query-split communicator), or the entity table is sharded over the ranks "
+                         "with a replicated 14 x 1024-query batch (strong scaling, local top-k + all-gather + merge)")
     ap.add_argument("--merge", default="nccl", choices=["nccl", "p2p", "torch"],
                     help="entity split: the library's NCCL all-gather + merge kernel (default), the all-gather "
                          "fused into the top-k over symmetric peer memory (N2), or torch.distributed + merge")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=14)
-    ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-structure submit measurement")
+    ap.add_argument("--no-per-type", action="store_true",
+                    help="skip the secondary per-type measurements (14 submits over streams; each type alone)")
+    ap.add_argument("--no-mixed", action="store_true", help=argparse.SUPPRESS)  # round-1 flag, = --no-per-type
     ap.add_argument("--no-c5a", action="store_true", help="skip the 2M-entity HBM (C5a) measurement")
     ap.add_argument("--workload", default="fb15k237", choices=["fb15k237", "c5a", "suite"])
     ap.add_argument("--suite", default="", help="comma list of SUITE configs (default: all)")
@@ -357,68 +377,99 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    S = max(1, args.streams)
+    mixed_mode = args.mode == "mixed"
+    S = 1 if mixed_mode else max(1, args.streams)
     # the query split runs through the library's NCCL communicator, which needs one GPU per rank:
     # the one-GPU path check uses the entity split with the torch.distributed merge instead
     qsplit = world > 1 and args.split == "queries" and not one_gpu
-    # per-type batch of the replicated input: W x 1024 in query split (each rank runs 1024 rows:
-    # weak scaling), else 1024 (entity split: strong scaling over the entity table)
-    Bg = BATCH * world if qsplit else BATCH
     merge = "nccl" if qsplit else (args.merge if not one_gpu else "torch")
     t = synth.make_tables("betae", N_ENT, N_REL, DIM, hidden=HID, seed=SEED)
-    engines = []
-    for _ in range(S):
-        se = ShardedEngine("betae", N_ENT, N_REL, DIM, split="queries" if qsplit else "entities", hidden=HID,
-                           max_batch=Bg, max_k=K, device=local, merge=merge)
-        se.load_tables(t)
-        se.p2p_check = False  # N2 errors are checked once after the timed steps
-        se.engine.ktime(True)  # in-kernel GEMM launch spans (roofline from this very pass)
-        engines.append(se)
-    streams = [torch.cuda.Stream() for _ in range(S)]
-    main_stream = torch.cuda.current_stream()
-    qs = {}
-    for s in STRUCTS:
-        if qsplit:  # the same per-rank 1024-query batches as N = 1, replicated over all ranks
-            parts = [synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s) + 7919 * w)
-                     for w in range(world)]
-            a, r = np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
-        else:
-            a, r = synth.make_queries(s, BATCH, N_ENT, N_REL, seed=synth.query_seed(SEED, s))
-        qs[s] = (a, r, torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda())
-    outs = {s: (torch.empty((Bg, K), device="cuda"), torch.empty((Bg, K), dtype=torch.int32, device="cuda"))
-            for s in STRUCTS}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
-    launches = [0]
-    lane = {s: i % S for i, s in enumerate(STRUCTS)}
-
-    def step(nlanes=S, count=True):
-        """One step: the 14 per-type submits dealt over `nlanes` streams, joined on the main
-        stream; returns the (start, end) events of the main stream."""
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(main_stream)
-        for st in streams[:nlanes]:
-            st.wait_event(e0)
-        for s in STRUCTS:
-            j = lane[s] % nlanes
-            engines[j].submit(s, qs[s][2], qs[s][3], K, stream=streams[j])
-            if count:
-                launches[0] += engines[j].last_launch_count()
-        for st in streams[:nlanes]:
-            ev = torch.cuda.Event()
-            ev.record(st)
-            main_stream.wait_event(ev)
-        e1.record(main_stream)
-        return e0, e1
+    main_stream = torch.cuda.current_stream()
+    per_rank_queries = len(STRUCTS) * BATCH  # per step (query split: each rank's own rows)
+    job_queries = per_rank_queries * (world if qsplit else 1)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(vals):
+        if world == 1:
+            return vals
+        tt = torch.tensor(vals, dtype=torch.float64, device="cuda" if not one_gpu else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return [float(x) for x in tt.tolist()]
+
+    # ---------------- the step's queries ----------------
+    groups = replicated_groups(world, qsplit)
+    Qg = sum(g[1] for g in groups)                      # replicated batch per step
+    g_structs, g_batches = [g[0] for g in groups], [g[1] for g in groups]
+    a_host = np.concatenate([g[2].reshape(-1) for g in groups])
+    r_host = np.concatenate([g[3].reshape(-1) for g in groups])
+    a_dev, r_dev = torch.from_numpy(a_host).cuda(), torch.from_numpy(r_host).cuda()
+
+    # ---------------- headline engines ----------------
+    launches = [0]
+    if mixed_mode:
+        se = ShardedEngine("betae", N_ENT, N_REL, DIM, split="queries" if qsplit else "entities", hidden=HID,
+                           max_batch=Qg, max_k=K, device=local, merge=merge)
+        se.load_tables(t)
+        se.p2p_check = False  # N2 errors are checked once after the timed steps
+        engines = [se]
+        mout = (torch.empty((Qg, K), device="cuda"), torch.empty((Qg, K), dtype=torch.int32, device="cuda"))
+        streams = [main_stream]
+
+        def submit_all(nlanes=1, count=True):
+            se.submit_mixed_packed(g_structs, g_batches, a_dev, r_dev, K, mout, stream=main_stream)
+            if count:
+                launches[0] += se.last_launch_count()
+    else:
+        engines = []
+        for _ in range(S):
+            e = ShardedEngine("betae", N_ENT, N_REL, DIM, split="queries" if qsplit else "entities", hidden=HID,
+                              max_batch=BATCH * (world if qsplit else 1), max_k=K, device=local, merge=merge)
+            e.load_tables(t)
+            e.p2p_check = False
+            engines.append(e)
+        streams = [torch.cuda.Stream() for _ in range(S)]
+        # per type: the W x 1024 replicated rows in rank order (query split), else the 1024
+        per_type_in = {}
+        for s in STRUCTS:
+            sel = [g for g in groups if g[0] == s]
+            per_type_in[s] = (torch.from_numpy(np.concatenate([g[2] for g in sel])).cuda(),
+                              torch.from_numpy(np.concatenate([g[3] for g in sel])).cuda())
+        lane = {s: i % S for i, s in enumerate(STRUCTS)}
+
+        def submit_all(nlanes=S, count=True):
+            for s in STRUCTS:
+                j = lane[s] % nlanes
+                engines[j].submit(s, *per_type_in[s], K, stream=streams[j])
+                if count:
+                    launches[0] += engines[j].last_launch_count()
+    for se_ in engines:
+        se_.engine.ktime(True)  # in-kernel GEMM launch spans (roofline from this very pass)
+
+    def step(nlanes=S, count=True):
+        """One step (all 14 x 1024 queries of this rank) between two events on the main stream
+        (per-type mode: forked over `nlanes` streams and joined before the end event)."""
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(main_stream)
+        for st in streams[:nlanes]:
+            if st is not main_stream:
+                st.wait_event(e0)
+        submit_all(nlanes, count)
+        for st in streams[:nlanes]:
+            if st is not main_stream:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                main_stream.wait_event(ev)
+        e1.record(main_stream)
+        return e0, e1
+
     def timed(nsteps, nlanes):
-        """nsteps steps, L2 flushed (untimed) before each; per-step device ms (start event on
-        the main stream before the fork, end event after every stream joined)."""
+        """nsteps steps, L2 flushed (untimed) before each; per-step device ms."""
         ms = []
         for _ in range(nsteps):
             flush.zero_()
@@ -427,108 +478,106 @@ def main():
             ms.append(e0.elapsed_time(e1))
         return ms
 
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         step(S, False)
-        step(1, False)  # the sequential pass's graphs (lane 0) are captured here too
+        if S > 1:
+            step(1, False)  # the sequential pass's graphs (lane 0) are captured here too
     barrier()
-    for se in engines:
-        se.engine.check_errors()
-        se.engine.ktime_read()
-        se.engine.ktime_log()
+    for se_ in engines:
+        se_.engine.check_errors()
+        se_.engine.ktime_read()
+        se_.engine.ktime_log()
     launches[0] = 0
     with ClockSampler(local) as clk:
         barrier()
         step_ms = timed(args.steps, S)
         barrier()
     n_launch = launches[0]
-    # GEMM launch spans of exactly these steps (every context's log, one clock per device)
-    logs = [se.engine.ktime_log() for se in engines]
-    kt = [se.engine.ktime_read() for se in engines]
+    logs = [se_.engine.ktime_log() for se_ in engines]
+    for se_ in engines:
+        se_.engine.ktime_read()
     spans = np.concatenate([lg for lg in logs if len(lg)]) if any(len(lg) for lg in logs) else np.zeros((0, 3), np.uint64)
     gemm_busy_ms = span_union_ms(spans[:, :2]) / args.steps
     dense_busy_ms = span_union_ms(spans[spans[:, 2] == 0][:, :2]) / args.steps
     score_busy_ms = span_union_ms(spans[spans[:, 2] == 1][:, :2]) / args.steps
-    dense_span_sum = sum(k["dense"][0] for k in kt) / args.steps
-    score_span_sum = sum(k["score"][0] for k in kt) / args.steps
-    gemm_launches = sum(k["dense"][1] + k["score"][1] for k in kt) / args.steps
+    gemm_launches = len(spans) / args.steps
     total_ms = sum(step_ms)
-    # sequential reference pass: the same steps on ONE stream (round-1's headline form)
-    seq_ms = None
-    seq_dense_ms = seq_score_ms = None
-    if S > 1:
+    seq_ms = seq_dense_ms = seq_score_ms = None
+    if S > 1:  # per-type mode: the same steps on ONE stream (each GEMM alone on the GPU)
         barrier()
-        seq = timed(args.steps, 1)
-        seq_ms = sum(seq)
-        lg = engines[0].engine.ktime_log()  # one stream: every GEMM alone on the GPU
+        seq_ms = sum(timed(args.steps, 1))
+        lg = engines[0].engine.ktime_log()
         seq_dense_ms = span_union_ms(lg[lg[:, 2] == 0][:, :2]) / args.steps
         seq_score_ms = span_union_ms(lg[lg[:, 2] == 1][:, :2]) / args.steps
-        for se in engines:
-            se.engine.ktime_log()
-            se.engine.ktime_read()
-    if world > 1:
-        tt = torch.tensor([total_ms, seq_ms or 0.0], dtype=torch.float64, device="cuda" if not one_gpu else "cpu")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, seq_ms = float(tt[0].item()), (float(tt[1].item()) or None)
-    per_rank_queries = len(STRUCTS) * BATCH  # per step (query split: each rank's own rows)
-    job_queries = per_rank_queries * (world if qsplit else 1)
+        for se_ in engines:
+            se_.engine.ktime_log()
+            se_.engine.ktime_read()
+    total_ms, seq_ms = max_over_ranks([total_ms, seq_ms or 0.0])
+    seq_ms = seq_ms or None
     value = job_queries * args.steps / (total_ms / 1e3)
+    for se_ in engines:
+        se_.engine.check_errors()
 
     # ---- algorithmic GEMM FLOPs per step (the library's own work counters, one profiled
-    # submit per type outside the timed region) ----
-    eng0 = engines[0].engine
-    eng0.ktime(False)
-    eng0.profile(True)
-    eng0.profile_read()
-    for s in STRUCTS:
-        engines[0].submit(s, qs[s][2], qs[s][3], K)
+    # step outside the timed region; this rank's rows) ----
+    for se_ in engines:
+        se_.engine.ktime(False)
+        se_.engine.profile(True)
+        se_.engine.profile_read()
+    step(1, False)
     torch.cuda.synchronize()
-    prof = eng0.profile_read()
-    eng0.profile(False)
-    d_fl, s_fl = prof["dense"][2], prof["score"][2]  # query split: this rank's rows (per-GPU FLOPs)
+    d_fl = s_fl = 0.0
+    for se_ in engines:
+        prof = se_.engine.profile_read()
+        se_.engine.profile(False)
+        d_fl += prof["dense"][2]
+        s_fl += prof["score"][2]
 
-    # ---- the same step as ONE mixed-structure submit (kgq_submit_mixed) ----
-    mixed = None
-    if world == 1 and not args.no_mixed:
-        meng = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH * len(STRUCTS), max_k=K, device=local)
-        meng.load_tables(t)
-        groups = [(s, qs[s][2].int(), qs[s][3].int()) for s in STRUCTS]
-        mout = (torch.empty((BATCH * len(STRUCTS), K), device="cuda"),
-                torch.empty((BATCH * len(STRUCTS), K), dtype=torch.int32, device="cuda"))
-        for _ in range(args.warmup):
-            meng.submit_mixed(groups, K, out=mout)
-        torch.cuda.synchronize()
-        meng.check_errors()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        mt = 0.0
-        for _ in range(args.steps):
-            flush.zero_()
-            e0.record()
-            meng.submit_mixed(groups, K, out=mout)
-            e1.record()
-            torch.cuda.synchronize()
-            mt += e0.elapsed_time(e1)
-        mixed = {"value": per_rank_queries * args.steps / (mt / 1e3), "unit": "queries/s",
-                 "ms_per_step": mt / args.steps,
-                 "how": "one kgq_submit_mixed per step with the same 14 x 1024 queries on one stream (L2 flushed "
-                        "between steps): each projection hop of all 14 types' branches is one MLP"}
-        meng.close()
+    # ---- secondary (1 GPU): the other step form, and every type alone ----
+    other = per_type = None
+    if world == 1 and not (args.no_per_type or args.no_mixed):
+        try:
+            other, per_type = secondary_passes(args, t, groups, mixed_mode, flush)
+        except Exception as ex:
+            print(f"bench: secondary passes failed: {type(ex).__name__}: {ex}", file=sys.stderr, flush=True)
 
-    # ---- end to end through the public API with host buffers (pinned), same streams ----
-    pin = {s: (torch.from_numpy(qs[s][0]).pin_memory(), torch.from_numpy(qs[s][1]).pin_memory()) for s in STRUCTS}
-    hout = {s: (torch.empty((Bg, K)).pin_memory(), torch.empty((Bg, K), dtype=torch.int32).pin_memory())
-            for s in STRUCTS}
-    h2d = sum(Bg * (qs[s][0].shape[1] + qs[s][1].shape[1]) * 4 for s in STRUCTS)
-    d2h = len(STRUCTS) * Bg * K * 8
+    # ---- end to end through the public API with host buffers (pinned) ----
     e2e_v = None
+    h2d = (a_host.size + r_host.size) * 4
+    d2h = Qg * K * 8
     try:
-        def e2e_step():
+        if mixed_mode and engines[0].merge_mode in ("local", "nccl"):
+            pa, pr = torch.from_numpy(a_host).pin_memory(), torch.from_numpy(r_host).pin_memory()
+            hd, hi = torch.empty((Qg, K)).pin_memory(), torch.empty((Qg, K), dtype=torch.int32).pin_memory()
+
+            def e2e_step():
+                engines[0].submit_mixed_host(g_structs, g_batches, pa.numpy(), pr.numpy(), K,
+                                             (hd.numpy(), hi.numpy()), stream=main_stream)
+                main_stream.synchronize()
+            e2e_how = ("per step: one kgq_submit_mixed_host_async (pinned H2D of the packed anchors / relations, "
+                       "the whole path, D2H of the top-k into pinned host outputs), stream synchronised")
+        else:
+            pin = {}
             for s in STRUCTS:
-                j = lane[s]
-                engines[j].engine.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K,
-                                              out=(hout[s][0].numpy(), hout[s][1].numpy()), stream=streams[j],
-                                              sync=False)
-            for st in streams:
-                st.synchronize()
+                sel = [g for g in groups if g[0] == s]
+                pin[s] = (torch.from_numpy(np.concatenate([g[2] for g in sel])).pin_memory(),
+                          torch.from_numpy(np.concatenate([g[3] for g in sel])).pin_memory())
+            nrow = BATCH * (world if qsplit else 1)
+            hout = {s: (torch.empty((nrow, K)).pin_memory(), torch.empty((nrow, K), dtype=torch.int32).pin_memory())
+                    for s in STRUCTS}
+            lane_e = {s: i % len(engines) for i, s in enumerate(STRUCTS)}
+            e2e_streams = streams if not mixed_mode else [main_stream]
+
+            def e2e_step():
+                for s in STRUCTS:
+                    j = lane_e[s]
+                    engines[j].engine.submit_host(s, pin[s][0].numpy(), pin[s][1].numpy(), K,
+                                                  out=(hout[s][0].numpy(), hout[s][1].numpy()),
+                                                  stream=e2e_streams[j % len(e2e_streams)], sync=False)
+                for st in e2e_streams:
+                    st.synchronize()
+            e2e_how = (f"per step: kgq_submit_host_async per type on {len(e2e_streams)} stream(s) (pinned H2D, path, "
+                       f"D2H of the top-k into pinned host outputs), every stream synchronised")
         e2e_step()
         e2e_step()
         e2e_s = 0.0
@@ -538,15 +587,13 @@ def main():
             t0 = time.perf_counter()
             e2e_step()
             e2e_s += time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda" if not one_gpu else "cpu")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        e2e_s = max_over_ranks([e2e_s])[0]
         e2e_v = job_queries * args.steps / e2e_s
     except Exception as ex:  # a failure here must not cost the headline line: e2e is then null
+        e2e_how = f"failed: {type(ex).__name__}: {ex}"
         print(f"bench: e2e failed: {type(ex).__name__}: {ex}", file=sys.stderr, flush=True)
-    for se in engines:
-        se.engine.check_errors()
+    for se_ in engines:
+        se_.engine.check_errors()
 
     # ---- C5a: the north-star HBM target (2M-entity scoring sweep, B in {1, 8}) ----
     peaks, peak_src = load_peaks()
@@ -561,89 +608,170 @@ def main():
     # dense layer of the chain and the BetaE scorer contraction.  Algorithmic work = useful fp32
     # FLOPs (2MNK, the library's counters); time = the union of the GEMM launches' in-kernel spans
     # (%globaltimer, first CTA start after the PDL wait -> last CTA end) over the timed steps of
-    # THIS pass, merged over the concurrent streams; peak = measured bf16 / 6 (six bf16 MMAs per
-    # useful fp32 multiply-add: x0w0, x0w1, x1w0, x0w2, x1w1, x2w0), the BURST figure: the
-    # scorer GEMM alone measures above the driver's sustained (4-s cuBLAS loop under the power
-    # cap) figure in this duty cycle, so only the burst one is a ceiling; the sustained fraction
-    # is quoted beside it.
+    # THIS pass; peak = measured bf16 / 6 (six bf16 MMAs per useful fp32 multiply-add: x0w0,
+    # x0w1, x1w0, x0w2, x1w1, x2w0), the BURST figure (the driver's sustained one is a 4-s cuBLAS
+    # loop under the power cap; the scorer GEMM alone measures above it), sustained quoted beside.
     peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 6.0
     peak_burst = peaks["bf16_tflops"] / 6.0
-    rate = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+    rate = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms and ms > 0 else 0.0
     achieved = rate(d_fl + s_fl, gemm_busy_ms)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "tc_gemm_traffic.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get("dram_bytes_per_launch")
-    if rank == 0:
-        ms_step = total_ms / args.steps
-        line = {
-            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak" if qsplit or world == 1 else "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(CONFIG, l2="flushed between timed steps (256 MiB write, untimed)",
-                           streams=S,
-                           parallelism=("1 GPU" if world == 1 else
-                                        f"query split x{world} (W x 1024 replicated rows per type, each rank its "
-                                        f"1024; library NCCL all-gather)" if qsplit else
-                                        f"entity shards x{world} ({engines[0].merge_mode})"),
-                           batch_per_type=Bg),
-            "how": (f"per step: the 14 per-type kgq_submit calls (1024 queries each per rank) dealt round-robin over "
-                    f"{S} CUDA streams, one library context per stream; device time from an event before the "
-                    f"fork to an event after the join, max over ranks"),
-            "sequential": None if seq_ms is None else {
-                "value": job_queries * args.steps / (seq_ms / 1e3), "ms_per_step": seq_ms / args.steps,
-                "how": "the same steps with the 14 submits on one stream (no overlap between types)"},
-            "gemm": {"busy_ms_per_step": gemm_busy_ms, "dense_busy_ms_per_step": dense_busy_ms,
-                     "score_busy_ms_per_step": score_busy_ms, "dense_span_sum_ms": dense_span_sum,
-                     "score_span_sum_ms": score_span_sum, "launches_per_step": gemm_launches,
-                     "share_of_step": gemm_busy_ms / ms_step,
-                     "how": "in-kernel %globaltimer spans of every k_gemm launch of the timed steps (kgq_ktime_log), "
-                            "union over the concurrent streams"},
-            "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",
-                         "bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
-                         "frac": achieved / peak_burst, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16 burst {peak_burst * 6:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
-                         "frac_vs_sustained": achieved / peak_sus,
-                         "work": f"useful fp32 FLOPs 2MNK per GEMM launch: {(d_fl + s_fl) / 1e9:.1f} GFLOP per step "
-                                 f"per rank (dense {d_fl / 1e9:.1f}, score {s_fl / 1e9:.1f})",
-                         "whole_step_rate": rate(d_fl + s_fl, ms_step),
-                         "parts": None if seq_dense_ms is None else {
-                             "how": "each part's GEMMs alone on the GPU: the sequential (one-stream) pass's in-kernel "
-                                    "spans; under the concurrent streams the parts overlap each other",
-                             "dense": {"ms_per_step": seq_dense_ms, "tflops": rate(d_fl, seq_dense_ms),
-                                       "frac": rate(d_fl, seq_dense_ms) / peak_burst},
-                             "score": {"ms_per_step": seq_score_ms, "tflops": rate(s_fl, seq_score_ms),
-                                       "frac": rate(s_fl, seq_score_ms) / peak_burst}}},
-            "gpu_launches": n_launch,
-            "mixed_submit": mixed,
-            "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "how": (f"per step: kgq_submit_host_async per type on the same {S} streams (pinned H2D of "
-                            f"anchors / relations, path, D2H of the top-k into pinned host outputs), every stream "
-                            f"synchronised; wall clock, L2 flushed before each step (untimed), max over ranks")},
-            "hbm": None if c5a is None else {
-                "workload": "BASELINE.json configs[4] latency regime: 2M entities, d 400, 1 GPU, GQE / BetaE, "
-                            "1p / 2u, B in {1, 8}",
-                "kernel": "k_score_stream (streaming entity scorer)", "bound": "hbm", "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "peak_source": f"{peak_src} copy bandwidth",
-                "work": "the shard's scoring table read once per batch: GQE 4 N d bytes, BetaE 8 N d (the centred "
-                        "fp32 u, v planes)",
-                "alu_peak": "148 SMs x 128 FP32 lanes x max SM clock (FFMA2 / FADD counted per lane operation)",
-                "results": {k: {"gbs": round(v["scorer_table_gbs"], 1), "frac": round(v["hbm_frac"], 4),
-                                "alu_frac": round(v["alu_frac"], 4), "bound": v["bound"],
-                                "frac_of_bound": round(v["hbm_frac"] if v["bound"] == "hbm" else v["alu_frac"], 4),
-                                "queries_per_s": round(v["queries_per_s"], 1)} for k, v in c5a.items()}},
-            "clocks": clk.summary(),
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            sec, n = timed_oracle_sample(args.cpu_queries, 0)
-            line["cpu_baseline"] = {"value": n / sec, "unit": "queries/s", "cores": blas_threads(),
-                                    "kind": "oracle",
-                                    "sample": f"{n} BetaE queries (1 per type), literal-KL scoring "
-                                              f"over all 14,505 entities + full sort, float64 numpy"}
-        print(json.dumps(line), flush=True)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    ms_step = total_ms / args.steps
+    # parts: each part's GEMMs alone on the GPU -- the headline pass itself in mixed mode (one
+    # stream: the launches run one after another), the sequential pass in per-type mode
+    p_dense, p_score = (dense_busy_ms, score_busy_ms) if S == 1 else (seq_dense_ms, seq_score_ms)
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak" if qsplit or world == 1 else "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict(CONFIG, l2="flushed between timed steps (256 MiB write, untimed)",
+                       step="mixed" if mixed_mode else f"per-type x {S} streams",
+                       parallelism=("1 GPU" if world == 1 else
+                                    f"query split x{world} (W x 14 x 1024 replicated queries, each rank its 14 x "
+                                    f"1024; library NCCL all-gather)" if qsplit else
+                                    f"entity shards x{world} ({engines[0].merge_mode})"),
+                       queries_per_step_per_rank=per_rank_queries),
+        "how": ("per step: ONE kgq_submit_mixed of the 14 x 1024 queries (BetaE level-synchronous: each projection "
+                "hop of all types' branches is one MLP, all intersections one attention GEMM pair, one scorer, one "
+                "top-k); device time between events on the launching stream, max over ranks" if mixed_mode else
+                f"per step: the 14 per-type kgq_submit calls dealt round-robin over {S} CUDA streams, one library "
+                f"context per stream; device time from an event before the fork to an event after the join, max "
+                f"over ranks"),
+        "per_type": per_type,
+        "other_step_form": other,
+        "sequential": None if seq_ms is None else {
+            "value": job_queries * args.steps / (seq_ms / 1e3), "ms_per_step": seq_ms / args.steps,
+            "how": "the same steps with the 14 submits on one stream (no overlap between types)"},
+        "gemm": {"busy_ms_per_step": gemm_busy_ms, "dense_busy_ms_per_step": dense_busy_ms,
+                 "score_busy_ms_per_step": score_busy_ms, "launches_per_step": gemm_launches,
+                 "share_of_step": gemm_busy_ms / ms_step,
+                 "how": "in-kernel %globaltimer spans of every k_gemm launch of the timed steps (kgq_ktime_log), "
+                        "union over the streams"},
+        "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",
+                     "bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
+                     "frac": achieved / peak_burst, "traffic": traffic,
+                     "peak_source": f"{peak_src} bf16 burst {peak_burst * 6:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
+                     "frac_vs_sustained": achieved / peak_sus,
+                     "work": f"useful fp32 FLOPs 2MNK per GEMM launch: {(d_fl + s_fl) / 1e9:.1f} GFLOP per step "
+                             f"per rank (dense {d_fl / 1e9:.1f}, score {s_fl / 1e9:.1f})",
+                     "whole_step_rate": rate(d_fl + s_fl, ms_step),
+                     "parts": None if not p_dense else {
+                         "how": "each part's GEMMs alone on the GPU (in-kernel spans)",
+                         "dense": {"ms_per_step": p_dense, "tflops": rate(d_fl, p_dense),
+                                   "frac": rate(d_fl, p_dense) / peak_burst},
+                         "score": {"ms_per_step": p_score, "tflops": rate(s_fl, p_score),
+                                   "frac": rate(s_fl, p_score) / peak_burst}}},
+        "gpu_launches": n_launch,
+        "e2e": {"value": e2e_v, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "how": e2e_how + "; wall clock, L2 flushed before each step (untimed), max over ranks"},
+        "hbm": None if c5a is None else {
+            "workload": "BASELINE.json configs[4] latency regime: 2M entities, d 400, 1 GPU, GQE / BetaE, "
+                        "1p / 2u, B in {1, 8}",
+            "kernel": "k_score_stream / k_score_uv_stream (streaming entity scorers)", "bound": "hbm",
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_source": f"{peak_src} copy bandwidth",
+            "work": "the shard's scoring table read once per batch: GQE 4 N d bytes, BetaE 8 N d (the centred "
+                    "fp32 u, v planes)",
+            "alu_peak": "148 SMs x 128 FP32 lanes x max SM clock (FFMA2 / FADD2 counted per lane operation)",
+            "results": {k: {"gbs": round(v["scorer_table_gbs"], 1), "frac": round(v["hbm_frac"], 4),
+                            "alu_frac": round(v["alu_frac"], 4), "bound": v["bound"],
+                            "frac_of_bound": round(v["hbm_frac"] if v["bound"] == "hbm" else v["alu_frac"], 4),
+                            "queries_per_s": round(v["queries_per_s"], 1)} for k, v in c5a.items()}},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        sec, n = timed_oracle_sample(args.cpu_queries, 0)
+        line["cpu_baseline"] = {"value": n / sec, "unit": "queries/s", "cores": blas_threads(),
+                                "kind": "oracle",
+                                "sample": f"{n} BetaE queries (1 per type), literal-KL scoring "
+                                          f"over all 14,505 entities + full sort, float64 numpy"}
+    print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def secondary_passes(args, t, groups, mixed_mode, flush):
+    """One GPU: (1) the step form the headline did not use -- the 14 per-type submits over 3
+    streams, or one mixed submit; (2) every query type alone (one kgq_submit of its 1024 queries,
+    nothing else on the GPU): the metric's "queries/sec per query type"."""
+    import torch
+    from paper_2503_02172_b200 import Engine
+    qs = {g[0]: (torch.from_numpy(g[2]).cuda(), torch.from_numpy(g[3]).cuda()) for g in groups}
+    main = torch.cuda.current_stream()
+
+    def time_fn(fn, n):
+        ms = 0.0
+        for _ in range(n):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+            fn()
+            e1.record(main)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        return ms / n
+
+    S = 3
+    engs = []
+    for _ in range(S):
+        e = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH, max_k=K)
+        e.load_tables(t)
+        engs.append(e)
+    out = {s: (torch.empty((BATCH, K), device="cuda"), torch.empty((BATCH, K), dtype=torch.int32, device="cuda"))
+           for s in STRUCTS}
+    per_type = {}
+    for s in STRUCTS:
+        fn = lambda s=s: engs[0].submit(s, *qs[s], K, out=out[s], stream=main)
+        for _ in range(3):
+            fn()
+        per_type[s] = BATCH / (time_fn(fn, args.steps) / 1e3)
+    per_type_info = {"qps": per_type, "how": "each type alone: one kgq_submit of its 1024 queries on one stream, "
+                                             "L2 flushed before each (device time)"}
+    if mixed_mode:
+        streams = [torch.cuda.Stream() for _ in range(S)]
+
+        def fork_join():
+            ev0 = torch.cuda.Event()
+            ev0.record(main)
+            for st in streams:
+                st.wait_event(ev0)
+            for i, s in enumerate(STRUCTS):
+                engs[i % S].submit(s, *qs[s], K, out=out[s], stream=streams[i % S])
+            for st in streams:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                main.wait_event(ev)
+        for _ in range(3):
+            fork_join()
+        ms = time_fn(fork_join, args.steps)
+        other = {"form": f"the 14 per-type kgq_submit calls over {S} streams (one context each)",
+                 "value": len(STRUCTS) * BATCH / (ms / 1e3), "ms_per_step": ms}
+    else:
+        meng = Engine("betae", N_ENT, N_REL, DIM, hidden=HID, max_batch=BATCH * len(STRUCTS), max_k=K)
+        meng.load_tables(t)
+        a = torch.from_numpy(np.concatenate([g[2].reshape(-1) for g in groups])).cuda()
+        r = torch.from_numpy(np.concatenate([g[3].reshape(-1) for g in groups])).cuda()
+        mo = (torch.empty((BATCH * len(STRUCTS), K), device="cuda"),
+              torch.empty((BATCH * len(STRUCTS), K), dtype=torch.int32, device="cuda"))
+        fn = lambda: meng.submit_mixed_packed([g[0] for g in groups], [g[1] for g in groups], a, r, K, mo, stream=main)
+        for _ in range(3):
+            fn()
+        ms = time_fn(fn, args.steps)
+        meng.check_errors()
+        meng.close()
+        other = {"form": "one kgq_submit_mixed of the 14 x 1024 queries", "value": len(STRUCTS) * BATCH / (ms / 1e3),
+                 "ms_per_step": ms}
+    for e in engs:
+        e.check_errors()
+        e.close()
+    return other, per_type_info
 
 
 if __name__ == "__main__":

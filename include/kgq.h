@@ -182,6 +182,15 @@ kgq_status kgq_submit_host_async(kgq_ctx* ctx, int32_t s, int32_t batch, const i
 kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures, const int32_t* batches,
                             const int32_t* anchors, const int32_t* rels, int32_t k, float* topk_dist,
                             int32_t* topk_id, kgq_stream stream);
+/* kgq_submit_mixed with HOST buffers, asynchronous (the end-to-end form of the mixed batch, as
+ * kgq_submit_host_async is for one structure): anchors / rels host int32 in the same packed
+ * group order, topk_dist / topk_id host [sum B_i, k]; the H2D copies, the whole path and the
+ * D2H copies are enqueued on `stream` and the call returns.  Outputs are valid (and the inputs
+ * reusable) once the stream is synchronised; use pinned buffers for overlap.  Errors as
+ * kgq_submit_mixed; with a communicator the outputs are the merged / gathered global top-k. */
+kgq_status kgq_submit_mixed_host_async(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures,
+                                       const int32_t* batches, const int32_t* anchors, const int32_t* rels,
+                                       int32_t k, float* topk_dist, int32_t* topk_id, kgq_stream stream);
 /* Operator chain only (parity aid): device out fp32 [batch, kgq_num_branches(s),
  * kgq_embedding_width(model, d)]. */
 kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,

@@ -1447,6 +1447,42 @@ kgq_status kgq_submit_host_async(kgq_ctx* ctx, int32_t s, int32_t batch, const i
   return KGQ_OK;
 }
 
+kgq_status kgq_submit_mixed_host_async(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures,
+                                       const int32_t* batches, const int32_t* anchors, const int32_t* rels, int32_t k,
+                                       float* topk_dist, int32_t* topk_id, kgq_stream stream) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (n_groups < 0 || (n_groups > 0 && (!structures || !batches)))
+    return fail(ctx, KGQ_EINVAL, "mixed submit: bad group arrays");
+  int64_t Q = 0, na = 0, nr = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    kgq_status st = check_submit(ctx, structures[i], batches[i], k, true);
+    if (st) return st;
+    const Plan* P = plan_of(structures[i]);
+    Q += batches[i];
+    na += (int64_t)batches[i] * P->n_anchor;
+    nr += (int64_t)batches[i] * P->n_rel;
+  }
+  if (Q > ctx->cfg.max_batch)
+    return fail(ctx, KGQ_EINVAL, "mixed submit: %lld queries > max_batch %d", (long long)Q, ctx->cfg.max_batch);
+  if (Q == 0) { ctx->launches = 0; return KGQ_OK; }
+  if (!anchors || !rels || !topk_dist || !topk_id) return fail(ctx, KGQ_EINVAL, "NULL host pointer");
+  DeviceGuard g(ctx->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  // staging holds max_batch x kMaxBranches ids: every structure has <= 3 anchors and relations
+  CK(cudaMemcpyAsync(ctx->d_anchor_stage, anchors, (size_t)na * sizeof(int32_t), cudaMemcpyHostToDevice, cs),
+     "anchor upload");
+  CK(cudaMemcpyAsync(ctx->d_rel_stage, rels, (size_t)nr * sizeof(int32_t), cudaMemcpyHostToDevice, cs),
+     "relation upload");
+  kgq_status st = kgq_submit_mixed(ctx, n_groups, structures, batches, ctx->d_anchor_stage, ctx->d_rel_stage, k,
+                                   ctx->d_topd_stage, ctx->d_topi_stage, stream);
+  if (st) return st;
+  CK(cudaMemcpyAsync(topk_dist, ctx->d_topd_stage, (size_t)Q * k * sizeof(float), cudaMemcpyDeviceToHost, cs),
+     "top-k download");
+  CK(cudaMemcpyAsync(topk_id, ctx->d_topi_stage, (size_t)Q * k * sizeof(int32_t), cudaMemcpyDeviceToHost, cs),
+     "top-k download");
+  return KGQ_OK;
+}
+
 kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,
                                const int32_t* rels, float* out, kgq_stream stream) {
   kgq_status st = check_submit(ctx, s, batch, 0, false);

@@ -1,9 +1,11 @@
 // Entity scorer (SURVEY §8(a) a6 + a7): distance of every query embedding to every entity of
 // this rank's shard, min over DNF branches (union, Eq. 1), written as dist[b, e].
 //
-//   GQE   sum_d |e - q|                                   2 FP32 ops per (q, e, d)
+//   GQE   sum_d |e - q|                                   2 FP32 ops per (q, e, d), issued as
+//                                                         1 packed FADD2 per (q, e, d) (l1_pair)
 //   Q2B   sum_d |e-c| - (1-cen) sum_d min(|e-c|, o)         4 ops  (== sum ReLU(|e-c|-o) +
-//                                                                   cen * sum min(|e-c|, o))
+//                                                                   cen * sum min(|e-c|, o)):
+//                                                         1.5 FADD2 + 1 FMNMX per (q, e, d)
 //   BetaE sum_d |L_q + C_e + a_q U_e + b_q V_e|             4 ops  (== sum_d |KL(e || q)|)
 //
 // Register-tiled SIMT "GEMM-like" kernel: the inner op is not a dot product, so tensor cores do
@@ -28,6 +30,43 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Packed FP32 pairs (sm_100 FADD2): (a0, a1) += (|e0 - q|, |e1 - q|) is two instructions for two
+// entities -- a sub with q broadcast as a scalar operand, then an add whose |.| is an operand
+// modifier -- instead of four scalar ones.  The same two RN operations per element in the same
+// order as fabsf(e - q) then +=, so results are bit-identical to the scalar form.
+__device__ __forceinline__ float2 fadd2(const float2 a, const float2 b) {
+  float2 c;
+  asm("{\n.reg .b64 x, y, z;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\n"
+      "add.rn.f32x2 z, x, y;\nmov.b64 {%0, %1}, z;\n}\n"
+      : "=f"(c.x), "=f"(c.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return c;
+}
+__device__ __forceinline__ float2 fsub2(const float2 a, const float2 b) {
+  float2 c;
+  asm("{\n.reg .b64 x, y, z;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\n"
+      "sub.rn.f32x2 z, x, y;\nmov.b64 {%0, %1}, z;\n}\n"
+      : "=f"(c.x), "=f"(c.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return c;
+}
+// GQE: acc += |e - q| for an entity pair.  Q2B (BOX): also acc2 += min(|e - c|, o) -- the min
+// stays scalar (FMNMX, on the ALU pipe next to the FADD2s on the FMA pipe).
+template <bool BOX>
+__device__ __forceinline__ void l1_pair(float& a0, float& a1, float& b0, float& b1, float e0, float e1, float q,
+                                        float o) {
+  const float2 t = fsub2(make_float2(e0, e1), make_float2(q, q));
+  const float2 at = make_float2(fabsf(t.x), fabsf(t.y));
+  const float2 a = fadd2(make_float2(a0, a1), at);
+  a0 = a.x;
+  a1 = a.y;
+  if (BOX) {
+    const float2 b = fadd2(make_float2(b0, b1), make_float2(fminf(at.x, o), fminf(at.y, o)));
+    b0 = b.x;
+    b1 = b.y;
+  }
 }
 
 template <int MODEL>
@@ -113,12 +152,10 @@ __global__ void __launch_bounds__(256, 2)
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          if (MODEL == KGQ_GQE) {
-            acc[i][j] += fabsf(e[0][j] - q[0][i]);
-          } else if (MODEL == KGQ_Q2B) {
-            const float t = fabsf(e[0][j] - q[0][i]);
-            acc[i][j] += t;
-            acc2[i][j] += fminf(t, q[1][i]);
+          if (MODEL != KGQ_BETAE) {
+            if (j % 2 == 0)
+              l1_pair<MODEL == KGQ_Q2B>(acc[i][j], acc[i][j + 1], acc2[i][j], acc2[i][j + 1], e[0][j], e[0][j + 1],
+                                        q[0][i], MODEL == KGQ_Q2B ? q[1][i] : 0.0f);
           } else {
             float t = e[0][j] + q[0][i];
             t = fmaf(q[1][i], e[1][j], t);
@@ -175,7 +212,7 @@ __global__ void __launch_bounds__(256, 2)
 #endif
 constexpr int kStreamUnroll = KGQ_STREAM_UNROLL;
 template <int MODEL, int NB, int QB>
-__global__ void __launch_bounds__(256, (MODEL == KGQ_GQE && QB * NB <= 8) ? KGQ_STREAM_MINB : 1)
+__global__ void __launch_bounds__(256, MODEL == KGQ_GQE ? KGQ_STREAM_MINB : 1)
     k_score_stream(const float* __restrict__ Qt, int64_t rpad, const float* __restrict__ tab,
                    int64_t np, int d, float cen, float* __restrict__ dist, int64_t ldd, int B) {
   constexpr int NQ = Planes<MODEL>::NQ, NE = Planes<MODEL>::NE, R = QB * NB;
@@ -220,12 +257,10 @@ __global__ void __launch_bounds__(256, (MODEL == KGQ_GQE && QB * NB <= 8) ? KGQ_
       for (int r = 0; r < R; ++r) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (MODEL == KGQ_GQE) {
-            acc[r][i] += fabsf(e[0][i] - qj[r]);
-          } else if (MODEL == KGQ_Q2B) {
-            const float t = fabsf(e[0][i] - qj[r]);
-            acc[r][i] += t;
-            acc2[r][i] += fminf(t, qj[R + r]);
+          if (MODEL != KGQ_BETAE) {
+            if (i % 2 == 0)
+              l1_pair<MODEL == KGQ_Q2B>(acc[r][i], acc[r][i + 1], acc2[r][i], acc2[r][i + 1], e[0][i], e[0][i + 1],
+                                        qj[r], MODEL == KGQ_Q2B ? qj[R + r] : 0.0f);
           } else {
             float t = e[0][i] + qj[r];
             t = fmaf(qj[R + r], e[1][i], t);

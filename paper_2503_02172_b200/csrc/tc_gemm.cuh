@@ -57,6 +57,15 @@ inline int gemm_clusters() {
   return v;
 }
 
+// Tile raster group (tile_mn): M blocks per group; KGQ_GEMM_GROUP_M overrides (0 = M fastest).
+inline int gemm_group_m() {
+  static const int v = [] {
+    const char* e = getenv("KGQ_GEMM_GROUP_M");
+    return e ? atoi(e) : 8;
+  }();
+  return v;
+}
+
 // ---- PTX wrappers -----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -312,7 +321,27 @@ struct Sched {
   float* ws;   // [tail units][16 epilogue warps][BN / 8][32 lanes] float4 partial sums
   int* cnt;    // [tail tiles][16] arrival counters (zero between launches; the last arriver resets)
   unsigned long long* kt = nullptr;  // launch-span accounting of this stage (GemmWs::kt), or null
+  int group_m = 0;   // tile raster: groups of group_m M-blocks, N-major inside a group (0: M fastest)
 };
+// Tile t -> (M block, N block).  Grouped raster: tiles of group_m consecutive M blocks (256 rows
+// each) are ordered M fastest, then N, then the next group -- so the ~74 tiles in flight cover
+// group_m row blocks x ~74 / group_m column blocks: the group's A rows (group_m x 256 x K x 6 B)
+// stay in L2 while every column of W passes, and A is read from DRAM about once.  With plain M-
+// fastest order every column of tiles swept all of A: at M = 14K, K = 1600 (137 MB of A, more
+// than L2) ncu measured 2.7 GB of DRAM reads for one 15 MB-weight layer (profiles/r02).
+__device__ __forceinline__ void tile_mn(int t, int m_pairs, int n_tiles, int group_m, int& m, int& n) {
+  if (group_m <= 0 || group_m >= m_pairs) {
+    m = t % m_pairs;
+    n = t / m_pairs;
+    return;
+  }
+  const int per_group = group_m * n_tiles;
+  const int g = t / per_group, r = t - g * per_group;
+  const int m0 = g * group_m;
+  const int gm = min(group_m, m_pairs - m0);
+  m = m0 + r % gm;
+  n = r / gm;
+}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -401,7 +430,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int m_pairs = (M + 2 * BM - 1) / (2 * BM);
-  const int ntiles = m_pairs * ((N + BN - 1) / BN);
+  const int n_tiles = (N + BN - 1) / BN;
+  const int ntiles = m_pairs * n_tiles;
   const int nunits = sc.full + (ntiles - sc.full) * sc.s_tail;
   const int nk = (K + BK - 1) / BK;
 
@@ -452,8 +482,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int u = cluster; u < nunits; u += nclusters) {
         int t, kb0, kb1, v;
         unit_of(u, sc, nk, t, kb0, kb1, v);
-        const int m0 = (t % m_pairs) * 2 * BM + (int)rank * BM;
-        const int nw = (t / m_pairs) * BN + (int)rank * (BN / 2);
+        int tm, tn;
+        tile_mn(t, m_pairs, n_tiles, sc.group_m, tm, tn);
+        const int m0 = tm * 2 * BM + (int)rank * BM;
+        const int nw = tn * BN + (int)rank * (BN / 2);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait_backoff(&empty[s], ((it / STAGES) - 1) & 1);
@@ -550,8 +582,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int t, kb0, kb1, v;
       unit_of(u, sc, nk, t, kb0, kb1, v);
       const int ng = (kb1 - kb0 + DRAIN - 1) / DRAIN;
-      const int row0 = (t % m_pairs) * 2 * BM + (int)rank * BM + q * 32;
-      const int n0 = (t / m_pairs) * BN + ch;
+      int tm, tn;
+      tile_mn(t, m_pairs, n_tiles, sc.group_m, tm, tn);
+      const int row0 = tm * 2 * BM + (int)rank * BM + q * 32;
+      const int n0 = tn * BN + ch;
       const auto pre = epi.template prefetch<CW>(row0 + lane, n0, lane);
       float acc[CW];
 #pragma unroll
@@ -788,6 +822,7 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   }
   const int units = sc.full + (tiles - sc.full) * sc.s_tail;
   const int clusters = units < max_clusters ? units : max_clusters;
+  if (sc.group_m == 0) sc.group_m = gemm_group_m();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(THREADS);

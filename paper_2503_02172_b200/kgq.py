@@ -35,7 +35,8 @@ EXPORTS = (
     "kgq_num_relations", "kgq_num_branches", "kgq_uses_negation", "kgq_structure_name",
     "kgq_structure_from_name", "kgq_embedding_width", "kgq_shard_range", "kgq_shard_begin",
     "kgq_shard_end", "kgq_load_entities", "kgq_load_relations", "kgq_load_linear",
-    "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_submit_host_async", "kgq_submit_mixed", "kgq_query_embedding", "kgq_merge_topk",
+    "kgq_finalize", "kgq_submit", "kgq_submit_host", "kgq_submit_host_async", "kgq_submit_mixed",
+    "kgq_submit_mixed_host_async", "kgq_query_embedding", "kgq_merge_topk",
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
     "kgq_profile_read", "kgq_rank_answers", "kgq_peer_bytes", "kgq_set_peers", "kgq_merge_peers",
     "kgq_query_range", "kgq_nccl_unique_id", "kgq_comm_init", "kgq_comm_destroy", "kgq_rank_metrics",
@@ -80,6 +81,7 @@ _sig = {
     "kgq_submit_host": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
     "kgq_submit_host_async": (_I32, [_P, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
     "kgq_submit_mixed": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P]),
+    "kgq_submit_mixed_host_async": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P]),
     "kgq_query_embedding": (_I32, [_P, _I32, _I32, _P, _P, _P, _P]),
     "kgq_merge_topk": (_I32, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
     "kgq_check_errors": (_I32, [_P, _P]),
@@ -316,6 +318,30 @@ class Engine:
             if groups:
                 self._mix_ev = torch.cuda.Event()
                 self._mix_ev.record()
+        return td, ti
+
+    def submit_mixed_packed(self, structures, batches, anchors, rels, k, out, stream=None):
+        """kgq_submit_mixed on inputs already packed in group order (int32 CUDA tensors: the groups'
+        [B_i, n_a] anchor blocks back to back, likewise the relations) -- no staging copy, so a
+        repeated call with the same tensors replays the library's captured graph as is."""
+        ss = (ctypes.c_int32 * len(structures))(*[structure_id(s) for s in structures])
+        bs = (ctypes.c_int32 * len(batches))(*[int(b) for b in batches])
+        td, ti = out
+        self._check(_lib.kgq_submit_mixed(self._h, len(structures), ss, bs, _ptr(anchors), _ptr(rels), k,
+                                          _ptr(td), _ptr(ti), _stream(stream)))
+        return td, ti
+
+    def submit_mixed_host(self, structures, batches, anchors: np.ndarray, rels: np.ndarray, k: int, out,
+                          stream=None):
+        """kgq_submit_mixed_host_async: host int32 inputs packed in group order (pinned for
+        overlap), host outputs out = (dist [Q, k] fp32, ids [Q, k] int32); asynchronous -- valid
+        after `stream` is synchronised."""
+        ss = (ctypes.c_int32 * len(structures))(*[structure_id(s) for s in structures])
+        bs = (ctypes.c_int32 * len(batches))(*[int(b) for b in batches])
+        td, ti = out
+        self._check(_lib.kgq_submit_mixed_host_async(self._h, len(structures), ss, bs, anchors.ctypes.data,
+                                                     rels.ctypes.data, k, td.ctypes.data, ti.ctypes.data,
+                                                     _stream(stream)))
         return td, ti
 
     def submit_host(self, structure, anchors: np.ndarray, rels: np.ndarray, k: int,

@@ -171,6 +171,21 @@ class ShardedEngine:
         td, ti = self.engine.submit_mixed(groups, k, stream=stream)
         return self._finish(td, ti, k, stream)
 
+    def submit_mixed_packed(self, structures, batches, anchors, rels, k, out, stream=None):
+        """kgq_submit_mixed on inputs packed in group order (Engine.submit_mixed_packed) -> global
+        top-k.  With the library communicator (merge "nccl") `out` receives the global result."""
+        td, ti = self.engine.submit_mixed_packed(structures, batches, anchors, rels, k, out, stream=stream)
+        return self._finish(td, ti, k, stream)
+
+    def submit_mixed_host(self, structures, batches, anchors, rels, k, out, stream=None):
+        """kgq_submit_mixed_host_async (host buffers, asynchronous): only where the library returns
+        the global result itself (one rank, or its communicator)."""
+        if self.merge_mode not in ("local", "nccl"):
+            raise KgqError(4, f"host-buffer mixed submit needs the library communicator (merge {self.merge_mode})")
+        self.engine.submit_mixed_host(structures, batches, anchors, rels, k, out, stream=stream)
+        self._launches = self.engine.last_launch_count()
+        return out
+
     def last_launch_count(self):
         return self._launches
 

@@ -541,6 +541,52 @@ def test_mixed_graph_replay_matches_eager():
     ee.close()
 
 
+def test_mixed_host_submit_matches_device_and_oracle():
+    """kgq_submit_mixed_host_async (bench.py's end-to-end call): pinned host inputs packed in
+    group order, host outputs.  Every row checked against the oracle, and bit-identical to the
+    device-pointer mixed submit over rounds that go eager -> capture -> graph replay, with new
+    query content every round (the staging buffers' addresses are what the graph keys on)."""
+    N, R, d, H = 1000, 20, 40, 96
+    t = synth.make_tables("betae", N, R, d, hidden=H, seed=8)
+    m = O.Model("betae", t, dim=d)
+    eh = Engine("betae", N, R, d, hidden=H, max_batch=160, max_k=16)
+    eh.load_tables(t)
+    ed = Engine("betae", N, R, d, hidden=H, max_batch=160, max_k=16)
+    ed.load_tables(t)
+    shapes = [("3i", 13), ("up", 9), ("pni", 17), ("1p", 6), ("inp", 11), ("2u-DM", 5)]
+    ss, bs = [s for s, _ in shapes], [b for _, b in shapes]
+    Q = sum(bs)
+    k = 12
+    hd = torch.empty((Q, k)).pin_memory()
+    hi = torch.empty((Q, k), dtype=torch.int32).pin_memory()
+    st = torch.cuda.Stream()
+    for rnd in range(4):
+        qs = [synth.make_queries(s, b, N, R, seed=700 + 10 * rnd + i) for i, (s, b) in enumerate(shapes)]
+        a = torch.from_numpy(np.concatenate([x[0].reshape(-1) for x in qs]).astype(np.int32)).pin_memory()
+        r = torch.from_numpy(np.concatenate([x[1].reshape(-1) for x in qs]).astype(np.int32)).pin_memory()
+        eh.submit_mixed_host(ss, bs, a.numpy(), r.numpy(), k, (hd.numpy(), hi.numpy()), stream=st)
+        st.synchronize()
+        dd, di = ed.submit_mixed([(s, dev(x[0].astype(np.int32)), dev(x[1].astype(np.int32)))
+                                  for s, x in zip(ss, qs)], k)
+        torch.cuda.synchronize()
+        assert np.array_equal(hi.numpy(), di.cpu().numpy()), rnd
+        assert np.array_equal(hd.numpy(), dd.cpu().numpy()), rnd
+        if rnd in (0, 3):
+            q = 0
+            for (s, b), (qa, qr) in zip(shapes, qs):
+                ref = m.scores(s, qa, qr)
+                for j in range(b):
+                    assert_topk_ok(hd.numpy()[q + j], hi.numpy()[q + j], ref[j], k, what=f"host mixed {s} row {j}")
+                q += b
+    eh.check_errors()
+    ed.check_errors()
+    with pytest.raises(KgqError, match="EINVAL"):  # more queries than max_batch
+        eh.submit_mixed_host(["1p"], [161], np.zeros(161, np.int32), np.zeros(161, np.int32), k,
+                             (np.empty((161, k), np.float32), np.empty((161, k), np.int32)))
+    eh.close()
+    ed.close()
+
+
 def test_ktime_launch_spans():
     """kgq_ktime_*: every tcgen05 GEMM launch of a submit logs one in-kernel span (bench.py's
     roofline time); the per-stage sums equal the logged spans, and toggling keeps results
