@@ -292,6 +292,20 @@ kgq_status kgq_rank_metrics(kgq_ctx* ctx, int32_t batch, const int32_t* ans_off,
  * an asynchronous error of the context's communicator. */
 kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream);
 
+/* ---- options -------------------------------------------------------------------------- */
+/* KGQ_OPT_FUSED_TOPK (BetaE tensor-core scorer, k <= 16, no shard_dist, not
+ * kgq_rank_answers): the scorer's epilogue keeps every query row's k smallest (distance, id) per
+ * N stripe of the entity table and a merge kernel returns the top-k -- the [batch, N] distance
+ * block is never written.  Values: KGQ_FUSED_OFF (always write the block; block-minima top-k),
+ * KGQ_FUSED_ON (fuse whenever eligible), KGQ_FUSED_AUTO (default: fuse scorer launches of >= 8,192
+ * query rows, where every stripe spans >= 16 tiles so the lists' warm-up amortises; measured,
+ * DESIGN.md §7).  Results are identical either way (same distances, same (dist, id) order).
+ * The environment KGQ_NO_FUSED_TOPK=1 makes OFF the default of new contexts.
+ * Returns KGQ_EINVAL for an unknown option or value. */
+typedef enum { KGQ_OPT_FUSED_TOPK = 1 } kgq_option;
+typedef enum { KGQ_FUSED_OFF = 0, KGQ_FUSED_ON = 1, KGQ_FUSED_AUTO = 2 } kgq_fused_mode;
+kgq_status kgq_set_option(kgq_ctx* ctx, int32_t option, int64_t value);
+
 /* ---- introspection (parity / bench) ----------------------------------------------------- */
 /* Number of this library's kernels launched by the last submit/query_embedding call. */
 int32_t kgq_last_launch_count(const kgq_ctx* ctx);

@@ -220,6 +220,25 @@ bool relterm_disabled() {  // KGQ_NO_RELTERM=1: first projection layer on the as
   }
   return v == 1;
 }
+// KGQ_NO_FUSED_TOPK=1: new contexts default to KGQ_FUSED_OFF (A/B runs)
+bool fused_topk_disabled() {
+  static const bool v = [] {
+    const char* e = getenv("KGQ_NO_FUSED_TOPK");
+    return e && e[0] && e[0] != '0';
+  }();
+  return v;
+}
+// Fused top-k for a tensor-core scorer launch of `rows` GEMM rows?  AUTO: only launches of
+// >= 8,192 rows -- each list's warm-up (the first ~10 chunks insert on almost every position,
+// and a warp pays for every lane's insert) costs about one tile, so stripes must be long and the
+// rows many for the saved top-k pass to win; measured on C2.
+// AUTO keeps every stripe >= 16 tiles long; ON (tests) lets the planner cut as many stripes as
+// balance the machine best (up to 64)
+static int topk_min_tiles(const kgq_ctx* ctx) { return ctx->fused_topk == KGQ_FUSED_ON ? 1 : 16; }
+static bool use_fused_topk(const kgq_ctx* ctx, int64_t rows, int k) {
+  if (k > kFusedTopkMax || ctx->fused_topk == KGQ_FUSED_OFF) return false;
+  return ctx->fused_topk == KGQ_FUSED_ON || rows >= 8192;
+}
 bool topk_cmin_disabled() {  // KGQ_NO_TOPK_CMIN=1: full-row top-k (A/B and debugging)
   static int v = -1;
   if (v < 0) {
@@ -530,6 +549,7 @@ kgq_status kgq_create(const kgq_config* cfg, kgq_ctx** out) {
   ctx->cfg = *cfg;
   const char* ng = getenv("KGQ_NO_GRAPHS");
   ctx->use_graphs = !(ng && ng[0] && ng[0] != '0');
+  ctx->fused_topk = fused_topk_disabled() ? KGQ_FUSED_OFF : KGQ_FUSED_AUTO;
   DeviceGuard g(cfg->device);
   kgq_shard_range(cfg->n_entity, cfg->world_size, cfg->rank, &ctx->e0, &ctx->e1);
   ctx->ns = ctx->e1 - ctx->e0;
@@ -559,7 +579,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   F(ctx->ent); F(ctx->rel[0]); F(ctx->rel[1]); F(ctx->score_tab);
   for (auto& l : ctx->lin) { F(l.W); F(l.Wsp.b0); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) F(s->b0);
-  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->d_err); F(ctx->d_invalid);
+  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->cand); F(ctx->d_err); F(ctx->d_invalid);
   F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum); F(ctx->uvT); F(ctx->lin1x.Wsp.b0); F(ctx->RW);
   F(ctx->mix_rid); F(ctx->mix_map);
   if (ctx->mix_map_host) cudaFreeHost(ctx->mix_map_host);
@@ -686,6 +706,8 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st) st = dalloc(ctx, &ctx->Qt, (size_t)(nplanes * d * ctx->rpad), "Qt");
   if (!st) st = dalloc(ctx, &ctx->dist, (size_t)(ctx->bchunk * ctx->np), "dist");
   if (!st && c.model == KGQ_BETAE) st = dalloc(ctx, &ctx->cmin, (size_t)(ctx->bchunk * (ctx->np / 32)), "block minima");
+  if (!st && c.model == KGQ_BETAE)
+    st = dalloc(ctx, &ctx->cand, (size_t)ctx->bchunk * kFusedTopkLists * kFusedTopkMax, "fused top-k lists");
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_d, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st) st = dalloc(ctx, &ctx->topk_tmp_i, (size_t)(ctx->bchunk * 4096), "top-k candidates");
   if (!st && c.model == KGQ_BETAE) {
@@ -754,12 +776,24 @@ static bool betae_stream_cuv() {
   return v;
 }
 
+// fused_k > 0 (BetaE tensor-core path only): the scorer keeps per-stripe top-k lists in its
+// epilogue (ctx->cand, *nlists per row) instead of writing ctx->dist.
 static int score_rows(kgq_ctx* ctx, const Plan* P, int64_t b0, int nb, cudaStream_t st, int B = 0,
-                      bool from_state = false) {
+                      bool from_state = false, int fused_k = 0, int* nlists = nullptr) {
   const kgq_config& c = ctx->cfg;
   int L = 0;
   const float* qb = ctx->Q + b0 * P->n_out * ctx->qw;
-  if (from_state) {  // BetaE, query state still in S (q_in_state): prep straight from the split rows
+  if (fused_k > 0) {
+    StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
+    if (from_state)
+      L += launch_mix_score_prep(nullptr, ctx->S, nb * P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc, ctx->Ptc,
+                                 st, B, b0, P->n_out);
+    else
+      L += launch_score_prep_tc(qb, nb * P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc, ctx->Ptc, st);
+    L += launch_score_tc_topk(nb * P->n_out, P->n_out, c.dim, ctx->Atc, ctx->Ptc, ctx->uv, ctx->Esum, ctx->np, ctx->ns,
+                              fused_k, ctx->cand, (int64_t)kFusedTopkLists * fused_k, &ctx->gws, st, nlists, topk_min_tiles(ctx));
+    check_site("tensor-core scorer (fused top-k)");
+  } else if (from_state) {  // BetaE, query state still in S (q_in_state): prep straight from the split rows
     StageTimer t(ctx, st, kStScore, 2.0 * nb * P->n_out * (double)ctx->ns * 2 * c.dim);
     L += launch_mix_score_prep(nullptr, ctx->S, nb * P->n_out, c.dim, ctx->uvsums, c.n_entity, ctx->Atc, ctx->Ptc,
                                st, B, b0, P->n_out);
@@ -809,18 +843,24 @@ static kgq_status submit_impl(kgq_ctx* ctx, int32_t s, int32_t B, const int32_t*
   check_site("operator chain");
   for (int64_t b0 = 0; b0 < B; b0 += ctx->bchunk) {
     const int nb = (int)std::min<int64_t>(ctx->bchunk, B - b0);
-    L += score_rows(ctx, P, b0, nb, st, B, from_state);
+    const bool tc = ctx->cfg.model == KGQ_BETAE && !score_uses_stream(ctx->cfg.model, P->n_out, nb);
+    // fused top-k in the tensor-core scorer's epilogue unless the distance rows are wanted
+    const bool fused = tc && !shard_dist && use_fused_topk(ctx, (int64_t)nb * P->n_out, k);
+    int nl = 0;
+    L += score_rows(ctx, P, b0, nb, st, B, from_state, fused ? k : 0, &nl);
     {
       StageTimer t(ctx, st, kStTopk);
       // the tensor-core scorer's epilogue wrote 32-entity block minima: pruned top-k
-      const bool blockmin = ctx->cfg.model == KGQ_BETAE && !score_uses_stream(ctx->cfg.model, P->n_out, nb) &&
-                            k <= 32 && !topk_cmin_disabled();
+      const bool blockmin = tc && k <= 32 && !topk_cmin_disabled();
       PeerPush pp{};
       if (push) {
         pp = ctx->peers;
         pp.row0 = ctx->push_row0 + (int)b0;
       }
-      if (blockmin) {
+      if (fused) {
+        L += launch_topk_lists(ctx->cand, (int64_t)kFusedTopkLists * k, k, nb, nb, nl, nl, ctx->e0,
+                               ctx->d_invalid + b0, nullptr, topk_dist + b0 * k, topk_id + b0 * k, st, pp);
+      } else if (blockmin) {
         L += launch_topk_cmin(ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, nb, ctx->ns, k, ctx->e0,
                               ctx->d_invalid + b0, topk_dist + b0 * k, topk_id + b0 * k, st, pp);
       } else {
@@ -1211,22 +1251,53 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
   if (!own_map) CK(cudaEventRecord(ctx->mix_map_ev, st), "mixed staging");
   const int64_t* d_srcrow = ctx->mix_map;
   const int32_t* d_outrow = reinterpret_cast<const int32_t*>(ctx->mix_map + (R1 + R2));
+  // fused top-k (k <= 16, use_fused_topk): the scorer epilogue keeps per-stripe lists and no
+  // distance block is written -- decided per scorer launch (single-branch rows, then union rows)
+  const bool f1 = use_fused_topk(ctx, R1, k), f2 = use_fused_topk(ctx, R2, k);
+  const int64_t ldc = (int64_t)kFusedTopkLists * k;
+  int nl1 = 0, nl2 = 0;
   {
     StageTimer t(ctx, st, kStScore, 2.0 * (R1 + R2) * (double)ctx->ns * 2 * d);
     L += launch_mix_score_prep(d_srcrow, ctx->S, R1 + R2, d, ctx->uvsums, ctx->cfg.n_entity, ctx->Atc, ctx->Ptc, st);
-    L += launch_score_tc_gemm(R1, 1, d, ctx->Atc, ctx->Ptc, ctx->uv, ctx->Esum, ctx->np, ctx->dist, ctx->np,
-                              ctx->cmin, ctx->np / 32, ctx->ns, &ctx->gws, st);
-    L += launch_score_tc_gemm(R2, 2, d, ctx->Atc.at(R1), ctx->Ptc + R1, ctx->uv, ctx->Esum, ctx->np,
-                              ctx->dist + (int64_t)Q1 * ctx->np, ctx->np, ctx->cmin + (int64_t)Q1 * (ctx->np / 32),
-                              ctx->np / 32, ctx->ns, &ctx->gws, st);
+    if (f1)
+      L += launch_score_tc_topk(R1, 1, d, ctx->Atc, ctx->Ptc, ctx->uv, ctx->Esum, ctx->np, ctx->ns, k, ctx->cand, ldc,
+                                &ctx->gws, st, &nl1, topk_min_tiles(ctx));
+    else
+      L += launch_score_tc_gemm(R1, 1, d, ctx->Atc, ctx->Ptc, ctx->uv, ctx->Esum, ctx->np, ctx->dist, ctx->np,
+                                ctx->cmin, ctx->np / 32, ctx->ns, &ctx->gws, st);
+    if (f2)
+      L += launch_score_tc_topk(R2, 2, d, ctx->Atc.at(R1), ctx->Ptc + R1, ctx->uv, ctx->Esum, ctx->np, ctx->ns, k,
+                                ctx->cand + (int64_t)Q1 * ldc, ldc, &ctx->gws, st, &nl2, topk_min_tiles(ctx));
+    else
+      L += launch_score_tc_gemm(R2, 2, d, ctx->Atc.at(R1), ctx->Ptc + R1, ctx->uv, ctx->Esum, ctx->np,
+                                ctx->dist + (int64_t)Q1 * ctx->np, ctx->np, ctx->cmin + (int64_t)Q1 * (ctx->np / 32),
+                                ctx->np / 32, ctx->ns, &ctx->gws, st);
     check_site("mixed scorer");
   }
   {
     StageTimer t(ctx, st, kStTopk);
     PeerPush pp{};
     if (ctx->peers.on()) pp = ctx->peers;  // N2: rows pushed by output row (row0 = 0)
-    L += launch_topk_cmin_map(ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, Q1 + Q2, ctx->ns, k, ctx->e0,
-                              ctx->d_invalid, d_outrow, topk_dist, topk_id, st, pp);
+    // score rows [0, Q1): single-branch groups, [Q1, Q1 + Q2): union groups; out_row maps both
+    if (f1 && f2) {
+      L += launch_topk_lists(ctx->cand, ldc, k, Q1 + Q2, Q1, nl1, nl2, ctx->e0, ctx->d_invalid, d_outrow, topk_dist,
+                             topk_id, st, pp);
+    } else if (!f1 && !f2) {
+      L += launch_topk_cmin_map(ctx->dist, ctx->np, ctx->cmin, ctx->np / 32, Q1 + Q2, ctx->ns, k, ctx->e0,
+                                ctx->d_invalid, d_outrow, topk_dist, topk_id, st, pp);
+    } else {
+      for (int part = 0; part < 2; ++part) {
+        const int r0 = part ? Q1 : 0, nr = part ? Q2 : Q1;
+        if (nr == 0) continue;
+        if (part ? f2 : f1)
+          L += launch_topk_lists(ctx->cand + (int64_t)r0 * ldc, ldc, k, nr, nr, part ? nl2 : nl1, part ? nl2 : nl1,
+                                 ctx->e0, ctx->d_invalid, d_outrow + r0, topk_dist, topk_id, st, pp);
+        else
+          L += launch_topk_cmin_map(ctx->dist + (int64_t)r0 * ctx->np, ctx->np, ctx->cmin + (int64_t)r0 * (ctx->np / 32),
+                                    ctx->np / 32, nr, ctx->ns, k, ctx->e0, ctx->d_invalid, d_outrow + r0, topk_dist,
+                                    topk_id, st, pp);
+      }
+    }
     check_site("mixed top-k");
   }
   ctx->launches = L;
@@ -1481,6 +1552,23 @@ kgq_status kgq_submit_mixed_host_async(kgq_ctx* ctx, int32_t n_groups, const int
   CK(cudaMemcpyAsync(topk_id, ctx->d_topi_stage, (size_t)Q * k * sizeof(int32_t), cudaMemcpyDeviceToHost, cs),
      "top-k download");
   return KGQ_OK;
+}
+
+kgq_status kgq_set_option(kgq_ctx* ctx, int32_t option, int64_t value) {
+  if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
+  if (option == KGQ_OPT_FUSED_TOPK) {
+    if (value != KGQ_FUSED_OFF && value != KGQ_FUSED_ON && value != KGQ_FUSED_AUTO)
+      return fail(ctx, KGQ_EINVAL, "KGQ_OPT_FUSED_TOPK: value %lld is not OFF / ON / AUTO", (long long)value);
+    if (ctx->fused_topk != (int)value) {
+      ctx->fused_topk = (int)value;
+      // captured graphs hold the previous path: re-capture
+      for (auto& g : ctx->graphs) destroy_graph_entry(g);
+      ctx->graphs.clear();
+      clear_mix_graphs(ctx);
+    }
+    return KGQ_OK;
+  }
+  return fail(ctx, KGQ_EINVAL, "unknown option %d", (int)option);
 }
 
 kgq_status kgq_query_embedding(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_t* anchors,

@@ -105,6 +105,7 @@ struct kgq_ctx {
   int64_t rpad = 0;
   float* dist = nullptr;                   // [bchunk, np]
   float* cmin = nullptr;                   // [bchunk, np / 32] block minima (tensor-core scorer)
+  unsigned long long* cand = nullptr;      // [bchunk, 128 lists, 16] fused top-k lists (BetaE scorer)
   int64_t bchunk = 0;
   float* topk_tmp_d = nullptr;             // chunked top-k candidates [<= 4096 per row]
   int32_t* topk_tmp_i = nullptr;
@@ -162,6 +163,7 @@ struct kgq_ctx {
   };
   std::vector<MixGraphEntry> mgraphs;
   bool use_graphs = true;
+  int fused_topk = KGQ_FUSED_AUTO;  // kgq_set_option(KGQ_OPT_FUSED_TOPK)
   uint64_t graph_clock = 0;
   cudaStream_t cap_stream = nullptr;
   // N2: fused top-k all-gather over peer memory (kgq_set_peers); peers.world == 0: off
@@ -266,6 +268,16 @@ int launch_score_tc_gemm(int rows, int nbq, int d, Split A, const float2* P, con
                          int64_t np, float* dist, int64_t ldd, float* cmin, int64_t ldc, int64_t nvalid,
                          const GemmWs* ws, cudaStream_t st);
 // block-minima top-k with an output row map (out_row[b] = output / invalid-flag row of dist row b)
+// fused top-k: the BetaE tensor-core scorer keeps per-stripe k-lists in its
+// epilogue (no distance block; k <= kFusedTopkMax); *nlists = lists per output row
+constexpr int kFusedTopkMax = 16;
+constexpr int kFusedTopkLists = 128;  // <= 64 stripes x 2 column halves (the merge's 4 heads per lane)
+int launch_score_tc_topk(int rows, int nbq, int d, Split A, const float2* P, const Split& uv, const float2* Esum,
+                         int64_t np, int64_t nvalid, int k, unsigned long long* cand, int64_t ldcand,
+                         const GemmWs* ws, cudaStream_t st, int* nlists, int min_tiles);
+int launch_topk_lists(const unsigned long long* cand, int64_t ldcand, int k, int B, int rows1, int nl1, int nl2,
+                      int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d, int32_t* out_i,
+                      cudaStream_t st, const PeerPush& pp);
 int launch_topk_cmin_map(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                          int k, int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d,
                          int32_t* out_i, cudaStream_t st, const PeerPush& pp);

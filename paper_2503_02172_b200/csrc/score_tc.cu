@@ -151,10 +151,12 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
   }
 }
 
-template <int NB>
+// TK (fused top-k): no distance block; the epilogue keeps every output row's k
+// smallest (dist, column) pairs per N stripe (tc_gemm.cuh TOPK) and writes only those lists.
+template <int NB, bool TK = false>
 struct EpiBetaScore {
   static constexpr int PLANES = 1, ROWDIV = NB;
-  static constexpr bool CMIN = true, INIT = false, STREAM_OUT = true;
+  static constexpr bool CMIN = !TK, INIT = false, STREAM_OUT = true, TOPK = TK;
   template <int CW>
   __device__ void init(int, int, float*) const {}
   const float2* P;  // [rows] (hi, lo)
@@ -164,6 +166,9 @@ struct EpiBetaScore {
   float* cmin = nullptr;  // [rows / NB][ldc] block minima, or nullptr
   int64_t ldc = 0;
   int64_t nvalid = 0;     // the shard's entity count ns (columns >= ns are padding)
+  unsigned long long* cand = nullptr;  // TK: [rows / NB][ldcand] per-stripe sorted key lists
+  int64_t ldcand = 0;
+  int k = 0;
   struct Pre {
     float2 p;       // P of this lane's row
     float2 e[4];    // E of columns n0 + lane + 32 j
@@ -239,6 +244,33 @@ int launch_score_tc_gemm(int rows, int nbq, int d, Split A, const float2* P, con
                                 ws, st);
   return tc::launch_gemm_auto(A, rows, uv, (int)np, 2 * d, o, EpiBetaScore<1>{P, Esum, rows, np, cmin, ldc, nvalid},
                               ws, st);
+}
+
+int launch_score_tc_topk(int rows, int nbq, int d, Split A, const float2* P, const Split& uv, const float2* Esum,
+                         int64_t np, int64_t nvalid, int k, unsigned long long* cand, int64_t ldcand,
+                         const GemmWs* ws, cudaStream_t st, int* nlists, int min_tiles) {
+  if (rows <= 0) {
+    *nlists = 0;
+    return 0;
+  }
+  int ns = 1, L;
+  if (nbq == 2) {
+    EpiBetaScore<2, true> e{P, Esum, rows, np};
+    e.nvalid = nvalid;
+    e.cand = cand;
+    e.ldcand = ldcand;
+    e.k = k;
+    L = tc::launch_gemm_topk(A, rows, uv, (int)np, 2 * d, e, ws, st, &ns, min_tiles);
+  } else {
+    EpiBetaScore<1, true> e{P, Esum, rows, np};
+    e.nvalid = nvalid;
+    e.cand = cand;
+    e.ldcand = ldcand;
+    e.k = k;
+    L = tc::launch_gemm_topk(A, rows, uv, (int)np, 2 * d, e, ws, st, &ns, min_tiles);
+  }
+  *nlists = 2 * ns;  // one list per (stripe, column half)
+  return L;
 }
 
 int launch_score_prep_tc(const float* q, int rows, int d, const double* sums, int64_t ns, Split A, float2* P,

@@ -322,7 +322,15 @@ struct Sched {
   int* cnt;    // [tail tiles][16] arrival counters (zero between launches; the last arriver resets)
   unsigned long long* kt = nullptr;  // launch-span accounting of this stage (GemmWs::kt), or null
   int group_m = 0;   // tile raster: groups of group_m M-blocks, N-major inside a group (0: M fastest)
+  int n_stripes = 0; // fused top-k epilogues (Epi::TOPK): N split into this many stripes of whole tiles
 };
+// Fused top-k epilogues (Epi::TOPK, score_tc.cu) keep per-row state across tiles, so their work
+// unit is a row stripe: one 256-row M block x a contiguous range of N tiles, run by one cluster
+// back to back (no split-K).  Other epilogues: one tile (or one K split of a tail tile) per unit.
+template <class E, class = void>
+struct epi_topk : std::false_type {};
+template <class E>
+struct epi_topk<E, std::void_t<decltype(E::TOPK)>> : std::integral_constant<bool, E::TOPK> {};
 // Tile t -> (M block, N block).  Grouped raster: tiles of group_m consecutive M blocks (256 rows
 // each) are ordered M fastest, then N, then the next group -- so the ~74 tiles in flight cover
 // group_m row blocks x ~74 / group_m column blocks: the group's A rows (group_m x 256 x K x 6 B)
@@ -378,6 +386,10 @@ __device__ __forceinline__ void kt_end(unsigned long long* kt) {
     __threadfence();
   }
 }
+// Unit u of a launch -> M block tm, N tiles [tn0, tn1), K blocks [kb0, kb1), tail slot v (-1: none).
+template <bool TOPK>
+__device__ __forceinline__ void unit_tiles(int u, const Sched& sc, int nk, int m_pairs, int n_tiles, int& tm,
+                                           int& tn0, int& tn1, int& kb0, int& kb1, int& v);
 __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, int& kb0, int& kb1, int& v) {
   if (u < sc.full) {
     t = u; kb0 = 0; kb1 = nk; v = -1;
@@ -387,6 +399,71 @@ __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, 
   t = sc.full + v / sc.s_tail;
   kb0 = (v % sc.s_tail) * sc.kper;
   kb1 = min(nk, kb0 + sc.kper);
+}
+
+template <class E>
+__device__ __forceinline__ int epi_rows(const E& e) {
+  if constexpr (epi_topk<E>::value) return e.rows;
+  else return 0;
+}
+
+template <bool TOPK>
+__device__ __forceinline__ void unit_tiles(int u, const Sched& sc, int nk, int m_pairs, int n_tiles, int& tm,
+                                           int& tn0, int& tn1, int& kb0, int& kb1, int& v) {
+  if constexpr (TOPK) {
+    int st;
+    tile_mn(u, m_pairs, sc.n_stripes, sc.group_m, tm, st);
+    tn0 = (int)((int64_t)st * n_tiles / sc.n_stripes);  // balanced stripes: floor / ceil tiles each
+    tn1 = (int)((int64_t)(st + 1) * n_tiles / sc.n_stripes);
+    kb0 = 0;
+    kb1 = nk;
+    v = -1;
+  } else {
+    int t;
+    unit_of(u, sc, nk, t, kb0, kb1, v);
+    tile_mn(t, m_pairs, n_tiles, sc.group_m, tm, tn0);
+    tn1 = tn0 + 1;
+  }
+}
+
+// Lane-private sorted list of the k smallest (order key, column) pairs of one output row, in
+// the epilogue warp's shared-memory slot (column-major [j][lane]: conflict-free).  Inserting a
+// key below the current k-th drops the k-th.
+__device__ __forceinline__ void topk_list_insert(unsigned long long* L, int lane, int k, int& cnt,
+                                                 unsigned long long& thr, unsigned long long key) {
+  int p = cnt < k ? cnt : k - 1;
+  while (p > 0) {
+    const unsigned long long prev = L[(p - 1) * 32 + lane];
+    if (prev < key) break;
+    L[p * 32 + lane] = prev;
+    --p;
+  }
+  L[p * 32 + lane] = key;
+  if (cnt < k) ++cnt;
+  thr = cnt == k ? L[(k - 1) * 32 + lane] : ~0ull;
+}
+// v[i] for a run-time i < 32 from a register array: a 5-level select tree (31 FSEL), no local
+// memory
+__device__ __forceinline__ float pick32(const float* v, int i) {
+  float t[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) t[j] = (i & 1) ? v[2 * j + 1] : v[2 * j];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) t[j] = (i & 2) ? t[2 * j + 1] : t[2 * j];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) t[j] = (i & 4) ? t[2 * j + 1] : t[2 * j];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) t[j] = (i & 8) ? t[2 * j + 1] : t[2 * j];
+  return (i & 16) ? t[1] : t[0];
+}
+__device__ __forceinline__ uint32_t topk_fkey(float f) {  // order-preserving (NaN max, -0 = +0)
+  if (f != f) return 0xFFFFFFFFu;
+  if (f == 0.0f) f = 0.0f;
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float topk_fkey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
 // Epilogue policy concept (linear_tc.cu, score_tc.cu):
@@ -402,6 +479,11 @@ __device__ __forceinline__ void unit_of(int u, const Sched& sc, int nk, int& t, 
 //       const float* v) const -- optional side output after the row-pair min (score top-k)
 //   static constexpr bool INIT; template <int CW> __device__ void init(int row, int n0,
 //       float* acc) const -- optional initial accumulator values (relation term of layer 1)
+//   static constexpr bool TOPK (optional) -- fused top-k: no output tensor; every output row's
+//       k (<= 16) smallest (value, column) pairs over the unit's stripe are kept in the warp's
+//       staging slot and written as one sorted list per (row, stripe, column half) to
+//       epi.cand[orow * epi.ldcand + (stripe * 2 + half) * epi.k + j] as (order key << 32 | col);
+//       epi.rows / epi.nvalid bound the valid rows / columns
 // Output tensor maps: PLANES 1: fp32, box {32 columns, 32 / ROWDIV rows}, 128-byte swizzle;
 // PLANES 3: bf16 plane p, box {16 columns, 32 rows}, 32-byte swizzle.
 template <int BN, class Epi>
@@ -430,9 +512,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int m_pairs = (M + 2 * BM - 1) / (2 * BM);
+  constexpr bool TOPK = epi_topk<Epi>::value;
   const int n_tiles = (N + BN - 1) / BN;
   const int ntiles = m_pairs * n_tiles;
-  const int nunits = sc.full + (ntiles - sc.full) * sc.s_tail;
+  const int nunits = TOPK ? m_pairs * sc.n_stripes : sc.full + (ntiles - sc.full) * sc.s_tail;
   const int nk = (K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -480,13 +563,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // ---------------- TMA producer (both CTAs; completions counted by the leader) ----------------
       uint32_t it = 0;
       for (int u = cluster; u < nunits; u += nclusters) {
-        int t, kb0, kb1, v;
-        unit_of(u, sc, nk, t, kb0, kb1, v);
-        int tm, tn;
-        tile_mn(t, m_pairs, n_tiles, sc.group_m, tm, tn);
+        int tm, tn0, tn1, kb0, kb1, v;
+        unit_tiles<TOPK>(u, sc, nk, m_pairs, n_tiles, tm, tn0, tn1, kb0, kb1, v);
         const int m0 = tm * 2 * BM + (int)rank * BM;
-        const int nw = tn * BN + (int)rank * (BN / 2);
+        for (int tn = tn0; tn < tn1; ++tn)
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int nw = tn * BN + (int)rank * (BN / 2);
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait_backoff(&empty[s], ((it / STAGES) - 1) & 1);
           uint8_t* st = smem + s * L::STAGE_BYTES;
@@ -514,9 +596,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                              ((uint32_t)((2 * BM) >> 4) << 24);
       uint32_t it = 0, g0 = 0;
       for (int u = cluster; u < nunits; u += nclusters) {
-        int t, kb0, kb1, v;
-        unit_of(u, sc, nk, t, kb0, kb1, v);
+        int tm, tn0, tn1, kb0, kb1, v;
+        unit_tiles<TOPK>(u, sc, nk, m_pairs, n_tiles, tm, tn0, tn1, kb0, kb1, v);
         TC_TRACE(u, 0);
+        for (int tn = tn0; tn < tn1; ++tn) {
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const int kr = kb - kb0;
@@ -568,6 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if ((kr % DRAIN) == DRAIN - 1 || kb == kb1 - 1) mma_commit_2sm(&accfull[a]);
         }
         g0 += (kb1 - kb0 + DRAIN - 1) / DRAIN;
+        }
         TC_TRACE(u, 2);
       }
     }
@@ -579,12 +663,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t accempty_leader = mapa_shared(smem_u32(&accempty[0]), 0);
     uint32_t g0 = 0, nchunk = 0;
     for (int u = cluster; u < nunits; u += nclusters) {
-      int t, kb0, kb1, v;
-      unit_of(u, sc, nk, t, kb0, kb1, v);
+      int tm, tn0, tn1, kb0, kb1, v;
+      unit_tiles<TOPK>(u, sc, nk, m_pairs, n_tiles, tm, tn0, tn1, kb0, kb1, v);
       const int ng = (kb1 - kb0 + DRAIN - 1) / DRAIN;
-      int tm, tn;
-      tile_mn(t, m_pairs, n_tiles, sc.group_m, tm, tn);
       const int row0 = tm * 2 * BM + (int)rank * BM + q * 32;
+      // fused top-k: this lane's output row, its sorted list (count, k-th key, k-th value)
+      const bool trow = TOPK && (row0 + lane) < epi_rows(epi) && (ROWDIV == 1 || (lane & 1) == 0);
+      int tcnt = 0;
+      unsigned long long tthr = ~0ull;
+      float tthr_f = __uint_as_float(0x7F800000u);
+      unsigned long long* tlist = reinterpret_cast<unsigned long long*>(stg);
+      for (int tn = tn0; tn < tn1; ++tn) {
       const int n0 = tn * BN + ch;
       const auto pre = epi.template prefetch<CW>(row0 + lane, n0, lane);
       float acc[CW];
@@ -656,6 +745,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 7);
       }
       // ---- epilogue of this tile (the MMA warp is already on the next tile's partials) ----
+      if constexpr (TOPK) {
+        static_assert(CH == 32 && L::BUF_BYTES >= 32 * 16 * 8, "top-k lists: 16 keys x 32 lanes per warp slot");
+#pragma unroll
+        for (int c = 0; c < CW; c += CH) {
+          float* v = acc + c;
+          epi.template chunk<CH>(pre, row0 + lane, c, v);
+          if (ROWDIV == 2) {
+#pragma unroll
+            for (int i = 0; i < CH; ++i) v[i] = fminf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1));
+          }
+          // candidates of this chunk: a 32-bit mask of the values <= the lane's k-th (ties and NaN
+          // are settled by the exact key test below), then a compact loop over the set bits -- one
+          // copy of the insertion code per chunk instead of 32 unrolled ones (the unrolled form
+          // overflowed the instruction cache: ncu stall_no_inst was the top epilogue stall)
+          const int cb = n0 + c;
+          unsigned pm = 0;
+#pragma unroll
+          for (int i = 0; i < CH; ++i) pm |= (v[i] <= tthr_f ? 1u : 0u) << i;
+          const int64_t left = epi.nvalid - cb;
+          if (left < CH) pm &= left > 0 ? (1u << left) - 1u : 0u;
+          if (!trow) pm = 0;
+          while (pm) {
+            const int i = __ffs(pm) - 1;
+            pm &= pm - 1;
+            const float vi = pick32(v, i);
+            const unsigned long long key = ((unsigned long long)topk_fkey(vi) << 32) | (uint32_t)(cb + i);
+            if (key < tthr) {
+              topk_list_insert(tlist, lane, epi.k, tcnt, tthr, key);
+              tthr_f = tcnt == epi.k ? topk_fkey_inv((uint32_t)(tthr >> 32)) : __uint_as_float(0x7F800000u);
+            }
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < CW; c += CH, ++nchunk) {
         float* v = acc + c;  // in place (unrolled: stays in registers)
@@ -707,6 +830,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #endif
       }
       if (warp == EPI_WARP0 && lane == 0 && leader) TC_TRACE(u, 4);
+      }  // tiles of the unit
+      if constexpr (TOPK) {  // the stripe's list of this (row, column half)
+        if (trow) {
+          int tm2, stripe;
+          tile_mn(u, m_pairs, sc.n_stripes, sc.group_m, tm2, stripe);
+          const int half = (warp - EPI_WARP0) >> 2;
+          unsigned long long* dst = epi.cand + (int64_t)((row0 + lane) / ROWDIV) * epi.ldcand +
+                                    (int64_t)(stripe * 2 + half) * epi.k;
+          for (int j = 0; j < epi.k; ++j) dst[j] = j < tcnt ? tlist[j * 32 + lane] : ~0ull;
+        }
+      }
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -801,7 +935,9 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
     ok = ok && make_operand_map(&mA[p], A.plane(p), M, K, A.ld, BM);
     ok = ok && make_operand_map(&mW[p], W.plane(p), N, K, W.ld, BN / 2);
   }
-  if (PLANES == 1) {
+  if constexpr (epi_topk<Epi>::value) {  // no output tensor: the lists go to epi.cand
+    mO[0] = mO[1] = mO[2] = mA[0];
+  } else if (PLANES == 1) {
     ok = ok && make_map(&mO[0], o.f32, false, o.rows, o.cols, o.ld, 32 / ROWDIV, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     mO[1] = mO[2] = mO[0];
   } else {
@@ -816,11 +952,16 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   static unsigned long long attr = 0;
   smem_attr_once(kern, Layout<BN, Epi::PLANES == 3>::TOTAL, attr);
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
-  if (sc.s_tail <= 1 || !sc.ws || !sc.cnt) {
+  if (sc.s_tail <= 1 || !sc.ws || !sc.cnt || epi_topk<Epi>::value) {
     sc.full = tiles;
     sc.s_tail = 1;
   }
-  const int units = sc.full + (tiles - sc.full) * sc.s_tail;
+  if constexpr (epi_topk<Epi>::value) {
+    const int nt = (N + BN - 1) / BN;
+    sc.n_stripes = std::max(1, std::min(sc.n_stripes, nt));
+  }
+  const int units = epi_topk<Epi>::value ? ((M + 2 * BM - 1) / (2 * BM)) * sc.n_stripes
+                                         : sc.full + (tiles - sc.full) * sc.s_tail;
   const int clusters = units < max_clusters ? units : max_clusters;
   if (sc.group_m == 0) sc.group_m = gemm_group_m();
   cudaLaunchConfig_t cfg = {};
@@ -901,6 +1042,57 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allo
     }
   }
   return best;
+}
+
+// Fused top-k launch plan: tile width and the number of N stripes (units = M blocks x stripes,
+// each unit's tiles run back to back on one cluster; <= 64 stripes: a row's 2 x stripes lists
+// are merged by one warp holding 4 list heads per lane).  Cost = rounds over the clusters x the longest stripe's
+// K-blocks (same per-K-block model as plan_gemm) + a per-unit list flush.
+struct PlanTopk {
+  int bn, n_stripes;
+};
+inline PlanTopk plan_gemm_topk(int64_t M, int64_t N, int64_t K, int min_tiles) {
+  static const int force_s = [] { const char* e = getenv("KGQ_TOPK_STRIPES"); return e ? atoi(e) : 0; }();
+  static const int force_bn = [] { const char* e = getenv("KGQ_TOPK_BN"); return e ? atoi(e) : 0; }();
+  const int64_t pairs_m = (M + 2 * BM - 1) / (2 * BM);
+  const int nk = (int)((K + BK - 1) / BK);
+  const int cl = gemm_clusters();
+  PlanTopk best{256, 1};
+  double best_cost = 1e300;
+  for (int bn : {128, 192, 256}) {
+    if (force_bn && bn != force_bn) continue;
+    const double kb = kKbUs[bn == 128 ? 1 : bn == 192 ? 3 : 4];
+    const int nt = (int)((N + bn - 1) / bn);
+    for (int s = 1; s <= std::min(64, std::max(1, nt / std::max(1, min_tiles))); ++s) {
+      if (force_s && s != std::min(force_s, nt)) continue;
+      // static round-robin of units over the clusters: the busiest cluster runs `rounds` units
+      // of nt / s tiles on average (stripes are balanced to floor / ceil)
+      const int64_t units = pairs_m * s;
+      const int64_t rounds = (units + cl - 1) / cl;
+      const double per = (double)nt / s;
+      const double cost = kC0Us + (double)rounds * (per * nk * kb + 1.0);  // + list warm-up and flush per unit
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        best = PlanTopk{bn, s};
+      }
+    }
+  }
+  return best;
+}
+
+template <class Epi>
+int launch_gemm_topk(const Split& A, int M, const Split& W, int N, int K, const Epi& epi, const GemmWs* ws,
+                     cudaStream_t st, int* n_stripes_out, int min_tiles) {
+  const PlanTopk p = plan_gemm_topk(M, N, K, min_tiles);
+  Sched sc{0, 1, (K + BK - 1) / BK, nullptr, nullptr, ws && ws->kt ? ws->kt + 8 : nullptr};
+  sc.n_stripes = std::min(p.n_stripes, (N + p.bn - 1) / p.bn);
+  *n_stripes_out = sc.n_stripes;
+  const OutDesc o{nullptr, 0, Split{}, 0, 0};
+  switch (p.bn) {
+    case 128: return launch_gemm<128>(A, M, W, N, K, o, epi, st, sc);
+    case 192: return launch_gemm<192>(A, M, W, N, K, o, epi, st, sc);
+    default: return launch_gemm<256>(A, M, W, N, K, o, epi, st, sc);
+  }
 }
 
 template <class Epi>

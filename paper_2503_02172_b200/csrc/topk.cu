@@ -488,6 +488,89 @@ int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t 
   return 1;
 }
 
+// ---- merge of the fused scorer's lists (score_tc.cu EpiBetaScore<NB, true>) -----------------
+// Output row b has nl (<= 128) sorted lists of k (order key << 32 | shard column) keys, ~0-padded
+// -- one per (N stripe, column half) of the tensor-core scorer -- at cand[b * ldcand + l * k].  One
+// warp per row: lane l holds the heads of lists l + 32 j, k rounds of warp arg-min, the winner
+// advances its list.  The
+// columns of different lists are disjoint, so keys are unique and the result is exactly the first
+// k of the row in (distance, id) order.  Rows [0, rows1) have nl1 lists, the rest nl2 (mixed
+// batches: non-union then union scorer launch).
+__global__ void __launch_bounds__(128)
+    k_topk_lists(const unsigned long long* __restrict__ cand, int64_t ldcand, int k, int rows1, int nl1, int nl2,
+                 int64_t id_base, const int32_t* __restrict__ invalid, const int32_t* __restrict__ out_row,
+                 float* __restrict__ od, int32_t* __restrict__ oi, int B, const PeerPush pp) {
+  pdl_grid_sync();
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const int ob = out_row ? out_row[b] : b;
+  od += (int64_t)ob * k;
+  oi += (int64_t)ob * k;
+  if (invalid && invalid[ob]) {
+    if (lane < k) {
+      od[lane] = __uint_as_float(0x7FFFFFFFu);
+      oi[lane] = -1;
+    }
+    if (pp.on()) peer_push_warp(pp, ob, k, ~0ull, lane);
+    return;
+  }
+  const int nl = b < rows1 ? nl1 : nl2;
+  // lane l holds the heads of lists l, l + 32, l + 64, l + 96 (<= 128 lists)
+  const unsigned long long* row = cand + (int64_t)b * ldcand;
+  int pos[4];
+  unsigned long long head[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    pos[j] = 0;
+    head[j] = lane + 32 * j < nl ? row[(int64_t)(lane + 32 * j) * k] : ~0ull;
+  }
+  unsigned long long key = ~0ull;  // output j = lane
+  for (int j = 0; j < k; ++j) {
+    unsigned long long mine = head[0];
+#pragma unroll
+    for (int q = 1; q < 4; ++q) mine = head[q] < mine ? head[q] : mine;
+    unsigned long long w = mine;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, w, o);
+      w = t < w ? t : w;
+    }
+    if (lane == j) key = w;
+    if (w == ~0ull) break;  // fewer than k entities
+    if (mine == w) {        // unique keys: exactly one head of one lane
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (head[q] == w) {
+          ++pos[q];
+          head[q] = pos[q] < k ? row[(int64_t)(lane + 32 * q) * k + pos[q]] : ~0ull;
+        }
+    }
+  }
+  unsigned long long gk = ~0ull;
+  if (lane < k) {
+    if (key == ~0ull) {
+      od[lane] = __uint_as_float(0x7FFFFFFFu);
+      oi[lane] = -1;
+    } else {
+      const uint32_t gid = (uint32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
+      od[lane] = fkey_inv((uint32_t)(key >> 32));
+      oi[lane] = (int32_t)gid;
+      gk = (key & 0xFFFFFFFF00000000ull) | gid;
+    }
+  }
+  if (pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
+}
+
+int launch_topk_lists(const unsigned long long* cand, int64_t ldcand, int k, int B, int rows1, int nl1, int nl2,
+                      int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d, int32_t* out_i,
+                      cudaStream_t st, const PeerPush& pp) {
+  if (B <= 0) return 0;
+  launch_pdl(k_topk_lists, dim3((B + 3) / 4), dim3(128), 0, st, cand, ldcand, k, rows1, nl1, nl2, id_base, invalid,
+             out_row, out_d, out_i, B, pp);
+  return 1;
+}
+
 int launch_topk_cmin_map(const float* dist, int64_t ldd, const float* cmin, int64_t ldc, int B, int64_t n,
                          int k, int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d,
                          int32_t* out_i, cudaStream_t st, const PeerPush& pp) {

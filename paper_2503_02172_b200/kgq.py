@@ -40,7 +40,7 @@ EXPORTS = (
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
     "kgq_profile_read", "kgq_rank_answers", "kgq_peer_bytes", "kgq_set_peers", "kgq_merge_peers",
     "kgq_query_range", "kgq_nccl_unique_id", "kgq_comm_init", "kgq_comm_destroy", "kgq_rank_metrics",
-    "kgq_ktime_enable", "kgq_ktime_read", "kgq_ktime_log",
+    "kgq_ktime_enable", "kgq_ktime_read", "kgq_ktime_log", "kgq_set_option",
 )
 RANK_LOCAL, RANK_DIST, RANK_COUNT, RANK_FILTERED = 0, 1, 2, 3
 SPLIT_ENTITIES, SPLIT_QUERIES = 0, 1
@@ -102,6 +102,7 @@ _sig = {
     "kgq_ktime_enable": (_I32, [_P, _I32]),
     "kgq_ktime_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
     "kgq_ktime_log": (_I64, [_P, _P, _I64]),
+    "kgq_set_option": (_I32, [_P, _I32, _I64]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -466,6 +467,11 @@ class Engine:
         out = torch.empty((3, self.dim, ns), dtype=torch.float32, device=f"cuda:{self.device}")
         self._check(_lib.kgq_entity_terms(self._h, _ptr(out), _stream(stream)))
         return out
+
+    def set_fused_topk(self, mode: str):
+        """kgq_set_option(KGQ_OPT_FUSED_TOPK): "off" (write the distance block), "on" (fuse the top-k
+        into the BetaE tensor-core scorer whenever eligible), "auto" (default)."""
+        self._check(_lib.kgq_set_option(self._h, 1, {"off": 0, "on": 1, "auto": 2}[mode]))
 
     def ktime(self, on: bool = True):
         """In-kernel launch spans of the tcgen05 GEMM (kgq_ktime_enable)."""

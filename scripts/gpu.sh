@@ -8,6 +8,10 @@
 #   reference  bench.py --impl reference (the oracle arm)
 #   suite      bench.py --workload suite (the other BASELINE configs)
 #   launches   ncu launch list of one bench step (gpu__time_duration, DRAM bytes per launch)
+#   launches-warm  the same launch list with warm caches (--cache-control none)
+#   ncu-small  ncu --set full of one mixed step's small kernels (gather / scatter / combine / score prep / top-k)
+#   ncu-score  ncu --set full of the two BetaE scorer launches of one mixed step
+#   quick      the default bench line without the side measurements (one summary line)
 #   ncu-gemm   ncu --set full of k_gemm launches of one bench step (a dense layer + the scorer)
 #   ncu-c5a    ncu --set full of the C5a streaming scorer (GQE 1p, B = 8)
 #   sanitize   compute-sanitizer memcheck / racecheck / synccheck on small configs
@@ -29,6 +33,15 @@ for task in "$@"; do
     suite) timeout 1500 python bench.py --workload suite --steps 5 --warmup 2 > $OUT/suite.jsonl 2> $OUT/suite.err ;;
     launches) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
                 --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-mixed --no-c5a > /dev/null 2>&1 ;;
+    launches-warm) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+                --cache-control none --csv --log-file $OUT/launches_warm.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
+                --no-per-type --no-c5a > /dev/null 2>&1 ;;
+    ncu-small) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_mix_score_prep|k_mix_gather|k_topk_cmin|k_mix_scatter|k_mix_combine" \
+                -s 11 -c 11 -o $OUT/prof_small -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-per-type --no-c5a > /dev/null 2>&1 ;;
+    ncu-score) timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:EpiBetaScore -s 2 -c 2 \
+                -o $OUT/prof_score -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-per-type --no-c5a > /dev/null 2>&1 ;;
+    quick) timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-per-type --no-c5a > $OUT/quick.json 2> $OUT/quick.err
+           python -c "import json; d=json.load(open('$OUT/quick.json')); p=d['roofline']['parts']; print('quick', round(d['value']), round(d['ms_per_step'], 3), 'dense', round(p['dense']['tflops'], 1), 'score', round(p['score']['tflops'], 1), p['score']['ms_per_step'])" ;;
     ncu-gemm) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 30 -c 4 -o $OUT/prof_gemm -f \
                 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-mixed --no-c5a --streams 1 > /dev/null 2>&1 ;;
     ncu-c5a) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score_stream -s 2 -c 1 -o $OUT/prof_c5a -f \

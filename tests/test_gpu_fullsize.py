@@ -48,12 +48,53 @@ def test_full_size_sampled(cfg):
         for j, b in enumerate(rows):
             assert_topk_ok(td[b], ti[b], ref[j], 10, what=f"{name} {s} row {b}")
         # whole distance rows at the real K = 800 contraction (north_star: 1e-4 relative)
-        _, _, sd = e.submit(s, dev(a), dev(r), 10, shard_dist=True)
+        bd, bi, sd = e.submit(s, dev(a), dev(r), 10, shard_dist=True)
         assert_dist_close(sd[torch.from_numpy(rows).cuda()].cpu().numpy(), ref, what=f"{name} {s} full rows")
+        # BetaE: the first submit took the fused top-k (per-stripe lists in the scorer epilogue,
+        # no distance block), this one the distance block + block-minima top-k: same values, so
+        # the whole batch's top-k must agree bit for bit
+        np.testing.assert_array_equal(bi.cpu().numpy(), ti, err_msg=f"{name} {s} fused vs block top-k ids")
+        np.testing.assert_array_equal(bd.cpu().numpy(), td, err_msg=f"{name} {s} fused vs block top-k dists")
         qe = e.query_embedding(s, dev(a), dev(r)).cpu().numpy()[rows]
         ref_q = m.query_embedding(s, a[rows], r[rows])
         # chain at H = 1600: the same per-structure bounds as the small configs
         assert_embedding_close(qe, ref_q, rel=chain_tolerance(s, "kgr-init", model), what=f"{name} {s} chain")
+
+
+def test_full_size_mixed_step_as_benched():
+    """bench.py's headline step: ONE kgq_submit_mixed of all 14 BetaE types x 1024 queries at the
+    FB15k-237 shape (the same tables, queries and launch configuration the bench times; the
+    scorer launch of the 12,288 single-branch rows takes the fused top-k under AUTO).  Sampled rows
+    of every type against the oracle (tie-aware top-k), and the whole batch bit for bit against
+    the same submit with the fused top-k OFF (distance block + block-minima top-k)."""
+    N, R, d, H, B = 14505, 237, 400, 1600, 1024
+    seed = 2503_02172 + 1
+    t = synth.make_tables("betae", N, R, d, hidden=H, seed=seed)
+    e = Engine("betae", N, R, d, hidden=H, max_batch=14 * B, max_k=16)
+    e.load_tables(t)
+    m = O.Model("betae", t, dim=d)
+    qs = [synth.make_queries(s, B, N, R, seed=synth.query_seed(seed, s)) for s in synth.STRUCTURES]
+    a = dev(np.concatenate([q[0].reshape(-1) for q in qs]).astype(np.int32))
+    r = dev(np.concatenate([q[1].reshape(-1) for q in qs]).astype(np.int32))
+    out = (torch.empty((14 * B, 10), device="cuda"), torch.empty((14 * B, 10), dtype=torch.int32, device="cuda"))
+    res = {}
+    for mode in ("auto", "off"):
+        e.set_fused_topk(mode)
+        for _ in range(3):  # eager, capture, replay (the bench times replays)
+            e.submit_mixed_packed(list(synth.STRUCTURES), [B] * 14, a, r, 10, out)
+        e.check_errors()
+        res[mode] = (out[0].cpu().numpy().copy(), out[1].cpu().numpy().copy())
+    np.testing.assert_array_equal(res["auto"][1], res["off"][1])
+    np.testing.assert_array_equal(res["auto"][0], res["off"][0])
+    td, ti = res["auto"]
+    assert np.all(np.isfinite(td))
+    rng = np.random.default_rng(3)
+    for i, s in enumerate(synth.STRUCTURES):
+        rows = np.unique(np.r_[0, rng.integers(0, B), B - 1])
+        ref = m.scores(s, qs[i][0][rows], qs[i][1][rows])
+        for j, b in enumerate(rows):
+            assert_topk_ok(td[i * B + b], ti[i * B + b], ref[j], 10, what=f"mixed full-size {s} row {b}")
+    e.close()
 
 
 def test_2m_entity_table_gqe_and_betae():

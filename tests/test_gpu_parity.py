@@ -365,13 +365,16 @@ def test_filtered_ranks_planted_and_sharded():
                 e.close()
 
 
-@pytest.mark.parametrize("N,k,model", [(5000, 10, "gqe"), (5000, 32, "gqe"), (40000, 16, "gqe"),
-                                       (5000, 10, "betae"), (3000, 32, "betae")])
-def test_topk_heavy_ties(N, k, model):
+@pytest.mark.parametrize("N,k,model,fused", [(5000, 10, "gqe", "auto"), (5000, 32, "gqe", "auto"),
+                                             (40000, 16, "gqe", "auto"), (5000, 10, "betae", "off"),
+                                             (3000, 32, "betae", "auto"), (5000, 10, "betae", "on"),
+                                             (20000, 16, "betae", "on")])
+def test_topk_heavy_ties(N, k, model, fused):
     """Q13/Q15 with massive exact ties: 7 distinct entity rows repeated over the table, so every
     query has ~N/7 entities at exactly its best distance (bit-identical: same row, same
     arithmetic).  The top-k must be those ties in ascending id order -- the filter buffer of
-    the top-k kernel overflows and folds many times; N > 32k also takes the chunked path."""
+    the top-k kernel overflows and folds many times; N > 32k also takes the chunked path; BetaE
+    with k <= 16 takes the fused per-stripe lists of the scorer epilogue."""
     d, R, B = 16, 4, 20   # BetaE: 20 query rows take the tensor-core scorer + block-minima top-k
     rng = np.random.default_rng(5)
     w = d if model == "gqe" else 2 * d
@@ -380,6 +383,7 @@ def test_topk_heavy_ties(N, k, model):
     t = synth.make_tables(model, N, R, d, hidden=8, seed=3)
     t["entity"] = pat[which].copy()
     e = Engine(model, N, R, d, hidden=8, max_batch=B, max_k=32)
+    e.set_fused_topk(fused)
     e.load_tables(t)
     m = O.Model(model, t, dim=d)
     a, r = synth.make_queries("1p", B, N, R, seed=4)
@@ -394,6 +398,98 @@ def test_topk_heavy_ties(N, k, model):
         np.testing.assert_array_equal(ti[b], ties[:k], err_msg=f"row {b}: tied ids not ascending")
         assert np.all(td[b] == td[b][0])
     e.close()
+
+
+@pytest.mark.parametrize("s", ["1p", "3in", "up", "pni", "2u", "ip"])
+def test_fused_topk_matches_distance_block_path(s):
+    """the BetaE tensor-core scorer keeps every row's k smallest (dist, id) per N
+    stripe in its epilogue (no [B, N] distance block; k <= 16) and a warp merge of the stripe
+    lists gives the top-k.  Checked against the oracle, and bit for bit against the same submit
+    with shard_dist (distance block written, block-minima top-k), for k = 1, 10, 16 and a batch
+    of 61 queries (ragged 256-row blocks; fused forced ON, so the planner cuts the 1000-entity
+    table into many stripes: up to 2 x 8 lists per row)."""
+    e, m, t = engine("betae", max_batch=64)
+    e.set_fused_topk("on")
+    a, r = synth.make_queries(s, 61, SMALL["N"], SMALL["R"], seed=synth.query_seed(29, s))
+    ref = m.scores(s, a, r)
+    for k in (1, 10, 16):
+        fd, fi = e.submit(s, dev(a), dev(r), k)
+        bd, bi, _ = e.submit(s, dev(a), dev(r), k, shard_dist=True)
+        e.check_errors()
+        assert torch.equal(fi, bi), (s, k)
+        assert torch.equal(fd, bd), (s, k)
+        fd, fi = fd.cpu().numpy(), fi.cpu().numpy()
+        for b in range(61):
+            assert_topk_ok(fd[b], fi[b], ref[b], k, what=f"fused {s} k={k} row {b}")
+    e.set_fused_topk("auto")
+
+
+def test_fused_topk_many_stripes_and_option():
+    """A 20,000-entity table with fused top-k forced ON: the planner cuts up to 64 stripes (128
+    lists per row, four list heads per lane in the merge).  Bit-identical to the same context with
+    the option OFF (distance block + block-minima top-k), through eager, captured and replayed
+    submits (set_option re-captures the graphs), and checked against the oracle."""
+    N, R, d = 20000, 10, 24
+    t = synth.make_tables("betae", N, R, d, hidden=40, seed=12)
+    m = O.Model("betae", t, dim=d)
+    e = Engine("betae", N, R, d, hidden=40, max_batch=64, max_k=16)
+    e.load_tables(t)
+    for s in ("1p", "up"):
+        a, r = synth.make_queries(s, 40, N, R, seed=77)
+        outs = {}
+        for mode in ("on", "off", "on"):
+            e.set_fused_topk(mode)
+            for _ in range(3):  # eager, capture, replay
+                od, oi = e.submit(s, dev(a), dev(r), 16)
+            outs.setdefault(mode, []).append((od.clone(), oi.clone()))
+        e.check_errors()
+        for od, oi in outs["on"]:
+            assert torch.equal(oi, outs["off"][0][1]) and torch.equal(od, outs["off"][0][0]), s
+        ref = m.scores(s, a, r)
+        od, oi = outs["on"][0][0].cpu().numpy(), outs["on"][0][1].cpu().numpy()
+        for b in range(40):
+            assert_topk_ok(od[b], oi[b], ref[b], 16, what=f"many stripes {s} row {b}")
+    from paper_2503_02172_b200 import kgq as K
+    with pytest.raises(KgqError, match="EINVAL"):  # a value outside OFF / ON / AUTO
+        e._check(K._lib.kgq_set_option(e._h, 1, 7))
+    with pytest.raises(KgqError, match="EINVAL"):  # an unknown option
+        e._check(K._lib.kgq_set_option(e._h, 99, 0))
+    e.close()
+
+
+def test_fused_topk_invalid_rows_and_tiny_table():
+    """Fused top-k edge cases: a query with an out-of-range relation gets NaN / -1 (the other
+    rows exact), and k = N on a 9-entity table (one ragged tile, most stripe lists padding)
+    returns every entity in (distance, id) order."""
+    e, m, t = engine("betae", max_batch=64)
+    e.set_fused_topk("on")
+    a, r = synth.make_queries("2p", 40, SMALL["N"], SMALL["R"], seed=3)
+    r = r.copy()
+    r[7, 1] = SMALL["R"] + 5
+    td, ti = e.submit("2p", dev(a), dev(r), 12)
+    with pytest.raises(KgqError, match="ERANGE"):
+        e.check_errors()
+    td, ti = td.cpu().numpy(), ti.cpu().numpy()
+    assert np.all(np.isnan(td[7])) and np.all(ti[7] == -1)
+    ok = [b for b in range(40) if b != 7]
+    ref = m.scores("2p", a[ok], r[ok])
+    for j, b in enumerate(ok):
+        assert_topk_ok(td[b], ti[b], ref[j], 12)
+    e.set_fused_topk("auto")
+    N = 9
+    t9 = synth.make_tables("betae", N, 5, 24, hidden=32, seed=4)
+    e9 = Engine("betae", N, 5, 24, hidden=32, max_batch=32, max_k=16)
+    e9.set_fused_topk("on")
+    e9.load_tables(t9)
+    a9, r9 = synth.make_queries("up", 30, N, 5, seed=6)
+    td, ti = e9.submit("up", dev(a9), dev(r9), N)
+    e9.check_errors()
+    td, ti = td.cpu().numpy(), ti.cpu().numpy()
+    ref9 = O.Model("betae", t9, dim=24).scores("up", a9, r9)
+    for b in range(30):
+        assert_topk_ok(td[b], ti[b], ref9[b], N, what=f"k = N row {b}")
+        assert sorted(ti[b].tolist()) == list(range(N))
+    e9.close()
 
 
 def test_betae_out_of_range_relation_at_later_hop():
@@ -417,12 +513,13 @@ def test_betae_out_of_range_relation_at_later_hop():
         assert_topk_ok(td[b], ti[b], ref[j], 5)
 
 
-@pytest.mark.parametrize("model", ["betae", "gqe"])
-def test_mixed_structure_batch(model):
+@pytest.mark.parametrize("model,fused", [("betae", "auto"), ("betae", "on"), ("gqe", "auto")])
+def test_mixed_structure_batch(model, fused):
     """kgq_submit_mixed: several structures in one call.  BetaE runs them
     level-synchronously (hops of all groups batched into one MLP, one scorer, one top-k), GQE
     group by group; every group's rows must match the oracle like a plain submit."""
     e, m, t = engine(model, max_batch=256)
+    e.set_fused_topk(fused)
     N, R = SMALL["N"], SMALL["R"]
     structs = STRUCTS[model]
     groups, refs = [], []
@@ -440,6 +537,7 @@ def test_mixed_structure_batch(model):
             assert_topk_ok(td[q + b], ti[q + b], ref[b], 10, what=f"mixed {model} {s} row {b}")
         q += a.shape[0]
     assert q == td.shape[0]
+    e.set_fused_topk("auto")
 
 
 def test_mixed_batch_out_of_range_and_equivalence():
