@@ -156,7 +156,16 @@ __global__ void k_mix_gather(MixSegs sg, const float* __restrict__ ent, Split S,
       if (threadIdx.x == 0) report_range(err, invalid, q, g.aslot, 0);
       a = 0;
     }
-    for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) store_split(Z, zrow + j, ent[(int64_t)a * 2 * d + j]);
+    const float* er = ent + (int64_t)a * 2 * d;
+    if ((d & 3) == 0 && (Z.ld & 7) == 0) {  // 8 elements per thread: two float4 loads, 16-byte plane stores
+      for (int j = 8 * threadIdx.x; j < 2 * d; j += 8 * blockDim.x) {
+        const float4 x0 = *reinterpret_cast<const float4*>(er + j), x1 = *reinterpret_cast<const float4*>(er + j + 4);
+        const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        store_split8(Z, zrow + j, x);
+      }
+    } else {
+      for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) store_split(Z, zrow + j, er[j]);
+    }
   } else {  // split -> split: a plane-wise copy, 16-byte vectors when aligned
     const Split& src = g.kind == 1 ? S : Mst;
     const int64_t srow = (g.src0 + b) * src.ld;

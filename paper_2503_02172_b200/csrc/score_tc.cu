@@ -134,12 +134,25 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
   const double inv = 1.0 / (double)ns;
   const int64_t srow = srcrow ? srcrow[r] : (int64_t)(r % nout) * B + b0 + r / nout;
   const int64_t s0 = srow * S.ld, a0 = (int64_t)r * A.ld;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    const float a = load_split(S, s0 + j), b = load_split(S, s0 + d + j);
-    store_split(A, a0 + j, a);
-    store_split(A, a0 + d + j, b);
-    const double da = a, db = b;
-    p += lnbeta_f64_tab(da, db, tab, tab + kLogTab) + da * sums[j] * inv + db * sums[d + j] * inv;
+  if ((d & 7) == 0 && (S.ld & 7) == 0 && (A.ld & 7) == 0) {
+    // the row copy as 16-byte plane accesses (a plain copy of the split planes), then the fp64
+    // P_q terms from the fp32 values
+    for (int j = 8 * threadIdx.x; j < 2 * d; j += 8 * blockDim.x)
+#pragma unroll
+      for (int p3 = 0; p3 < 3; ++p3)
+        *reinterpret_cast<uint4*>(A.plane(p3) + a0 + j) = *reinterpret_cast<const uint4*>(S.plane(p3) + s0 + j);
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const double da = load_split(S, s0 + j), db = load_split(S, s0 + d + j);
+      p += lnbeta_f64_tab(da, db, tab, tab + kLogTab) + da * sums[j] * inv + db * sums[d + j] * inv;
+    }
+  } else {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const float a = load_split(S, s0 + j), b = load_split(S, s0 + d + j);
+      store_split(A, a0 + j, a);
+      store_split(A, a0 + d + j, b);
+      const double da = a, db = b;
+      p += lnbeta_f64_tab(da, db, tab, tab + kLogTab) + da * sums[j] * inv + db * sums[d + j] * inv;
+    }
   }
   p = warp_sum(p);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;

@@ -216,6 +216,20 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t da, uint6
       "}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
+// Same MMA with an A-collector hint (tcgen05.mma ... .collector::a::{fill,use,lastuse}): the
+// tensor core keeps the A slice it read in its collector buffer and the following MMAs of the
+// same A re-use it instead of re-reading shared memory.
+#define KGQ_MMA_COLLECTOR(NAME, Q)                                                                         \
+  __device__ __forceinline__ void NAME(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,          \
+                                       uint32_t accumulate) {                                              \
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"                                             \
+                 "tcgen05.mma.cta_group::2.kind::f16" Q " [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),         \
+                 "l"(da), "l"(db), "r"(idesc), "r"(accumulate));                                          \
+  }
+KGQ_MMA_COLLECTOR(mma_bf16_2sm_afill, ".collector::a::fill")
+KGQ_MMA_COLLECTOR(mma_bf16_2sm_ause, ".collector::a::use")
+KGQ_MMA_COLLECTOR(mma_bf16_2sm_alast, ".collector::a::lastuse")
+#undef KGQ_MMA_COLLECTOR
 // A operand from TMEM ("ts" form): D[tmem] (+)= A[tmem] . B[smem]; tmem_a = the A slice's first
 // column (128 lanes = this CTA's rows, 8 columns = 16 bf16 of K per lane).
 __device__ __forceinline__ void mma_bf16_2sm_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
@@ -278,6 +292,9 @@ constexpr int DRAIN = KGQ_TC_DRAIN;
 // tensor map's box -- then the barriers.
 #ifndef KGQ_TC_ATMEM
 #define KGQ_TC_ATMEM 0
+#endif
+#ifndef KGQ_TC_COLLECTOR  // A-grouped MMA order with collector re-use (see the MMA issuer)
+#define KGQ_TC_COLLECTOR 1
 #endif
 template <int BN, bool NBUF2 = false>
 struct Layout {
@@ -632,6 +649,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               mma_bf16_2sm_ts(d, t0, umma_desc_sw64(w1 + off), idesc, 1u);
               mma_bf16_2sm_ts(d, t1, umma_desc_sw64(w0 + off), idesc, 1u);
               mma_bf16_2sm_ts(d, t0, umma_desc_sw64(w0 + off), idesc, 1u);
+            }
+          } else if constexpr (KGQ_TC_COLLECTOR) {
+            // A-grouped order with collector re-use: each A plane is read from shared memory
+            // once per K16 step (3 reads instead of 6) -- less SMEM traffic and power for the
+            // same MMAs; small terms still first, x0 w0 last
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t off = kk * 32;
+              mma_bf16_2sm(d, umma_desc_sw64(a2 + off), umma_desc_sw64(w0 + off), idesc, (first && kk == 0) ? 0u : 1u);
+              mma_bf16_2sm_afill(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w1 + off), idesc, 1u);
+              mma_bf16_2sm_alast(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w0 + off), idesc, 1u);
+              mma_bf16_2sm_afill(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w2 + off), idesc, 1u);
+              mma_bf16_2sm_ause(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w1 + off), idesc, 1u);
+              mma_bf16_2sm_alast(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w0 + off), idesc, 1u);
             }
           } else {
 #pragma unroll
