@@ -35,6 +35,13 @@ for s in ("1p", "3in", "up", "pni"):
 groups = [(s, dev(a), dev(r)) for s, (a, r) in
           ((s, synth.make_queries(s, 20 + 3 * i, N, R, seed=40 + i)) for i, s in enumerate(("2p", "ip", "2u-DM")))]
 case("betae mixed", lambda: e.submit_mixed(groups, 10))
+# fused top-k (per-stripe lists in the scorer epilogue + list merge): forced ON, many stripes
+e.set_fused_topk("on")
+for s in ("1p", "up"):
+    a, r = synth.make_queries(s, B, N, R, seed=5)
+    case(f"betae {s} fused top-k", lambda: e.submit(s, dev(a), dev(r), 10))
+case("betae mixed fused top-k", lambda: e.submit_mixed(groups, 10))
+e.set_fused_topk("auto")
 e.check_errors()
 e.close()
 
