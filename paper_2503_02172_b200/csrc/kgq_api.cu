@@ -255,16 +255,16 @@ void check_site(const char* site) {
 
 // dense layer into a split (bf16x3) state, or into an fp32 buffer [M, ld]
 int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, const Split& out, int neg0,
-          int neg1, cudaStream_t st) {
+          int neg1, cudaStream_t st, const GemmWs* ws = nullptr) {
   StageTimer t(ctx, st, kStDense, 2.0 * M * (double)L.out_f * K);
-  const int r = launch_linear(A, M, K, L, epi, out, nullptr, 0, neg0, neg1, &ctx->gws, st);
+  const int r = launch_linear(A, M, K, L, epi, out, nullptr, 0, neg0, neg1, ws ? ws : &ctx->gws, st);
   check_site("dense layer");
   return r;
 }
 int dense(kgq_ctx* ctx, const Split& A, int M, int K, const Linear& L, int epi, float* out, int64_t ld,
-          cudaStream_t st) {
+          cudaStream_t st, const GemmWs* ws = nullptr) {
   StageTimer t(ctx, st, kStDense, 2.0 * M * (double)L.out_f * K);
-  const int r = launch_linear(A, M, K, L, epi, Split{}, out, ld, 0, 0, &ctx->gws, st);
+  const int r = launch_linear(A, M, K, L, epi, Split{}, out, ld, 0, 0, ws ? ws : &ctx->gws, st);
   check_site("dense layer");
   return r;
 }
@@ -584,7 +584,10 @@ void kgq_destroy(kgq_ctx* ctx) {
   F(ctx->mix_rid); F(ctx->mix_map);
   if (ctx->mix_map_host) cudaFreeHost(ctx->mix_map_host);
   if (ctx->mix_map_ev) cudaEventDestroy(ctx->mix_map_ev);
-  F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt);
+  for (auto& e : ctx->side_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->side_st) cudaStreamDestroy(ctx->side_st);
+  F(ctx->uvsums); F(ctx->Atc.b0); F(ctx->Ptc); F(ctx->gws.ws); F(ctx->gws.cnt); F(ctx->gws2.ws); F(ctx->gws2.cnt);
   F(ctx->d_anchor_stage); F(ctx->d_rel_stage); F(ctx->d_topd_stage); F(ctx->d_topi_stage); F(ctx->d_epoch);
   if (ctx->comm) nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
   F(ctx->cm_d); F(ctx->cm_i); F(ctx->cg_d); F(ctx->cg_i); F(ctx->kt_buf);
@@ -730,6 +733,10 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   if (!st) st = dalloc(ctx, &ctx->gws.ws, kGemmWsFloats, "gemm split workspace");
   if (!st) st = dalloc(ctx, &ctx->gws.cnt, (size_t)kGemmCntInts, "gemm split counters");
   if (!st) CK(cudaMemset(ctx->gws.cnt, 0, kGemmCntInts * sizeof(int)), "gemm split counters");
+  // the side stream's own split-K workspace (mixed path: two row halves' GEMMs run concurrently)
+  if (!st) st = dalloc(ctx, &ctx->gws2.ws, kGemmWsFloats, "gemm split workspace (side)");
+  if (!st) st = dalloc(ctx, &ctx->gws2.cnt, (size_t)kGemmCntInts, "gemm split counters (side)");
+  if (!st) CK(cudaMemset(ctx->gws2.cnt, 0, kGemmCntInts * sizeof(int)), "gemm split counters (side)");
   if (!st) st = dalloc(ctx, &ctx->score_tab, (size_t)((c.model == KGQ_BETAE ? 3 : 1) * d * ctx->np), "score table");
   if (!st) st = dalloc(ctx, &ctx->d_anchor_stage, (size_t)(Bm * kMaxBranches), "staging");
   if (!st) st = dalloc(ctx, &ctx->d_rel_stage, (size_t)(Bm * kMaxBranches), "staging");
@@ -1068,35 +1075,85 @@ struct MixGroup {
 };
 }  // namespace
 
-// one MLP over a hop batch (segments already describe the batch rows); negated rows are last
+// The projection MLP (Eq. 4) over rows [r0, r0 + M) of a hop batch already gathered into Z
+// (relation ids in mix_rid); rows >= neg0 (batch-relative) are negated.  On `st` with split-K
+// workspace / span group `ws`.
+static int mlp_rows(kgq_ctx* ctx, int r0, int M, int neg0, cudaStream_t st, const GemmWs* ws) {
+  const int d = ctx->cfg.dim;
+  int L = 0;
+  RelTerm rt;
+  rt.RW = ctx->RW;
+  rt.ldrw = ctx->cfg.hidden;
+  rt.M = M;
+  rt.rid = ctx->mix_rid + r0;
+  {
+    StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
+    L += launch_linear_rel(ctx->Z.at(r0), M, 2 * d, ctx->lin1x, rt, ctx->H[0].at(r0), ws, st);
+  }
+  Split A = ctx->H[0].at(r0);
+  int K = ctx->lin1x.out_f;
+  for (int l = 1; l < ctx->cfg.n_hidden_layers; ++l) {
+    const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
+    L += dense(ctx, A, M, K, lin, kEpiRelu, ctx->H[l & 1].at(r0), 0, 0, st, ws);
+    A = ctx->H[l & 1].at(r0);
+    K = lin.out_f;
+  }
+  const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
+  const int ng = std::max(0, std::min(neg0 - r0, M));  // negated rows of this range: [ng, M)
+  if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
+    float* T = ctx->T + (int64_t)r0 * 2 * d;
+    L += dense(ctx, A, M, K, lo, kEpiNone, T, 2 * d, st);
+    L += launch_softmax_terminal(T, 2 * d, M, 2 * d, ctx->I.at(r0), 0, ng, M, st);
+  } else {
+    L += dense(ctx, A, M, K, lo, kEpiBetaReg, ctx->I.at(r0), ng, M, st, ws);
+  }
+  return L;
+}
+
+// KGQ_NO_SPLIT_MLP=1: every hop MLP as one chain of launches on the context's stream
+static bool split_mlp_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("KGQ_NO_SPLIT_MLP");
+    return !(e && e[0] && e[0] != '0');
+  }();
+  return v;
+}
+static bool side_stream(kgq_ctx* ctx) {  // lazily created; false if CUDA refuses
+  if (ctx->side_st && ctx->side_ev[0] && ctx->side_ev[1]) return true;
+  if (!ctx->side_st && cudaStreamCreateWithFlags(&ctx->side_st, cudaStreamNonBlocking) != cudaSuccess) {
+    ctx->side_st = nullptr;
+    cudaGetLastError();
+    return false;
+  }
+  for (auto& e : ctx->side_ev)
+    if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      e = nullptr;
+      cudaGetLastError();
+      return false;
+    }
+  return true;
+}
+
+// one MLP over a hop batch (segments already describe the batch rows); negated rows are last.
+// Large batches (>= 8,192 rows) run as two row halves on two streams (the context's and its
+// side stream, each with its own split-K workspace): both halves' GEMMs want the whole GPU, so
+// each launch's last, partly filled round of tiles overlaps the other half's tiles instead of
+// leaving SMs idle (the per-launch tail), and PDL / graph ordering stays per stream.
 static int mix_mlp(kgq_ctx* ctx, const MixSegs& sg, int M, int neg0, cudaStream_t st) {
   const int d = ctx->cfg.dim;
   int L = 0;
   L += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,
                          ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
-  RelTerm rt;
-  rt.RW = ctx->RW;
-  rt.ldrw = ctx->cfg.hidden;
-  rt.M = M;
-  rt.rid = ctx->mix_rid;
-  {
-    StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
-    L += launch_linear_rel(ctx->Z, M, 2 * d, ctx->lin1x, rt, ctx->H[0], &ctx->gws, st);
-  }
-  Split A = ctx->H[0];
-  int K = ctx->lin1x.out_f;
-  for (int l = 1; l < ctx->cfg.n_hidden_layers; ++l) {
-    const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
-    L += dense(ctx, A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
-    A = ctx->H[l & 1];
-    K = lin.out_f;
-  }
-  const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
-  if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
-    L += dense(ctx, A, M, K, lo, kEpiNone, ctx->T, 2 * d, st);
-    L += launch_softmax_terminal(ctx->T, 2 * d, M, 2 * d, ctx->I, 0, neg0, M, st);
+  const int half = ((M / 2 + 255) / 256) * 256;  // 256-row (one tile pair) aligned cut
+  // (a failing fork / join call leaves its error for the submit's final cudaGetLastError check)
+  if (M >= 8192 && split_mlp_enabled() && side_stream(ctx) && cudaEventRecord(ctx->side_ev[0], st) == cudaSuccess &&
+      cudaStreamWaitEvent(ctx->side_st, ctx->side_ev[0], 0) == cudaSuccess) {
+    L += mlp_rows(ctx, 0, half, neg0, st, &ctx->gws);
+    L += mlp_rows(ctx, half, M - half, neg0, ctx->side_st, &ctx->gws2);
+    cudaEventRecord(ctx->side_ev[1], ctx->side_st);
+    cudaStreamWaitEvent(st, ctx->side_ev[1], 0);
   } else {
-    L += dense(ctx, A, M, K, lo, kEpiBetaReg, ctx->I, neg0, M, st);
+    L += mlp_rows(ctx, 0, M, neg0, st, &ctx->gws);
   }
   L += launch_mix_scatter(sg, M, ctx->I, ctx->S, 2 * d, st);
   check_site("mixed hop");
@@ -1146,8 +1203,24 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
     }
     // ---- intersections: one attention GEMM pair over every intersection group's branch rows ----
     if (inter_rows > 0) {
-      L += dense(ctx, ctx->S, (int)inter_rows, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I, 0, 0, st);
-      L += dense(ctx, ctx->I, (int)inter_rows, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone, ctx->T, ctx->tw, st);
+      // the attention GEMM pair over rows [r0, r0 + m); >= 8,192 rows: two halves on two streams
+      // (as mix_mlp)
+      auto attn = [&](int r0, int m, cudaStream_t s2, const GemmWs* w) {
+        L += dense(ctx, ctx->S.at(r0), m, 2 * d, ctx->lin[KGQ_LAYER_INTER_1], kEpiRelu, ctx->I.at(r0), 0, 0, s2, w);
+        L += dense(ctx, ctx->I.at(r0), m, 2 * d, ctx->lin[KGQ_LAYER_INTER_2], kEpiNone, ctx->T + (int64_t)r0 * ctx->tw,
+                   ctx->tw, s2, w);
+      };
+      const int ir = (int)inter_rows, ih = ((ir / 2 + 255) / 256) * 256;
+      if (ir >= 8192 && split_mlp_enabled() && side_stream(ctx) &&
+          cudaEventRecord(ctx->side_ev[0], st) == cudaSuccess &&
+          cudaStreamWaitEvent(ctx->side_st, ctx->side_ev[0], 0) == cudaSuccess) {
+        attn(0, ih, st, &ctx->gws);
+        attn(ih, ir - ih, ctx->side_st, &ctx->gws2);
+        cudaEventRecord(ctx->side_ev[1], ctx->side_st);
+        cudaStreamWaitEvent(st, ctx->side_ev[1], 0);
+      } else {
+        attn(0, ir, st, &ctx->gws);
+      }
       MixCombine mc;
       int total = 0;
       for (auto& g : G) {
@@ -1897,9 +1970,12 @@ kgq_status kgq_rank_answers(kgq_ctx* ctx, int32_t s, int32_t batch, const int32_
   return KGQ_OK;
 }
 
-static const unsigned long long kKtInit[24] = {~0ull, 0, 0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 1, 0, 0,
+// four span groups (dense / score on the context's stream, dense / score on its side stream:
+// tc_gemm.cuh kt_end), the log count at [32], the log from [40]
+static const unsigned long long kKtInit[40] = {~0ull, 0, 0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 1, 0, 0,
+                                               ~0ull, 0, 0, 0, 0, 2, 0, 0, ~0ull, 0, 0, 0, 0, 3, 0, 0,
                                                0,    0, 0, 0, 0, 0, 0, 0};
-constexpr size_t kKtWords = 24 + 3 * kKtLogCap;
+constexpr size_t kKtWords = 40 + 3 * kKtLogCap;
 
 kgq_status kgq_ktime_enable(kgq_ctx* ctx, int32_t on) {
   if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
@@ -1919,6 +1995,7 @@ kgq_status kgq_ktime_enable(kgq_ctx* ctx, int32_t on) {
     ctx->graphs.clear();
     clear_mix_graphs(ctx);
     ctx->gws.kt = want;
+    ctx->gws2.kt = want ? want + 16 : nullptr;
   }
   return KGQ_OK;
 }
@@ -1929,14 +2006,14 @@ kgq_status kgq_ktime_read(kgq_ctx* ctx, double* ms, int64_t* n) {
   n[0] = n[1] = 0;
   if (!ctx->kt_buf) return KGQ_OK;
   DeviceGuard g(ctx->cfg.device);
-  unsigned long long h[16];  // the two stage word groups (the log stays: kgq_ktime_log)
+  unsigned long long h[32];  // the four span groups (the log stays: kgq_ktime_log)
   CK(cudaDeviceSynchronize(), "ktime read");
   CK(cudaMemcpy(h, ctx->kt_buf, sizeof h, cudaMemcpyDeviceToHost), "ktime read");
-  for (int s = 0; s < 2; ++s) {
-    ms[s] = (double)h[8 * s + 3] * 1e-6;
-    n[s] = (int64_t)h[8 * s + 4];
+  for (int s = 0; s < 2; ++s) {  // stage s: group s (context stream) + group s + 2 (side stream)
+    ms[s] = (double)(h[8 * s + 3] + h[8 * (s + 2) + 3]) * 1e-6;
+    n[s] = (int64_t)(h[8 * s + 4] + h[8 * (s + 2) + 4]);
   }
-  CK(cudaMemcpy(ctx->kt_buf, kKtInit, 16 * sizeof(unsigned long long), cudaMemcpyHostToDevice), "ktime reset");
+  CK(cudaMemcpy(ctx->kt_buf, kKtInit, 32 * sizeof(unsigned long long), cudaMemcpyHostToDevice), "ktime reset");
   return KGQ_OK;
 }
 
@@ -1946,13 +2023,13 @@ int64_t kgq_ktime_log(kgq_ctx* ctx, uint64_t* out, int64_t cap) {
   DeviceGuard g(ctx->cfg.device);
   unsigned long long n = 0;
   if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-  if (cudaMemcpy(&n, ctx->kt_buf + 16, sizeof n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  if (cudaMemcpy(&n, ctx->kt_buf + 32, sizeof n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   n = std::min<unsigned long long>(n, kKtLogCap);
   const int64_t m = std::min<int64_t>((int64_t)n, cap);
-  if (m > 0 && cudaMemcpy(out, ctx->kt_buf + 24, (size_t)m * 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (m > 0 && cudaMemcpy(out, ctx->kt_buf + 40, (size_t)m * 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
   const unsigned long long zero = 0;
-  if (cudaMemcpy(ctx->kt_buf + 16, &zero, sizeof zero, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+  if (cudaMemcpy(ctx->kt_buf + 32, &zero, sizeof zero, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
   return (int64_t)n;
 }
 

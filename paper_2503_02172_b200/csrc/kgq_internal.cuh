@@ -166,6 +166,9 @@ struct kgq_ctx {
   int fused_topk = KGQ_FUSED_AUTO;  // kgq_set_option(KGQ_OPT_FUSED_TOPK)
   uint64_t graph_clock = 0;
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t side_st = nullptr;          // mixed path: the second row half of a large MLP hop
+  cudaEvent_t side_ev[2] = {nullptr, nullptr};
+  kgq::GemmWs gws2{};                      // the side stream's split-K workspace / span group
   // N2: fused top-k all-gather over peer memory (kgq_set_peers); peers.world == 0: off
   kgq::PeerPush peers{};
   uint32_t* d_epoch = nullptr;             // [2]: epoch, merge CTA counter

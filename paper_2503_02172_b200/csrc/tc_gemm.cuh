@@ -373,11 +373,13 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 // Launch span = last CTA's end - first CTA's start (after griddepcontrol.wait, so a PDL-early
-// CTA's wait for the predecessor is not counted); the last CTA to finish adds it to the stage's
-// sum, appends (start, end, stage) to the context's span log (base - 8 stage: [16] = count,
-// [24 + 3 i ..] = entries, kKtLogCap of them) and re-arms the words for the next launch of the
-// stage (stream-ordered: that launch's CTAs pass griddepcontrol.wait only after this grid
-// completed).  Layout of the words: [start, end, ctas done, summed ns, launches, stage, -, -].
+// CTA's wait for the predecessor is not counted); the last CTA to finish adds it to the group's
+// sum, appends (start, end, stage) to the context's span log (base = kt - 8 group: [32] = count,
+// [40 + 3 i ..] = entries, kKtLogCap of them) and re-arms the words for the next launch of the
+// group (stream-ordered: that launch's CTAs pass griddepcontrol.wait only after this grid
+// completed).  Groups: 0 dense, 1 score on the context's stream, 2 / 3 the same on its side
+// stream (concurrent launches must not share a group).  Layout of a group's words:
+// [start, end, ctas done, summed ns, launches, group, -, -].
 __device__ __forceinline__ void kt_begin(unsigned long long* kt) {
   if (kt) atomicMin(&kt[0], globaltimer_ns());
 }
@@ -391,11 +393,11 @@ __device__ __forceinline__ void kt_end(unsigned long long* kt) {
     kt[3] += t1 > t0 ? t1 - t0 : 0ull;
     kt[4] += 1ull;
     unsigned long long* base = kt - 8 * kt[5];
-    const unsigned long long i = atomicAdd(&base[16], 1ull);
+    const unsigned long long i = atomicAdd(&base[32], 1ull);
     if (i < kKtLogCap) {
-      base[24 + 3 * i] = t0;
-      base[25 + 3 * i] = t1;
-      base[26 + 3 * i] = kt[5];
+      base[40 + 3 * i] = t0;
+      base[41 + 3 * i] = t1;
+      base[42 + 3 * i] = kt[5] & 1;  // stage: 0 dense, 1 score (groups 2 / 3: the side stream's)
     }
     kt[0] = ~0ull;
     kt[1] = 0ull;
