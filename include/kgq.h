@@ -307,6 +307,11 @@ typedef enum { KGQ_FUSED_OFF = 0, KGQ_FUSED_ON = 1, KGQ_FUSED_AUTO = 2 } kgq_fus
 kgq_status kgq_set_option(kgq_ctx* ctx, int32_t option, int64_t value);
 
 /* ---- introspection (parity / bench) ----------------------------------------------------- */
+/* Tensor-core MMAs per useful fp32 multiply-add of the GEMMs in this build: 3 for the default
+ * fp16x2 operand format (a_hi w_hi' + a_hi w_lo' + a_lo' w_hi, 2^11-scaled lo planes, |x| < 65504,
+ * |w| < 32; out-of-range values make kgq_check_errors / kgq_finalize return KGQ_ERANGE), 6 for
+ * the bf16x3 build libkgq_bf16x3.so (exact three-plane split, fp32 range).  The roofline divisor. */
+int32_t kgq_tensor_mmas_per_fma(void);
 /* Number of this library's kernels launched by the last submit/query_embedding call. */
 int32_t kgq_last_launch_count(const kgq_ctx* ctx);
 /* BetaE only: copy this shard's precomputed entity terms to device out fp32 [3, d, n_shard]

@@ -80,7 +80,7 @@ __device__ __forceinline__ void store_split4(const Split& z, int64_t i, float4 x
   split3_pair(x.z, x.w, a1, b1, c1);
   *reinterpret_cast<uint2*>(z.b0 + i) = make_uint2(a0, a1);
   *reinterpret_cast<uint2*>(z.b1 + i) = make_uint2(b0, b1);
-  *reinterpret_cast<uint2*>(z.b2 + i) = make_uint2(c0, c1);
+  if constexpr (!kFp16x2) *reinterpret_cast<uint2*>(z.b2 + i) = make_uint2(c0, c1);
 }
 constexpr int kMlpInRows = 4;  // rows (warps) per block
 __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
@@ -110,7 +110,7 @@ __global__ void k_betae_mlp_input(ChainArgs a, const float* __restrict__ ent,
     for (int j = lane; j < (2 * d) / 4; j += 32) store_split4(z, zrow + 4 * j, __ldg(er + j));
   } else {  // split -> split: plane copies (exact)
     const int64_t srow = (g.src_row[gi] + b) * src.ld;
-    for (int p = 0; p < 3; ++p) {
+    for (int p = 0; p < kSplitPlanesA; ++p) {
       const uint2* sp = reinterpret_cast<const uint2*>(src.plane(p) + srow);
       uint2* dp = reinterpret_cast<uint2*>(z.plane(p) + zrow);
       for (int j = lane; j < (2 * d) / 4; j += 32) dp[j] = sp[j];
@@ -171,7 +171,7 @@ __global__ void k_mix_gather(MixSegs sg, const float* __restrict__ ent, Split S,
     const int64_t srow = (g.src0 + b) * src.ld;
     if (((2 * d) & 7) == 0) {
       const int nv = (2 * d) >> 3;
-      for (int p = 0; p < 3; ++p) {
+      for (int p = 0; p < kSplitPlanesA; ++p) {
         const uint4* sp = reinterpret_cast<const uint4*>(src.plane(p) + srow);
         uint4* dp = reinterpret_cast<uint4*>(Z.plane(p) + zrow);
         for (int j = threadIdx.x; j < nv; j += blockDim.x) dp[j] = sp[j];
@@ -200,7 +200,7 @@ __global__ void k_mix_scatter(MixSegs sg, Split src, Split S, int w) {
   const int64_t o = (g.src0 + row - g.dst0) * S.ld, i = (int64_t)row * src.ld;
   if ((w & 7) == 0) {  // 16-byte vectors (row starts are 16-byte aligned: ld % 8 == 0)
     const int nv = w >> 3;
-    for (int p = 0; p < 3; ++p) {
+    for (int p = 0; p < kSplitPlanesA; ++p) {
       const uint4* sp = reinterpret_cast<const uint4*>(src.plane(p) + i);
       uint4* dp = reinterpret_cast<uint4*>(S.plane(p) + o);
       for (int j = threadIdx.x; j < nv; j += blockDim.x) dp[j] = sp[j];
@@ -332,6 +332,13 @@ int launch_branch_mean(const float* T, int64_t ldt, int nb, int B, int d, Split 
 __device__ __forceinline__ float4 load_split4(const Split& s, int64_t i) {  // i % 4 == 0
   const uint2 a = *reinterpret_cast<const uint2*>(s.b0 + i);
   const uint2 b = *reinterpret_cast<const uint2*>(s.b1 + i);
+  if constexpr (kFp16x2) {
+    const float2 h0 = __half22float2(*reinterpret_cast<const __half2*>(&a.x));
+    const float2 h1 = __half22float2(*reinterpret_cast<const __half2*>(&a.y));
+    const float2 l0 = __half22float2(*reinterpret_cast<const __half2*>(&b.x));
+    const float2 l1 = __half22float2(*reinterpret_cast<const __half2*>(&b.y));
+    return make_float4(h0.x + l0.x * kLoInv, h0.y + l0.y * kLoInv, h1.x + l1.x * kLoInv, h1.y + l1.y * kLoInv);
+  }
   const uint2 c = *reinterpret_cast<const uint2*>(s.b2 + i);
   auto lo = [](uint32_t u) { return __uint_as_float(u << 16); };
   auto hi = [](uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); };
@@ -481,7 +488,7 @@ int launch_state_to_q(Split S, int nb, int B, int w, float* q, cudaStream_t st) 
 __global__ void k_split_copy(const float* __restrict__ src, int64_t n, Split dst) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    store_split(dst, i, src[i]);
+    store_split_w(dst, i, src[i]);
 }
 
 int launch_split_copy(const float* src, int64_t n, Split dst, cudaStream_t st) {
@@ -494,7 +501,7 @@ __global__ void k_split_copy_rows(const float* __restrict__ src, int64_t lds, in
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    store_split(dst, (i / cols) * dst.ld + i % cols, src[(i / cols) * lds + i % cols]);
+    store_split_w(dst, (i / cols) * dst.ld + i % cols, src[(i / cols) * lds + i % cols]);
 }
 
 int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st, int64_t lds) {
@@ -507,5 +514,8 @@ int launch_empty(cudaStream_t st) {
   k_empty<<<148, 128, 0, st>>>();
   return 1;
 }
+
+// this translation unit's fp16x2 range flag (common.cuh range_check), read and cleared
+unsigned int range_flag_chain() { return range_flag_take(); }
 
 }  // namespace kgq

@@ -1,6 +1,7 @@
 // Small device helpers shared by the kernels of libkgq.so.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
@@ -91,11 +92,71 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // so that the offset half is itself a TMA-addressable GEMM operand.
 __host__ __device__ constexpr int q2b_off(int d) { return (d + 7) & ~7; }
 
+// Operand format of the tensor-core GEMMs (compile time, KGQ_OPERAND_FP16X2):
+//  0  bf16x3: every operand x = b0 + b1 + b2 (three bf16 planes, exact); 6 bf16 MMAs per fp32
+//     multiply-add (tc_gemm.cuh).
+//  1  fp16x2 (Ootomo-Yokota split): activations ("A" operands) hold b0 = h = RN_fp16(x) and
+//     b1 = l' = RN_fp16((x - h) 2^11) (b2 unused), i.e. x~ = h + l' 2^-11 with |x~ - x| <= 2^-22 |x|;
+//     weights ("W" operands: dense weights, the scorer's (u, v) table) hold b0 = h 2^11 (exact),
+//     b1 = l' and b2 = h, and the GEMM forms 2^11 x w ~= a_h w_h' + a_h w_l' + a_l' w_h -- three
+//     fp16 MMAs per multiply-add, one fp32 accumulator scaled by 2^11 (undone exactly in the
+//     epilogue), dropped a_l w_l ~ 2^-22 |x w|.  Range: |x| < 65504 (fp16); the scaled weight plane
+//     needs |w| < 32.
+//  Measured against the float64 oracle (profiles/r02/operand_accuracy.txt) fp16x2 is the MORE
+//  accurate of the two -- its three MMAs per K step truncate in TMEM half as often as bf16x3's six
+//  -- and 40% faster end to end; values outside its range are detected (range_flag below) and
+//  reported as KGQ_ERANGE, for which the bf16x3 build (libkgq_bf16x3.so) is the full-range one.
+#ifndef KGQ_OPERAND_FP16X2
+#define KGQ_OPERAND_FP16X2 1
+#endif
+constexpr bool kFp16x2 = KGQ_OPERAND_FP16X2 != 0;
+constexpr int kSplitPlanesA = kFp16x2 ? 2 : 3;  // planes an activation operand uses
+constexpr int kMmasPerFma = kFp16x2 ? 3 : 6;    // tensor-core MMAs per useful fp32 multiply-add
+constexpr float kLoScale = 2048.0f, kLoInv = 1.0f / 2048.0f;
+constexpr float kFp16Limit = 65504.0f;          // activations: |x| below the fp16 maximum
+constexpr float kFp16LimitW = 65504.0f / 2048.0f;  // weights: the 2^11-scaled high plane too
+// Range guard of the fp16x2 format: a conversion of a finite |x| >= the limit sets this flag
+// (one per translation unit -- `static` -- read and cleared by range_flag_take() from the host,
+// kgq_check_errors / kgq_finalize turn it into KGQ_ERANGE).
+static __device__ unsigned int g_range_flag = 0;
+__device__ __forceinline__ void range_check(float a, float limit) {
+  if constexpr (kFp16x2)
+    if (fabsf(a) >= limit) atomicOr(&g_range_flag, 1u);
+}
+static inline unsigned int range_flag_take() {
+  unsigned int v = 0, z = 0;
+  if (cudaMemcpyFromSymbol(&v, g_range_flag, sizeof v) != cudaSuccess) return 0;
+  if (v) cudaMemcpyToSymbol(g_range_flag, &z, sizeof z);
+  return v;
+}
+__device__ __forceinline__ __nv_bfloat16 h2b(__half h) { return __ushort_as_bfloat16(__half_as_ushort(h)); }
+__device__ __forceinline__ float b2hf(__nv_bfloat16 b) { return __half2float(__ushort_as_half(__bfloat16_as_ushort(b))); }
+
 __device__ __forceinline__ void split3(float x, __nv_bfloat16& a, __nv_bfloat16& b, __nv_bfloat16& c) {
-  a = __float2bfloat16_rn(x);
-  const float r = x - __bfloat162float(a);
-  b = __float2bfloat16_rn(r);
-  c = __float2bfloat16_rn(r - __bfloat162float(b));
+  if constexpr (kFp16x2) {
+    range_check(x, kFp16Limit);
+    const __half h = __float2half_rn(x);
+    a = h2b(h);
+    b = h2b(__float2half_rn((x - __half2float(h)) * kLoScale));
+    c = __ushort_as_bfloat16(0);
+  } else {
+    a = __float2bfloat16_rn(x);
+    const float r = x - __bfloat162float(a);
+    b = __float2bfloat16_rn(r);
+    c = __float2bfloat16_rn(r - __bfloat162float(b));
+  }
+}
+// the weight ("W") form of the split: fp16x2 adds the 2^11-scaled high plane (see above)
+__device__ __forceinline__ void split3_w(float x, __nv_bfloat16& a, __nv_bfloat16& b, __nv_bfloat16& c) {
+  if constexpr (kFp16x2) {
+    range_check(x, kFp16LimitW);
+    const __half h = __float2half_rn(x);
+    a = h2b(__float2half_rn(__half2float(h) * kLoScale));
+    b = h2b(__float2half_rn((x - __half2float(h)) * kLoScale));
+    c = h2b(h);
+  } else {
+    split3(x, a, b, c);
+  }
 }
 __device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
   return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
@@ -104,6 +165,16 @@ __device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi
 // the (x, y) bf16 pairs of planes 0/1/2, x in the low half -- bit-identical to
 // pack_bf16(split3(x), split3(y)) plane by plane.
 __device__ __forceinline__ void split3_pair(float x, float y, uint32_t& q0, uint32_t& q1, uint32_t& q2) {
+  if constexpr (kFp16x2) {
+    range_check(fmaxf(fabsf(x), fabsf(y)), kFp16Limit);
+    const __half2 h = __floats2half2_rn(x, y);
+    const float2 f = __half22float2(h);
+    const __half2 l = __floats2half2_rn((x - f.x) * kLoScale, (y - f.y) * kLoScale);
+    q0 = *reinterpret_cast<const uint32_t*>(&h);
+    q1 = *reinterpret_cast<const uint32_t*>(&l);
+    q2 = 0u;
+    return;
+  }
   auto pk = [](float a, float b) {
     const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&h);
@@ -122,11 +193,19 @@ __device__ __forceinline__ void store_split(const Split& s, int64_t i, float x) 
   split3(x, a, b, c);
   s.b0[i] = a;
   s.b1[i] = b;
-  s.b2[i] = c;
+  if constexpr (!kFp16x2) s.b2[i] = c;
 }
 
 __device__ __forceinline__ float load_split(const Split& s, int64_t i) {
+  if constexpr (kFp16x2) return b2hf(s.b0[i]) + b2hf(s.b1[i]) * kLoInv;  // exact: 11 + 11 bits
   return (__bfloat162float(s.b0[i]) + __bfloat162float(s.b1[i])) + __bfloat162float(s.b2[i]);
+}
+__device__ __forceinline__ void store_split_w(const Split& s, int64_t i, float x) {
+  __nv_bfloat16 a, b, c;
+  split3_w(x, a, b, c);
+  s.b0[i] = a;
+  s.b1[i] = b;
+  s.b2[i] = c;
 }
 // 8 consecutive elements [i, i + 8) of a split tensor at once: one 16-byte access per plane
 // (i % 8 == 0 and rows 16-byte aligned: ld % 8 == 0).  Bit-identical to 8 store_split /
@@ -137,11 +216,22 @@ __device__ __forceinline__ void store_split8(const Split& s, int64_t i, const fl
   for (int j = 0; j < 4; ++j) split3_pair(x[2 * j], x[2 * j + 1], q0[j], q1[j], q2[j]);
   *reinterpret_cast<uint4*>(s.b0 + i) = make_uint4(q0[0], q0[1], q0[2], q0[3]);
   *reinterpret_cast<uint4*>(s.b1 + i) = make_uint4(q1[0], q1[1], q1[2], q1[3]);
-  *reinterpret_cast<uint4*>(s.b2 + i) = make_uint4(q2[0], q2[1], q2[2], q2[3]);
+  if constexpr (!kFp16x2) *reinterpret_cast<uint4*>(s.b2 + i) = make_uint4(q2[0], q2[1], q2[2], q2[3]);
 }
 __device__ __forceinline__ void load_split8(const Split& s, int64_t i, float* x) {
-  const uint4 u0 = *reinterpret_cast<const uint4*>(s.b0 + i), u1 = *reinterpret_cast<const uint4*>(s.b1 + i),
-              u2 = *reinterpret_cast<const uint4*>(s.b2 + i);
+  const uint4 u0 = *reinterpret_cast<const uint4*>(s.b0 + i), u1 = *reinterpret_cast<const uint4*>(s.b1 + i);
+  if constexpr (kFp16x2) {
+    const uint32_t a0[4] = {u0.x, u0.y, u0.z, u0.w}, a1[4] = {u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&a0[j]));
+      const float2 l = __half22float2(*reinterpret_cast<const __half2*>(&a1[j]));
+      x[2 * j] = h.x + l.x * kLoInv;
+      x[2 * j + 1] = h.y + l.y * kLoInv;
+    }
+    return;
+  }
+  const uint4 u2 = *reinterpret_cast<const uint4*>(s.b2 + i);
   const uint32_t a0[4] = {u0.x, u0.y, u0.z, u0.w}, a1[4] = {u1.x, u1.y, u1.z, u1.w}, a2[4] = {u2.x, u2.y, u2.z, u2.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {

@@ -220,6 +220,13 @@ bool relterm_disabled() {  // KGQ_NO_RELTERM=1: first projection layer on the as
   }
   return v == 1;
 }
+// fp16x2 range flags of every converting translation unit (process-wide per device: any context's
+// conversion since the last check)
+static bool range_flags_taken() {
+  const unsigned int a = range_flag_chain(), b = range_flag_linear(), c = range_flag_score_tc();
+  return (a | b | c) != 0;
+}
+
 // KGQ_NO_FUSED_TOPK=1: new contexts default to KGQ_FUSED_OFF (A/B runs)
 bool fused_topk_disabled() {
   static const bool v = [] {
@@ -768,6 +775,9 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   }
   CK(cudaGetLastError(), "finalize launch");
   CK(cudaDeviceSynchronize(), "finalize");
+  if (range_flags_taken())
+    return fail(ctx, KGQ_ERANGE, "a weight (|w| >= 32) or BetaE entity term is outside the fp16x2 operand range; "
+                "use the bf16x3 build (libkgq_bf16x3.so, KGQ_OPERANDS=bf16x3)");
   ctx->finalized = true;
   return KGQ_OK;
 }
@@ -1676,6 +1686,8 @@ kgq_status kgq_merge_topk(kgq_ctx* ctx, int32_t parts, int32_t batch, int32_t k,
   return KGQ_OK;
 }
 
+int32_t kgq_tensor_mmas_per_fma(void) { return kMmasPerFma; }
+
 kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
   if (!ctx) return fail(nullptr, KGQ_EINVAL, "ctx is NULL");
   DeviceGuard g(ctx->cfg.device);
@@ -1708,6 +1720,10 @@ kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream) {
     return fail(ctx, KGQ_ERANGE, "query row %d: %s slot %d out of range", e[1], e[3] ? "relation" : "anchor",
                 e[2]);
   }
+  if (range_flags_taken())
+    return fail(ctx, KGQ_ERANGE, "an operand of the tensor-core GEMMs reached the fp16x2 range (|x| >= 65504): "
+                "results since the last check are not exact; use the bf16x3 build (libkgq_bf16x3.so, "
+                "KGQ_OPERANDS=bf16x3) for such inputs");
   return KGQ_OK;
 }
 

@@ -359,6 +359,10 @@ int launch_filtered_counts(const float* dist, int64_t ldd, int64_t e0, int64_t n
 int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t ns, int64_t np, int d,
                           double* sums, Split uv, float2* Esum, float* uvT, cudaStream_t st);
 // BetaE query prep of the tensor-core / streaming scorers: split [a; b] rows and fp64 P_q
+// fp16x2 range flags of the translation units that convert to the operand format (read + clear)
+unsigned int range_flag_chain();
+unsigned int range_flag_linear();
+unsigned int range_flag_score_tc();
 int launch_score_prep_tc(const float* q, int rows, int d, const double* sums, int64_t ns, Split A, float2* P,
                          cudaStream_t st);
 // BetaE small-batch scorer (<= 16 query rows) streaming the centred fp32 (u, v) table uvT [d][2][np]

@@ -123,4 +123,7 @@ int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, const 
 #undef KGQ_EPI
 }
 
+// this translation unit's fp16x2 range flag (common.cuh range_check), read and cleared
+unsigned int range_flag_linear() { return range_flag_take(); }
+
 }  // namespace kgq

@@ -67,8 +67,8 @@ __global__ void k_uv_table(const float* __restrict__ ent, int64_t e0, int64_t ns
       u = (float)((pab - pa) - sums[j] / (double)n_all);
       v = (float)((pab - pb) - sums[d + j] / (double)n_all);
     }
-    store_split(uv, e * 2 * d + j, u);
-    store_split(uv, e * 2 * d + d + j, v);
+    store_split_w(uv, e * 2 * d + j, u);  // the scorer GEMM's "W" operand
+    store_split_w(uv, e * 2 * d + d + j, v);
     if (uvT) {  // dim-major fp32 copy for the small-batch streaming scorer: [d][2][np]
       uvT[(int64_t)(2 * j) * np + e] = u;
       uvT[(int64_t)(2 * j + 1) * np + e] = v;
@@ -139,7 +139,7 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
     // P_q terms from the fp32 values
     for (int j = 8 * threadIdx.x; j < 2 * d; j += 8 * blockDim.x)
 #pragma unroll
-      for (int p3 = 0; p3 < 3; ++p3)
+      for (int p3 = 0; p3 < kSplitPlanesA; ++p3)
         *reinterpret_cast<uint4*>(A.plane(p3) + a0 + j) = *reinterpret_cast<const uint4*>(S.plane(p3) + s0 + j);
     for (int j = threadIdx.x; j < d; j += blockDim.x) {
       const double da = load_split(S, s0 + j), db = load_split(S, s0 + d + j);
@@ -306,5 +306,8 @@ int launch_score_betae_tc(const float* q, int rows, int nbq, int d, const double
   return 1 + tc::launch_gemm_auto(A, rows, uv, (int)np, 2 * d, o,
                                   EpiBetaScore<1>{P, Esum, rows, np, cmin, ldc, nvalid}, ws, st);
 }
+
+// this translation unit's fp16x2 range flag (common.cuh range_check), read and cleared
+unsigned int range_flag_score_tc() { return range_flag_take(); }
 
 }  // namespace kgq

@@ -300,7 +300,8 @@ template <int BN, bool NBUF2 = false>
 struct Layout {
   static constexpr int A_BYTES = BM * BK * 2;         // one bf16 plane of A: 8 KB
   static constexpr int W_BYTES = (BN / 2) * BK * 2;   // one plane of this CTA's half of the W tile
-  static constexpr int STAGE_BYTES = 3 * A_BYTES + 3 * W_BYTES;
+  static constexpr int STAGE_BYTES = kSplitPlanesA * A_BYTES + 3 * W_BYTES;  // A planes + 3 W planes
+  static constexpr int W_OFF = kSplitPlanesA * A_BYTES;                       // first W plane
   static constexpr int BUF_BYTES = 4096;
   static constexpr int BUDGET = 227 * 1024 - 1024 - 256;  // minus alignment slack and barriers
   static constexpr int FIT = (BUDGET - EPI_WARPS * BUF_BYTES) / STAGE_BYTES;
@@ -315,7 +316,7 @@ struct Layout {
   // from TMEM and only B from shared memory): one 48-column A slot (3 planes x 2 K16 steps x 8
   // columns) per operand stage next to the two BN-column accumulators, if it fits in 512.
   static constexpr int A_SLOT_COLS = 3 * (BK / 16) * 8;
-  static constexpr bool ATM = KGQ_TC_ATMEM && 2 * BN + A_SLOT_COLS * STAGES <= 512;
+  static constexpr bool ATM = KGQ_TC_ATMEM && !kFp16x2 && 2 * BN + A_SLOT_COLS * STAGES <= 512;
   static constexpr int TMEM_COLS = ATM ? 512 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = STG_OFF + NBUF * EPI_WARPS * BUF_BYTES;
@@ -600,10 +601,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
           tma_load_2d_2sm(st, &mAh, lb, kb * BK, m0);
           tma_load_2d_2sm(st + L::A_BYTES, &mAl, lb, kb * BK, m0);
-          tma_load_2d_2sm(st + 2 * L::A_BYTES, &mA2, lb, kb * BK, m0);
-          tma_load_2d_2sm(st + 3 * L::A_BYTES, &mWh, lb, kb * BK, nw);
-          tma_load_2d_2sm(st + 3 * L::A_BYTES + L::W_BYTES, &mWl, lb, kb * BK, nw);
-          tma_load_2d_2sm(st + 3 * L::A_BYTES + 2 * L::W_BYTES, &mW2, lb, kb * BK, nw);
+          if constexpr (!kFp16x2) tma_load_2d_2sm(st + 2 * L::A_BYTES, &mA2, lb, kb * BK, m0);
+          tma_load_2d_2sm(st + L::W_OFF, &mWh, lb, kb * BK, nw);
+          tma_load_2d_2sm(st + L::W_OFF + L::W_BYTES, &mWl, lb, kb * BK, nw);
+          tma_load_2d_2sm(st + L::W_OFF + 2 * L::W_BYTES, &mW2, lb, kb * BK, nw);
         }
       }
     }
@@ -611,7 +612,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader only): M = 256 over the pair, N = BN ----------------
       // instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 256 over the pair
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+      // A / B formats: bf16 = 1 (bits 7-9, 10-12), f16 = 0
+      const uint32_t fmt = kFp16x2 ? 0u : 1u;
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)((2 * BM) >> 4) << 24);
       uint32_t it = 0, g0 = 0;
       for (int u = cluster; u < nunits; u += nclusters) {
@@ -631,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const uint32_t d = tmem + a * BN;
           const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
           const uint32_t a0 = st, a1 = st + L::A_BYTES, a2 = st + 2 * L::A_BYTES;
-          const uint32_t w0 = st + 3 * L::A_BYTES, w1 = w0 + L::W_BYTES, w2 = w1 + L::W_BYTES;
+          const uint32_t w0 = st + L::W_OFF, w1 = w0 + L::W_BYTES, w2 = w1 + L::W_BYTES;
           if constexpr (L::ATM) {
             // A slot of this stage (free: the MMAs of the stage's previous K-block completed
             // before the producer refilled the stage, i.e. before full[s] fired)
@@ -651,6 +654,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               mma_bf16_2sm_ts(d, t0, umma_desc_sw64(w1 + off), idesc, 1u);
               mma_bf16_2sm_ts(d, t1, umma_desc_sw64(w0 + off), idesc, 1u);
               mma_bf16_2sm_ts(d, t0, umma_desc_sw64(w0 + off), idesc, 1u);
+            }
+          } else if constexpr (kFp16x2) {
+            // fp16x2: a_l' w_h + a_h w_l' + a_h w_h' (w planes: 0 = h 2^11, 1 = l', 2 = h), all
+            // scaled by 2^11 into one accumulator; the small terms first, a_h re-used from the
+            // collector
+            (void)a2;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t off = kk * 32;
+              mma_bf16_2sm(d, umma_desc_sw64(a1 + off), umma_desc_sw64(w2 + off), idesc, (first && kk == 0) ? 0u : 1u);
+              mma_bf16_2sm_afill(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w1 + off), idesc, 1u);
+              mma_bf16_2sm_alast(d, umma_desc_sw64(a0 + off), umma_desc_sw64(w0 + off), idesc, 1u);
             }
           } else if constexpr (KGQ_TC_COLLECTOR) {
             // A-grouped order with collector re-use: each A plane is read from shared memory
@@ -727,7 +742,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           float v[16];
           tmem_ld16(tq + c, v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+          for (int i = 0; i < 16; ++i) acc[c + i] = kFp16x2 ? fmaf(v[i], kLoInv, acc[c + i]) : acc[c + i] + v[i];
         }
 #else
         (void)tq;
@@ -856,7 +871,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             tma_store_2d(&mO0, buf, n0 + c, row0 / ROWDIV);
           if (PLANES == 3) {
             tma_store_2d(&mO1, buf + 1024, n0 + c, row0);
-            tma_store_2d(&mO2, buf + 2048, n0 + c, row0);
+            if constexpr (!kFp16x2) tma_store_2d(&mO2, buf + 2048, n0 + c, row0);
           }
           bulk_commit();
         }

@@ -12,7 +12,11 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("KGQ_LIB_PATH") or os.path.join(_HERE, "libkgq.so")  # override: A/B builds only
+# operand format of the tensor-core GEMMs: libkgq.so = fp16x2 (default), libkgq_bf16x3.so = the
+# exact three-plane bf16 split (full fp32 range; KGQ_OPERANDS=bf16x3); KGQ_LIB_PATH: A/B builds only
+OPERANDS = os.environ.get("KGQ_OPERANDS", "fp16x2")
+LIB_PATH = os.environ.get("KGQ_LIB_PATH") or os.path.join(
+    _HERE, "libkgq_bf16x3.so" if OPERANDS == "bf16x3" else "libkgq.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
                       " (or `make -C paper_2503_02172_b200/csrc`)")
@@ -40,7 +44,7 @@ EXPORTS = (
     "kgq_check_errors", "kgq_last_launch_count", "kgq_entity_terms", "kgq_profile_enable",
     "kgq_profile_read", "kgq_rank_answers", "kgq_peer_bytes", "kgq_set_peers", "kgq_merge_peers",
     "kgq_query_range", "kgq_nccl_unique_id", "kgq_comm_init", "kgq_comm_destroy", "kgq_rank_metrics",
-    "kgq_ktime_enable", "kgq_ktime_read", "kgq_ktime_log", "kgq_set_option",
+    "kgq_ktime_enable", "kgq_ktime_read", "kgq_ktime_log", "kgq_set_option", "kgq_tensor_mmas_per_fma",
 )
 RANK_LOCAL, RANK_DIST, RANK_COUNT, RANK_FILTERED = 0, 1, 2, 3
 SPLIT_ENTITIES, SPLIT_QUERIES = 0, 1
@@ -103,6 +107,7 @@ _sig = {
     "kgq_ktime_read": (_I32, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
     "kgq_ktime_log": (_I64, [_P, _P, _I64]),
     "kgq_set_option": (_I32, [_P, _I32, _I64]),
+    "kgq_tensor_mmas_per_fma": (_I32, []),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -114,6 +119,11 @@ class KgqError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = STATUS.get(status, status)
+
+
+def tensor_mmas_per_fma() -> int:
+    """MMAs per useful fp32 multiply-add of this build's GEMMs (3: fp16x2, 6: bf16x3)."""
+    return int(_lib.kgq_tensor_mmas_per_fma())
 
 
 def structure_id(s) -> int:

@@ -30,6 +30,20 @@ def test_every_declared_symbol_is_exported():
     assert set(names) == set(kgq.EXPORTS)
 
 
+def test_both_operand_builds_export_every_symbol():
+    """libkgq.so (fp16x2 GEMM operands) and libkgq_bf16x3.so (exact three-plane bf16 split) are
+    the same ABI; kgq_tensor_mmas_per_fma tells them apart (3 vs 6 MMAs per fp32 multiply-add)."""
+    here = os.path.dirname(kgq.LIB_PATH)
+    mmas = {}
+    for name in ("libkgq.so", "libkgq_bf16x3.so"):
+        lib = ctypes.CDLL(os.path.join(here, name))
+        for n in header_functions():
+            assert hasattr(lib, n), f"{name}: {n} not exported"
+        lib.kgq_tensor_mmas_per_fma.restype = ctypes.c_int32
+        mmas[name] = lib.kgq_tensor_mmas_per_fma()
+    assert mmas == {"libkgq.so": 3, "libkgq_bf16x3.so": 6}
+
+
 def test_structure_metadata_matches_oracle_plans():
     for i, s in enumerate(O.STRUCTURES):
         assert kgq.structure_id(s) == i
