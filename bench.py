@@ -41,6 +41,10 @@ CONFIG = {
 }
 
 
+def operand_format(mmas):
+    return {3: "fp16x2", 6: "bf16x3"}.get(mmas, f"{mmas}-MMA")
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
@@ -223,12 +227,14 @@ def run_suite(args):
     """One JSON line per BASELINE.json config other than the headline one: device
     q/s with L2 flushed between steps, stage split, and the dominant kernel against its roofline
     (SIMT scorers: FP32 lane-instructions vs 148 SMs x 128 lanes x SM clock; tensor path: useful
-    fp32 FLOPs vs the bf16x3 peak = measured bf16 / 6)."""
+    fp32 FLOPs vs the tensor peak = measured bf16 (= fp16) / MMAs per fp32 FMA of the build)."""
     import torch
     from paper_2503_02172_b200 import Engine
     peaks, src = load_peaks()
     alu_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # lane-instr/s
-    tc_peak = peaks["bf16_tflops"] / 6.0
+    from paper_2503_02172_b200.kgq import tensor_mmas_per_fma
+    mmas = tensor_mmas_per_fma()
+    tc_peak = peaks["bf16_tflops"] / mmas
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     names = args.suite.split(",") if args.suite else list(SUITE)
     for name in names:
@@ -279,7 +285,8 @@ def run_suite(args):
         d_ms, _, d_w = prof["dense"]
         if model == "betae" and B > 16:
             ach = (sc_w + d_w) / ((sc_ms + d_ms) / 1e3) / 1e12
-            roof = {"kernel": "k_gemm (tcgen05 bf16x3: dense layers + BetaE scorer)", "bound": "tensor",
+            roof = {"kernel": f"k_gemm (tcgen05, {operand_format(mmas)} operands: dense layers + BetaE scorer)",
+                    "bound": "tensor",
                     "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak}
         else:
             ach = sc_w / (sc_ms / 1e3) if sc_ms > 0 else 0.0
@@ -604,15 +611,18 @@ def main():
         except Exception as ex:
             print(f"bench: C5a failed: {type(ex).__name__}: {ex}", file=sys.stderr, flush=True)
 
-    # ---- roofline of the dominant kernel: the tcgen05 bf16x3 GEMM (k_gemm), which runs every
+    # ---- roofline of the dominant kernel: the tcgen05 GEMM (k_gemm), which runs every
     # dense layer of the chain and the BetaE scorer contraction.  Algorithmic work = useful fp32
     # FLOPs (2MNK, the library's counters); time = the union of the GEMM launches' in-kernel spans
     # (%globaltimer, first CTA start after the PDL wait -> last CTA end) over the timed steps of
-    # THIS pass; peak = measured bf16 / 6 (six bf16 MMAs per useful fp32 multiply-add: x0w0,
-    # x0w1, x1w0, x0w2, x1w1, x2w0), the BURST figure (the driver's sustained one is a 4-s cuBLAS
-    # loop under the power cap; the scorer GEMM alone measures above it), sustained quoted beside.
-    peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 6.0
-    peak_burst = peaks["bf16_tflops"] / 6.0
+    # THIS pass; peak = measured bf16 (fp16 MMAs run at the same rate) / the build's MMAs per
+    # useful fp32 multiply-add (fp16x2: a_h w_h' + a_h w_l' + a_l' w_h = 3; bf16x3: 6), the BURST
+    # figure (the driver's sustained one is a 4-s cuBLAS loop under the power cap), sustained
+    # quoted beside.
+    from paper_2503_02172_b200.kgq import tensor_mmas_per_fma
+    mmas = tensor_mmas_per_fma()  # 3: fp16x2 operands (default build), 6: bf16x3 (libkgq_bf16x3.so)
+    peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / mmas
+    peak_burst = peaks["bf16_tflops"] / mmas
     rate = lambda fl, ms: fl / (ms / 1e3) / 1e12 if ms and ms > 0 else 0.0
     achieved = rate(d_fl + s_fl, gemm_busy_ms)
     traffic = None
@@ -638,7 +648,10 @@ def main():
                                     f"query split x{world} (W x 14 x 1024 replicated queries, each rank its 14 x "
                                     f"1024; library NCCL all-gather)" if qsplit else
                                     f"entity shards x{world} ({engines[0].merge_mode})"),
-                       queries_per_step_per_rank=per_rank_queries),
+                       queries_per_step_per_rank=per_rank_queries,
+                       gemm_operands=("fp16x2 split: fp32 operands as fp16 hi + 2^11-scaled fp16 lo, 3 fp16 MMAs "
+                                      "per fp32 multiply-add, fp32 accumulation (DESIGN.md §7)" if mmas == 3 else
+                                      "bf16x3 split: exact three bf16 planes, 6 MMAs per fp32 multiply-add")),
         "how": ("per step: ONE kgq_submit_mixed of the 14 x 1024 queries (BetaE level-synchronous: each projection "
                 "hop of all types' branches is one MLP, all intersections one attention GEMM pair, one scorer, one "
                 "top-k); device time between events on the launching stream, max over ranks" if mixed_mode else
@@ -655,10 +668,11 @@ def main():
                  "share_of_step": gemm_busy_ms / ms_step,
                  "how": "in-kernel %globaltimer spans of every k_gemm launch of the timed steps (kgq_ktime_log), "
                         "union over the streams"},
-        "roofline": {"kernel": "k_gemm (tcgen05 bf16x3: chain dense layers + BetaE scorer)",
+        "roofline": {"kernel": f"k_gemm (tcgen05, {operand_format(mmas)} operands: chain dense layers + BetaE scorer)",
                      "bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
                      "frac": achieved / peak_burst, "traffic": traffic,
-                     "peak_source": f"{peak_src} bf16 burst {peak_burst * 6:.1f} / 6 (bf16x3: 6 MMAs per fp32 MAC)",
+                     "peak_source": f"{peak_src} bf16 burst {peak_burst * mmas:.1f} TFLOP/s (fp16 MMAs run at the bf16 "
+                                    f"rate) / {mmas} ({operand_format(mmas)}: {mmas} MMAs per useful fp32 multiply-add)",
                      "frac_vs_sustained": achieved / peak_sus,
                      "work": f"useful fp32 FLOPs 2MNK per GEMM launch: {(d_fl + s_fl) / 1e9:.1f} GFLOP per step "
                              f"per rank (dense {d_fl / 1e9:.1f}, score {s_fl / 1e9:.1f})",

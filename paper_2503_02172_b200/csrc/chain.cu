@@ -497,15 +497,24 @@ int launch_split_copy(const float* src, int64_t n, Split dst, cudaStream_t st) {
 }
 
 // [rows, cols] fp32 with row stride lds -> split planes with row stride dst.ld (>= cols)
-__global__ void k_split_copy_rows(const float* __restrict__ src, int64_t lds, int64_t rows, int cols, Split dst) {
+// weight form (store_split_w: the GEMMs' W operand) or, act = true, the activation form
+__global__ void k_split_copy_rows(const float* __restrict__ src, int64_t lds, int64_t rows, int cols, Split dst,
+                                  bool act) {
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    store_split_w(dst, (i / cols) * dst.ld + i % cols, src[(i / cols) * lds + i % cols]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (i / cols) * dst.ld + i % cols;
+    const float x = src[(i / cols) * lds + i % cols];
+    if (act)
+      store_split(dst, o, x);
+    else
+      store_split_w(dst, o, x);
+  }
 }
 
-int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st, int64_t lds) {
-  k_split_copy_rows<<<1024, 256, 0, st>>>(src, lds > 0 ? lds : cols, rows, cols, dst);
+int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st, int64_t lds,
+                           bool act) {
+  k_split_copy_rows<<<1024, 256, 0, st>>>(src, lds > 0 ? lds : cols, rows, cols, dst, act);
   return 1;
 }
 

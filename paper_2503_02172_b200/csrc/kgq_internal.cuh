@@ -393,5 +393,8 @@ int launch_transpose_shard(const float* ent, int64_t e0, int64_t ns, int d, int 
 int launch_betae_entity_terms(const float* ent, int64_t e0, int64_t ns, int d, float* tab,
                               int64_t np, cudaStream_t st);
 int launch_split_copy(const float* src, int64_t n, Split dst, cudaStream_t st);
-int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st, int64_t lds = 0);
+// fp32 [rows, cols] (row stride lds) -> split planes: the weight (W operand) form, or act = true
+// the activation (A operand) form (common.cuh split3 / split3_w)
+int launch_split_copy_rows(const float* src, int64_t rows, int cols, Split dst, cudaStream_t st, int64_t lds = 0,
+                           bool act = false);
 }  // namespace kgq

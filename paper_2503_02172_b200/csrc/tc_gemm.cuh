@@ -281,8 +281,12 @@ __device__ unsigned long long* g_tc_trace;
 // non-negation structures at up to 9.9e-5 of the 1e-4 bound, DRAIN 4 at <= 6.5e-5 for -1% of
 // the C2 step, DRAIN 2 at <= 2.6e-5 for -5% (its shorter partials hide the accumulator hand-off
 // -- MMA commit -> epilogue drain -> accempty -- worse).
+// fp16x2 operands (3 MMAs per K16 step instead of 6): DRAIN 8 puts the same 48 truncating MMA
+// accumulations into a partial as bf16x3's DRAIN 4 -- chain errors vs the oracle at C2 <= 5.2e-5
+// without negation (DRAIN 4: 3.1e-5, 16: 9.8e-5), inp 5.8e-4 (16: 1.2e-3, over its bound) -- for
+// +5% on the C2 step (profiles/r02/operand_accuracy.txt).
 #ifndef KGQ_TC_DRAIN
-#define KGQ_TC_DRAIN 4
+#define KGQ_TC_DRAIN (KGQ_OPERAND_FP16X2 ? 8 : 4)
 #endif
 constexpr int DRAIN = KGQ_TC_DRAIN;
 
@@ -1038,8 +1042,14 @@ struct Plan {
 //   t = c0 + whole rounds x nk x kb[BN] + tail kper x kb[BN] + [split] (pub + (s-1) part) x BN
 // (picks a plan within 3.4 us of the best over all 17 shapes; the previous clock-count model
 // lost ~14 us, mostly on the N = 400 / 1600, K = 800 layers at M = 1-3K).
-constexpr double kKbUs[5] = {0.623, 0.675, 0.687, 0.760, 1.004};  // BN 64 128 160 192 256
-constexpr double kC0Us = 3.40, kPubUs = 0.0230, kPartUs = 0.0113;
+// bf16x3 operands (6 MMAs per K16 step; profiles/r01/tc_plan_fit.txt)
+constexpr double kKbUsB[5] = {0.623, 0.675, 0.687, 0.760, 1.004};  // BN 64 128 160 192 256
+// fp16x2 operands (3 MMAs per K16 step, DRAIN 8), refit on 26 shapes incl. the mixed step's M = 4-28K
+// layers (profiles/r02/tc_plan_fit_fp16x2.txt): per column BN = 256 is now the cheapest tile
+constexpr double kKbUsH[5] = {0.493, 0.494, 0.516, 0.533, 0.633};
+constexpr const double* kKbUs = kFp16x2 ? kKbUsH : kKbUsB;
+constexpr double kC0Us = kFp16x2 ? -1.12 : 3.40, kPubUs = kFp16x2 ? 0.0281 : 0.0230,
+                 kPartUs = kFp16x2 ? 0.0163 : 0.0113;
 // 160 (split-output dense layers only: 16-column chunks) tiles N = 800 / 1600 exactly
 constexpr int kTileBN[5] = {64, 128, 160, 192, 256};
 struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN, KGQ_GEMM_KB128 (us per K-block)

@@ -51,7 +51,7 @@ int main(int argc, char** argv) {
     return s;
   };
   Split A = mk(M, K), Wsp = mk(N, K), Ysp = mk(M, N);
-  launch_split_copy_rows(dx, M, K, A, 0);
+  launch_split_copy_rows(dx, M, K, A, 0, 0, true);
   launch_split_copy_rows(dw, N, K, Wsp, 0);
   GemmWs gws;
   cudaMalloc(&gws.ws, kGemmWsFloats * 4);
@@ -86,9 +86,21 @@ int main(int argc, char** argv) {
           want = ref[(size_t)m * N + n] + b[n];
           if (form == 1) want = fmax(want, 0.0);
           scale = mag[(size_t)m * N + n];
-          if (form == 1) {  // three bf16 planes, exact sum
+          if (form == 1) {  // the activation split: three bf16 planes (exact sum) or fp16 hi + 2^11-scaled lo
             const size_t o = (size_t)m * Ysp.ld + n;
-            got = (bf(hb[o]) + bf(hb[pl + o])) + bf(hb[2 * pl + o]);
+            if (kgq::kFp16x2) {
+              auto hf = [](uint16_t u) {  // fp16 bits -> float
+                const uint32_t sgn = (u & 0x8000u) << 16, ex = (u >> 10) & 0x1F, man = u & 0x3FF;
+                if (ex == 0) return (sgn ? -1.0f : 1.0f) * ldexpf((float)man, -24);
+                const uint32_t v = sgn | ((ex + 112) << 23) | (man << 13);
+                float f;
+                memcpy(&f, &v, 4);
+                return f;
+              };
+              got = hf(hb[o]) + hf(hb[pl + o]) * (1.0f / 2048.0f);
+            } else {
+              got = (bf(hb[o]) + bf(hb[pl + o])) + bf(hb[2 * pl + o]);
+            }
           } else {
             got = y[(size_t)m * N + n];
           }

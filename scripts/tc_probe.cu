@@ -36,7 +36,11 @@ int main() {
                           {3072, 400, 800, false},   {1024, 800, 1600, false}, {1024, 1600, 1600, false},
                           {1024, 1600, 800, false},  {2048, 1600, 800, false},  {3072, 1600, 800, false},
                           {2048, 1600, 1600, false}, {3072, 800, 1600, false},  {3072, 800, 800, false},
-                          {1024, 400, 800, false}};
+                          {1024, 400, 800, false},
+                          // the mixed-submit step's shapes (M = rows of all types' branches per hop)
+                          {27648, 1600, 800, false}, {27648, 1600, 1600, false}, {27648, 800, 1600, false},
+                          {7168, 1600, 800, false},  {7168, 1600, 1600, false},  {7168, 800, 1600, false},
+                          {20480, 800, 800, false},  {20480, 400, 800, false},   {4096, 14592, 800, true}};
 #ifdef KGQ_TC_TRACE
   unsigned long long* tr;
   cudaMalloc(&tr, 8192 * 64);
@@ -63,7 +67,7 @@ int main() {
       return s;
     };
     Split A = mk(M, K), Wsp = mk(N, K), Ysp = mk(M, N);
-    launch_split_copy_rows(xf, M, K, A, 0);
+    launch_split_copy_rows(xf, M, K, A, 0, 0, true);
     launch_split_copy_rows(wf, N, K, Wsp, 0);
     cudaMemset(b, 0, N * 4); cudaMemset(P, 0, M * 8); cudaMemset(E, 0, N * 8);
     static GemmWs gws;
