@@ -227,6 +227,17 @@ static bool range_flags_taken() {
   return (a | b | c) != 0;
 }
 
+// Hop-0 first layer from a per-entity precompute (chain.cu k_mix_h0_pre) when the [N, H] fp32
+// table fits this budget; KGQ_NO_HPRE=1 disables it (A/B)
+constexpr double kHpreBytesMax = 2.0 * (1ull << 30);
+static bool hpre_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("KGQ_NO_HPRE");
+    return !(e && e[0] && e[0] != '0');
+  }();
+  return v;
+}
+
 // KGQ_NO_FUSED_TOPK=1: new contexts default to KGQ_FUSED_OFF (A/B runs)
 bool fused_topk_disabled() {
   static const bool v = [] {
@@ -299,28 +310,41 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
   if (ctx->RW) {
     // first layer with the relation input factored out (RelTerm): K = 2d straight from the state
     // rows (contiguous run) or from the gathered anchor rows; accumulators start at RW[r]
-    if (src_row0 < 0) {
-      L += launch_betae_mlp_input(ca, ctx->ent, ctx->rel[0], B, g, src_state, ctx->Z, st, false);
-      A = ctx->Z;
+    if (src_row0 < 0 && ctx->Hpre) {
+      // hop 0 from the per-entity precompute: H0 = ReLU(Hpre[anchor] + RW[r] + b1), no GEMM
+      MixSegs sg;
+      for (int gi = 0; gi < n; ++gi) {
+        MixSeg& m = sg.s[sg.n++];
+        m.dst0 = gi * B; m.B = B; m.q0 = 0; m.kind = 0; m.src0 = 0;
+        m.anchors = ca.anchors; m.n_a = ca.n_a; m.aslot = g.anchor_slot[gi];
+        m.rels = ca.rels; m.n_r = ca.n_r; m.rslot = g.rel_slot[gi];
+      }
+      L += launch_mix_h0_pre(sg, M, ctx->Hpre, ctx->RW, ctx->lin1x.b, ctx->lin1x.out_f, ctx->H[0], ctx->cfg.n_entity,
+                             ctx->cfg.n_relation, ca.err, ca.invalid, st);
     } else {
-      A = src_state.at(src_row0);
-    }
-    RelTerm rt;
-    rt.RW = ctx->RW;
-    rt.ldrw = ctx->cfg.hidden;
-    rt.M = M;
-    rt.B = B;
-    rt.rels = ca.rels;
-    rt.n_r = ca.n_r;
-    rt.n_relation = ca.n_relation;
-    for (int gi = 0; gi < n; ++gi) rt.rel_slot[gi] = g.rel_slot[gi];
-    rt.err = ca.err;
-    rt.invalid = ca.invalid;
-    {
-      StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
-      L += launch_linear_rel(A, M, 2 * d, ctx->lin1x, rt, ctx->H[0], &ctx->gws, st);
-      check_site("dense layer (relation term)");
-    }
+      if (src_row0 < 0) {
+        L += launch_betae_mlp_input(ca, ctx->ent, ctx->rel[0], B, g, src_state, ctx->Z, st, false);
+        A = ctx->Z;
+      } else {
+        A = src_state.at(src_row0);
+      }
+      RelTerm rt;
+      rt.RW = ctx->RW;
+      rt.ldrw = ctx->cfg.hidden;
+      rt.M = M;
+      rt.B = B;
+      rt.rels = ca.rels;
+      rt.n_r = ca.n_r;
+      rt.n_relation = ca.n_relation;
+      for (int gi = 0; gi < n; ++gi) rt.rel_slot[gi] = g.rel_slot[gi];
+      rt.err = ca.err;
+      rt.invalid = ca.invalid;
+      {
+        StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
+        L += launch_linear_rel(A, M, 2 * d, ctx->lin1x, rt, ctx->H[0], &ctx->gws, st);
+        check_site("dense layer (relation term)");
+      }
+    }  // first layer done (precompute gather or GEMM)
     A = ctx->H[0];
     K = ctx->lin1x.out_f;
     l0 = 1;
@@ -586,7 +610,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   F(ctx->ent); F(ctx->rel[0]); F(ctx->rel[1]); F(ctx->score_tab);
   for (auto& l : ctx->lin) { F(l.W); F(l.Wsp.b0); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) F(s->b0);
-  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->cand); F(ctx->d_err); F(ctx->d_invalid);
+  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->cand); F(ctx->Hpre); F(ctx->zero_bias); F(ctx->d_err); F(ctx->d_invalid);
   F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum); F(ctx->uvT); F(ctx->lin1x.Wsp.b0); F(ctx->RW);
   F(ctx->mix_rid); F(ctx->mix_map);
   if (ctx->mix_map_host) cudaFreeHost(ctx->mix_map_host);
@@ -770,6 +794,37 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
     launch_betae_entity_terms(ctx->ent, ctx->e0, ctx->ns, d, ctx->score_tab, ctx->np, 0);
     launch_betae_uv_table(ctx->ent, c.n_entity, ctx->e0, ctx->ns, ctx->np, d, ctx->uvsums, ctx->uv,
                           ctx->Esum, ctx->uvT, 0);
+    // weights / entity terms converted so far must be in the operand format's range
+    CK(cudaDeviceSynchronize(), "finalize");
+    if (range_flags_taken())
+      return fail(ctx, KGQ_ERANGE, "a weight (|w| >= 32) or BetaE entity term is outside the fp16x2 operand range; "
+                  "use the bf16x3 build (libkgq_bf16x3.so, KGQ_OPERANDS=bf16x3)");
+    if (ctx->RW && hpre_enabled() && (double)c.n_entity * ctx->lin1x.out_f * sizeof(float) <= kHpreBytesMax) {
+      // hop-0 first layer per entity: Hpre = X W1[:, :2d]^T over the regularised table (the same
+      // tensor-core GEMM as the layer itself, no bias), through a temporary split copy of X.  An
+      // entity row outside the fp16x2 range only disables the precompute (hop 0 then gathers and
+      // multiplies per query, and flags such an anchor when a query uses it).
+      const int H = ctx->lin1x.out_f;
+      if (!ctx->Hpre) {
+        kgq_status st2 = dalloc(ctx, &ctx->Hpre, (size_t)c.n_entity * H, "hop-0 layer-1 precompute");
+        if (!st2) st2 = dalloc(ctx, &ctx->zero_bias, (size_t)H, "zero bias");
+        if (st2) return st2;
+        CK(cudaMemset(ctx->zero_bias, 0, (size_t)H * sizeof(float)), "zero bias");
+      }
+      Split X;
+      kgq_status st2 = alloc_split(ctx, &X, c.n_entity, 2 * d, "entity split (finalize)");
+      if (st2) return st2;
+      launch_split_copy_rows(ctx->ent, c.n_entity, 2 * d, X, 0, 2 * d, true);
+      Linear l0 = ctx->lin1x;
+      l0.b = ctx->zero_bias;
+      launch_linear(X, (int)c.n_entity, 2 * d, l0, kEpiNone, Split{}, ctx->Hpre, H, 0, 0, &ctx->gws, 0);
+      CK(cudaDeviceSynchronize(), "hop-0 precompute");
+      cudaFree(X.b0);
+      if (range_flag_chain()) {  // the X split (the only conversion of this interval) overflowed
+        cudaFree(ctx->Hpre);
+        ctx->Hpre = nullptr;
+      }
+    }
   } else {
     launch_transpose_shard(ctx->ent, ctx->e0, ctx->ns, d, ctx->ew, ctx->score_tab, ctx->np, 0);
   }
@@ -1088,7 +1143,7 @@ struct MixGroup {
 // The projection MLP (Eq. 4) over rows [r0, r0 + M) of a hop batch already gathered into Z
 // (relation ids in mix_rid); rows >= neg0 (batch-relative) are negated.  On `st` with split-K
 // workspace / span group `ws`.
-static int mlp_rows(kgq_ctx* ctx, int r0, int M, int neg0, cudaStream_t st, const GemmWs* ws) {
+static int mlp_rows(kgq_ctx* ctx, int r0, int M, int neg0, cudaStream_t st, const GemmWs* ws, bool l1_done) {
   const int d = ctx->cfg.dim;
   int L = 0;
   RelTerm rt;
@@ -1096,7 +1151,7 @@ static int mlp_rows(kgq_ctx* ctx, int r0, int M, int neg0, cudaStream_t st, cons
   rt.ldrw = ctx->cfg.hidden;
   rt.M = M;
   rt.rid = ctx->mix_rid + r0;
-  {
+  if (!l1_done) {  // else H0 rows came from the per-entity precompute (hop 0)
     StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
     L += launch_linear_rel(ctx->Z.at(r0), M, 2 * d, ctx->lin1x, rt, ctx->H[0].at(r0), ws, st);
   }
@@ -1152,18 +1207,25 @@ static bool side_stream(kgq_ctx* ctx) {  // lazily created; false if CUDA refuse
 static int mix_mlp(kgq_ctx* ctx, const MixSegs& sg, int M, int neg0, cudaStream_t st) {
   const int d = ctx->cfg.dim;
   int L = 0;
-  L += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,
-                         ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
+  // hop 0 (every row anchor-sourced) with the per-entity precompute: the first layer is a gather
+  bool pre = ctx->Hpre != nullptr;
+  for (int i = 0; i < sg.n && pre; ++i) pre = sg.s[i].kind == 0;
+  if (pre)
+    L += launch_mix_h0_pre(sg, M, ctx->Hpre, ctx->RW, ctx->lin1x.b, ctx->lin1x.out_f, ctx->H[0], ctx->cfg.n_entity,
+                           ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
+  else
+    L += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,
+                           ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
   const int half = ((M / 2 + 255) / 256) * 256;  // 256-row (one tile pair) aligned cut
   // (a failing fork / join call leaves its error for the submit's final cudaGetLastError check)
   if (M >= 8192 && split_mlp_enabled() && side_stream(ctx) && cudaEventRecord(ctx->side_ev[0], st) == cudaSuccess &&
       cudaStreamWaitEvent(ctx->side_st, ctx->side_ev[0], 0) == cudaSuccess) {
-    L += mlp_rows(ctx, 0, half, neg0, st, &ctx->gws);
-    L += mlp_rows(ctx, half, M - half, neg0, ctx->side_st, &ctx->gws2);
+    L += mlp_rows(ctx, 0, half, neg0, st, &ctx->gws, pre);
+    L += mlp_rows(ctx, half, M - half, neg0, ctx->side_st, &ctx->gws2, pre);
     cudaEventRecord(ctx->side_ev[1], ctx->side_st);
     cudaStreamWaitEvent(st, ctx->side_ev[1], 0);
   } else {
-    L += mlp_rows(ctx, 0, M, neg0, st, &ctx->gws);
+    L += mlp_rows(ctx, 0, M, neg0, st, &ctx->gws, pre);
   }
   L += launch_mix_scatter(sg, M, ctx->I, ctx->S, 2 * d, st);
   check_site("mixed hop");
