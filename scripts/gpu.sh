@@ -36,7 +36,7 @@ for task in "$@"; do
     launches-warm) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
                 --cache-control none --csv --log-file $OUT/launches_warm.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
                 --no-per-type --no-c5a > /dev/null 2>&1 ;;
-    ncu-small) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_mix_score_prep|k_mix_gather|k_topk_cmin|k_mix_scatter|k_mix_combine" \
+    ncu-small) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_mix_score_prep|k_mix_gather|k_topk_cmin|k_topk_lists|k_mix_scatter|k_mix_combine|k_mix_h0_pre" \
                 -s 11 -c 11 -o $OUT/prof_small -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-per-type --no-c5a > /dev/null 2>&1 ;;
     ncu-score) timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:EpiBetaScore -s 2 -c 2 \
                 -o $OUT/prof_score -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-per-type --no-c5a > /dev/null 2>&1 ;;
