@@ -5,6 +5,8 @@
 // embeddings q are [B, nb, w] fp32 (w = d GQE, 2d Q2B [centre; offset], 2d BetaE
 // [alpha; beta]).  All index reads are range-checked on the device (kgq.h: dist NaN,
 // id -1, KGQ_ERANGE), with the offending id clamped to 0 so no read is out of bounds.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kgq_internal.cuh"
 
@@ -263,7 +265,10 @@ __global__ void k_mix_h0_pre(MixSegs sg, const float* __restrict__ Hpre, const f
 int launch_mix_h0_pre(const MixSegs& sg, int M, const float* Hpre, const float* RW, const float* bias, int H,
                       Split H0, int64_t n_entity, int n_relation, int32_t* err, int32_t* invalid, cudaStream_t st) {
   if (M <= 0) return 0;
-  launch_pdl(k_mix_h0_pre, dim3(M), dim3(256), 0, st, sg, Hpre, RW, bias, H, H0, n_entity, n_relation, err, invalid);
+  // one thread per 8 columns: H = 1600 -> 200 threads, a 224-thread block (89% of its lanes busy)
+  const int threads = std::min(256, std::max(32, ((H / 8 + 31) / 32) * 32));
+  launch_pdl(k_mix_h0_pre, dim3(M), dim3(threads), 0, st, sg, Hpre, RW, bias, H, H0, n_entity, n_relation, err,
+             invalid);
   return 1;
 }
 

@@ -121,15 +121,21 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
 // Mixed batches: score row r is the split state row srcrow[r] of S (no fp32 round trip).
 // Single-structure submits (srcrow == nullptr): score row r of the chunk starting at query b0 is
 // branch r % nout of query b0 + r / nout, i.e. state row (r % nout) * B + b0 + r / nout.
-__global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, int d,
-                                 const double* __restrict__ sums, int64_t ns, Split A, float2* __restrict__ P,
-                                 int64_t B, int64_t b0, int nout) {
+// One WARP per score row, four rows per 128-thread block (the log table staged once per block):
+// d = 400 dims are 12-13 per lane instead of 3-4 per thread of a 128-thread block per row, whose
+// 16 four-dim threads left the other 112 idle for the last chain (25% of the fp64 time), and the
+// row sum is a shuffle tree without __syncthreads.
+constexpr int kPrepRows = 4;
+__global__ void __launch_bounds__(32 * kPrepRows)
+    k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, int d, const double* __restrict__ sums, int64_t ns,
+                     Split A, float2* __restrict__ P, int64_t B, int64_t b0, int nout, int rows) {
   pdl_grid_sync();
-  const int r = blockIdx.x;
-  __shared__ double red[32];
   __shared__ double tab[2 * kLogTab];  // ln c_i, 1 / c_i (stored after the [2][d] sums)
   for (int i = threadIdx.x; i < 2 * kLogTab; i += blockDim.x) tab[i] = sums[2 * d + i];
   __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kPrepRows + (threadIdx.x >> 5);
+  if (r >= rows) return;
   double p = 0.0;
   const double inv = 1.0 / (double)ns;
   const int64_t srow = srcrow ? srcrow[r] : (int64_t)(r % nout) * B + b0 + r / nout;
@@ -137,16 +143,16 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
   if ((d & 7) == 0 && (S.ld & 7) == 0 && (A.ld & 7) == 0) {
     // the row copy as 16-byte plane accesses (a plain copy of the split planes), then the fp64
     // P_q terms from the fp32 values
-    for (int j = 8 * threadIdx.x; j < 2 * d; j += 8 * blockDim.x)
+    for (int j = 8 * lane; j < 2 * d; j += 8 * 32)
 #pragma unroll
       for (int p3 = 0; p3 < kSplitPlanesA; ++p3)
         *reinterpret_cast<uint4*>(A.plane(p3) + a0 + j) = *reinterpret_cast<const uint4*>(S.plane(p3) + s0 + j);
-    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    for (int j = lane; j < d; j += 32) {
       const double da = load_split(S, s0 + j), db = load_split(S, s0 + d + j);
       p += lnbeta_f64_tab(da, db, tab, tab + kLogTab) + da * sums[j] * inv + db * sums[d + j] * inv;
     }
   } else {
-    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    for (int j = lane; j < d; j += 32) {
       const float a = load_split(S, s0 + j), b = load_split(S, s0 + d + j);
       store_split(A, a0 + j, a);
       store_split(A, a0 + d + j, b);
@@ -155,13 +161,7 @@ __global__ void k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, in
     }
   }
   p = warp_sum(p);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) P[r] = split_f64(t);
-  }
+  if (lane == 0) P[r] = split_f64(p);
 }
 
 // TK (fused top-k): no distance block; the epilogue keeps every output row's k
@@ -243,7 +243,8 @@ int launch_betae_uv_table(const float* ent, int64_t n_all, int64_t e0, int64_t n
 int launch_mix_score_prep(const int64_t* srcrow, Split S, int rows, int d, const double* sums, int64_t ns,
                           Split A, float2* P, cudaStream_t st, int64_t B, int64_t b0, int nout) {
   if (rows <= 0) return 0;
-  launch_pdl(k_mix_score_prep, dim3(rows), dim3(128), 0, st, srcrow, S, d, sums, ns, A, P, B, b0, nout);
+  launch_pdl(k_mix_score_prep, dim3((rows + kPrepRows - 1) / kPrepRows), dim3(32 * kPrepRows), 0, st, srcrow, S, d,
+             sums, ns, A, P, B, b0, nout, rows);
   return 1;
 }
 

@@ -496,6 +496,24 @@ int launch_topk_cmin(const float* dist, int64_t ldd, const float* cmin, int64_t 
 // columns of different lists are disjoint, so keys are unique and the result is exactly the first
 // k of the row in (distance, id) order.  Rows [0, rows1) have nl1 lists, the rest nl2 (mixed
 // batches: non-union then union scorer launch).
+// lane j < k writes output j of the row from its merged key (fewer than k entities: NaN / -1)
+__device__ __forceinline__ void topk_lists_out(unsigned long long key, int lane, int k, int ob, int64_t id_base,
+                                               float* od, int32_t* oi, const PeerPush& pp) {
+  unsigned long long gk = ~0ull;
+  if (lane < k) {
+    if (key == ~0ull) {
+      od[lane] = __uint_as_float(0x7FFFFFFFu);
+      oi[lane] = -1;
+    } else {
+      const uint32_t gid = (uint32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
+      od[lane] = fkey_inv((uint32_t)(key >> 32));
+      oi[lane] = (int32_t)gid;
+      gk = (key & 0xFFFFFFFF00000000ull) | gid;
+    }
+  }
+  if (pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
+}
+
 __global__ void __launch_bounds__(128)
     k_topk_lists(const unsigned long long* __restrict__ cand, int64_t ldcand, int k, int rows1, int nl1, int nl2,
                  int64_t id_base, const int32_t* __restrict__ invalid, const int32_t* __restrict__ out_row,
@@ -516,8 +534,33 @@ __global__ void __launch_bounds__(128)
     return;
   }
   const int nl = b < rows1 ? nl1 : nl2;
-  // lane l holds the heads of lists l, l + 32, l + 64, l + 96 (<= 128 lists)
   const unsigned long long* row = cand + (int64_t)b * ldcand;
+  if (nl <= 32 && k <= 16) {
+    // <= 32 lists: lane l loads its whole list up front (independent loads, no load per round)
+    // and shifts it down as its head is consumed
+    unsigned long long lst[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) lst[j] = (lane < nl && j < k) ? row[(int64_t)lane * k + j] : ~0ull;
+    unsigned long long key = ~0ull;  // output j = lane
+    for (int j = 0; j < k; ++j) {
+      unsigned long long w = lst[0];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, w, o);
+        w = t < w ? t : w;
+      }
+      if (lane == j) key = w;
+      if (w == ~0ull) break;  // fewer than k entities
+      if (lst[0] == w) {      // unique keys: exactly one lane's head
+#pragma unroll
+        for (int q = 0; q < 15; ++q) lst[q] = lst[q + 1];
+        lst[15] = ~0ull;
+      }
+    }
+    topk_lists_out(key, lane, k, ob, id_base, od, oi, pp);
+    return;
+  }
+  // lane l holds the heads of lists l, l + 32, l + 64, l + 96 (<= 128 lists)
   int pos[4];
   unsigned long long head[4];
 #pragma unroll
@@ -547,19 +590,7 @@ __global__ void __launch_bounds__(128)
         }
     }
   }
-  unsigned long long gk = ~0ull;
-  if (lane < k) {
-    if (key == ~0ull) {
-      od[lane] = __uint_as_float(0x7FFFFFFFu);
-      oi[lane] = -1;
-    } else {
-      const uint32_t gid = (uint32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
-      od[lane] = fkey_inv((uint32_t)(key >> 32));
-      oi[lane] = (int32_t)gid;
-      gk = (key & 0xFFFFFFFF00000000ull) | gid;
-    }
-  }
-  if (pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
+  topk_lists_out(key, lane, k, ob, id_base, od, oi, pp);
 }
 
 int launch_topk_lists(const unsigned long long* cand, int64_t ldcand, int k, int B, int rows1, int nl1, int nl2,
