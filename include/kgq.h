@@ -289,7 +289,10 @@ kgq_status kgq_rank_metrics(kgq_ctx* ctx, int32_t batch, const int32_t* ans_off,
                             const uint8_t* hard, double* metrics, kgq_stream stream);
 /* Synchronise `stream`; KGQ_ERANGE (message names query row and slot) if any submit since
  * the last check saw an out-of-range id, KGQ_ECUDA on an asynchronous CUDA error, KGQ_ENCCL on
- * an asynchronous error of the context's communicator. */
+ * an asynchronous error of the context's communicator.  KGQ_ERANGE also when a GEMM operand
+ * reached the fp16x2 range (|x| >= 65504, see kgq_tensor_mmas_per_fma): that flag is kept per
+ * device and process (any context's conversion on this device since the last check reports it),
+ * and the affected results are not exact -- rerun with the bf16x3 build. */
 kgq_status kgq_check_errors(kgq_ctx* ctx, kgq_stream stream);
 
 /* ---- options -------------------------------------------------------------------------- */

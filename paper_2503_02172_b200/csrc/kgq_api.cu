@@ -1706,8 +1706,14 @@ kgq_status kgq_set_option(kgq_ctx* ctx, int32_t option, int64_t value) {
       return fail(ctx, KGQ_EINVAL, "KGQ_OPT_FUSED_TOPK: value %lld is not OFF / ON / AUTO", (long long)value);
     if (ctx->fused_topk != (int)value) {
       ctx->fused_topk = (int)value;
-      // captured graphs hold the previous path: re-capture
-      for (auto& g : ctx->graphs) destroy_graph_entry(g);
+      // captured graphs hold the previous path: re-capture (after the device drained them and
+      // their stage events were harvested, as kgq_ktime_enable does)
+      DeviceGuard g(ctx->cfg.device);
+      CK(cudaDeviceSynchronize(), "set_option");
+      for (auto& gr : ctx->graphs) {
+        if (gr.pending) harvest(ctx, gr.evs, false);
+        destroy_graph_entry(gr);
+      }
       ctx->graphs.clear();
       clear_mix_graphs(ctx);
     }
