@@ -1143,7 +1143,10 @@ struct MixGroup {
 // The projection MLP (Eq. 4) over rows [r0, r0 + M) of a hop batch already gathered into Z
 // (relation ids in mix_rid); rows >= neg0 (batch-relative) are negated.  On `st` with split-K
 // workspace / span group `ws`.
-static int mlp_rows(kgq_ctx* ctx, int r0, int M, int neg0, cudaStream_t st, const GemmWs* ws, bool l1_done) {
+// rm (optional, regulariser terminal): the last layer writes its rows straight into S through
+// this remap (batch row -> S row) instead of into I (then no scatter is needed).
+static int mlp_rows(kgq_ctx* ctx, int r0, int M, int neg0, cudaStream_t st, const GemmWs* ws, bool l1_done,
+                    const RowMap* rm = nullptr) {
   const int d = ctx->cfg.dim;
   int L = 0;
   RelTerm rt;
@@ -1169,10 +1172,25 @@ static int mlp_rows(kgq_ctx* ctx, int r0, int M, int neg0, cudaStream_t st, cons
     float* T = ctx->T + (int64_t)r0 * 2 * d;
     L += dense(ctx, A, M, K, lo, kEpiNone, T, 2 * d, st);
     L += launch_softmax_terminal(T, 2 * d, M, 2 * d, ctx->I.at(r0), 0, ng, M, st);
+  } else if (rm) {
+    RowMap h = *rm;  // this range's rows are batch rows r0 + i: shift the segment starts by r0
+    for (int i = 0; i < h.n; ++i) h.dst0[i] -= r0;
+    StageTimer t(ctx, st, kStDense, 2.0 * M * (double)lo.out_f * K);
+    L += launch_linear_map(A, M, K, lo, kEpiBetaReg, ctx->S, ctx->rows_max, h, ng, M, ws, st);
+    check_site("dense layer (remapped into S)");
   } else {
     L += dense(ctx, A, M, K, lo, kEpiBetaReg, ctx->I.at(r0), ng, M, st, ws);
   }
   return L;
+}
+
+// KGQ_NO_REMAP=1: the last MLP layer writes the scratch I and a scatter kernel moves its rows to S
+static bool remap_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("KGQ_NO_REMAP");
+    return !(e && e[0] && e[0] != '0');
+  }();
+  return v;
 }
 
 // KGQ_NO_SPLIT_MLP=1: every hop MLP as one chain of launches on the context's stream
@@ -1216,18 +1234,29 @@ static int mix_mlp(kgq_ctx* ctx, const MixSegs& sg, int M, int neg0, cudaStream_
   else
     L += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,
                            ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
+  // the last layer writes S directly when every segment is whole 32-row boxes (B % 32 == 0 for
+  // every group: the TMA store boxes of the epilogue never straddle two segments)
+  RowMap rm;
+  bool remap = ctx->cfg.terminal == KGQ_TERM_REGULARIZER && sg.n <= kMaxRowMap && remap_enabled();
+  for (int i = 0; i < sg.n && remap; ++i) {
+    remap = sg.s[i].dst0 % 32 == 0 && sg.s[i].B % 32 == 0;
+    rm.dst0[i] = sg.s[i].dst0;
+    rm.src0[i] = (int)sg.s[i].src0;
+  }
+  rm.n = remap ? sg.n : 0;
+  const RowMap* rmp = remap ? &rm : nullptr;
   const int half = ((M / 2 + 255) / 256) * 256;  // 256-row (one tile pair) aligned cut
   // (a failing fork / join call leaves its error for the submit's final cudaGetLastError check)
   if (M >= 8192 && split_mlp_enabled() && side_stream(ctx) && cudaEventRecord(ctx->side_ev[0], st) == cudaSuccess &&
       cudaStreamWaitEvent(ctx->side_st, ctx->side_ev[0], 0) == cudaSuccess) {
-    L += mlp_rows(ctx, 0, half, neg0, st, &ctx->gws, pre);
-    L += mlp_rows(ctx, half, M - half, neg0, ctx->side_st, &ctx->gws2, pre);
+    L += mlp_rows(ctx, 0, half, neg0, st, &ctx->gws, pre, rmp);
+    L += mlp_rows(ctx, half, M - half, neg0, ctx->side_st, &ctx->gws2, pre, rmp);
     cudaEventRecord(ctx->side_ev[1], ctx->side_st);
     cudaStreamWaitEvent(st, ctx->side_ev[1], 0);
   } else {
-    L += mlp_rows(ctx, 0, M, neg0, st, &ctx->gws, pre);
+    L += mlp_rows(ctx, 0, M, neg0, st, &ctx->gws, pre, rmp);
   }
-  L += launch_mix_scatter(sg, M, ctx->I, ctx->S, 2 * d, st);
+  if (!remap) L += launch_mix_scatter(sg, M, ctx->I, ctx->S, 2 * d, st);
   check_site("mixed hop");
   return L;
 }

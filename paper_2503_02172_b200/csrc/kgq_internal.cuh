@@ -242,6 +242,18 @@ struct RelTerm {
 };
 int launch_linear_rel(const Split& A, int M, int K, const Linear& L, const RelTerm& rt, const Split& out,
                       const GemmWs* ws, cudaStream_t st);
+// Output row remap of a dense layer (the mixed path's last MLP layer writes its rows straight into
+// the state S instead of a scratch + scatter): GEMM row r of segment i (dst0[i] <= r, segments
+// ascending, every segment a multiple of 32 rows) goes to output row src0[i] + r - dst0[i].
+constexpr int kMaxRowMap = 48;
+struct RowMap {
+  int n = 0;
+  int dst0[kMaxRowMap];
+  int src0[kMaxRowMap];
+};
+// launch_linear with the split output rows remapped (out = the whole target, out_rows its rows)
+int launch_linear_map(const Split& A, int M, int K, const Linear& L, int epi, const Split& out, int64_t out_rows,
+                      const RowMap& rm, int neg0, int neg1, const GemmWs* ws, cudaStream_t st);
 // ---- mixed-structure batches (kgq_submit_mixed) ----------------------------
 // One block of B query rows inside a batched hop: rows [dst0, dst0 + B) of the batch come from
 // anchor slot aslot (kind 0), state rows src0 + b of S (kind 1) or of the combined state Mst

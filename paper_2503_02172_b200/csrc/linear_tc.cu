@@ -33,6 +33,16 @@ struct EpiLinear {
   const float* bias;
   int N, neg0, neg1;
   RelTerm rt;
+  RowMap rm{};   // optional output row remap (rm.n > 0): rows >= rows are not stored
+  int rows = 0;
+  // destination row of the 32-row output box starting at GEMM row row0 (-1: nothing to store)
+  __device__ __forceinline__ int out_row(int row0) const {
+    if (rm.n == 0) return row0;
+    if (row0 >= rows) return -1;
+    int i = 0;
+    while (i + 1 < rm.n && rm.dst0[i + 1] <= row0) ++i;
+    return rm.src0[i] + row0 - rm.dst0[i];
+  }
   template <int CW>
   __device__ __forceinline__ void init(int row, int n0, float* acc) const {
     if (row >= rt.M) return;
@@ -107,6 +117,25 @@ int launch_linear_rel(const Split& A, int M, int K, const Linear& L, const RelTe
   const tc::OutDesc o{nullptr, 0, out, M, L.out_f};
   return tc::launch_gemm_auto(A, M, L.Wsp, L.out_f, K, o, EpiLinear<kEpiRelu, true, true>{L.b, L.out_f, 0, 0, rt},
                               ws, st);
+}
+
+int launch_linear_map(const Split& A, int M, int K, const Linear& L, int epi, const Split& out, int64_t out_rows,
+                      const RowMap& rm, int neg0, int neg1, const GemmWs* ws, cudaStream_t st) {
+  if (M <= 0) return 0;
+  const tc::OutDesc o{nullptr, 0, out, out_rows, L.out_f};
+#define KGQ_EPI_MAP(E)                                                             \
+  do {                                                                             \
+    EpiLinear<E, true> e{L.b, L.out_f, neg0, neg1, RelTerm{}};                     \
+    e.rm = rm;                                                                     \
+    e.rows = M;                                                                    \
+    return tc::launch_gemm_auto(A, M, L.Wsp, L.out_f, K, o, e, ws, st);            \
+  } while (0)
+  switch (epi) {
+    case kEpiRelu: KGQ_EPI_MAP(kEpiRelu);
+    case kEpiBetaReg: KGQ_EPI_MAP(kEpiBetaReg);
+    default: KGQ_EPI_MAP(kEpiNone);
+  }
+#undef KGQ_EPI_MAP
 }
 
 int launch_linear(const Split& A, int M, int K, const Linear& L, int epi, const Split& out_sp, float* out_f32,

@@ -182,6 +182,7 @@ struct EpiBetaScore {
   unsigned long long* cand = nullptr;  // TK: [rows / NB][ldcand] per-stripe sorted key lists
   int64_t ldcand = 0;
   int k = 0;
+  __device__ __forceinline__ int out_row(int row0) const { return row0 / NB; }  // no remap
   struct Pre {
     float2 p;       // P of this lane's row
     float2 e[4];    // E of columns n0 + lane + 32 j

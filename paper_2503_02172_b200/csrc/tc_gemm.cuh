@@ -503,6 +503,8 @@ __device__ __forceinline__ float topk_fkey_inv(uint32_t k) {
 //       const float* v) const -- optional side output after the row-pair min (score top-k)
 //   static constexpr bool INIT; template <int CW> __device__ void init(int row, int n0,
 //       float* acc) const -- optional initial accumulator values (relation term of layer 1)
+//   __device__ int out_row(int row0) const -- output tensor row of the 32 / ROWDIV-row box that
+//       starts at GEMM row row0 (row0 / ROWDIV, or a remapped row; -1: do not store the box)
 //   static constexpr bool TOPK (optional) -- fused top-k: no output tensor; every output row's
 //       k (<= 16) smallest (value, column) pairs over the unit's stripe are kept in the warp's
 //       staging slot and written as one sorted list per (row, stripe, column half) to
@@ -869,13 +871,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         __syncwarp();
 #ifndef KGQ_TC_DBG_NO_STORE  // perf probe only: skip the output stores
         if (lane == 0) {
-          if (Epi::STREAM_OUT)
-            tma_store_2d_evict_first(&mO0, buf, n0 + c, row0 / ROWDIV);
-          else
-            tma_store_2d(&mO0, buf, n0 + c, row0 / ROWDIV);
-          if (PLANES == 3) {
-            tma_store_2d(&mO1, buf + 1024, n0 + c, row0);
-            if constexpr (!kFp16x2) tma_store_2d(&mO2, buf + 2048, n0 + c, row0);
+          const int orow = epi.out_row(row0);  // row0 / ROWDIV, or the remapped row (-1: none)
+          if (orow >= 0) {
+            if (Epi::STREAM_OUT)
+              tma_store_2d_evict_first(&mO0, buf, n0 + c, orow);
+            else
+              tma_store_2d(&mO0, buf, n0 + c, orow);
+            if (PLANES == 3) {
+              tma_store_2d(&mO1, buf + 1024, n0 + c, orow);
+              if constexpr (!kFp16x2) tma_store_2d(&mO2, buf + 2048, n0 + c, orow);
+            }
           }
           bulk_commit();
         }

@@ -540,6 +540,42 @@ def test_mixed_structure_batch(model, fused):
     e.set_fused_topk("auto")
 
 
+def test_mixed_batch_aligned_groups_remap():
+    """Groups of 32 / 64 queries: every hop segment is whole 32-row boxes, so the last MLP layer
+    of each batched hop writes its rows straight into the state through the epilogue's row remap
+    (no scatter kernel).  Every row against the oracle, both fused-top-k modes, and a bad relation
+    id at a later hop still flags exactly its query."""
+    e, m, t = engine("betae", max_batch=1024)
+    N, R = SMALL["N"], SMALL["R"]
+    structs = synth.ALL_STRUCTURES
+    for fused in ("auto", "on"):
+        e.set_fused_topk(fused)
+        groups, refs = [], []
+        for i, s in enumerate(structs):
+            B = 32 if i % 2 else 64
+            a, r = synth.make_queries(s, B, N, R, seed=900 + i)
+            if s == "3p":
+                r = r.copy()
+                r[5, 2] = R + 1  # bad id at hop 2
+            groups.append((s, dev(a.astype(np.int32)), dev(r.astype(np.int32))))
+            refs.append((a, r))
+        td, ti = e.submit_mixed(groups, 10)
+        with pytest.raises(KgqError, match="ERANGE"):
+            e.check_errors()
+        td, ti = td.cpu().numpy(), ti.cpu().numpy()
+        q = 0
+        for (s, a, _), (qa, qr) in zip(groups, refs):
+            B = a.shape[0]
+            ok = [b for b in range(B) if not (s == "3p" and b == 5)]
+            ref = m.scores(s, qa[ok], qr[ok])
+            for j, b in enumerate(ok):
+                assert_topk_ok(td[q + b], ti[q + b], ref[j], 10, what=f"aligned mixed {fused} {s} row {b}")
+            if s == "3p":
+                assert np.all(np.isnan(td[q + 5])) and np.all(ti[q + 5] == -1)
+            q += B
+    e.set_fused_topk("auto")
+
+
 def test_mixed_batch_out_of_range_and_equivalence():
     """A bad relation id in one group flags exactly that query (global index); the other rows
     agree with one kgq_submit per group (same arithmetic, different batching: 1e-5)."""
