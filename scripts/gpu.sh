@@ -20,6 +20,10 @@
 #   streams    the headline step over 1-4 streams, and with the GEMM grid capped (KGQ_GEMM_CLUSTERS)
 #   multirank  the N > 1 bench path with both ranks on the one GPU (gloo; a path check, numbers meaningless)
 #   probes     tcgen05 GEMM checker / throughput probe / MMA issue probe (built by scripts/tc_probe.sh)
+#   accuracy   chain / whole-row distance errors vs the oracle for both operand builds (fp16x2 libkgq.so,
+#              bf16x3 libkgq_bf16x3.so) on the small, spread, medium, C2 and C4 configs
+#   raster-ab  the headline step with the GEMM tile raster group at 0 (M fastest) / 4 / 8 / 16
+#   fp32-pipe  FP32 issue-rate probe (FADD / FFMA / FADD2 / FFMA2 / FMNMX lane-ops per clock)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 OUT=gpurun_out
@@ -65,6 +69,14 @@ for task in "$@"; do
                  --master-port 29517 bench.py --gpus 2 --steps 3 --warmup 3 --no-c5a --no-mixed > $OUT/multirank.json 2> $OUT/multirank.err
                tail -3 $OUT/multirank.err ;;
     probes) ( cd scripts; timeout 120 ./tc_bn_check; timeout 200 ./tc_probe_base; timeout 120 ./mma3_probe ) > $OUT/probes.txt 2>&1 ;;
+    accuracy) for lib in libkgq.so libkgq_bf16x3.so; do echo "== $lib"
+                KGQ_LIB_PATH=$PWD/paper_2503_02172_b200/$lib timeout 900 python scripts/diag_chain_err.py small small_spread \
+                  medium c2 c4 2>&1 | tail -5
+              done > $OUT/accuracy.jsonl ;;
+    raster-ab) for g in 0 4 8 16; do KGQ_GEMM_GROUP_M=$g bash "$0" quick | grep "^quick [0-9]" | sed "s/^/group_m $g /"; done \
+                 | tee $OUT/raster_ab.txt ;;
+    fp32-pipe) ( cd scripts; /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp32_pipe_probe \
+                 fp32_pipe_probe.cu && timeout 120 ./fp32_pipe_probe ) > $OUT/fp32_pipe.txt 2>&1 ;;
     *) echo "unknown task $task" ;;
   esac
 done
