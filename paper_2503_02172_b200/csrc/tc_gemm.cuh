@@ -288,7 +288,13 @@ __device__ unsigned long long* g_tc_trace;
 #ifndef KGQ_TC_DRAIN
 #define KGQ_TC_DRAIN (KGQ_OPERAND_FP16X2 ? 8 : 4)
 #endif
-constexpr int DRAIN = KGQ_TC_DRAIN;
+constexpr int DRAIN_DEFAULT = KGQ_TC_DRAIN;
+// An epilogue may set its own partial length (static constexpr int DRAIN): the BetaE scorer's
+// contraction terms are small (centred u, v) and its K = 800 fits fewer, longer partials.
+template <class E, class = void>
+struct epi_drain : std::integral_constant<int, DRAIN_DEFAULT> {};
+template <class E>
+struct epi_drain<E, std::void_t<decltype(E::DRAIN)>> : std::integral_constant<int, E::DRAIN> {};
 
 // Per-CTA shared memory: STAGES operand stages, then the epilogue staging buffers -- each
 // epilogue warp owns NBUF x 4 KB holding a 32-row chunk of its columns in the 128-byte
@@ -539,6 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int m_pairs = (M + 2 * BM - 1) / (2 * BM);
   constexpr bool TOPK = epi_topk<Epi>::value;
+  constexpr int DRAIN = epi_drain<Epi>::value;
   const int n_tiles = (N + BN - 1) / BN;
   const int ntiles = m_pairs * n_tiles;
   const int nunits = TOPK ? m_pairs * sc.n_stripes : sc.full + (ntiles - sc.full) * sc.s_tail;
