@@ -252,10 +252,18 @@ bool fused_topk_disabled() {
 // rows many for the saved top-k pass to win; measured on C2.
 // AUTO keeps every stripe >= 16 tiles long; ON (tests) lets the planner cut as many stripes as
 // balance the machine best (up to 64)
-static int topk_min_tiles(const kgq_ctx* ctx) { return ctx->fused_topk == KGQ_FUSED_ON ? 1 : 16; }
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && e[0] ? atoi(e) : dflt;
+}
+static int topk_min_tiles(const kgq_ctx* ctx) {
+  static const int auto_min = env_int("KGQ_TOPK_MIN_TILES", 16);  // tuning experiments only
+  return ctx->fused_topk == KGQ_FUSED_ON ? 1 : auto_min;
+}
 static bool use_fused_topk(const kgq_ctx* ctx, int64_t rows, int k) {
+  static const int auto_rows = env_int("KGQ_TOPK_AUTO_ROWS", 8192);  // tuning experiments only
   if (k > kFusedTopkMax || ctx->fused_topk == KGQ_FUSED_OFF) return false;
-  return ctx->fused_topk == KGQ_FUSED_ON || rows >= 8192;
+  return ctx->fused_topk == KGQ_FUSED_ON || rows >= auto_rows;
 }
 bool topk_cmin_disabled() {  // KGQ_NO_TOPK_CMIN=1: full-row top-k (A/B and debugging)
   static int v = -1;
