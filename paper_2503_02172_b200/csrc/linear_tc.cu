@@ -77,7 +77,8 @@ struct EpiLinear {
   }
   struct Pre {
     float b[4];  // bias of columns n0 + lane + 32 j
-    bool neg;
+    bool neg;      // this lane's row is negated
+    bool any_neg;  // some row of this warp's 32-row box is (warp-uniform)
   };
   template <int CW>
   __device__ __forceinline__ Pre prefetch(int row, int n0, int lane) const {
@@ -85,6 +86,7 @@ struct EpiLinear {
 #pragma unroll
     for (int j = 0; j < (CW + 31) / 32; ++j) p.b[j] = n0 + lane + 32 * j < N ? __ldg(bias + n0 + lane + 32 * j) : 0.0f;
     p.neg = row >= neg0 && row < neg1;
+    p.any_neg = __any_sync(0xffffffffu, p.neg);
     return p;
   }
   template <int CH>
@@ -93,11 +95,17 @@ struct EpiLinear {
     for (int i = 0; i < CH; ++i) {
       float y = v[i] + __shfl_sync(0xffffffffu, p.b[(c + i) >> 5], (c + i) & 31);
       if (EPI == kEpiRelu) y = fmaxf(y, 0.0f);
-      if (EPI == kEpiBetaReg) {
-        y = beta_reg(y);
-        if (p.neg) y = 1.0f / y;
-      }
+      if (EPI == kEpiBetaReg) y = beta_reg(y);
       v[i] = y;
+    }
+    // negation (1/x, Q5) behind a warp-uniform branch: the IEEE division is ~10 instructions with
+    // a slow-path check, and only the negated branches' rows (a few 32-row boxes) need it -- as a
+    // select on every element it made the regulariser layer's epilogue outlast the MMAs it
+    // overlaps (hop-0 last layer: tensor pipe 55% active vs 88% for the ReLU layer before it)
+    if (EPI == kEpiBetaReg && p.any_neg) {
+#pragma unroll
+      for (int i = 0; i < CH; ++i)
+        if (p.neg) v[i] = 1.0f / v[i];
     }
   }
 };

@@ -840,6 +840,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         continue;
       }
+      // output row of this warp's 32 / ROWDIV-row box (row0 / ROWDIV, or the remapped row; -1:
+      // none): once per tile, not per chunk (the remap's segment search is ~50 instructions)
+      const int orow = epi.out_row(row0);
 #pragma unroll
       for (int c = 0; c < CW; c += CH, ++nchunk) {
         float* v = acc + c;  // in place (unrolled: stays in registers)
@@ -878,7 +881,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         __syncwarp();
 #ifndef KGQ_TC_DBG_NO_STORE  // perf probe only: skip the output stores
         if (lane == 0) {
-          const int orow = epi.out_row(row0);  // row0 / ROWDIV, or the remapped row (-1: none)
           if (orow >= 0) {
             if (Epi::STREAM_OUT)
               tma_store_2d_evict_first(&mO0, buf, n0 + c, orow);
@@ -1038,6 +1040,13 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_gemm_enabled() ? 1 : 0;
+  // KGQ_PLAN_LOG=1 (diagnostics, scripts/diag_gemm_launches.py): one stderr line per launch, in
+  // launch order, to pair with the kgq_ktime_log spans of the same sequence
+  static const bool plan_log = [] { const char* e = getenv("KGQ_PLAN_LOG"); return e && e[0] == '1'; }();
+  if (plan_log)
+    fprintf(stderr, "KGQ_PLAN M=%d N=%d K=%d BN=%d tiles=%d full=%d s_tail=%d kper=%d stripes=%d clusters=%d topk=%d planes=%d\n",
+            M, N, K, BN, tiles, sc.full, sc.s_tail, sc.kper, sc.n_stripes, clusters, (int)epi_topk<Epi>::value,
+            Epi::PLANES);
   cudaLaunchKernelEx(&cfg, kern, mA[0], mA[1], mW[0], mW[1], mA[2], mW[2], mO[0], mO[1], mO[2], M, N, K, sc, epi);
   return 1;
 }
