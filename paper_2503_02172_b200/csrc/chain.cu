@@ -132,10 +132,17 @@ int launch_betae_mlp_input(const ChainArgs& a, const float* ent, const float* re
 }
 
 // ---- mixed-structure batches: hop gather / scatter over row blocks (MixSegs) ----------------
+// the last segment with dst0 <= row (segments are in ascending dst0 order): a binary search --
+// the linear scan over the ~27 segments of a hop-0 batch (dynamically indexed parameter loads)
+// was a large share of the per-row instructions of the one-row-per-block kernels
 __device__ __forceinline__ int mix_seg_of(const MixSegs& sg, int row) {
-  int i = 0;
-  while (i + 1 < sg.n && sg.s[i + 1].dst0 <= row) ++i;
-  return i;
+  int lo = 0, hi = sg.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sg.s[mid].dst0 <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 __global__ void k_mix_gather(MixSegs sg, const float* __restrict__ ent, Split S, Split Mst, Split Z,

@@ -147,10 +147,23 @@ __global__ void __launch_bounds__(32 * kPrepRows)
 #pragma unroll
       for (int p3 = 0; p3 < kSplitPlanesA; ++p3)
         *reinterpret_cast<uint4*>(A.plane(p3) + a0 + j) = *reinterpret_cast<const uint4*>(S.plane(p3) + s0 + j);
-    for (int j = lane; j < d; j += 32) {
+    // two dims per iteration with two partial sums: independent fp64 chains in flight (the
+    // FP64 pipe is this kernel's bound; one chain per lane left it ~58% busy)
+    double p1 = 0.0;
+    int j = lane;
+    for (; j + 32 < d; j += 64) {
+      const double da = load_split(S, s0 + j), db = load_split(S, s0 + d + j);
+      const double ea = load_split(S, s0 + j + 32), eb = load_split(S, s0 + d + j + 32);
+      const double t0 = lnbeta_f64_tab(da, db, tab, tab + kLogTab);
+      const double t1 = lnbeta_f64_tab(ea, eb, tab, tab + kLogTab);
+      p += t0 + da * sums[j] * inv + db * sums[d + j] * inv;
+      p1 += t1 + ea * sums[j + 32] * inv + eb * sums[d + j + 32] * inv;
+    }
+    if (j < d) {
       const double da = load_split(S, s0 + j), db = load_split(S, s0 + d + j);
       p += lnbeta_f64_tab(da, db, tab, tab + kLogTab) + da * sums[j] * inv + db * sums[d + j] * inv;
     }
+    p += p1;
   } else {
     for (int j = lane; j < d; j += 32) {
       const float a = load_split(S, s0 + j), b = load_split(S, s0 + d + j);
