@@ -286,6 +286,20 @@ __device__ __forceinline__ double log_pos(double x) {
                    z * (1.0 / 15 + z * (1.0 / 17 + z * (1.0 / 19))))))));
   return (double)e * 0.69314718055994530942 + (2.0 * sq + 2.0 * sq * z * p);
 }
+// Rising factorial x (x + 1) ... (x + 7) for x > 0 in Horner form: x (x^7 + 28 x^6 + 322 x^5 +
+// 1960 x^4 + 6769 x^3 + 13132 x^2 + 13068 x + 5040) (unsigned Stirling numbers of the first kind
+// c(8, k)) -- 8 fp64 operations instead of the product's 14; every coefficient and x are
+// positive, so no cancellation (a few ulp, like the product)
+__device__ __forceinline__ double rise8(double x) {
+  double t = x + 28.0;
+  t = fma(t, x, 322.0);
+  t = fma(t, x, 1960.0);
+  t = fma(t, x, 6769.0);
+  t = fma(t, x, 13132.0);
+  t = fma(t, x, 13068.0);
+  t = fma(t, x, 5040.0);
+  return t * x;
+}
 // ln B(a, b) = ln Gamma(a) + ln Gamma(b) - ln Gamma(a + b) for a, b > 0 (Eq. 3), the
 // query-side P_q precompute of the tensor-core scorer.  ln Gamma(y) for y >= 8 by Stirling:
 // (y - 1/2) ln y - y + ln(2 pi)/2 + sum_k B_2k / (2k (2k-1) y^(2k-1)).  Branch-free: every argument x is shifted
@@ -296,13 +310,7 @@ __device__ __forceinline__ double log_pos(double x) {
 // the other O(0.1), where the libdevice formula loses the same digits).
 __device__ __forceinline__ double lnbeta_f64(double a, double b) {
   const double c = a + b;
-  double pa = a, pb = b, pc = c;
-#pragma unroll
-  for (int i = 1; i < 8; ++i) {
-    pa *= a + i;
-    pb *= b + i;
-    pc *= c + i;
-  }
+  const double pa = rise8(a), pb = rise8(b), pc = rise8(c);
   const double ya = a + 8.0, yb = b + 8.0, yc = c + 8.0;
   const double yab = ya * yb;
   const double rall = rcp_nr(yab * yc);  // <= (2e9 + 8)^3: inside the fp32 seed range
@@ -337,13 +345,7 @@ __device__ __forceinline__ double log_tab(double x, const double* lnc, const dou
 // lnbeta_f64 with the table log (same formula and error budget)
 __device__ __forceinline__ double lnbeta_f64_tab(double a, double b, const double* lnc, const double* invc) {
   const double c = a + b;
-  double pa = a, pb = b, pc = c;
-#pragma unroll
-  for (int i = 1; i < 8; ++i) {
-    pa *= a + i;
-    pb *= b + i;
-    pc *= c + i;
-  }
+  const double pa = rise8(a), pb = rise8(b), pc = rise8(c);
   const double ya = a + 8.0, yb = b + 8.0, yc = c + 8.0;
   const double yab = ya * yb;
   const double rall = rcp_nr(yab * yc);
