@@ -176,8 +176,9 @@ __global__ void k_mix_gather(MixSegs sg, const float* __restrict__ ent, Split S,
       for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) store_split(Z, zrow + j, er[j]);
     }
   } else {  // split -> split: a plane-wise copy, 16-byte vectors when aligned
+    // kind 1: the state rows src0 + b of S; kind 2: the combine's output rows q0 + b of M
     const Split& src = g.kind == 1 ? S : Mst;
-    const int64_t srow = (g.src0 + b) * src.ld;
+    const int64_t srow = ((g.kind == 1 ? g.src0 : (int64_t)g.q0) + b) * src.ld;
     if (((2 * d) & 7) == 0) {
       const int nv = (2 * d) >> 3;
       for (int p = 0; p < kSplitPlanesA; ++p) {

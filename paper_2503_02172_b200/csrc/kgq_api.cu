@@ -1286,10 +1286,23 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
         }
   {
     StageTimer t(ctx, st, kStChain);
-    // ---- branch hops ----
-    int maxh = 0;
-    for (auto& g : G) maxh = std::max(maxh, g.maxh);
-    for (int h = 0; h < maxh; ++h) {
+    // ---- projection hops, level by level ----
+    // Hops of the intersection groups' branches run first (levels [0, H1)), then the attention
+    // pair and the combine; every later level batches the remaining branch hops (e.g. 3p's third)
+    // TOGETHER with the post-intersection hops of the same depth (ip / inp / up-DM) into one MLP
+    // -- the projection weights are shared, so the two small batches (1K + 2K rows at C2) become
+    // one launch chain of 3K rows (fewer one-wave launches, one gather / scatter pair).
+    int maxh = 0, H1 = 0, maxpost = 0;
+    for (auto& g : G) {
+      maxh = std::max(maxh, g.maxh);
+      if (g.P->kind == kInter) {
+        H1 = std::max(H1, g.maxh);
+        maxpost = std::max(maxpost, g.P->npost);
+      }
+    }
+    // level h of the branch chains (groups with a branch longer than h) plus, post >= 0, the
+    // post-intersection hop `post` of every intersection group that has one; negated rows last
+    auto hop = [&](int h, int post) -> kgq_status {
       MixSegs sg;
       int M = 0, neg0 = 0;
       for (int negpass = 0; negpass < 2; ++negpass) {
@@ -1301,14 +1314,30 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
             MixSeg& m = sg.s[sg.n++];
             m.dst0 = M; m.B = g.B; m.q0 = g.q0;
             m.kind = h == 0 ? 0 : 1;
-            m.src0 = g.srow[br];
+            m.src0 = g.srow[br];  // gather source = scatter target: the branch's S rows
             m.anchors = g.anchors; m.n_a = g.P->n_anchor; m.aslot = g.P->br[br].anchor;
             m.rels = g.rels; m.n_r = g.P->n_rel; m.rslot = g.proj[br][h];
             M += g.B;
           }
+        if (negpass == 0 && post >= 0)  // post-intersection hops are never negated
+          for (auto& g : G) {
+            if (g.P->kind != kInter || g.P->npost <= post) continue;
+            if (sg.n == kMaxMixSegs) return fail(ctx, KGQ_EINVAL, "mixed submit: too many groups");
+            MixSeg& m = sg.s[sg.n++];
+            m.dst0 = M; m.B = g.B; m.q0 = g.q0;
+            m.kind = post == 0 ? 2 : 1;  // 2: the combine's output rows (M at q0); 1: S rows
+            m.src0 = g.srow[0];          // the group's branch-0 block holds the embedding
+            m.anchors = g.anchors; m.n_a = g.P->n_anchor; m.aslot = 0;
+            m.rels = g.rels; m.n_r = g.P->n_rel; m.rslot = g.P->post[post];
+            M += g.B;
+          }
       }
-      // scatter targets: the same blocks' S rows (src0 already = srow)
-      L += mix_mlp(ctx, sg, M, neg0, st);
+      if (M > 0) L += mix_mlp(ctx, sg, M, neg0, st);
+      return KGQ_OK;
+    };
+    for (int h = 0; h < H1; ++h) {
+      const kgq_status hs = hop(h, -1);
+      if (hs != KGQ_OK) return hs;
     }
     // ---- intersections: one attention GEMM pair over every intersection group's branch rows ----
     if (inter_rows > 0) {
@@ -1348,56 +1377,12 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
         total += g.B;
       }
       L += launch_mix_combine(mc, total, ctx->S, ctx->T, ctx->tw, ctx->M, st);
-      // ---- post-intersection projections (ip, inp, up-DM) ----
-      int maxpost = 0;
-      for (auto& g : G) maxpost = std::max(maxpost, g.P->kind == kInter ? g.P->npost : 0);
-      for (int p = 0; p < maxpost; ++p) {
-        MixSegs sg;
-        int M = 0;
-        for (auto& g : G) {
-          if (g.P->kind != kInter || g.P->npost <= p) continue;
-          MixSeg& m = sg.s[sg.n++];
-          m.dst0 = M; m.B = g.B; m.q0 = g.q0;
-          m.kind = p == 0 ? 2 : 1;
-          m.src0 = p == 0 ? g.q0 : g.srow[0];
-          m.anchors = g.anchors; m.n_a = g.P->n_anchor; m.aslot = 0;
-          m.rels = g.rels; m.n_r = g.P->n_rel; m.rslot = g.P->post[p];
-          M += g.B;
-        }
-        // the hop's output goes to the group's branch-0 block; src0 of the scatter = srow[0]
-        MixSegs out = sg;
-        for (int i = 0; i < out.n; ++i) out.s[i].src0 = 0;
-        int gi = 0;
-        for (auto& g : G)
-          if (g.P->kind == kInter && g.P->npost > p) out.s[gi++].src0 = g.srow[0];
-        int Lh = 0;
-        Lh += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,
-                                ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
-        // reuse mix_mlp's layers without its gather/scatter: run them here
-        RelTerm rt;
-        rt.RW = ctx->RW; rt.ldrw = ctx->cfg.hidden; rt.M = M; rt.rid = ctx->mix_rid;
-        {
-          StageTimer t(ctx, st, kStDense, 2.0 * M * (double)ctx->lin1x.out_f * 2 * d);
-          Lh += launch_linear_rel(ctx->Z, M, 2 * d, ctx->lin1x, rt, ctx->H[0], &ctx->gws, st);
-        }
-        Split A = ctx->H[0];
-        int K = ctx->lin1x.out_f;
-        for (int l = 1; l < ctx->cfg.n_hidden_layers; ++l) {
-          const Linear& lin = ctx->lin[KGQ_LAYER_PROJ_HIDDEN + l];
-          Lh += dense(ctx, A, M, K, lin, kEpiRelu, ctx->H[l & 1], 0, 0, st);
-          A = ctx->H[l & 1];
-          K = lin.out_f;
-        }
-        const Linear& lo = ctx->lin[KGQ_LAYER_PROJ_OUT];
-        if (ctx->cfg.terminal == KGQ_TERM_SOFTMAX) {
-          Lh += dense(ctx, A, M, K, lo, kEpiNone, ctx->T, 2 * d, st);
-          Lh += launch_softmax_terminal(ctx->T, 2 * d, M, 2 * d, ctx->I, 0, M, M, st);
-        } else {
-          Lh += dense(ctx, A, M, K, lo, kEpiBetaReg, ctx->I, M, M, st);
-        }
-        Lh += launch_mix_scatter(out, M, ctx->I, ctx->S, 2 * d, st);
-        L += Lh;
-      }
+    }
+    // ---- the remaining branch hops and the post-intersection hops, one MLP per depth ----
+    const int late = std::max(maxh - H1, maxpost);
+    for (int lv = 0; lv < late; ++lv) {
+      const kgq_status hs = hop(H1 + lv, lv < maxpost ? lv : -1);
+      if (hs != KGQ_OK) return hs;
     }
   }
   // ---- score rows: single-embedding groups first (query order), then the DNF-union groups
