@@ -653,8 +653,8 @@ def main():
                                       "per fp32 multiply-add, fp32 accumulation (DESIGN.md §7)" if mmas == 3 else
                                       "bf16x3 split: exact three bf16 planes, 6 MMAs per fp32 multiply-add")),
         "how": ("per step: ONE kgq_submit_mixed of the 14 x 1024 queries (BetaE level-synchronous: each projection "
-                "hop of all types' branches is one MLP, all intersections one attention GEMM pair, one scorer, one "
-                "top-k); device time between events on the launching stream, max over ranks" if mixed_mode else
+                "hop of all types' branches is one MLP, all intersections one attention GEMM pair, later branch hops "
+                "batched with the post-intersection hops, one scorer, one top-k); device time between events on the launching stream, max over ranks" if mixed_mode else
                 f"per step: the 14 per-type kgq_submit calls dealt round-robin over {S} CUDA streams, one library "
                 f"context per stream; device time from an event before the fork to an event after the join, max "
                 f"over ranks"),

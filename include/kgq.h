@@ -176,7 +176,8 @@ kgq_status kgq_submit_host_async(kgq_ctx* ctx, int32_t s, int32_t batch, const i
  * and [B_i, n_r(s_i)] blocks concatenated in group order; topk_dist / topk_id: device
  * [sum B_i, k], rows in the same order.  Sum B_i <= max_batch.  BetaE runs the groups
  * level-synchronously (each projection hop of all groups' branches is one MLP, all
- * intersections one attention GEMM pair, one scorer and one top-k for all queries); GQE / Q2B
+ * intersections one attention GEMM pair, the branch hops past the intersections' depth batched
+ * with the post-intersection hops of equal depth, one scorer and one top-k for all queries); GQE / Q2B
  * (and BetaE with k > 32) run group by group.  Same results and error behaviour as one
  * kgq_submit per group (global query index in error reports). */
 kgq_status kgq_submit_mixed(kgq_ctx* ctx, int32_t n_groups, const int32_t* structures, const int32_t* batches,
