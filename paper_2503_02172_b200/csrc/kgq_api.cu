@@ -260,10 +260,16 @@ static int topk_min_tiles(const kgq_ctx* ctx) {
   static const int auto_min = env_int("KGQ_TOPK_MIN_TILES", 16);  // tuning experiments only
   return ctx->fused_topk == KGQ_FUSED_ON ? 1 : auto_min;
 }
+// AUTO: fuse launches of >= 8,192 rows, or any launch whose 256 x 256 tiles per cluster (74 per
+// B200) reach 64 -- long stripes amortise the lists' warm-up: the 2M-entity table (C5b) at 1,024
+// rows has ~420 tiles per cluster and gains 13% from the fused top-k (no 8 GB distance block per
+// chunk), while C2's 4,096 union rows (~12 tiles per cluster) lose with it
 static bool use_fused_topk(const kgq_ctx* ctx, int64_t rows, int k) {
   static const int auto_rows = env_int("KGQ_TOPK_AUTO_ROWS", 8192);  // tuning experiments only
+  static const int auto_tiles = env_int("KGQ_TOPK_AUTO_TILES", 64);  // tuning experiments only
   if (k > kFusedTopkMax || ctx->fused_topk == KGQ_FUSED_OFF) return false;
-  return ctx->fused_topk == KGQ_FUSED_ON || rows >= auto_rows;
+  const double tiles_per_cluster = (double)((rows + 255) / 256) * (double)((ctx->np + 255) / 256) / 74.0;
+  return ctx->fused_topk == KGQ_FUSED_ON || rows >= auto_rows || tiles_per_cluster >= auto_tiles;
 }
 bool topk_cmin_disabled() {  // KGQ_NO_TOPK_CMIN=1: full-row top-k (A/B and debugging)
   static int v = -1;
@@ -728,7 +734,21 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   ctx->tw = 2 * d;
   ctx->rpad = round_up(2 * Bm, kRowPad);
   const int nplanes = c.model == KGQ_GQE ? 1 : (c.model == KGQ_Q2B ? 2 : 3);
-  const int64_t budget = (int64_t)4 << 30;  // bytes for the distance scratch
+  // bytes for the distance scratch [bchunk, np] fp32: queries are scored in chunks of bchunk.
+  // Every chunk re-reads the whole scoring table, so on large tables the chunk must hold enough
+  // rows for the tensor-core scorer to stay compute-bound: at 2M entities a 4 GB scratch gave
+  // 512-query chunks (2 M blocks per table tile: ~4.4 TB/s of table reads plus the 1.9 TB/s of
+  // distance writes -- HBM-bound at 0.6 of the tensor peak).  Up to 16 GB, at most a quarter of
+  // the free memory (KGQ_DIST_BUDGET_MB overrides).
+  int64_t budget = (int64_t)16 << 30;
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min<int64_t>(budget, (int64_t)(fr / 4));
+    else cudaGetLastError();
+    const char* e = getenv("KGQ_DIST_BUDGET_MB");
+    if (e && atoll(e) > 0) budget = atoll(e) << 20;
+    budget = std::max<int64_t>(budget, (int64_t)256 << 20);
+  }
   ctx->bchunk = std::max<int64_t>(1, std::min<int64_t>(Bm, budget / (ctx->np * 4)));
   kgq_status st = KGQ_OK;
   const int iw = c.model == KGQ_BETAE ? 2 * d : d;
