@@ -278,6 +278,35 @@ def run_suite(args):
         prof = eng.profile_read()
         eng.profile(False)
         eng.close()
+        mixed = None
+        if model == "betae" and len(structs) > 1:
+            # the same queries as ONE kgq_submit_mixed (level-synchronous batching across the
+            # types, the headline's step form), L2 flushed before each step, device time
+            meng = Engine(model, N, R, d, hidden=H, max_batch=B * len(structs), max_k=K)
+            meng.load_tables(synth.make_tables(model, N, R, d, hidden=H, seed=SEED + 10))
+            pa = torch.cat([qs[s][0].reshape(-1) for s in structs]).int().contiguous()
+            pr = torch.cat([qs[s][1].reshape(-1) for s in structs]).int().contiguous()
+            mo = (torch.empty((B * len(structs), K), device="cuda"),
+                  torch.empty((B * len(structs), K), dtype=torch.int32, device="cuda"))
+            bl = [B] * len(structs)
+            for _ in range(max(args.warmup, 2)):
+                meng.submit_mixed_packed(list(structs), bl, pa, pr, K, mo)
+            torch.cuda.synchronize()
+            meng.check_errors()
+            mt = 0.0
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for _ in range(args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                e0.record()
+                meng.submit_mixed_packed(list(structs), bl, pa, pr, K, mo)
+                e1.record()
+                torch.cuda.synchronize()
+                mt += e0.elapsed_time(e1)
+            meng.check_errors()
+            meng.close()
+            mixed = {"form": f"one kgq_submit_mixed of the {len(structs)} x {B} queries per step",
+                     "queries_per_s": args.steps * len(structs) * B / (mt / 1e3), "ms_per_step": mt / args.steps}
         tot = sum(per.values())
         q = args.steps * len(structs) * B
         st = {k: v[0] / args.steps for k, v in prof.items()}
@@ -298,7 +327,7 @@ def run_suite(args):
                           "queries_per_s": q / (tot / 1e3), "ms_per_batch": tot / args.steps / len(structs),
                           "per_type_qps": {s: B * args.steps / (per[s] / 1e3) for s in structs},
                           "stage_ms_per_step": st, "roofline": roof, "peak_source": src,
-                          "l2": "flushed between steps"}), flush=True)
+                          "mixed_submit": mixed, "l2": "flushed between steps"}), flush=True)
 
 
 def span_union_ms(spans):
