@@ -739,15 +739,15 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
   // rows for the tensor-core scorer to stay compute-bound: at 2M entities a 4 GB scratch gave
   // 512-query chunks (2 M blocks per table tile: ~4.4 TB/s of table reads plus the 1.9 TB/s of
   // distance writes -- HBM-bound at 0.6 of the tensor peak).  Up to 16 GB, at most a quarter of
-  // the free memory (KGQ_DIST_BUDGET_MB overrides).
+  // the free memory, at least 256 MB (KGQ_DIST_BUDGET_MB overrides: tests of the chunked path).
   int64_t budget = (int64_t)16 << 30;
   {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min<int64_t>(budget, (int64_t)(fr / 4));
     else cudaGetLastError();
+    budget = std::max<int64_t>(budget, (int64_t)256 << 20);
     const char* e = getenv("KGQ_DIST_BUDGET_MB");
     if (e && atoll(e) > 0) budget = atoll(e) << 20;
-    budget = std::max<int64_t>(budget, (int64_t)256 << 20);
   }
   ctx->bchunk = std::max<int64_t>(1, std::min<int64_t>(Bm, budget / (ctx->np * 4)));
   kgq_status st = KGQ_OK;

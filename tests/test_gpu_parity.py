@@ -641,6 +641,43 @@ def test_virtual_shards_mixed_batch():
     full.close()
 
 
+@pytest.mark.parametrize("model", ["betae", "gqe"])
+def test_scorer_row_chunks(model):
+    """Batches larger than the distance scratch are scored in chunks of rows (kgq_api.cu bchunk:
+    each chunk re-reads the table).  KGQ_DIST_BUDGET_MB = 7 on a 100K-entity table gives 18-query
+    chunks, so B = 37 runs two tensor-core / tiled chunks and a 1-query streaming chunk (BetaE), and
+    a mixed submit larger than one chunk falls back to group-by-group submits.  Every row vs the
+    oracle (top-k ids and distances, tie-aware)."""
+    import os
+    N, R, d, H, B, k = 100_003, 20, 16, 32, 37, 10
+    t = synth.make_tables(model, N, R, d, hidden=H, seed=31)
+    os.environ["KGQ_DIST_BUDGET_MB"] = "7"
+    try:
+        e = Engine(model, N, R, d, hidden=H, max_batch=128, max_k=k)
+        e.load_tables(t)  # the scratch is sized at finalize
+    finally:
+        del os.environ["KGQ_DIST_BUDGET_MB"]
+    m = O.Model(model, t, dim=d)
+    groups, refs = [], []
+    for s in ("1p", "2u", "ip"):
+        a, r = synth.make_queries(s, B, N, R, seed=synth.query_seed(31, s))
+        td, ti = e.submit(s, dev(a), dev(r), k)
+        e.check_errors()
+        ref = m.scores(s, a, r)
+        td, ti = td.cpu().numpy(), ti.cpu().numpy()
+        for b in range(B):
+            assert_topk_ok(td[b], ti[b], ref[b], k, what=f"chunked {model} {s} row {b}")
+        groups.append((s, dev(a.astype(np.int32)), dev(r.astype(np.int32))))
+        refs.append(ref)
+    md, mi = e.submit_mixed(groups, k)
+    e.check_errors()
+    md, mi = md.cpu().numpy(), mi.cpu().numpy()
+    for gi, ref in enumerate(refs):
+        for b in range(B):
+            assert_topk_ok(md[gi * B + b], mi[gi * B + b], ref[b], k, what=f"chunked mixed {model} row {b}")
+    e.close()
+
+
 def test_mixed_graph_replay_matches_eager():
     """The second identical kgq_submit_mixed is captured into a CUDA graph and later calls
     replay it (inputs repacked into the same staging buffers, new query content every round):
