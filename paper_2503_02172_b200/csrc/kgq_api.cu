@@ -1229,6 +1229,12 @@ static bool split_mlp_enabled() {
   }();
   return v;
 }
+// rows from which a batched MLP / attention pair runs as two row halves on two streams
+// (KGQ_SPLIT_MLP_ROWS: tuning experiments only)
+static int split_mlp_rows() {
+  static const int v = env_int("KGQ_SPLIT_MLP_ROWS", 8192);
+  return v;
+}
 static bool side_stream(kgq_ctx* ctx) {  // lazily created; false if CUDA refuses
   if (ctx->side_st && ctx->side_ev[0] && ctx->side_ev[1]) return true;
   if (!ctx->side_st && cudaStreamCreateWithFlags(&ctx->side_st, cudaStreamNonBlocking) != cudaSuccess) {
@@ -1275,7 +1281,7 @@ static int mix_mlp(kgq_ctx* ctx, const MixSegs& sg, int M, int neg0, cudaStream_
   const RowMap* rmp = remap ? &rm : nullptr;
   const int half = ((M / 2 + 255) / 256) * 256;  // 256-row (one tile pair) aligned cut
   // (a failing fork / join call leaves its error for the submit's final cudaGetLastError check)
-  if (M >= 8192 && split_mlp_enabled() && side_stream(ctx) && cudaEventRecord(ctx->side_ev[0], st) == cudaSuccess &&
+  if (M >= split_mlp_rows() && split_mlp_enabled() && side_stream(ctx) && cudaEventRecord(ctx->side_ev[0], st) == cudaSuccess &&
       cudaStreamWaitEvent(ctx->side_st, ctx->side_ev[0], 0) == cudaSuccess) {
     L += mlp_rows(ctx, 0, half, neg0, st, &ctx->gws, pre, rmp);
     L += mlp_rows(ctx, half, M - half, neg0, ctx->side_st, &ctx->gws2, pre, rmp);
@@ -1369,7 +1375,7 @@ static kgq_status mixed_betae(kgq_ctx* ctx, std::vector<MixGroup>& G, int Q, int
                    ctx->tw, s2, w);
       };
       const int ir = (int)inter_rows, ih = ((ir / 2 + 255) / 256) * 256;
-      if (ir >= 8192 && split_mlp_enabled() && side_stream(ctx) &&
+      if (ir >= split_mlp_rows() && split_mlp_enabled() && side_stream(ctx) &&
           cudaEventRecord(ctx->side_ev[0], st) == cudaSuccess &&
           cudaStreamWaitEvent(ctx->side_st, ctx->side_ev[0], 0) == cudaSuccess) {
         attn(0, ih, st, &ctx->gws);
