@@ -306,8 +306,12 @@ struct epi_drain<E, std::void_t<decltype(E::DRAIN)>> : std::integral_constant<in
 #ifndef KGQ_TC_COLLECTOR  // A-grouped MMA order with collector re-use (see the MMA issuer)
 #define KGQ_TC_COLLECTOR 1
 #endif
-template <int BN, bool NBUF2 = false>
+#ifndef KGQ_TC_NBUF2  // split-output launches trade one operand stage for double-buffered staging
+#define KGQ_TC_NBUF2 1
+#endif
+template <int BN, bool NBUF2_ = false>
 struct Layout {
+  static constexpr bool NBUF2 = NBUF2_ && KGQ_TC_NBUF2;
   static constexpr int A_BYTES = BM * BK * 2;         // one bf16 plane of A: 8 KB
   static constexpr int W_BYTES = (BN / 2) * BK * 2;   // one plane of this CTA's half of the W tile
   static constexpr int STAGE_BYTES = kSplitPlanesA * A_BYTES + 3 * W_BYTES;  // A planes + 3 W planes
