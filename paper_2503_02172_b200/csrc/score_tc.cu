@@ -126,7 +126,14 @@ __global__ void k_score_prep_tc(const float* __restrict__ q, int rows, int d,
 // 16 four-dim threads left the other 112 idle for the last chain (25% of the fp64 time), and the
 // row sum is a shuffle tree without __syncthreads.
 constexpr int kPrepRows = 4;
-__global__ void __launch_bounds__(32 * kPrepRows)
+// Register cap: ten resident 128-thread blocks per SM (48 registers, 8 bytes spilled) instead of
+// the 64-register default's eight -- more rows in flight for the latency-bound fp64 chains:
+// 109 -> 92.5 us per C2 step (ncu), C2 +0.8%; twelve blocks (40 registers) spill 120 bytes
+// (95.7 us), sixteen 276 (101.6 us)
+#ifndef KGQ_PREP_MINB
+#define KGQ_PREP_MINB 10
+#endif
+__global__ void __launch_bounds__(32 * kPrepRows, KGQ_PREP_MINB)
     k_mix_score_prep(const int64_t* __restrict__ srcrow, Split S, int d, const double* __restrict__ sums, int64_t ns,
                      Split A, float2* __restrict__ P, int64_t B, int64_t b0, int nout, int rows) {
   pdl_grid_sync();
