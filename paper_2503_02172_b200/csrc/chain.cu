@@ -513,7 +513,14 @@ __global__ void k_attention_combine(CombineArgs c, Split S, const float* __restr
 
 // Mixed batches: the attention combine of every intersection group in one launch.  Block i is
 // query i of the concatenation of the groups (MixCombine::q_begin prefix).
-__global__ void k_mix_combine(MixCombine mc, Split S, const float* __restrict__ logits, int64_t ldl, Split Mst) {
+// Register cap: 16 resident 128-thread blocks per SM (32 registers, ~100 bytes spilled) instead of
+// ~10 at 48 registers -- more queries in flight for the latency-bound loads and exp / divide
+// chains: 47.4 -> 31.2 us per C2 step (ncu; 12 blocks / 40 registers: 34.1 us)
+#ifndef KGQ_COMBINE_MINB
+#define KGQ_COMBINE_MINB 16
+#endif
+__global__ void __launch_bounds__(128, KGQ_COMBINE_MINB)
+    k_mix_combine(MixCombine mc, Split S, const float* __restrict__ logits, int64_t ldl, Split Mst) {
   pdl_grid_sync();
   const int i = blockIdx.x;
   int g = 0;

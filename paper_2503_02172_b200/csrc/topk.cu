@@ -514,7 +514,7 @@ __device__ __forceinline__ void topk_lists_out(unsigned long long key, int lane,
   if (pp.on()) peer_push_warp(pp, ob, k, gk, lane);  // N2: fused all-gather
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128)  // (a register cap for 12 / 16 blocks per SM spills: slower)
     k_topk_lists(const unsigned long long* __restrict__ cand, int64_t ldcand, int k, int rows1, int nl1, int nl2,
                  int64_t id_base, const int32_t* __restrict__ invalid, const int32_t* __restrict__ out_row,
                  float* __restrict__ od, int32_t* __restrict__ oi, int B, const PeerPush pp) {
