@@ -226,12 +226,12 @@ __global__ void k_mix_scatter(MixSegs sg, Split src, Split S, int w) {
 
 // ---- hop-0 first projection layer from the per-entity precompute ------------------------------
 // Every hop-0 MLP row starts from an anchor entity e and a relation r, so its first layer is
-// W1 [x_e; R_r] + b1 = Hpre[e] + RW[r] + b1 with Hpre = X W1[:, :2d]^T precomputed for every entity
+// W1 [x_e; R_r] + b1 = Hpre[e] + RW[r] with Hpre = X W1[:, :2d]^T + b1 precomputed for every entity
 // at finalize (kgq_api.cu) -- the distributive law, as the relation term RW already is.  One block
-// per row: H0[row] = split(ReLU(Hpre[e] + RW[r] + b1)), 8 columns per thread; ids range-checked as
+// per row: H0[row] = split(ReLU(Hpre[e] + RW[r])), 8 columns per thread; ids range-checked as
 // in k_mix_gather (a bad id: row computed from id 0, query flagged).
 __global__ void k_mix_h0_pre(MixSegs sg, const float* __restrict__ Hpre, const float* __restrict__ RW,
-                             const float* __restrict__ bias, int H, Split H0, int64_t n_entity, int n_relation,
+                             int H, Split H0, int64_t n_entity, int n_relation,
                              int32_t* err, int32_t* invalid) {
   pdl_grid_sync();
   const int row = blockIdx.x;
@@ -257,25 +257,24 @@ __global__ void k_mix_h0_pre(MixSegs sg, const float* __restrict__ Hpre, const f
       for (int h = 0; h < 8; h += 4) {
         const float4 u = __ldg(reinterpret_cast<const float4*>(hp + j + h));
         const float4 v = __ldg(reinterpret_cast<const float4*>(rw + j + h));
-        const float4 w = __ldg(reinterpret_cast<const float4*>(bias + j + h));
-        x[h] = fmaxf((u.x + v.x) + w.x, 0.0f);
-        x[h + 1] = fmaxf((u.y + v.y) + w.y, 0.0f);
-        x[h + 2] = fmaxf((u.z + v.z) + w.z, 0.0f);
-        x[h + 3] = fmaxf((u.w + v.w) + w.w, 0.0f);
+        x[h] = fmaxf(u.x + v.x, 0.0f);
+        x[h + 1] = fmaxf(u.y + v.y, 0.0f);
+        x[h + 2] = fmaxf(u.z + v.z, 0.0f);
+        x[h + 3] = fmaxf(u.w + v.w, 0.0f);
       }
       store_split8(H0, o + j, x);
     }
   } else {
-    for (int j = threadIdx.x; j < H; j += blockDim.x) store_split(H0, o + j, fmaxf((hp[j] + rw[j]) + bias[j], 0.0f));
+    for (int j = threadIdx.x; j < H; j += blockDim.x) store_split(H0, o + j, fmaxf(hp[j] + rw[j], 0.0f));
   }
 }
 
-int launch_mix_h0_pre(const MixSegs& sg, int M, const float* Hpre, const float* RW, const float* bias, int H,
+int launch_mix_h0_pre(const MixSegs& sg, int M, const float* Hpre, const float* RW, int H,
                       Split H0, int64_t n_entity, int n_relation, int32_t* err, int32_t* invalid, cudaStream_t st) {
   if (M <= 0) return 0;
   // one thread per 8 columns: H = 1600 -> 200 threads, a 224-thread block (89% of its lanes busy)
   const int threads = std::min(256, std::max(32, ((H / 8 + 31) / 32) * 32));
-  launch_pdl(k_mix_h0_pre, dim3(M), dim3(threads), 0, st, sg, Hpre, RW, bias, H, H0, n_entity, n_relation, err,
+  launch_pdl(k_mix_h0_pre, dim3(M), dim3(threads), 0, st, sg, Hpre, RW, H, H0, n_entity, n_relation, err,
              invalid);
   return 1;
 }

@@ -325,7 +325,7 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
     // first layer with the relation input factored out (RelTerm): K = 2d straight from the state
     // rows (contiguous run) or from the gathered anchor rows; accumulators start at RW[r]
     if (src_row0 < 0 && ctx->Hpre) {
-      // hop 0 from the per-entity precompute: H0 = ReLU(Hpre[anchor] + RW[r] + b1), no GEMM
+      // hop 0 from the per-entity precompute: H0 = ReLU(Hpre[anchor] + RW[r]) (b1 is in Hpre), no GEMM
       MixSegs sg;
       for (int gi = 0; gi < n; ++gi) {
         MixSeg& m = sg.s[sg.n++];
@@ -333,7 +333,7 @@ int betae_hop(kgq_ctx* ctx, const ChainArgs& ca, int B, int hop, int br0, int n,
         m.anchors = ca.anchors; m.n_a = ca.n_a; m.aslot = g.anchor_slot[gi];
         m.rels = ca.rels; m.n_r = ca.n_r; m.rslot = g.rel_slot[gi];
       }
-      L += launch_mix_h0_pre(sg, M, ctx->Hpre, ctx->RW, ctx->lin1x.b, ctx->lin1x.out_f, ctx->H[0], ctx->cfg.n_entity,
+      L += launch_mix_h0_pre(sg, M, ctx->Hpre, ctx->RW, ctx->lin1x.out_f, ctx->H[0], ctx->cfg.n_entity,
                              ctx->cfg.n_relation, ca.err, ca.invalid, st);
     } else {
       if (src_row0 < 0) {
@@ -624,7 +624,7 @@ void kgq_destroy(kgq_ctx* ctx) {
   F(ctx->ent); F(ctx->rel[0]); F(ctx->rel[1]); F(ctx->score_tab);
   for (auto& l : ctx->lin) { F(l.W); F(l.Wsp.b0); F(l.b); }
   for (Split* s : {&ctx->S, &ctx->Z, &ctx->H[0], &ctx->H[1], &ctx->I, &ctx->M}) F(s->b0);
-  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->cand); F(ctx->Hpre); F(ctx->zero_bias); F(ctx->d_err); F(ctx->d_invalid);
+  F(ctx->T); F(ctx->T2); F(ctx->Q); F(ctx->Qt); F(ctx->dist); F(ctx->cmin); F(ctx->cand); F(ctx->Hpre); F(ctx->d_err); F(ctx->d_invalid);
   F(ctx->topk_tmp_d); F(ctx->topk_tmp_i); F(ctx->uv.b0); F(ctx->Esum); F(ctx->uvT); F(ctx->lin1x.Wsp.b0); F(ctx->RW);
   F(ctx->mix_rid); F(ctx->mix_map);
   if (ctx->mix_map_host) cudaFreeHost(ctx->mix_map_host);
@@ -828,24 +828,21 @@ kgq_status kgq_finalize(kgq_ctx* ctx) {
       return fail(ctx, KGQ_ERANGE, "a weight (|w| >= 32) or BetaE entity term is outside the fp16x2 operand range; "
                   "use the bf16x3 build (libkgq_bf16x3.so, KGQ_OPERANDS=bf16x3)");
     if (ctx->RW && hpre_enabled() && (double)c.n_entity * ctx->lin1x.out_f * sizeof(float) <= kHpreBytesMax) {
-      // hop-0 first layer per entity: Hpre = X W1[:, :2d]^T over the regularised table (the same
-      // tensor-core GEMM as the layer itself, no bias), through a temporary split copy of X.  An
+      // hop-0 first layer per entity: Hpre = X W1[:, :2d]^T + b1 over the regularised table (the
+      // same tensor-core GEMM as the layer itself, its bias folded in so the per-query gather adds
+      // only RW[r]), through a temporary split copy of X.  An
       // entity row outside the fp16x2 range only disables the precompute (hop 0 then gathers and
       // multiplies per query, and flags such an anchor when a query uses it).
       const int H = ctx->lin1x.out_f;
       if (!ctx->Hpre) {
         kgq_status st2 = dalloc(ctx, &ctx->Hpre, (size_t)c.n_entity * H, "hop-0 layer-1 precompute");
-        if (!st2) st2 = dalloc(ctx, &ctx->zero_bias, (size_t)H, "zero bias");
         if (st2) return st2;
-        CK(cudaMemset(ctx->zero_bias, 0, (size_t)H * sizeof(float)), "zero bias");
       }
       Split X;
       kgq_status st2 = alloc_split(ctx, &X, c.n_entity, 2 * d, "entity split (finalize)");
       if (st2) return st2;
       launch_split_copy_rows(ctx->ent, c.n_entity, 2 * d, X, 0, 2 * d, true);
-      Linear l0 = ctx->lin1x;
-      l0.b = ctx->zero_bias;
-      launch_linear(X, (int)c.n_entity, 2 * d, l0, kEpiNone, Split{}, ctx->Hpre, H, 0, 0, &ctx->gws, 0);
+      launch_linear(X, (int)c.n_entity, 2 * d, ctx->lin1x, kEpiNone, Split{}, ctx->Hpre, H, 0, 0, &ctx->gws, 0);
       CK(cudaDeviceSynchronize(), "hop-0 precompute");
       cudaFree(X.b0);
       if (range_flag_chain()) {  // the X split (the only conversion of this interval) overflowed
@@ -1263,7 +1260,7 @@ static int mix_mlp(kgq_ctx* ctx, const MixSegs& sg, int M, int neg0, cudaStream_
   bool pre = ctx->Hpre != nullptr;
   for (int i = 0; i < sg.n && pre; ++i) pre = sg.s[i].kind == 0;
   if (pre)
-    L += launch_mix_h0_pre(sg, M, ctx->Hpre, ctx->RW, ctx->lin1x.b, ctx->lin1x.out_f, ctx->H[0], ctx->cfg.n_entity,
+    L += launch_mix_h0_pre(sg, M, ctx->Hpre, ctx->RW, ctx->lin1x.out_f, ctx->H[0], ctx->cfg.n_entity,
                            ctx->cfg.n_relation, ctx->d_err, ctx->d_invalid, st);
   else
     L += launch_mix_gather(sg, M, ctx->ent, ctx->S, ctx->M, ctx->Z, ctx->mix_rid, d, ctx->cfg.n_entity,

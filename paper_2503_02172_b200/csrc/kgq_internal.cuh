@@ -113,8 +113,7 @@ struct kgq_ctx {
   kgq::Split uv{};                         // [np][2d] centred (u; v), bf16x3
   kgq::Linear lin1x{};                     // BetaE first projection layer, state columns W1[:, :2d]
   float* RW = nullptr;                     // [n_relation, H] relation term R W1[:, 2d:]^T (fp64 -> fp32)
-  float* Hpre = nullptr;                   // [n_entity, H] X W1[:, :2d]^T of every (regularised) entity row
-  float* zero_bias = nullptr;              // [H] zeros (the Hpre GEMM has no bias)
+  float* Hpre = nullptr;                   // [n_entity, H] X W1[:, :2d]^T + b1 of every (regularised) entity row
   int32_t* mix_rid = nullptr;              // mixed batches: per-row relation ids of a hop batch [rows_max]
   int64_t* mix_map = nullptr;              // mixed batches: score-row source rows [2 max_batch] + output rows
   int64_t* mix_map_host = nullptr;         // pinned staging of mix_map
@@ -276,7 +275,7 @@ int launch_mix_gather(const MixSegs& sg, int M, const float* ent, Split S, Split
                       int64_t n_entity, int n_relation, int32_t* err, int32_t* invalid, cudaStream_t st);
 // hop-0 first projection layer from the per-entity precompute: H0[row] = split(ReLU(Hpre[anchor]
 // + RW[rel] + bias)) for batch rows whose segments are anchor-sourced (kind 0); ids range-checked
-int launch_mix_h0_pre(const MixSegs& sg, int M, const float* Hpre, const float* RW, const float* bias, int H,
+int launch_mix_h0_pre(const MixSegs& sg, int M, const float* Hpre, const float* RW, int H,
                       Split H0, int64_t n_entity, int n_relation, int32_t* err, int32_t* invalid, cudaStream_t st);
 // batch rows [dst0 + b] of src -> S rows src0 + b (width w)
 int launch_mix_scatter(const MixSegs& sg, int M, Split src, Split S, int w, cudaStream_t st);
