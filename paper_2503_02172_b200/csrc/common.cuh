@@ -1,5 +1,6 @@
 // Small device helpers shared by the kernels of libkgq.so.
 #pragma once
+#include <mutex>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -13,16 +14,25 @@ namespace kgq {
 // Opt a kernel into more than 48 KB of dynamic shared memory on the CURRENT device.  The
 // attribute is per (function, device): a process-wide "done" flag would leave a second
 // context on another device launching with the 48 KB default (every launch there fails), so
-// the flag is one bit per device, per call site (F = the kernel's function pointer type +
-// the calling template instance).  cudaGetDevice is a host-side lookup (no sync).
+// the cache is per device, per call site (F = the kernel's function pointer type + the calling
+// template instance).  It holds the LARGEST value set: the attribute is a limit, and a call
+// site whose size depends on the problem (the streaming scorers: d x query rows) must never
+// lower it -- caching only "done" once let a d = 40 context set 5 KB and a later d = 400 one
+// launch 51 KB against it ("invalid argument").  cudaGetDevice is a host-side lookup.
+struct SmemAttr {
+  int set[64] = {};  // per device: the largest MaxDynamicSharedMemorySize set so far
+};
 template <class F>
-inline void smem_attr_once(F* kern, int bytes, unsigned long long& done_mask) {
+inline void smem_attr_once(F* kern, int bytes, SmemAttr& a) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (__atomic_load_n(&done_mask, __ATOMIC_ACQUIRE) & bit) return;
+  int* s = &a.set[dev & 63];
+  if (__atomic_load_n(s, __ATOMIC_ACQUIRE) >= bytes) return;
+  static std::mutex mu;  // set + record atomically, so racing callers never lower the limit
+  std::lock_guard<std::mutex> g(mu);
+  if (*s >= bytes) return;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  __atomic_fetch_or(&done_mask, bit, __ATOMIC_ACQ_REL);
+  __atomic_store_n(s, bytes, __ATOMIC_RELEASE);
 }
 
 // fp32 tensor held as three bf16 planes, the operand format of the tensor-core GEMMs

@@ -138,7 +138,7 @@ int launch_peer_merge(const PeerPush& pp, int B, int k, float* out_d, int32_t* o
                       long long timeout_ns, cudaStream_t st) {
   if (B <= 0) return 0;
   const size_t smem = (size_t)kMergeWarps * pp.world * k * sizeof(unsigned long long);
-  static unsigned long long attr = 0;
+  static SmemAttr attr;
   smem_attr_once(k_peer_merge, 200 * 1024, attr);
   launch_pdl(k_peer_merge, dim3((B + kMergeWarps - 1) / kMergeWarps), dim3(32 * kMergeWarps), smem, st, pp, B, k,
              out_d, out_i, err, timeout_ns, const_cast<uint32_t*>(pp.epoch), const_cast<uint32_t*>(pp.epoch) + 1);

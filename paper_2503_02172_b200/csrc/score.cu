@@ -408,7 +408,7 @@ void launch_uv_stream_t(const Split& A, const float2* P, const float* uvT, const
                         float* dist, int64_t ldd, int B, cudaStream_t st) {
   constexpr int HALVES = QB * NB >= 16 ? 2 : 1;
   const size_t smem = (size_t)d * QB * NB * sizeof(float2);
-  static unsigned long long attr = 0;
+  static SmemAttr attr;
   smem_attr_once(k_score_uv_stream<NB, QB>, (int)smem, attr);
   const int64_t gpb = 8 * 32 / HALVES;
   const int64_t want = (np / 4 + gpb - 1) / gpb;
@@ -442,7 +442,7 @@ void launch_t(const float* Qt, int64_t rpad, const float* tab, int64_t np, int d
               float* dist, int64_t ldd, int B, cudaStream_t st) {
   constexpr int NQ = Planes<MODEL>::NQ, NE = Planes<MODEL>::NE;
   const size_t smem = (size_t)2 * (NQ * DK * TQ + NE * DK * TE) * sizeof(float);
-  static unsigned long long attr = 0;
+  static SmemAttr attr;
   smem_attr_once(k_score<MODEL, NB>, (int)smem, attr);
   const int rows = B * NB;
   dim3 grid((unsigned)(np / TE), (unsigned)((rows + TQ - 1) / TQ));

@@ -1019,7 +1019,7 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
     return -1;
   }
   auto kern = k_gemm<BN, Epi>;
-  static unsigned long long attr = 0;
+  static SmemAttr attr;
   smem_attr_once(kern, Layout<BN, Epi::PLANES == 3>::TOTAL, attr);
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
   if (sc.s_tail <= 1 || !sc.ws || !sc.cnt || epi_topk<Epi>::value) {

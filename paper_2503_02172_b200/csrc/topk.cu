@@ -593,10 +593,68 @@ __global__ void __launch_bounds__(128)  // (a register cap for 12 / 16 blocks pe
   topk_lists_out(key, lane, k, ob, id_base, od, oi, pp);
 }
 
+// <= 8 lists per row, k <= 16, no peer push (the mixed step's fused rows: 3 stripes x 2 column
+// halves): eight lanes per row, four rows per warp -- three shuffle levels per round instead of
+// five and a quarter of the warps (the one-row-per-warp merge is latency-bound: 21 us for the C2
+// step's 12,288 rows).  Same keys, same order as k_topk_lists: bit-identical outputs.
+__global__ void __launch_bounds__(128)
+    k_topk_lists8(const unsigned long long* __restrict__ cand, int64_t ldcand, int k, int rows1, int nl1, int nl2,
+                  int64_t id_base, const int32_t* __restrict__ invalid, const int32_t* __restrict__ out_row,
+                  float* __restrict__ od, int32_t* __restrict__ oi, int B) {
+  pdl_grid_sync();
+  const int lane = threadIdx.x & 31, gl = lane & 7;
+  const int b = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + (lane >> 3);
+  const bool live = b < B;
+  const int ob = live ? (out_row ? out_row[b] : b) : 0;
+  const bool bad = live && invalid && invalid[ob];
+  const int nl = b < rows1 ? nl1 : nl2;
+  const unsigned long long* row = cand + (int64_t)(live ? b : 0) * ldcand;
+  unsigned long long lst[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) lst[j] = (live && !bad && gl < nl && j < k) ? row[(int64_t)gl * k + j] : ~0ull;
+  unsigned long long o0 = ~0ull, o1 = ~0ull;  // outputs gl and gl + 8 of this lane's row
+  for (int j = 0; j < k; ++j) {               // k is warp-uniform: the shuffles stay converged
+    unsigned long long w = lst[0];
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, w, o);
+      w = t < w ? t : w;
+    }
+    if (j == gl) o0 = w;
+    if (j == gl + 8) o1 = w;
+    if (w != ~0ull && lst[0] == w) {  // unique keys: exactly one lane's head
+#pragma unroll
+      for (int q = 0; q < 15; ++q) lst[q] = lst[q + 1];
+      lst[15] = ~0ull;
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int jj = gl + 8 * h;
+    if (jj >= k) continue;
+    const unsigned long long key = h ? o1 : o0;
+    float* d = od + (int64_t)ob * k + jj;
+    int32_t* i = oi + (int64_t)ob * k + jj;
+    if (bad || key == ~0ull) {
+      *d = __uint_as_float(0x7FFFFFFFu);
+      *i = -1;
+    } else {
+      *d = fkey_inv((uint32_t)(key >> 32));
+      *i = (int32_t)(uint32_t)(id_base + (int64_t)(uint32_t)(key & 0xFFFFFFFFu));
+    }
+  }
+}
+
 int launch_topk_lists(const unsigned long long* cand, int64_t ldcand, int k, int B, int rows1, int nl1, int nl2,
                       int64_t id_base, const int32_t* invalid, const int32_t* out_row, float* out_d, int32_t* out_i,
                       cudaStream_t st, const PeerPush& pp) {
   if (B <= 0) return 0;
+  if (nl1 <= 8 && nl2 <= 8 && k <= 16 && !pp.on()) {
+    launch_pdl(k_topk_lists8, dim3((B + 15) / 16), dim3(128), 0, st, cand, ldcand, k, rows1, nl1, nl2, id_base,
+               invalid, out_row, out_d, out_i, B);
+    return 1;
+  }
   launch_pdl(k_topk_lists, dim3((B + 3) / 4), dim3(128), 0, st, cand, ldcand, k, rows1, nl1, nl2, id_base, invalid,
              out_row, out_d, out_i, B, pp);
   return 1;
@@ -641,7 +699,7 @@ void launch_topk_kernel(dim3 grid, const float* dist, int64_t ldd, int64_t n, in
   int Q = 1;
   while (Q < (kTopkThreads / 32) * k) Q <<= 1;
   const int smem = (int)(((kTopkThreads / 32) * P + Q) * sizeof(unsigned long long));
-  static unsigned long long attr = 0;
+  static SmemAttr attr;
   smem_attr_once(k_topk, 64 * 1024, attr);
   k_topk<<<grid, kTopkThreads, smem, st>>>(dist, ldd, n, chunk, k, id_base, invalid, od, oi, B, P);
 }

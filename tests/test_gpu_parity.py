@@ -678,6 +678,26 @@ def test_scorer_row_chunks(model):
     e.close()
 
 
+def test_streaming_scorer_shared_memory_limit_across_dims():
+    """The small-batch streaming scorers stage the query rows in dynamic shared memory sized
+    d x rows: a d = 40 context first (5 KB for BetaE 2u at B = 8), then a d = 400 one in the same
+    process (51 KB, above the 48 KB default) -- the opt-in limit is cached per call site and must
+    only ever be raised (a cached "done" flag once left it at 5 KB: invalid argument)."""
+    for d, N in ((40, 1000), (400, 3000)):
+        t = synth.make_tables("betae", N, 20, d, hidden=64, seed=41)
+        e = Engine("betae", N, 20, d, hidden=64, max_batch=8, max_k=10)
+        e.load_tables(t)
+        m = O.Model("betae", t, dim=d)
+        a, r = synth.make_queries("2u", 8, N, 20, seed=42)
+        td, ti = e.submit("2u", dev(a), dev(r), 10)
+        e.check_errors()
+        ref = m.scores("2u", a, r)
+        td, ti = td.cpu().numpy(), ti.cpu().numpy()
+        for b in range(8):
+            assert_topk_ok(td[b], ti[b], ref[b], 10, what=f"stream d={d} row {b}")
+        e.close()
+
+
 def test_mixed_graph_replay_matches_eager():
     """The second identical kgq_submit_mixed is captured into a CUDA graph and later calls
     replay it (inputs repacked into the same staging buffers, new query content every round):
