@@ -3,13 +3,14 @@
 // Used by the BetaE projection MLP (Eq. 4) and the intersection attention nets
 // -- the only dense contractions on the path.  B200 has no fp32-input MMA,
 // and single-pass TF32 / BF16 miss the 1e-4 parity bound (SURVEY §0 finding 5), so operands are
-// held as three bf16 planes x = x0 + x1 + x2 (exact, common.cuh Split) and
-//   x w ~= x0 w0 + x0 w1 + x1 w0 + x0 w2 + x1 w1 + x2 w0     (dropped terms <= 2^-23 |x w|)
-// accumulated in fp32 in TMEM (bf16x3, tc_gemm.cuh).  Operands are produced already split (every
+// held split (common.cuh Split): by default fp16x2 (x = h + l' 2^-11, three fp16 MMAs per fp32
+// multiply-add), in the full-range build bf16x3 (x = x0 + x1 + x2, exact;
+//   x w ~= x0 w0 + x0 w1 + x1 w0 + x0 w2 + x1 w1 + x2 w0     (dropped terms <= 2^-23 |x w|)),
+// accumulated in fp32 in TMEM (tc_gemm.cuh).  Operands are produced already split (every
 // producer kernel writes the three planes), so the mainloop is a pure TMA -> tcgen05.mma
 // pipeline; the GEMM core (persistent CTA-pair kernel, TMA-store epilogue) is tc_gemm.cuh.  This
 // file supplies the epilogue: bias + ReLU / BetaE regulariser (+ negation) fused, split
-// (bf16x3) or fp32 output.
+// (split planes) or fp32 output.
 #include <stdint.h>
 
 #include "tc_gemm.cuh"
@@ -20,7 +21,7 @@ namespace {
 using tc::BM;
 
 // nn.Linear epilogue: + bias, ReLU / BetaE regulariser (clamp(y+1,.05,1e9)) with 1/x on rows
-// [neg0, neg1) (negation fused, Q5); output split (bf16x3, PLANES 3) for a next dense layer,
+// [neg0, neg1) (negation fused, Q5); output split (PLANES 3) for a next dense layer,
 // or fp32.
 // REL: first BetaE projection layer with the relation input factored out (RelTerm below): the
 // accumulator of row (group gi, query b) starts at RW[r] for r = rels[b, rel_slot[gi]].

@@ -13,7 +13,8 @@
 // (Sterbenz; the usual case, P ~ -E) and otherwise errs by <= 2^-24 |P + E| ~ 2^-24 dist, the
 // dropped lo-lo rounding is ~2^-48 |P|, so dist carries ~1e-7 relative -- three FADDs instead
 // of fp64 adds and conversions, and no fp64 registers next to the row accumulators.
-// The last term is a dense contraction [rows, 2d] x [2d, N] -> bf16x3 on tcgen05 (tc_gemm.cuh).
+// The last term is a dense contraction [rows, 2d] x [2d, N] on tcgen05 with split fp32 operands
+// (fp16x2 by default, bf16x3 in the full-range build; tc_gemm.cuh, common.cuh).
 // Centring keeps its terms ~0.1 (|u|, |v| << |U|, |V| ~ 1), so the fp32 partial sums carry
 // ~1e-7 of sum|terms| ~ 1e-5 absolute instead of ~1e-4 for the uncentred sum, and the large,
 // cancelling P_q + E_e (~ +-800 at d = 400) are added in fp64 in the epilogue.  DNF union:

@@ -1,5 +1,8 @@
-// tcgen05 bf16x3 GEMM core shared by the dense layers (linear_tc.cu) and the tensor-core
-// BetaE scorer (score_tc.cu).
+// tcgen05 GEMM core on split fp32 operands, shared by the dense layers (linear_tc.cu) and the
+// tensor-core BetaE scorer (score_tc.cu).  Two operand formats (common.cuh KGQ_OPERAND_FP16X2):
+// fp16x2 -- the default build, three fp16 MMAs per fp32 multiply-add into one 2^11-scaled fp32
+// accumulator (see common.cuh) -- and bf16x3, the full-range build (libkgq_bf16x3.so) described
+// here; the pipeline below is the same for both, only the plane count and MMA list differ.
 //
 // acc[m, n] = sum_k A[m, k] W[n, k] in bf16x3: every fp32 operand is held as three bf16 planes
 // x = x0 + x1 + x2 (exact; written by every upstream kernel, common.cuh), and
