@@ -1082,7 +1082,7 @@ constexpr double kC0Us = kFp16x2 ? -1.12 : 3.40, kPubUs = kFp16x2 ? 0.0281 : 0.0
 constexpr int kTileBN[5] = {64, 128, 160, 192, 256};
 struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN, KGQ_GEMM_KB128 (us per K-block)
   int force_bn = 0;
-  double kb128 = 0.0;
+  double kb128 = 0.0, kb256 = 0.0;
   bool no160 = false;
   bool deterministic = true;  // KGQ_DETERMINISTIC=0 allows more than two K-splits (plan_gemm)
   PlanKnobs() {
@@ -1094,6 +1094,8 @@ struct PlanKnobs {  // tuning experiments only (scripts/gpu_ab.sh): KGQ_GEMM_BN,
     if (e) force_bn = atoi(e);
     e = getenv("KGQ_GEMM_KB128");
     if (e) kb128 = atof(e);
+    e = getenv("KGQ_GEMM_KB256");
+    if (e) kb256 = atof(e);
   }
 };
 inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allow160) {
@@ -1110,6 +1112,7 @@ inline Plan plan_gemm(int64_t M, int64_t N, int64_t K, bool can_split, bool allo
     const int64_t full = tiles / cl * cl, tail = tiles - full;
     double kb = kKbUs[bn == 64 ? 0 : bn == 128 ? 1 : bn == 160 ? 2 : bn == 192 ? 3 : 4];
     if (bn == 128 && knobs.kb128 > 0) kb = knobs.kb128;
+    if (bn == 256 && knobs.kb256 > 0) kb = knobs.kb256;
     // Two partials commute exactly; with three or more the last-arriving split adds the others
     // after its own, so the fp32 grouping (and the last bit) depends on arrival order.
     // Default: at most two splits, so reruns are bit-identical (measured cost on C2: ~0.1%);
