@@ -68,6 +68,17 @@ inline int gemm_group_m() {
   }();
   return v;
 }
+// the dense layers' raster group: 6 (same-box A/B of the final step: 6 -> 7.125M, 4 -> 7.11M, 8 ->
+// 7.09M q/s; the scorer keeps 8).  KGQ_GEMM_GROUP_M_DENSE overrides, KGQ_GEMM_GROUP_M sets both.
+inline int gemm_group_m_dense() {
+  static const int v = [] {
+    const char* e = getenv("KGQ_GEMM_GROUP_M_DENSE");
+    if (e) return atoi(e);
+    e = getenv("KGQ_GEMM_GROUP_M");
+    return e ? atoi(e) : 6;
+  }();
+  return v;
+}
 
 // ---- PTX wrappers -----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1036,7 +1047,7 @@ int launch_gemm(const Split& A, int M, const Split& W, int N, int K, const OutDe
   const int units = epi_topk<Epi>::value ? ((M + 2 * BM - 1) / (2 * BM)) * sc.n_stripes
                                          : sc.full + (tiles - sc.full) * sc.s_tail;
   const int clusters = units < max_clusters ? units : max_clusters;
-  if (sc.group_m == 0) sc.group_m = gemm_group_m();
+  if (sc.group_m == 0) sc.group_m = (Epi::CMIN || epi_topk<Epi>::value) ? gemm_group_m() : gemm_group_m_dense();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(THREADS);
